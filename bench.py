@@ -1,0 +1,336 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 Strassen DGEMM (driver contract).
+
+One step = one strassen_gemm call (C := alpha A B + C) on the workload
+m = n = k = 16384, column-major fp64, uniform[-1, 1) synthetic inputs
+(BASELINE.json configs[1], top of the square sweep; it fits one GPU).
+Default variant: ABC, two levels.  Prints ONE JSON line on rank 0.
+
+  value     effective FP64 TFLOP/s (2mnk / t, summed over ranks), device
+            pointers, inputs resident in HBM, CUDA events on the launch stream
+  e2e       the same metric through the C ABI with pinned HOST buffers:
+            H2D of A, B, C and D2H of C inside the timed region
+  roofline  executed flops of the mm_kernel launch / its CUDA-event duration
+            vs the measured FP64 DMMA peak (profiles/fp64_peaks.json)
+  cpu_baseline  the reference library itself (oracle/_ref, compiled from the
+            reference sources with its own flags) on a bounded sample
+  --impl reference  times that reference CPU path alone (rank 0).
+
+Multi-GPU (torchrun, N > 1): every rank runs its own 16384^3 instance
+("replicas", weak scaling); time = max over ranks.  The SUMMA distributed
+layer is benchmarked separately.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CPU_SAMPLE = 4096  # bounded reference sample: m = n = k = 4096
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    p.add_argument("--variant", default="abc", choices=["dgemm", "abc", "ab", "naive"])
+    p.add_argument("--level", type=int, default=2)
+    p.add_argument("--dim", type=int, default=16384)
+    p.add_argument("--m", type=int, default=0)
+    p.add_argument("--n", type=int, default=0)
+    p.add_argument("--k", type=int, default=0)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-classical", action="store_true")
+    p.add_argument("--cpu-sample", type=int, default=CPU_SAMPLE)
+    a = p.parse_args()
+    if a.variant == "dgemm":
+        a.level = 0
+    a.m = a.m or a.dim
+    a.n = a.n or a.dim
+    a.k = a.k or a.dim
+    return a
+
+
+def table_counts(level):
+    return {0: (1, 0, 0, 1), 1: (7, 5, 5, 12), 2: (49, 95, 95, 144)}[level]
+
+
+def executed_flops(m, n, k, level):
+    """F_exec (implementation counts, 144 C updates at L2)."""
+    if level == 0:
+        return 2.0 * m * n * k
+    s = 1 << level
+    qm, qn, qk = -(-m // s), -(-n // s), -(-k // s)
+    mul, aa, ba, cu = table_counts(level)
+    return mul * 2.0 * qm * qn * qk + 2.0 * (aa * qm * qk + ba * qk * qn + cu * qm * qn)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def reference_cpu(dim, variant, level, reps=2, warmup=1):
+    """The reference library itself on the host cores (bounded sample)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import numpy as np
+
+    import oracle_lib as O
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    kind, path = "reference", O.REF_SO
+    if not O.RefStrassen.available():
+        raise RuntimeError("oracle/_ref/libstrassen_ref.so missing (make -C oracle ref)")
+    ref = O.RefStrassen(path)
+    ref.set_threads(cores)
+    rng = np.random.default_rng(0)
+    a = np.asfortranarray(rng.uniform(-1, 1, (dim, dim)))
+    b = np.asfortranarray(rng.uniform(-1, 1, (dim, dim)))
+    c = np.asfortranarray(rng.uniform(-1, 1, (dim, dim)))
+    times = []
+    for i in range(warmup + reps):
+        t0 = time.perf_counter()
+        ref.gemm(variant, level, 1.0, a, b, c)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+    return {"kind": kind, "cores": cores, "times": times,
+            "sample": f"m=n=k={dim} {variant}{level} via the reference C ABI "
+                      f"(oracle/_ref, -O3 -DNDEBUG -fopenmp, threads={cores}), column-major, "
+                      f"uniform[-1,1); best of {reps} after {warmup} warm-up"}
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    dim = args.cpu_sample
+    r = reference_cpu(dim, args.variant, args.level, reps=args.steps, warmup=args.warmup)
+    t = sum(r["times"]) / len(r["times"])
+    tf = 2.0 * dim ** 3 / t / 1e12
+    line = {
+        "impl": "reference", "metric": "effective FP64 TFLOPS (2mnk/t)", "value": tf,
+        "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic uniform[-1,1)",
+        "config": {"workload": f"square m=n=k={args.m} {args.variant} level {args.level} "
+                   f"(bounded CPU sample m=n=k={dim})", "variant": args.variant,
+                   "level": args.level, "m": dim, "n": dim, "k": dim},
+        "cpu_baseline": {"value": tf, "unit": "TFLOP/s", "cores": r["cores"], "kind": r["kind"],
+                         "sample": r["sample"]},
+        "e2e": {"value": tf, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1605_01078_b200 as S
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    m, n, k = args.m, args.n, args.k
+    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
+
+    def colmajor(r, c):
+        x = torch.empty((c, r), dtype=torch.float64, device="cuda")
+        x.uniform_(-1.0, 1.0, generator=g)
+        return x.t()  # (r, c) with strides (1, r)
+
+    A, B, C = colmajor(m, k), colmajor(k, n), colmajor(m, n)
+    ctx = S.Ctx()
+    stream = torch.cuda.current_stream()
+
+    def time_device(variant, level, steps, warmup):
+        for _ in range(warmup):
+            ctx.gemm_device(variant, level, 1.0, A, B, C, stream)
+        barrier()
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(steps)]
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for e0, e1 in evs:
+            e0.record(stream)
+            ctx.gemm_device(variant, level, 1.0, A, B, C, stream)
+            e1.record(stream)
+        t1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        total_ms = t0.elapsed_time(t1)
+        per = [e0.elapsed_time(e1) for e0, e1 in evs]
+        return total_ms, per, ctx.last_launches()
+
+    with ClockSampler(local) as clk:
+        total_ms, per_ms, launches = time_device(args.variant, args.level, args.steps, args.warmup)
+    total_ms = max_over_ranks(total_ms)
+    ms_per_step = total_ms / args.steps
+    flops = 2.0 * m * n * k
+    value = world * flops / (ms_per_step * 1e-3) / 1e12
+
+    # roofline of the dominant kernel (the only launch of an aligned ABC/DGEMM call)
+    peaks = json.load(open(os.path.join(ROOT, "profiles", "fp64_peaks.json")))
+    kern_ms = statistics.mean(per_ms)
+    f_exec = executed_flops(m, n, k, args.level)
+    achieved = f_exec / (kern_ms * 1e-3) / 1e12
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        t = json.load(open(tpath))
+        key = f"{args.variant}{args.level}_{m}x{n}x{k}"
+        if key in t:
+            traffic = t[key]
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["dmma_tflops"],
+                "unit": "TFLOP/s", "frac": achieved / peaks["dmma_tflops"], "traffic": traffic,
+                "flops_per_launch": f_exec, "kernel_ms": kern_ms, "launches_per_step": launches,
+                "peak_source": "measured FP64 DMMA peak, profiles/fp64_peaks.json "
+                               "(MEASURED_PEAKS.json has bf16/HBM only)"}
+
+    line = {
+        "metric": "effective FP64 TFLOPS (2mnk/t)", "value": value, "unit": "TFLOP/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic uniform[-1,1) (torch generator, column-major, inputs > L2)",
+        "config": {"workload": f"square m=n=k={m}" if m == n == k else f"{m}x{n}x{k}",
+                   "variant": args.variant, "level": args.level, "m": m, "n": n, "k": k,
+                   "layout": "column-major lda=m", "alpha": 1.0, "beta": 1.0,
+                   "l2": "inputs (3 x 2 GiB) larger than the 126 MB L2",
+                   "parallelism": "replicas" if world > 1 else "single"},
+        "roofline": roofline, "clocks": clk.summary(),
+        "gpu_launches": launches * args.steps,
+    }
+
+    if not args.no_classical and args.variant != "dgemm":
+        c_total, c_per, _ = time_device("dgemm", 0, max(2, args.steps // 2), 1)
+        c_ms = max_over_ranks(c_total) / max(2, args.steps // 2)
+        line["classical"] = {"variant": "dgemm (this library's B200 classical kernel)",
+                             "value": world * flops / (c_ms * 1e-3) / 1e12, "ms_per_step": c_ms}
+        # cuBLAS DGEMM via torch for context (library ceiling, not our path)
+        D = torch.empty_like(C)
+        for _ in range(2):
+            torch.matmul(A, B, out=D)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            torch.matmul(A, B, out=D)
+        e1.record()
+        torch.cuda.synchronize()
+        cb = e0.elapsed_time(e1) / 3
+        line["cublas_dgemm"] = {"value": flops / (cb * 1e-3) / 1e12, "ms_per_step": cb}
+        del D
+
+    if not args.no_e2e:
+        # end to end through the C ABI with pinned host buffers: H2D(A, B, C) + D2H(C)
+        Ah = A.t().cpu().pin_memory().t()
+        Bh = B.t().cpu().pin_memory().t()
+        Ch = C.t().cpu().pin_memory().t()
+        e2e_steps = max(2, min(args.steps, 3))
+        ctx.gemm(args.variant, args.level, 1.0, Ah, Bh, Ch)  # warm (staging buffers)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            ctx.gemm(args.variant, args.level, 1.0, Ah, Bh, Ch)
+        dt = max_over_ranks((time.perf_counter() - t0) / e2e_steps)
+        line["e2e"] = {"value": world * flops / dt / 1e12, "unit": "TFLOP/s",
+                       "h2d_bytes_per_step": 8 * (m * k + k * n + m * n),
+                       "d2h_bytes_per_step": 8 * m * n, "ms_per_step": dt * 1e3,
+                       "api": "strassen_gemm (C ABI, pinned host pointers)"}
+        line["gpu_launches"] += ctx.last_launches() * e2e_steps
+
+    if rank == 0 and world == 1 and not args.no_cpu:
+        r = reference_cpu(args.cpu_sample, args.variant, args.level)
+        t = min(r["times"])
+        line["cpu_baseline"] = {"value": 2.0 * args.cpu_sample ** 3 / t / 1e12, "unit": "TFLOP/s",
+                                "cores": r["cores"], "kind": r["kind"], "sample": r["sample"]}
+
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,203 @@
+/*
+ * strassen.h -- C ABI of the B200 (sm_100a) Strassen DGEMM library
+ * (libstrassen_b200.so).
+ *
+ * Drop-in for the reference library's public interface
+ * (/root/reference/proj/include/strassen.h, shared target `strassen`,
+ * proj/CMakeLists.txt:28-30).  Every declaration in PART 1 keeps the
+ * reference's name, argument meaning, status codes and validation order; the
+ * comment on each cites the reference declaration (strassen.h:line) and its
+ * implementation (capi.cpp:line).  PART 2 adds B200 entry points that the
+ * reference does not have (device-pointer / stream entry, column-major dgemm
+ * shim with beta, launch accounting).
+ *
+ * Semantics (reference strassen.h:1-6, matrix.hpp:9-27): all matrices are
+ * double precision, addressed as (base pointer, row stride, column stride)
+ * in elements; element (i, j) lives at p[i*rs + j*cs]; a transpose is a
+ * stride swap.  Every multiply computes C := alpha * A * B + C (no beta).
+ *
+ * Pointers may be host memory (pageable or pinned) or device memory (cudaMalloc /
+ * managed).  Host operands are staged through device memory inside the call;
+ * device operands are used in place.  strassen_gemm returns after C is
+ * updated (synchronous, like the reference).  There is no CPU fallback: when
+ * no CUDA device is usable, compute entry points return STRASSEN_ERR_DEVICE.
+ */
+#ifndef STRASSEN_B200_H
+#define STRASSEN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ============================ PART 1: reference ABI ======================== */
+
+/* reference strassen.h:16-23 */
+typedef enum strassen_status {
+    STRASSEN_OK = 0,
+    STRASSEN_ERR_DIMENSION = 1,
+    STRASSEN_ERR_PARAM = 2,
+    STRASSEN_ERR_DOMAIN = 3,
+    STRASSEN_ERR_ALLOC = 4,
+    STRASSEN_ERR_NULL = 5,
+    /* B200 addition: CUDA device missing / kernel launch or copy failed. */
+    STRASSEN_ERR_DEVICE = 6
+} strassen_status;
+
+/* reference strassen.h:25-30 */
+typedef enum strassen_variant {
+    STRASSEN_DGEMM = 0, /* classical gemm; level must be 0 */
+    STRASSEN_ABC = 1,   /* operand sums formed on chip, multi-destination epilogue */
+    STRASSEN_AB = 2,    /* operand sums on chip, products to temporaries, streamed C */
+    STRASSEN_NAIVE = 3  /* operand sums and products materialised */
+} strassen_variant;
+
+/* reference strassen.h:32-35.  Kept for ABI parity: validated exactly like the
+ * reference (all > 0, mc % mr == 0, nc % nr == 0, mr, nr <= 32) and used by
+ * the instrumentation counters and the analytical model; the GPU tiling is
+ * fixed by the kernels. */
+typedef struct strassen_blocking {
+    long mc, nc, kc;
+    long mr, nr;
+} strassen_blocking;
+
+/* reference strassen.h:37-42 */
+typedef struct strassen_model_params {
+    double tau_a;          /* seconds per flop */
+    double tau_b;          /* seconds per 8-byte element from slow memory */
+    double lambda;         /* prefetch efficiency on kernel C traffic, [0.5, 1] */
+    double channel_factor; /* multiplier on tau_b */
+} strassen_model_params;
+
+/* reference strassen.h:44-49 */
+typedef struct strassen_breakdown {
+    double ta_mul, ta_a_add, ta_b_add, ta_c_add;
+    double tm_a_mul, tm_b_mul, tm_c_mul;
+    double tm_a_add, tm_b_add, tm_c_add;
+    double total;
+} strassen_breakdown;
+
+/* reference strassen.h:51-61.  Filled analytically from the operand table and
+ * the ctx blocking so the values equal the reference's instrumented counts. */
+typedef struct strassen_counter_values {
+    int64_t pack_a_calls, pack_b_calls;
+    int64_t pack_a_elems, pack_b_elems;
+    int64_t pack_a_add_flops, pack_b_add_flops;
+    int64_t kernel_calls, kernel_fma_flops;
+    int64_t kernel_c_elems, kernel_update_flops;
+    int64_t a_plus_passes, a_plus_elems, a_plus_flops;
+    int64_t b_plus_passes, b_plus_elems, b_plus_flops;
+    int64_t c_plus_passes, c_plus_elems, c_plus_flops;
+} strassen_counter_values;
+
+/* Opaque context (reference capi.cpp:12-18): blocking, thread count, counters,
+ * plus the B200 state (device workspace, stream, cached plans).  Not safe for
+ * concurrent calls (same as the reference). */
+typedef struct strassen_ctx strassen_ctx;
+
+strassen_status strassen_ctx_create(strassen_ctx** out);            /* strassen.h:67, capi.cpp:65-69 */
+void strassen_ctx_destroy(strassen_ctx* ctx);                      /* strassen.h:68, capi.cpp:71 */
+strassen_status strassen_ctx_set_blocking(strassen_ctx* ctx,        /* strassen.h:70-71, capi.cpp:73-81 */
+                                          const strassen_blocking* bp);
+strassen_status strassen_ctx_get_blocking(const strassen_ctx* ctx,  /* strassen.h:72-73, capi.cpp:83-89 */
+                                          strassen_blocking* out);
+/* threads >= 1 (capi.cpp:91-96); recorded, the GPU path does not use it. */
+strassen_status strassen_ctx_set_threads(strassen_ctx* ctx, int threads);
+strassen_status strassen_ctx_enable_counters(strassen_ctx* ctx, int enabled);   /* capi.cpp:98-102 */
+strassen_status strassen_ctx_reset_counters(strassen_ctx* ctx);                 /* capi.cpp:104-108 */
+strassen_status strassen_ctx_get_counters(const strassen_ctx* ctx,              /* capi.cpp:110-125 */
+                                          strassen_counter_values* out);
+
+/* THE HOT PATH.  reference strassen.h:82-86, capi.cpp:127-145.
+ * C := alpha A B + C, A m x k, B k x n, C m x n.
+ * level: 0 for STRASSEN_DGEMM, 1 or 2 for the Strassen variants.
+ * Validation order: NULL ctx/a/b/c -> STRASSEN_ERR_NULL; DGEMM with level != 0
+ * or a Strassen variant with level not in {1, 2} -> STRASSEN_ERR_PARAM;
+ * m, n or k < 1 -> STRASSEN_ERR_PARAM; invalid ctx blocking -> PARAM;
+ * allocation failure -> STRASSEN_ERR_ALLOC; CUDA failure -> STRASSEN_ERR_DEVICE. */
+strassen_status strassen_gemm(strassen_ctx* ctx, strassen_variant variant, int level, long m,
+                              long n, long k, double alpha, const double* a, long rs_a, long cs_a,
+                              const double* b, long rs_b, long cs_b, double* c, long rs_c,
+                              long cs_c);
+
+/* Triple-loop oracle on the HOST (strassen.h:89-93, matrix.cpp:37-52):
+ * accumulation over p strictly ascending; the rounding reference for tests. */
+strassen_status strassen_reference_gemm(long m, long n, long k, double alpha, const double* a,
+                                        long rs_a, long cs_a, const double* b, long rs_b,
+                                        long cs_b, double* c, long rs_c, long cs_c);
+
+/* ||C_test - C_ref||_F / max(||C_ref||_F, 1) on host buffers
+ * (strassen.h:96-99, matrix.cpp:54-66). */
+strassen_status strassen_rel_error(long rows, long cols, const double* c_test, long rs_t,
+                                   long cs_t, const double* c_ref, long rs_r, long cs_r,
+                                   double* out);
+
+/* Analytical model, same coefficients as the reference (strassen.h:102-108,
+ * model.cpp:48-134; level 2 uses the paper's 154/462/194). */
+strassen_status strassen_model_predict(strassen_variant variant, int level, long m, long n, long k,
+                                       const strassen_blocking* bp,
+                                       const strassen_model_params* mp,
+                                       strassen_breakdown* breakdown_out, double* egf_out);
+
+/* 2mnk / seconds * 1e-9; seconds <= 0 -> STRASSEN_ERR_DOMAIN (model.cpp:113-117). */
+strassen_status strassen_effective_gflops(long m, long n, long k, double seconds, double* out);
+
+/* Ivy Bridge single-core preset (strassen.h:112-114, model.cpp:39-46). */
+void strassen_model_params_ivy_bridge(strassen_model_params* out);
+/* mc=96 nc=4096 kc=256 mr=8 nr=4 (kernel.hpp:11-17). */
+void strassen_blocking_defaults(strassen_blocking* out);
+
+/* out = {mults, a_adds, b_adds, c_updates} for level 1 or 2
+ * (strassen.h:117-119, table.cpp:104-113): (7,5,5,12) and (49,95,95,144). */
+strassen_status strassen_table_counts(int level, long out[4]);
+
+const char* strassen_status_str(strassen_status s);  /* capi.cpp:225-235 */
+
+/* ============================ PART 2: B200 additions ======================= */
+
+/* Device-pointer entry on a caller-provided CUDA stream (cudaStream_t passed
+ * as void*; NULL = the ctx stream).  A, B, C must be device (or managed)
+ * memory.  Asynchronous: returns after enqueueing; C is updated in stream
+ * order.  Same validation and semantics as strassen_gemm. */
+strassen_status strassen_gemm_device(strassen_ctx* ctx, void* stream, strassen_variant variant,
+                                     int level, long m, long n, long k, double alpha,
+                                     const double* a, long rs_a, long cs_a, const double* b,
+                                     long rs_b, long cs_b, double* c, long rs_c, long cs_c);
+
+/* Column-major BLAS-style shim (the north-star dgemm entry): op(A) = A or A^T
+ * per transa ('N'/'n' or 'T'/'t'/'C'/'c'), likewise transb;
+ * C := alpha op(A) op(B) + beta C.  beta != 1 pre-scales C on the device
+ * (exactly 0 clears it, BLAS convention) before the Strassen call.
+ * lda/ldb/ldc >= max(1, rows) else STRASSEN_ERR_PARAM. */
+strassen_status strassen_dgemm(strassen_ctx* ctx, strassen_variant variant, int level, char transa,
+                               char transb, long m, long n, long k, double alpha, const double* a,
+                               long lda, const double* b, long ldb, double beta, double* c,
+                               long ldc);
+
+/* Stream used by strassen_gemm / strassen_dgemm (cudaStream_t as void*). */
+strassen_status strassen_ctx_set_stream(strassen_ctx* ctx, void* stream);
+
+/* Number of CUDA kernels the last compute call on this ctx launched. */
+strassen_status strassen_ctx_last_launches(const strassen_ctx* ctx, long* out);
+
+/* Device memory currently held by the ctx workspace, in bytes. */
+strassen_status strassen_ctx_workspace_bytes(const strassen_ctx* ctx, long* out);
+
+/* Counter values one strassen_gemm(variant, level, m, n, k) call adds under
+ * blocking *bp (the analytic instrumentation; no device needed).  Same
+ * validation as strassen_gemm for variant / level / dimensions / blocking. */
+strassen_status strassen_count_call(strassen_variant variant, int level, long m, long n, long k,
+                                    const strassen_blocking* bp, strassen_counter_values* out);
+
+/* Library build string (architecture and kernel configuration). */
+const char* strassen_build_info(void);
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* strassen_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STRASSEN_B200_H */

@@ -1,0 +1,253 @@
+// Instrumentation counters and the analytical model of the reference, kept for
+// ABI parity (strassen_ctx_get_counters, strassen_model_predict, ...).
+//
+// Counters: the reference increments atomics inside its CPU packing, micro-
+// kernel and streaming loops (counters.hpp:8-49, blocking.cpp:33-37 / 61-65,
+// kernel.cpp:42-47 / 71-75, variants.cpp:67-108).  The GPU path has no such
+// loops, so the same numbers are produced here analytically by walking the
+// reference's loop structure (jc / pc / ic / ir) for the ctx blocking without
+// touching data -- O((n/nc)(k/kc)(m/mr)) integer work, only when enabled.
+//
+// Model: the paper's T = T_a + T_m (model.cpp:8-134) with the reference's
+// coefficient table (including its 154/462/194 level-2 figures).
+#include "accounting.hpp"
+
+#include <algorithm>
+#include <stdexcept>
+
+#include "table.hpp"
+
+namespace sb200 {
+namespace {
+
+long ceil_div(long a, long b) { return (a + b - 1) / b; }
+long clampl(long v, long lo, long hi) { return std::max(lo, std::min(hi, v)); }
+
+struct Ext {
+    long rows, cols;
+    bool empty() const { return rows <= 0 || cols <= 0; }
+};
+
+bool all_empty(const std::vector<Ext>& v) {
+    for (const Ext& e : v)
+        if (!e.empty()) return false;
+    return true;
+}
+
+// gemm_five_loop (blocking.cpp:82-131) counting only.
+void five_loop(long lm, long ln, long lk, const std::vector<Ext>& a, const std::vector<Ext>& b,
+               const std::vector<Ext>& d, const strassen_blocking& bp,
+               strassen_counter_values& c) {
+    if (lm <= 0 || ln <= 0 || lk <= 0) return;
+    if (all_empty(a) || all_empty(b) || all_empty(d)) return;
+    for (long jc = 0; jc < ln; jc += bp.nc) {
+        const long n_c = std::min(bp.nc, ln - jc);
+        for (long pc = 0; pc < lk; pc += bp.kc) {
+            const long k_c = std::min(bp.kc, lk - pc);
+            c.pack_b_calls += 1;
+            for (size_t t = 0; t < b.size(); ++t) {
+                const long depth = clampl(b[t].rows - pc, 0, k_c);
+                const long cols = clampl(b[t].cols - jc, 0, n_c);
+                c.pack_b_elems += cols * depth;
+                if (t > 0) c.pack_b_add_flops += 2 * cols * depth;
+            }
+            for (long ic = 0; ic < lm; ic += bp.mc) {
+                const long m_c = std::min(bp.mc, lm - ic);
+                c.pack_a_calls += 1;
+                for (size_t t = 0; t < a.size(); ++t) {
+                    const long rows = clampl(a[t].rows - ic, 0, m_c);
+                    const long depth = clampl(a[t].cols - pc, 0, k_c);
+                    c.pack_a_elems += rows * depth;
+                    if (t > 0) c.pack_a_add_flops += 2 * rows * depth;
+                }
+                // macro_kernel (kernel.cpp:79-102): tiles in range of any dest
+                const long m_tiles = ceil_div(m_c, bp.mr), n_tiles = ceil_div(n_c, bp.nr);
+                for (long ir = 0; ir < m_tiles; ++ir) {
+                    const long tr = ic + ir * bp.mr;
+                    long cmax = -1;
+                    for (const Ext& e : d)
+                        if (tr < e.rows) cmax = std::max(cmax, e.cols);
+                    if (cmax <= jc) continue;
+                    const long n_in = std::min(n_tiles, ceil_div(cmax - jc, bp.nr));
+                    const long in_rows = std::min(bp.mr, m_c - ir * bp.mr);
+                    const long width = std::min(n_in * bp.nr, n_c);
+                    c.kernel_calls += n_in;
+                    c.kernel_fma_flops += 2 * k_c * std::min(in_rows, bp.mr) * width;
+                    for (const Ext& e : d) {
+                        if (tr >= e.rows) continue;
+                        const long rw = std::min(bp.mr, e.rows - tr);
+                        const long cw = std::max(0L, std::min(e.cols, jc + n_in * bp.nr) - jc);
+                        c.kernel_c_elems += 2 * rw * cw;
+                        c.kernel_update_flops += 2 * rw * cw;
+                    }
+                }
+            }
+        }
+    }
+}
+
+std::vector<Ext> partition(long rows, long cols, int level, long& qr, long& qc) {
+    const long side = 1L << level;
+    qr = ceil_div(rows, side);
+    qc = ceil_div(cols, side);
+    std::vector<Ext> v(static_cast<size_t>(side * side));
+    for (long I = 0; I < side; ++I)
+        for (long J = 0; J < side; ++J)
+            v[I * side + J] = {clampl(rows - I * qr, 0, qr), clampl(cols - J * qc, 0, qc)};
+    return v;
+}
+
+std::vector<Ext> pick(const Terms& t, const std::vector<Ext>& g) {
+    std::vector<Ext> out;
+    for (const auto& x : t) out.push_back(g[x.first]);
+    return out;
+}
+
+// materialize_sum (variants.cpp:53-96) pass accounting.
+void materialize(size_t nterms, long rows, long cols, int64_t& passes, int64_t& elems,
+                 int64_t& flops) {
+    const int64_t rc = static_cast<int64_t>(rows) * cols;
+    if (nterms == 1) {
+        passes += 2;
+        elems += 2 * rc;
+    } else {
+        passes += 3;
+        elems += 3 * rc;
+        flops += 2 * rc;
+    }
+    for (size_t s = 2; s < nterms; ++s) {
+        passes += 3;
+        elems += 3 * rc;
+        flops += 2 * rc;
+    }
+}
+
+}  // namespace
+
+void count_call(strassen_variant variant, int level, long m, long n, long k,
+                const strassen_blocking& bp, strassen_counter_values& c) {
+    if (variant == STRASSEN_DGEMM || level == 0) {
+        five_loop(m, n, k, {{m, k}}, {{k, n}}, {{m, n}}, bp, c);
+        return;
+    }
+    long qm, qk, qk2, qn, qm2, qn2;
+    const std::vector<Ext> ga = partition(m, k, level, qm, qk);
+    const std::vector<Ext> gb = partition(k, n, level, qk2, qn);
+    const std::vector<Ext> gc = partition(m, n, level, qm2, qn2);
+    for (const Product& e : program_for_level(level).products) {
+        const std::vector<Ext> a = pick(e.a, ga), b = pick(e.b, gb), d = pick(e.c, gc);
+        if (all_empty(a) || all_empty(b) || all_empty(d)) continue;
+        if (variant == STRASSEN_ABC) {
+            five_loop(qm, qn, qk, a, b, d, bp, c);
+            continue;
+        }
+        if (variant == STRASSEN_AB) {
+            five_loop(qm, qn, qk, a, b, {{qm, qn}}, bp, c);
+        } else {
+            materialize(e.a.size(), qm, qk, c.a_plus_passes, c.a_plus_elems, c.a_plus_flops);
+            materialize(e.b.size(), qk, qn, c.b_plus_passes, c.b_plus_elems, c.b_plus_flops);
+            five_loop(qm, qn, qk, {{qm, qk}}, {{qk, qn}}, {{qm, qn}}, bp, c);
+        }
+        for (const Ext& x : d) {
+            if (x.empty()) continue;
+            c.c_plus_passes += 3;
+            c.c_plus_elems += 3 * static_cast<int64_t>(qm) * qn;
+            c.c_plus_flops += 2 * static_cast<int64_t>(qm) * qn;
+        }
+    }
+}
+
+void add_counters(strassen_counter_values& acc, const strassen_counter_values& d) {
+    int64_t* a = &acc.pack_a_calls;
+    const int64_t* b = &d.pack_a_calls;
+    for (int i = 0; i < 19; ++i) a[i] += b[i];
+}
+
+// ------------------------------------------------------------------- model --
+void validate_blocking(const strassen_blocking& p) {
+    if (p.mc <= 0 || p.nc <= 0 || p.kc <= 0 || p.mr <= 0 || p.nr <= 0)
+        throw std::invalid_argument("blocking: all parameters must be > 0");
+    if (p.mc % p.mr != 0 || p.nc % p.nr != 0)
+        throw std::invalid_argument("blocking: mc % mr and nc % nr must be 0");
+    if (p.mr > 32 || p.nr > 32) throw std::invalid_argument("blocking: register tile too large");
+}
+
+static void validate_model(const strassen_model_params& p) {
+    if (p.tau_a <= 0.0 || p.tau_b <= 0.0)
+        throw std::invalid_argument("model: tau_a and tau_b must be > 0");
+    if (p.lambda < 0.5 || p.lambda > 1.0)
+        throw std::invalid_argument("model: lambda must be in [0.5, 1]");
+}
+
+double effective_gflops(long m, long n, long k, double seconds) {
+    if (seconds <= 0.0) throw std::domain_error("effective_gflops: time must be > 0");
+    return 2.0 * m * n * k / seconds * 1e-9;
+}
+
+namespace {
+struct Coef {
+    long a_mul, b_mul, c_mul, a_add, b_add, c_add;
+};
+Coef coefficients(strassen_variant v, int level) {
+    if (level == 0 || v == STRASSEN_DGEMM) return {1, 1, 1, 0, 0, 0};
+    if (level == 1) {
+        if (v == STRASSEN_ABC) return {12, 12, 12, 0, 0, 0};
+        if (v == STRASSEN_AB) return {12, 12, 7, 0, 0, 36};
+        if (v == STRASSEN_NAIVE) return {7, 7, 7, 19, 19, 36};
+    }
+    if (level == 2) {  // the paper's figures (model.cpp:59-66)
+        if (v == STRASSEN_ABC) return {194, 194, 154, 0, 0, 0};
+        if (v == STRASSEN_AB) return {194, 194, 49, 0, 0, 462};
+        if (v == STRASSEN_NAIVE) return {49, 49, 49, 293, 293, 462};
+    }
+    throw std::invalid_argument("model: unsupported variant configuration");
+}
+void op_counts(int level, long& mul, long& a, long& b, long& c) {
+    switch (level) {
+        case 0: mul = 1, a = 0, b = 0, c = 0; return;
+        case 1: mul = 7, a = 5, b = 5, c = 12; return;
+        case 2: mul = 49, a = 95, b = 95, c = 154; return;  // model.cpp:31
+        default: throw std::invalid_argument("model: level must be 0, 1 or 2");
+    }
+}
+}  // namespace
+
+void model_predict(strassen_variant v, int level, long m, long n, long k,
+                   const strassen_blocking& bp, const strassen_model_params& mp,
+                   strassen_breakdown& out, double& egf) {
+    if (m < 1 || n < 1 || k < 1) throw std::invalid_argument("model: dimensions must be >= 1");
+    validate_model(mp);
+    strassen_breakdown t{};
+    // arithmetic (model.cpp:70-87)
+    if (level == 0 || v == STRASSEN_DGEMM) {
+        t.ta_mul = 2.0 * m * n * k * mp.tau_a;
+    } else {
+        long cm, ca, cb, cc;
+        op_counts(level, cm, ca, cb, cc);
+        const long s = 1L << level;
+        const long qm = ceil_div(m, s), qn = ceil_div(n, s), qk = ceil_div(k, s);
+        t.ta_mul = cm * 2.0 * qm * qn * qk * mp.tau_a;
+        t.ta_a_add = ca * 2.0 * qm * qk * mp.tau_a;
+        t.ta_b_add = cb * 2.0 * qk * qn * mp.tau_a;
+        t.ta_c_add = cc * 2.0 * qm * qn * mp.tau_a;
+    }
+    // memory (model.cpp:89-111)
+    validate_blocking(bp);
+    const Coef cs = coefficients(v, level);
+    const int lvl = (v == STRASSEN_DGEMM) ? 0 : level;
+    const long s = 1L << lvl;
+    const long qm = ceil_div(m, s), qn = ceil_div(n, s), qk = ceil_div(k, s);
+    const double tb = mp.tau_b * mp.channel_factor;
+    t.tm_a_mul = cs.a_mul * static_cast<double>(qm) * qk * ceil_div(qn, bp.nc) * tb;
+    t.tm_b_mul = cs.b_mul * static_cast<double>(qn) * qk * tb;
+    t.tm_c_mul = cs.c_mul * mp.lambda * 2.0 * qm * qn * ceil_div(qk, bp.kc) * tb;
+    t.tm_a_add = cs.a_add * static_cast<double>(qm) * qk * tb;
+    t.tm_b_add = cs.b_add * static_cast<double>(qn) * qk * tb;
+    t.tm_c_add = cs.c_add * static_cast<double>(qm) * qn * tb;
+    t.total = (t.ta_mul + t.ta_a_add + t.ta_b_add + t.ta_c_add) +
+              (t.tm_a_mul + t.tm_b_mul + t.tm_c_mul + t.tm_a_add + t.tm_b_add + t.tm_c_add);
+    out = t;
+    egf = effective_gflops(m, n, k, t.total);
+}
+
+}  // namespace sb200

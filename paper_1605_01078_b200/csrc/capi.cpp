@@ -1,0 +1,377 @@
+// The C ABI (include/strassen.h).  Mirrors the reference's capi.cpp:1-237:
+// same validation order and status mapping (guarded(): invalid_argument ->
+// PARAM, or DIMENSION when the message says "mismatch"; domain_error ->
+// DOMAIN; bad_alloc -> ALLOC), plus STRASSEN_ERR_DEVICE for CUDA failures.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+#include <string_view>
+#include <vector>
+
+#include "accounting.hpp"
+#include "engine.hpp"
+#include "kernels.hpp"
+#include "strassen.h"
+#include "table.hpp"
+
+struct strassen_ctx {
+    strassen_blocking blocking{96, 4096, 256, 8, 4};  // kernel.hpp:11-17
+    int threads = 1;
+    bool counters_enabled = false;
+    strassen_counter_values counters{};
+    sb200::Engine engine;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename F>
+strassen_status guarded(F&& f) {
+    try {
+        f();
+        return STRASSEN_OK;
+    } catch (const sb200::Error& e) {
+        g_last_error = e.what();
+        return e.status;
+    } catch (const std::invalid_argument& e) {
+        g_last_error = e.what();
+        return std::string_view(e.what()).find("mismatch") != std::string_view::npos
+                   ? STRASSEN_ERR_DIMENSION
+                   : STRASSEN_ERR_PARAM;
+    } catch (const std::domain_error& e) {
+        g_last_error = e.what();
+        return STRASSEN_ERR_DOMAIN;
+    } catch (const std::bad_alloc& e) {
+        g_last_error = e.what();
+        return STRASSEN_ERR_ALLOC;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return STRASSEN_ERR_PARAM;
+    }
+}
+
+strassen_status check_variant_level(strassen_variant variant, int level) {
+    if (variant == STRASSEN_DGEMM && level != 0) return STRASSEN_ERR_PARAM;
+    if (variant != STRASSEN_DGEMM && (level < 1 || level > 2)) return STRASSEN_ERR_PARAM;
+    return STRASSEN_OK;
+}
+
+void validate_call(strassen_variant variant, long m, long n, long k, const strassen_blocking& bp) {
+    if (variant != STRASSEN_DGEMM && variant != STRASSEN_ABC && variant != STRASSEN_AB &&
+        variant != STRASSEN_NAIVE)
+        throw std::invalid_argument("unknown variant");
+    if (m < 1 || n < 1 || k < 1) throw std::invalid_argument("gemm: dimensions must be >= 1");
+    sb200::validate_blocking(bp);
+    if (m > (1L << 31) - 1 || n > (1L << 31) - 1 || k > (1L << 31) - 1)
+        throw std::invalid_argument("gemm: dimensions must be < 2^31");
+}
+
+// Element span of a strided view: [lo, hi] offsets from the base pointer.
+void span_of(long rows, long cols, long rs, long cs, long& lo, long& hi) {
+    lo = hi = 0;
+    const long a = (rows - 1) * rs, b = (cols - 1) * cs;
+    lo += std::min(0L, a) + std::min(0L, b);
+    hi += std::max(0L, a) + std::max(0L, b);
+}
+
+void cuda_ck(cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation) throw sb200::Error(STRASSEN_ERR_ALLOC, what);
+    if (e != cudaSuccess)
+        throw sb200::Error(STRASSEN_ERR_DEVICE, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Host operand -> device view (copy of the view's span); device -> as is.
+sb200::DView stage_in(sb200::Engine& e, cudaStream_t s, const double* p, long rows, long cols,
+                      long rs, long cs, sb200::DeviceBuffer& buf, bool copy, bool& staged) {
+    sb200::DView v;
+    v.rows = rows;
+    v.cols = cols;
+    v.rs = rs;
+    v.cs = cs;
+    staged = !sb200::is_device_pointer(p);
+    if (!staged) {
+        v.p = const_cast<double*>(p);
+        return v;
+    }
+    long lo, hi;
+    span_of(rows, cols, rs, cs, lo, hi);
+    const size_t count = static_cast<size_t>(hi - lo + 1);
+    double* d = e.ensure(buf, count * 8);
+    if (copy)
+        cuda_ck(cudaMemcpyAsync(d, p + lo, count * 8, cudaMemcpyHostToDevice, s), "H2D operand");
+    v.p = d - lo;
+    return v;
+}
+
+strassen_status gemm_impl(strassen_ctx* ctx, cudaStream_t user_stream, bool device_only,
+                          strassen_variant variant, int level, long m, long n, long k,
+                          double alpha, const double* a, long rs_a, long cs_a, const double* b,
+                          long rs_b, long cs_b, double* c, long rs_c, long cs_c, bool has_beta,
+                          double beta) {
+    if (!ctx || !a || !b || !c) return STRASSEN_ERR_NULL;
+    if (strassen_status st = check_variant_level(variant, level)) return st;
+    return guarded([&] {
+        validate_call(variant, m, n, k, ctx->blocking);
+        sb200::Engine& e = ctx->engine;
+        e.init();
+        cudaStream_t s = user_stream ? user_stream : e.stream();
+        long launches = 0;
+        bool sa = false, sb = false, sc = false;
+        const sb200::DView A = stage_in(e, s, a, m, k, rs_a, cs_a, e.stage_a, true, sa);
+        const sb200::DView B = stage_in(e, s, b, k, n, rs_b, cs_b, e.stage_b, true, sb);
+        const sb200::DView C = stage_in(e, s, c, m, n, rs_c, cs_c, e.stage_c, true, sc);
+        if (device_only && (sa || sb || sc))
+            throw std::invalid_argument("strassen_gemm_device: operands must be device memory");
+        if (has_beta && beta != 1.0) launches += sb200::scale_device(e, s, C, beta);
+        launches += sb200::run_device(e, s, variant, level, alpha, A, B, C);
+        if (sc) {
+            long lo, hi;
+            span_of(m, n, rs_c, cs_c, lo, hi);
+            cuda_ck(cudaMemcpyAsync(c + lo, C.p + lo, static_cast<size_t>(hi - lo + 1) * 8,
+                                    cudaMemcpyDeviceToHost, s),
+                    "D2H result");
+        }
+        if (!device_only) cuda_ck(cudaStreamSynchronize(s), "kernel execution");
+        else cuda_ck(cudaGetLastError(), "kernel launch");
+        e.last_launches = launches;
+        if (ctx->counters_enabled) {
+            strassen_counter_values d{};
+            sb200::count_call(variant, level, m, n, k, ctx->blocking, d);
+            sb200::add_counters(ctx->counters, d);
+        }
+    });
+}
+
+}  // namespace
+
+extern "C" {
+
+strassen_status strassen_ctx_create(strassen_ctx** out) {
+    if (!out) return STRASSEN_ERR_NULL;
+    *out = new (std::nothrow) strassen_ctx();
+    return *out ? STRASSEN_OK : STRASSEN_ERR_ALLOC;
+}
+
+void strassen_ctx_destroy(strassen_ctx* ctx) { delete ctx; }
+
+strassen_status strassen_ctx_set_blocking(strassen_ctx* ctx, const strassen_blocking* bp) {
+    if (!ctx || !bp) return STRASSEN_ERR_NULL;
+    return guarded([&] {
+        sb200::validate_blocking(*bp);
+        ctx->blocking = *bp;
+    });
+}
+
+strassen_status strassen_ctx_get_blocking(const strassen_ctx* ctx, strassen_blocking* out) {
+    if (!ctx || !out) return STRASSEN_ERR_NULL;
+    *out = ctx->blocking;
+    return STRASSEN_OK;
+}
+
+strassen_status strassen_ctx_set_threads(strassen_ctx* ctx, int threads) {
+    if (!ctx) return STRASSEN_ERR_NULL;
+    if (threads < 1) return STRASSEN_ERR_PARAM;
+    ctx->threads = threads;
+    return STRASSEN_OK;
+}
+
+strassen_status strassen_ctx_enable_counters(strassen_ctx* ctx, int enabled) {
+    if (!ctx) return STRASSEN_ERR_NULL;
+    ctx->counters_enabled = enabled != 0;
+    return STRASSEN_OK;
+}
+
+strassen_status strassen_ctx_reset_counters(strassen_ctx* ctx) {
+    if (!ctx) return STRASSEN_ERR_NULL;
+    ctx->counters = strassen_counter_values{};
+    return STRASSEN_OK;
+}
+
+strassen_status strassen_ctx_get_counters(const strassen_ctx* ctx, strassen_counter_values* out) {
+    if (!ctx || !out) return STRASSEN_ERR_NULL;
+    *out = ctx->counters;
+    return STRASSEN_OK;
+}
+
+strassen_status strassen_gemm(strassen_ctx* ctx, strassen_variant variant, int level, long m,
+                              long n, long k, double alpha, const double* a, long rs_a, long cs_a,
+                              const double* b, long rs_b, long cs_b, double* c, long rs_c,
+                              long cs_c) {
+    return gemm_impl(ctx, nullptr, false, variant, level, m, n, k, alpha, a, rs_a, cs_a, b, rs_b,
+                     cs_b, c, rs_c, cs_c, false, 1.0);
+}
+
+strassen_status strassen_gemm_device(strassen_ctx* ctx, void* stream, strassen_variant variant,
+                                     int level, long m, long n, long k, double alpha,
+                                     const double* a, long rs_a, long cs_a, const double* b,
+                                     long rs_b, long cs_b, double* c, long rs_c, long cs_c) {
+    return gemm_impl(ctx, static_cast<cudaStream_t>(stream), true, variant, level, m, n, k, alpha,
+                     a, rs_a, cs_a, b, rs_b, cs_b, c, rs_c, cs_c, false, 1.0);
+}
+
+strassen_status strassen_dgemm(strassen_ctx* ctx, strassen_variant variant, int level, char transa,
+                               char transb, long m, long n, long k, double alpha, const double* a,
+                               long lda, const double* b, long ldb, double beta, double* c,
+                               long ldc) {
+    if (!ctx || !a || !b || !c) return STRASSEN_ERR_NULL;
+    auto trans = [](char t, bool& out) {
+        if (t == 'N' || t == 'n') return out = false, true;
+        if (t == 'T' || t == 't' || t == 'C' || t == 'c') return out = true, true;
+        return false;
+    };
+    bool ta = false, tb = false;
+    if (!trans(transa, ta) || !trans(transb, tb)) return STRASSEN_ERR_PARAM;
+    const long arows = ta ? k : m, brows = tb ? n : k;
+    if (lda < std::max(1L, arows) || ldb < std::max(1L, brows) || ldc < std::max(1L, m))
+        return STRASSEN_ERR_PARAM;
+    // column-major storage: element (r, c) of the stored matrix at p[r + c*ld];
+    // a transpose is the stride swap (reference strassen.h:1-6).
+    const long rs_a = ta ? lda : 1, cs_a = ta ? 1 : lda;
+    const long rs_b = tb ? ldb : 1, cs_b = tb ? 1 : ldb;
+    return gemm_impl(ctx, nullptr, false, variant, level, m, n, k, alpha, a, rs_a, cs_a, b, rs_b,
+                     cs_b, c, 1, ldc, true, beta);
+}
+
+strassen_status strassen_ctx_set_stream(strassen_ctx* ctx, void* stream) {
+    if (!ctx) return STRASSEN_ERR_NULL;
+    ctx->engine.user_stream = static_cast<cudaStream_t>(stream);
+    ctx->engine.has_user_stream = stream != nullptr;
+    return STRASSEN_OK;
+}
+
+strassen_status strassen_ctx_last_launches(const strassen_ctx* ctx, long* out) {
+    if (!ctx || !out) return STRASSEN_ERR_NULL;
+    *out = ctx->engine.last_launches;
+    return STRASSEN_OK;
+}
+
+strassen_status strassen_ctx_workspace_bytes(const strassen_ctx* ctx, long* out) {
+    if (!ctx || !out) return STRASSEN_ERR_NULL;
+    *out = static_cast<long>(ctx->engine.workspace_bytes());
+    return STRASSEN_OK;
+}
+
+strassen_status strassen_reference_gemm(long m, long n, long k, double alpha, const double* a,
+                                        long rs_a, long cs_a, const double* b, long rs_b,
+                                        long cs_b, double* c, long rs_c, long cs_c) {
+    if (!a || !b || !c) return STRASSEN_ERR_NULL;
+    return guarded([&] {
+        if (m < 1 || n < 1 || k < 1) throw std::invalid_argument("gemm: dimensions must be >= 1");
+        // matrix.cpp:37-52: per row, accumulate over p ascending into a row buffer
+        std::vector<double> acc(static_cast<size_t>(n));
+        for (long i = 0; i < m; ++i) {
+            std::fill(acc.begin(), acc.end(), 0.0);
+            for (long p = 0; p < k; ++p) {
+                const double av = a[i * rs_a + p * cs_a];
+                for (long j = 0; j < n; ++j) acc[j] += av * b[p * rs_b + j * cs_b];
+            }
+            for (long j = 0; j < n; ++j) c[i * rs_c + j * cs_c] += alpha * acc[j];
+        }
+    });
+}
+
+strassen_status strassen_rel_error(long rows, long cols, const double* c_test, long rs_t,
+                                   long cs_t, const double* c_ref, long rs_r, long cs_r,
+                                   double* out) {
+    if (!c_test || !c_ref || !out) return STRASSEN_ERR_NULL;
+    return guarded([&] {
+        double diff2 = 0.0, ref2 = 0.0;
+        for (long i = 0; i < rows; ++i)
+            for (long j = 0; j < cols; ++j) {
+                const double r = c_ref[i * rs_r + j * cs_r];
+                const double d = c_test[i * rs_t + j * cs_t] - r;
+                diff2 += d * d;
+                ref2 += r * r;
+            }
+        *out = std::sqrt(diff2) / std::max(std::sqrt(ref2), 1.0);
+    });
+}
+
+strassen_status strassen_model_predict(strassen_variant variant, int level, long m, long n, long k,
+                                       const strassen_blocking* bp,
+                                       const strassen_model_params* mp,
+                                       strassen_breakdown* breakdown_out, double* egf_out) {
+    if (!bp || !mp) return STRASSEN_ERR_NULL;
+    if (strassen_status st = check_variant_level(variant, level)) return st;
+    return guarded([&] {
+        if (variant != STRASSEN_DGEMM && variant != STRASSEN_ABC && variant != STRASSEN_AB &&
+            variant != STRASSEN_NAIVE)
+            throw std::invalid_argument("unknown variant");
+        strassen_breakdown bd;
+        double egf = 0.0;
+        sb200::model_predict(variant, level, m, n, k, *bp, *mp, bd, egf);
+        if (breakdown_out) *breakdown_out = bd;
+        if (egf_out) *egf_out = egf;
+    });
+}
+
+strassen_status strassen_effective_gflops(long m, long n, long k, double seconds, double* out) {
+    if (!out) return STRASSEN_ERR_NULL;
+    return guarded([&] { *out = sb200::effective_gflops(m, n, k, seconds); });
+}
+
+void strassen_model_params_ivy_bridge(strassen_model_params* out) {
+    if (!out) return;
+    *out = {1.0 / 28.32e9, 8.0 / 59.7 * 1e-9, 0.7, 4.0};  // model.cpp:39-46
+}
+
+void strassen_blocking_defaults(strassen_blocking* out) {
+    if (!out) return;
+    *out = {96, 4096, 256, 8, 4};
+}
+
+strassen_status strassen_table_counts(int level, long out[4]) {
+    if (!out) return STRASSEN_ERR_NULL;
+    return guarded([&] {
+        const sb200::OpCounts c = sb200::count_ops(sb200::program_for_level(level));
+        out[0] = c.mults;
+        out[1] = c.a_adds;
+        out[2] = c.b_adds;
+        out[3] = c.c_updates;
+    });
+}
+
+const char* strassen_status_str(strassen_status s) {
+    switch (s) {
+        case STRASSEN_OK: return "ok";
+        case STRASSEN_ERR_DIMENSION: return "dimension mismatch";
+        case STRASSEN_ERR_PARAM: return "invalid parameter";
+        case STRASSEN_ERR_DOMAIN: return "domain error";
+        case STRASSEN_ERR_ALLOC: return "allocation failure";
+        case STRASSEN_ERR_NULL: return "null argument";
+        case STRASSEN_ERR_DEVICE: return "CUDA device error";
+    }
+    return "unknown";
+}
+
+strassen_status strassen_count_call(strassen_variant variant, int level, long m, long n, long k,
+                                    const strassen_blocking* bp, strassen_counter_values* out) {
+    if (!bp || !out) return STRASSEN_ERR_NULL;
+    if (strassen_status st = check_variant_level(variant, level)) return st;
+    return guarded([&] {
+        validate_call(variant, m, n, k, *bp);
+        strassen_counter_values d{};
+        sb200::count_call(variant, level, m, n, k, *bp, d);
+        *out = d;
+    });
+}
+
+const char* strassen_build_info(void) {
+    static const std::string info = [] {
+        return std::string("libstrassen_b200 sm_100a; mm_kernel tile ") + std::to_string(sb200::kBM) +
+               "x" + std::to_string(sb200::kBN) + "x" + std::to_string(sb200::kBK) +
+               " DMMA.8 (mma.sync m8n8k4 f64); TMA ring " + std::to_string(sb200::kRawSlots) +
+               " x 16 KB, " + std::to_string(sb200::kStages) + " summed stages; 1 TMA + " +
+               std::to_string(sb200::kSummerWarps) + " sum + " +
+               std::to_string(sb200::kConsumerWarps) + " DMMA warps";
+    }();
+    return info.c_str();
+}
+
+const char* strassen_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"

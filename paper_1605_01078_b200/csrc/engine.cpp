@@ -1,0 +1,387 @@
+// Host engine (see engine.hpp).
+#include "engine.hpp"
+
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "kernels.hpp"
+#include "table.hpp"
+
+namespace sb200 {
+
+namespace {
+
+void ck(cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation) throw Error(STRASSEN_ERR_ALLOC, what);
+    if (e != cudaSuccess)
+        throw Error(STRASSEN_ERR_DEVICE, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda).
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    if (!fn) throw Error(STRASSEN_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+// Column-major (rows x cols, leading dimension ld) fp64 tensor map.
+void encode_map(CUtensorMap* map, const double* base, long rows, long cols, long long ld,
+                uint32_t box0, uint32_t box1, bool swizzle128) {
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(cols)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 8};
+    cuuint32_t box[2] = {box0, box1};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                             const_cast<double*>(base), dims, strides, box, estr,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(STRASSEN_ERR_DEVICE, "cuTensorMapEncodeTiled failed");
+}
+
+long ceil_div(long a, long b) { return (a + b - 1) / b; }
+long clip(long v, long lo, long hi) { return std::max(lo, std::min(hi, v)); }
+
+// An operand prepared for TMA: column-major, 16-byte aligned quadrant origins.
+struct TmaOperand {
+    const double* base = nullptr;
+    long long ld = 0;
+    long q_rows_al = 0;  // row offset between quadrant rows (>= logical q rows)
+    long rows = 0, cols = 0;
+    long q_rows = 0, q_cols = 0;  // logical quadrant extents
+};
+
+bool tma_ready(const DView& v, long q_rows, int side) {
+    const uintptr_t addr = reinterpret_cast<uintptr_t>(v.p);
+    if (v.rs != 1) return false;
+    if (v.cs < v.rows || (v.cs % 2) != 0) return false;
+    if (addr % 16 != 0) return false;
+    if (side > 1 && (q_rows % 2) != 0) return false;
+    if (v.cs * 8 >= (1LL << 40)) return false;
+    return true;
+}
+
+TmaOperand prepare(Engine& e, cudaStream_t s, const DView& v, long q_rows, long q_cols, int side,
+                   DeviceBuffer& scratch, long& launches) {
+    TmaOperand t;
+    t.rows = v.rows;
+    t.cols = v.cols;
+    t.q_rows = q_rows;
+    t.q_cols = q_cols;
+    if (tma_ready(v, q_rows, side)) {
+        t.base = v.p;
+        t.ld = v.cs;
+        t.q_rows_al = q_rows;
+        return t;
+    }
+    // Normalise into column-major with each quadrant row block at a 32-byte
+    // aligned offset: O(rows*cols) copy, negligible against the O(mnk) work.
+    const long q_al = (side > 1) ? ((q_rows + 3) / 4) * 4 : q_rows;
+    long long ld = static_cast<long long>(side > 1 ? q_al * side : v.rows);
+    ld = std::max<long long>(((ld + 3) / 4) * 4, 4);
+    double* dst = e.ensure(scratch, static_cast<size_t>(ld) * v.cols * 8);
+    ck(launch_repack(v.p, v.rs, v.cs, v.rows, v.cols, dst, ld, side > 1 ? q_rows : v.rows + 1,
+                     side > 1 ? q_al : v.rows + 1, s),
+       "repack");
+    ++launches;
+    t.base = dst;
+    t.ld = ld;
+    t.q_rows_al = q_al;
+    return t;
+}
+
+// Quadrant (I, J) of a prepared operand: origin and clipped extent.
+const double* quad_origin(const TmaOperand& t, long I, long J) {
+    return t.base + I * t.q_rows_al + J * t.q_cols * t.ld;
+}
+long quad_rows(const TmaOperand& t, long I) { return clip(t.rows - I * t.q_rows, 0, t.q_rows); }
+long quad_cols(const TmaOperand& t, long J) { return clip(t.cols - J * t.q_cols, 0, t.q_cols); }
+
+struct QuadView {
+    double* p;
+    long rows, cols;
+};
+
+QuadView c_quad(const DView& C, long qm, long qn, long I, long J) {
+    QuadView q;
+    q.rows = clip(C.rows - I * qm, 0, qm);
+    q.cols = clip(C.cols - J * qn, 0, qn);
+    q.p = (q.rows > 0 && q.cols > 0) ? C.p + I * qm * C.rs + J * qn * C.cs : C.p;
+    return q;
+}
+
+const Program& program(int level) {
+    static const Program p0 = identity_program();
+    return level == 0 ? p0 : program_for_level(level);
+}
+
+// Filter one product's terms to the non-empty quadrants (reference
+// all_empty / clamped packing, variants.cpp:26-47, blocking.cpp:21-22: an
+// empty view contributes exactly nothing).
+Terms live_terms(const Terms& t, const std::vector<bool>& nonempty) {
+    Terms out;
+    for (const auto& x : t)
+        if (nonempty[x.first]) out.push_back(x);
+    return out;
+}
+
+void fill_desc(ProductDesc& d, const Terms& a, const Terms& b, const Terms& c) {
+    std::memset(&d, 0, sizeof(d));
+    d.na = static_cast<int8_t>(a.size());
+    d.nb = static_cast<int8_t>(b.size());
+    d.nc = static_cast<int8_t>(c.size());
+    for (size_t u = 0; u < a.size(); ++u) {
+        d.aq[u] = static_cast<int8_t>(a[u].first);
+        d.as[u] = static_cast<int8_t>(a[u].second);
+    }
+    for (size_t u = 0; u < b.size(); ++u) {
+        d.bq[u] = static_cast<int8_t>(b[u].first);
+        d.bs[u] = static_cast<int8_t>(b[u].second);
+    }
+    for (size_t u = 0; u < c.size(); ++u) {
+        d.cq[u] = static_cast<int8_t>(c[u].first);
+        d.cs[u] = static_cast<int8_t>(c[u].second);
+    }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ Engine --
+Engine::~Engine() {
+    if (!initialised) return;
+    for (DeviceBuffer* b : {&stage_a, &stage_b, &stage_c, &pack_a, &pack_b, &mbuf, &tabuf, &tbbuf})
+        if (b->ptr) cudaFree(b->ptr);
+    if (own_stream) cudaStreamDestroy(own_stream);
+}
+
+void Engine::init() {
+    if (initialised) return;
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+        throw Error(STRASSEN_ERR_DEVICE, "no CUDA device");
+    ck(cudaGetDevice(&device), "cudaGetDevice");
+    ck(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    initialised = true;
+}
+
+cudaStream_t Engine::stream() { return has_user_stream ? user_stream : own_stream; }
+
+double* Engine::ensure(DeviceBuffer& b, size_t bytes) {
+    if (bytes == 0) bytes = 8;
+    if (b.bytes < bytes) {
+        if (b.ptr) {
+            ck(cudaStreamSynchronize(stream()), "sync before realloc");
+            cudaFree(b.ptr);
+            b.ptr = nullptr;
+            b.bytes = 0;
+        }
+        ck(cudaMalloc(&b.ptr, bytes), "cudaMalloc workspace");
+        b.bytes = bytes;
+    }
+    return static_cast<double*>(b.ptr);
+}
+
+size_t Engine::workspace_bytes() const {
+    size_t t = 0;
+    for (const DeviceBuffer* b : {&stage_a, &stage_b, &stage_c, &pack_a, &pack_b, &mbuf, &tabuf, &tbbuf})
+        t += b->bytes;
+    return t;
+}
+
+bool is_device_pointer(const void* p) {
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+// ------------------------------------------------------------- run_device --
+long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, double alpha,
+                const DView& A, const DView& B, const DView& C) {
+    const int L = (variant == STRASSEN_DGEMM) ? 0 : level;
+    const int side = 1 << L;
+    const long m = A.rows, k = A.cols, n = B.cols;
+    const long qm = ceil_div(m, side), qk = ceil_div(k, side), qn = ceil_div(n, side);
+    long launches = 0;
+
+    const TmaOperand ta = prepare(e, s, A, qm, qk, side, e.pack_a, launches);
+    const TmaOperand tb = prepare(e, s, B, qk, qn, side, e.pack_b, launches);
+
+    const int nq = side * side;
+    std::vector<bool> a_live(nq), b_live(nq), c_live(nq);
+    std::vector<QuadView> cq(nq);
+    for (int I = 0; I < side; ++I)
+        for (int J = 0; J < side; ++J) {
+            a_live[I * side + J] = quad_rows(ta, I) > 0 && quad_cols(ta, J) > 0;
+            b_live[I * side + J] = quad_rows(tb, I) > 0 && quad_cols(tb, J) > 0;
+            cq[I * side + J] = c_quad(C, qm, qn, I, J);
+            c_live[I * side + J] = cq[I * side + J].rows > 0 && cq[I * side + J].cols > 0;
+        }
+
+    MMParams P;
+    std::memset(&P, 0, sizeof(P));
+    for (int I = 0; I < side; ++I)
+        for (int J = 0; J < side; ++J) {
+            const int qi = I * side + J;
+            if (a_live[qi])
+                encode_map(&P.tmA[qi], quad_origin(ta, I, J), quad_rows(ta, I), quad_cols(ta, J),
+                           ta.ld, kBM, kBK, false);
+            if (b_live[qi])
+                encode_map(&P.tmB[qi], quad_origin(tb, I, J), quad_rows(tb, I), quad_cols(tb, J),
+                           tb.ld, kBK, kBN, true);
+            P.cptr[qi] = cq[qi].p;
+            P.crows[qi] = static_cast<int>(cq[qi].rows);
+            P.ccols[qi] = static_cast<int>(cq[qi].cols);
+        }
+    P.rs_c = C.rs;
+    P.cs_c = C.cs;
+    P.alpha = alpha;
+    P.qm = static_cast<int>(qm);
+    P.qn = static_cast<int>(qn);
+    P.qk = static_cast<int>(qk);
+    P.tiles_m = static_cast<int>(ceil_div(qm, kBM));
+    P.tiles_n = static_cast<int>(ceil_div(qn, kBN));
+    P.ktiles = static_cast<int>(ceil_div(qk, kBK));
+    P.group_m = 8;
+
+    // Live products in table order (variants.cpp:130-133 skip rule).
+    struct Live {
+        Terms a, b, c;
+    };
+    std::vector<Live> live;
+    for (const Product& pr : program(L).products) {
+        Live l{live_terms(pr.a, a_live), live_terms(pr.b, b_live), live_terms(pr.c, c_live)};
+        if (l.a.empty() || l.b.empty() || l.c.empty()) continue;
+        live.push_back(std::move(l));
+    }
+    if (live.empty()) return launches;
+
+    if (variant == STRASSEN_DGEMM || variant == STRASSEN_ABC) {
+        P.mode = kEpiRMW;
+        P.nprod = static_cast<int>(live.size());
+        for (size_t p = 0; p < live.size(); ++p) fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);
+        ck(launch_mm(P, s), "mm_kernel");
+        return launches + 1;
+    }
+
+    // AB / Naive: products to quadrant-sized temporaries, then streamed into C.
+    const long long ldm = qm;
+    const long long mstride = ldm * qn;
+    StreamParams S;
+    std::memset(&S, 0, sizeof(S));
+    S.rs_c = C.rs;
+    S.cs_c = C.cs;
+    S.alpha = alpha;
+    S.ldm = ldm;
+    S.mstride = mstride;
+    S.nquad = nq;
+    S.qm = static_cast<int>(qm);
+    S.qn = static_cast<int>(qn);
+    for (int qi = 0; qi < nq; ++qi) {
+        S.cptr[qi] = cq[qi].p;
+        S.crows[qi] = static_cast<int>(cq[qi].rows);
+        S.ccols[qi] = static_cast<int>(cq[qi].cols);
+    }
+    P.mode = kEpiStore;
+    P.ldm = ldm;
+    P.mstride = mstride;
+
+    if (variant == STRASSEN_AB) {
+        // One launch computes every product into its own temporary (all 7^L
+        // batched); one launch streams them into C in table order.
+        double* M = e.ensure(e.mbuf, static_cast<size_t>(mstride) * live.size() * 8);
+        P.mbase = M;
+        P.nprod = static_cast<int>(live.size());
+        for (size_t p = 0; p < live.size(); ++p) {
+            fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);
+            for (const auto& [q, g] : live[p].c) {
+                S.src_prod[q][S.nsrc[q]] = static_cast<int8_t>(p);
+                S.src_coeff[q][S.nsrc[q]] = static_cast<int8_t>(g);
+                ++S.nsrc[q];
+            }
+        }
+        ck(launch_mm(P, s), "mm_kernel (AB)");
+        S.mbase = M;
+        ck(launch_stream_update(S, s), "stream_update");
+        return launches + 2;
+    }
+
+    // Naive: per product, materialise T_A (qm x qk) and T_B (qk x qn) with
+    // zero padding, multiply them as single terms, stream M into C.
+    const long long lda_t = ((qm + 3) / 4) * 4, ldb_t = ((qk + 3) / 4) * 4;
+    double* TA = e.ensure(e.tabuf, static_cast<size_t>(lda_t) * qk * 8);
+    double* TB = e.ensure(e.tbbuf, static_cast<size_t>(ldb_t) * qn * 8);
+    double* M = e.ensure(e.mbuf, static_cast<size_t>(mstride) * 8);
+    MMParams Q = P;
+    encode_map(&Q.tmA[0], TA, qm, qk, lda_t, kBM, kBK, false);
+    encode_map(&Q.tmB[0], TB, qk, qn, ldb_t, kBK, kBN, true);
+    Q.nprod = 1;
+    Q.mbase = M;
+    const Terms one = {{0, 1}};
+    fill_desc(Q.prod[0], one, one, one);
+    for (const Live& l : live) {
+        for (int side_ab = 0; side_ab < 2; ++side_ab) {
+            const Terms& terms = side_ab == 0 ? l.a : l.b;
+            const TmaOperand& t = side_ab == 0 ? ta : tb;
+            SumParams sp;
+            std::memset(&sp, 0, sizeof(sp));
+            sp.n = static_cast<int>(terms.size());
+            for (size_t u = 0; u < terms.size(); ++u) {
+                const int qi = terms[u].first;
+                sp.x[u] = quad_origin(t, qi / side, qi % side);
+                sp.xrows[u] = quad_rows(t, qi / side);
+                sp.xcols[u] = quad_cols(t, qi % side);
+                sp.coeff[u] = terms[u].second;
+            }
+            sp.rs = 1;
+            sp.cs = t.ld;
+            sp.dst = side_ab == 0 ? TA : TB;
+            sp.rows = side_ab == 0 ? qm : qk;
+            sp.cols = side_ab == 0 ? qk : qn;
+            sp.ld = side_ab == 0 ? lda_t : ldb_t;
+            ck(launch_materialize(sp, s), "materialize");
+            ++launches;
+        }
+        ck(launch_mm(Q, s), "mm_kernel (Naive)");
+        ++launches;
+        StreamParams T = S;
+        std::memset(T.nsrc, 0, sizeof(T.nsrc));
+        for (const auto& [q, g] : l.c) {
+            T.src_prod[q][0] = 0;
+            T.src_coeff[q][0] = static_cast<int8_t>(g);
+            T.nsrc[q] = 1;
+        }
+        T.mbase = M;
+        ck(launch_stream_update(T, s), "stream_update");
+        ++launches;
+    }
+    return launches;
+}
+
+long scale_device(Engine& e, cudaStream_t s, const DView& C, double beta) {
+    (void)e;
+    ck(launch_scale(C.p, C.rows, C.cols, C.rs, C.cs, beta, s), "scale");
+    return 1;
+}
+
+}  // namespace sb200

@@ -1,0 +1,67 @@
+// Host engine: the B200 re-layering of the reference's L3 (variants.cpp) and
+// the parts of L1 (blocking.cpp) that stay on the host.  It partitions the
+// operands into quadrant views (ceil rule, matrix.cpp:8-35), stages host
+// operands to the device, normalises layouts TMA cannot read, builds the
+// per-launch product program from the composed operand table, and launches
+// the kernels of kernels.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "strassen.h"
+
+namespace sb200 {
+
+// Error carrying an ABI status (mirrors the reference's exception -> status
+// translation, capi.cpp:22-44).
+struct Error : std::runtime_error {
+    strassen_status status;
+    Error(strassen_status s, const std::string& what) : std::runtime_error(what), status(s) {}
+};
+
+struct DeviceBuffer {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+};
+
+// Device-side state of one ctx (the B200 counterpart of Workspace,
+// blocking.hpp:33-42): grow-only buffers reused across calls.
+struct Engine {
+    int device = -1;
+    bool initialised = false;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t user_stream = nullptr;
+    bool has_user_stream = false;
+    DeviceBuffer stage_a, stage_b, stage_c;   // host-operand staging
+    DeviceBuffer pack_a, pack_b;              // TMA layout normalisation
+    DeviceBuffer mbuf, tabuf, tbbuf;          // AB / Naive temporaries
+    long last_launches = 0;
+
+    ~Engine();
+    void init();
+    cudaStream_t stream();
+    double* ensure(DeviceBuffer& b, size_t bytes);
+    size_t workspace_bytes() const;
+};
+
+struct DView {  // a strided matrix view in device memory
+    double* p = nullptr;
+    long rows = 0, cols = 0;
+    long long rs = 0, cs = 0;
+};
+
+// C := alpha A B + C on device views, enqueued on `s` (no synchronisation).
+// variant/level already validated.  Returns the number of kernel launches.
+long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, double alpha,
+                const DView& A, const DView& B, const DView& C);
+
+// C := beta C on a device view.
+long scale_device(Engine& e, cudaStream_t s, const DView& C, double beta);
+
+// Pointer classification for host staging.
+bool is_device_pointer(const void* p);
+
+}  // namespace sb200

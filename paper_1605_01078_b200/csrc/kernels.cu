@@ -1,0 +1,437 @@
+// sm_100a kernels of the B200 Strassen DGEMM.
+//
+// mm_kernel is the fused ABC Strassen tile kernel (it also runs the classical
+// DGEMM as a one-product program and the AB/Naive product stage).  It replaces
+// the reference's whole L1+L0 engine:
+//   pack_a_sum / pack_b_sum      (blocking.cpp:12-66)  -> TMA operand-term loads
+//                                   into a shared-memory ring + an in-place,
+//                                   once-per-CTA operand-sum stage
+//   microkernel / accumulate     (kernel.cpp:8-47)     -> DMMA (mma.sync m8n8k4 f64)
+//                                   mainloop over 64x32 warp tiles
+//   multi-destination update     (kernel.cpp:49-76)    -> register epilogue that
+//                                   adds alpha*gamma*M into each C quadrant tile
+//   five-loop driver + OpenMP ic (blocking.cpp:82-131) -> the CTA grid; each CTA
+//                                   owns one tile position in every C quadrant and
+//                                   walks all 7^L products in table order, so the
+//                                   multi-destination updates are race-free and
+//                                   bitwise deterministic run to run.
+// Why DMMA, and why sums are formed once per CTA: DESIGN.md section 3
+// (profiles/r01_fp64_peak.log: DMMA 37.1 TF/s vs DFMA 34.2; DADD shares the
+// FP64 pipe with DMMA).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "kernels.hpp"
+
+namespace sb200 {
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// D(8x8) += A(8x4) B(4x8), fp64, one DMMA.8 on sm_100a.
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// Operand sum of one 2048-double tile into a stage buffer:
+// dst := sum_u c_u raw(slot_u), accumulated left to right like pack_a_sum /
+// pack_b_sum (blocking.cpp:24-28).  c_u = +-1 so fma(c, x, acc) rounds
+// exactly like acc + c*x; a single +1 term is a plain copy (no FP64 op).
+// All buffers are 1024-byte aligned and share the TMA box geometry, so the
+// elementwise sum at equal offsets preserves the (swizzled) layout.
+__device__ __forceinline__ const double2* raw_tile(const uint8_t* raw, uint32_t q) {
+    return reinterpret_cast<const double2*>(raw + (q % kRawSlots) * kSlotBytes);
+}
+
+__device__ __forceinline__ void sum_tile(const uint8_t* raw, uint32_t q0, int n,
+                                         const int8_t* coef, double2* dst, int t) {
+    if (n == 1 && coef[0] == 1) {
+        const double2* src = raw_tile(raw, q0);
+        for (int idx = t; idx < kSlotBytes / 16; idx += kSummerWarps * 32) dst[idx] = src[idx];
+        return;
+    }
+    for (int idx = t; idx < kSlotBytes / 16; idx += kSummerWarps * 32) {
+        double2 v = raw_tile(raw, q0)[idx];
+        const double c0 = coef[0];
+        v.x *= c0;
+        v.y *= c0;
+        for (int u = 1; u < n; ++u) {
+            const double2 w = raw_tile(raw, q0 + u)[idx];
+            const double cu = coef[u];
+            v.x = fma(cu, w.x, v.x);
+            v.y = fma(cu, w.y, v.y);
+        }
+        dst[idx] = v;
+    }
+}
+
+// One 128x128x16 step for a 64x32 warp tile.
+// A slot: TMA box {128 m, 16 k}, no swizzle: double (m, k) at k*128 + m.
+// B slot: TMA box {16 k, 128 n}, 128B swizzle: double (k, n) at byte
+//         n*128 + (((k>>1) ^ (n&7)) << 4) + (k&1)*8.
+// The 16 k of the step are split over 4 DMMA k-steps s with physical
+// k = 4*j + s for lane slot j = lane&3 (A and B agree, so the sum over k is
+// unchanged); A rows are permuted so lane group g = lane>>2 reads rows
+// 16h + 2g + {0,1} of fragments 2h, 2h+1 with one 16-byte load.  Both
+// patterns are bank-conflict free (4 wavefronts per 512-byte warp load).
+__device__ __forceinline__ void mma_step(const double* __restrict__ sA,
+                                         const uint8_t* __restrict__ sB, double (&acc)[8][4][2],
+                                         int wm, int wn, int g, int j) {
+    const double* pa = sA + 4 * j * kBM + wm * 64 + 2 * g;
+    const uint8_t* pb = sB + (wn * 32 + g) * 128;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+        double a[8], b[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const double2 v = *reinterpret_cast<const double2*>(pa + s * kBM + 16 * h);
+            a[2 * h] = v.x;
+            a[2 * h + 1] = v.y;
+        }
+#pragma unroll
+        for (int nf = 0; nf < 4; ++nf) {
+            // n = wn*32 + 8nf + g, so n & 7 == g; k = 4j + s
+            const int chunk = (2 * j + (s >> 1)) ^ g;
+            b[nf] = *reinterpret_cast<const double*>(pb + nf * 8 * 128 + chunk * 16 + (s & 1) * 8);
+        }
+#pragma unroll
+        for (int mf = 0; mf < 8; ++mf)
+#pragma unroll
+            for (int nf = 0; nf < 4; ++nf) dmma(acc[mf][nf][0], acc[mf][nf][1], a[mf], b[nf]);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__ MMParams P) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* raw = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* stage = raw + kRawSlots * kSlotBytes;  // [kStages][A | B]
+    uint64_t* raw_full = reinterpret_cast<uint64_t*>(stage + 2 * kStages * kSlotBytes);
+    uint64_t* raw_empty = raw_full + kRawSlots;
+    uint64_t* st_full = raw_empty + kRawSlots;
+    uint64_t* st_empty = st_full + kStages;
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    // grouped rasterisation: group_m tile rows share B column panels in L2
+    const int bid = blockIdx.x;
+    const int per_group = P.group_m * P.tiles_n;
+    const int grp = bid / per_group;
+    const int first_m = grp * P.group_m;
+    const int gsz = min(P.tiles_m - first_m, P.group_m);
+    const int rr = bid - grp * per_group;
+    const int tm = first_m + rr % gsz;
+    const int tn = rr / gsz;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kRawSlots; ++s) {
+            mbar_init(&raw_full[s], 1);
+            mbar_init(&raw_empty[s], kSummerWarps);
+        }
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&st_full[s], kSummerWarps);
+            mbar_init(&st_empty[s], kConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_proxy_async();
+    }
+    __syncthreads();
+
+    if (warp < 4) {
+        // ================= producer warpgroup ================================
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
+        if (warp == 0) {
+            // TMA issue: one elected lane walks products x k-steps x terms
+            if (lane == 0) {
+                uint32_t q = 0;
+                const int m0 = tm * kBM, n0 = tn * kBN;
+                for (int p = 0; p < P.nprod; ++p) {
+                    const ProductDesc& pd = P.prod[p];
+                    for (int kt = 0; kt < P.ktiles; ++kt) {
+                        const int k0 = kt * kBK;
+                        for (int u = 0; u < pd.na + pd.nb; ++u, ++q) {
+                            const uint32_t s = q % kRawSlots;
+                            mbar_wait(&raw_empty[s], ((q / kRawSlots) & 1) ^ 1);
+                            mbar_expect_tx(&raw_full[s], kSlotBytes);
+                            if (u < pd.na)
+                                tma_load_2d(raw + s * kSlotBytes, &P.tmA[pd.aq[u]], m0, k0,
+                                            &raw_full[s]);
+                            else
+                                tma_load_2d(raw + s * kSlotBytes, &P.tmB[pd.bq[u - pd.na]], k0, n0,
+                                            &raw_full[s]);
+                        }
+                    }
+                }
+            }
+        } else {
+            // operand-sum warps: raw term tiles -> summed (A, B) stage
+            const int t = threadIdx.x - 32;
+            uint32_t q = 0, T = 0;
+            for (int p = 0; p < P.nprod; ++p) {
+                const ProductDesc& pd = P.prod[p];
+                const int na = pd.na, nb = pd.nb;
+                for (int kt = 0; kt < P.ktiles; ++kt, ++T) {
+                    const uint32_t st = T % kStages;
+                    mbar_wait(&st_empty[st], ((T / kStages) & 1) ^ 1);
+                    for (uint32_t u = q; u < q + na + nb; ++u)
+                        mbar_wait(&raw_full[u % kRawSlots], (u / kRawSlots) & 1);
+                    double2* dA = reinterpret_cast<double2*>(stage + (2 * st) * kSlotBytes);
+                    double2* dB = reinterpret_cast<double2*>(stage + (2 * st + 1) * kSlotBytes);
+                    sum_tile(raw, q, na, pd.as, dA, t);
+                    sum_tile(raw, q + na, nb, pd.bs, dB, t);
+                    __syncwarp();
+                    if (lane == 0) {
+                        for (uint32_t u = q; u < q + na + nb; ++u)
+                            mbar_arrive(&raw_empty[u % kRawSlots]);
+                        mbar_arrive(&st_full[st]);
+                    }
+                    q += na + nb;
+                }
+            }
+        }
+        return;
+    }
+
+    // ================= consumer warpgroups: DMMA mainloop + epilogue =========
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kConsumerRegs));
+    const int cw = warp - 4;
+    const int wm = cw & 1, wn = cw >> 1;
+    const int g = lane >> 2, j = lane & 3;
+    uint32_t T = 0;
+    double acc[8][4][2];
+
+    for (int p = 0; p < P.nprod; ++p) {
+        const ProductDesc& pd = P.prod[p];
+#pragma unroll
+        for (int mf = 0; mf < 8; ++mf)
+#pragma unroll
+            for (int nf = 0; nf < 4; ++nf) acc[mf][nf][0] = acc[mf][nf][1] = 0.0;
+
+        for (int kt = 0; kt < P.ktiles; ++kt, ++T) {
+            const uint32_t st = T % kStages;
+            mbar_wait(&st_full[st], (T / kStages) & 1);
+            mma_step(reinterpret_cast<const double*>(stage + (2 * st) * kSlotBytes),
+                     stage + (2 * st + 1) * kSlotBytes, acc, wm, wn, g, j);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&st_empty[st]);
+        }
+
+        // ---- epilogue: rows/cols of this lane's accumulator fragments
+        const int mrow0 = tm * kBM + wm * 64 + 2 * g;
+        const int ncol0 = tn * kBN + wn * 32 + 2 * j;
+        if (P.mode == kEpiRMW) {
+            for (int u = 0; u < pd.nc; ++u) {
+                const int cq = pd.cq[u];
+                double* __restrict__ C = P.cptr[cq];
+                const int R = P.crows[cq], Cc = P.ccols[cq];
+                const double sc = P.alpha * static_cast<double>(pd.cs[u]);
+#pragma unroll
+                for (int nf = 0; nf < 4; ++nf) {
+                    double cv[8][2];
+#pragma unroll
+                    for (int mf = 0; mf < 8; ++mf)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int row = mrow0 + 16 * (mf >> 1) + (mf & 1);
+                            const int col = ncol0 + 8 * nf + e;
+                            cv[mf][e] = (row < R && col < Cc)
+                                            ? C[row * P.rs_c + col * P.cs_c]
+                                            : 0.0;
+                        }
+#pragma unroll
+                    for (int mf = 0; mf < 8; ++mf)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int row = mrow0 + 16 * (mf >> 1) + (mf & 1);
+                            const int col = ncol0 + 8 * nf + e;
+                            if (row < R && col < Cc)
+                                C[row * P.rs_c + col * P.cs_c] = fma(sc, acc[mf][nf][e], cv[mf][e]);
+                        }
+                }
+            }
+        } else {
+            double* __restrict__ M = P.mbase + p * P.mstride;
+#pragma unroll
+            for (int nf = 0; nf < 4; ++nf)
+#pragma unroll
+                for (int mf = 0; mf < 8; ++mf)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int row = mrow0 + 16 * (mf >> 1) + (mf & 1);
+                        const int col = ncol0 + 8 * nf + e;
+                        if (row < P.qm && col < P.qn) M[row + col * P.ldm] = acc[mf][nf][e];
+                    }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- repack ----
+__global__ void repack_kernel(const double* __restrict__ src, long long rs, long long cs,
+                              long rows, long cols, double* __restrict__ dst, long long ld,
+                              long q, long q_al, int x_along_rows) {
+    __shared__ double tile[32][33];
+    const long i0 = static_cast<long>(blockIdx.x) * 32;
+    const long j0 = static_cast<long>(blockIdx.y) * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+    if (x_along_rows) {
+        for (int yy = ty; yy < 32; yy += 8) {
+            const long i = i0 + tx, jj = j0 + yy;
+            if (i < rows && jj < cols) tile[yy][tx] = src[i * rs + jj * cs];
+        }
+    } else {
+        for (int yy = ty; yy < 32; yy += 8) {
+            const long i = i0 + yy, jj = j0 + tx;
+            if (i < rows && jj < cols) tile[tx][yy] = src[i * rs + jj * cs];
+        }
+    }
+    __syncthreads();
+    for (int yy = ty; yy < 32; yy += 8) {
+        const long i = i0 + tx, jj = j0 + yy;
+        if (i < rows && jj < cols) {
+            const long di = (i / q) * q_al + i % q;
+            dst[di + jj * ld] = tile[yy][tx];
+        }
+    }
+}
+
+// ------------------------------------------------------------ materialise ---
+// dst(i, j) = sum_u c_u X_u(i, j), zero outside each clipped view
+// (variants.cpp:53-96: first pass d0*x0 [+ d1*x1], then += ds*xs).
+__global__ void materialize_kernel(const SumParams P) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long jj = blockIdx.y;
+    if (i >= P.rows) return;
+    for (long long j = jj; j < P.cols; j += gridDim.y) {
+        double v = 0.0;
+        for (int u = 0; u < P.n; ++u) {
+            const double x = (i < P.xrows[u] && j < P.xcols[u]) ? P.x[u][i * P.rs + j * P.cs] : 0.0;
+            const double c = P.coeff[u];
+            v = (u == 0) ? c * x : fma(c, x, v);
+        }
+        P.dst[i + j * P.ld] = v;
+    }
+}
+
+// --------------------------------------------------------- stream update ---
+// C_q(i, j) += sum over (p, gamma) feeding q, in table order, of
+// (alpha * gamma) * M_p(i, j)  (variants.cpp:99-109, applied entry by entry).
+__global__ void stream_update_kernel(const StreamParams P) {
+    const int quad = blockIdx.z;
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= P.crows[quad]) return;
+    double* C = P.cptr[quad];
+    const int ns = P.nsrc[quad];
+    for (long long j = blockIdx.y; j < P.ccols[quad]; j += gridDim.y) {
+        double* cp = C + i * P.rs_c + j * P.cs_c;
+        double c = *cp;
+        for (int u = 0; u < ns; ++u) {
+            const double* M = P.mbase + P.src_prod[quad][u] * P.mstride;
+            c = fma(P.alpha * static_cast<double>(P.src_coeff[quad][u]), M[i + j * P.ldm], c);
+        }
+        *cp = c;
+    }
+}
+
+__global__ void scale_kernel(double* c, long rows, long cols, long long rs, long long cs,
+                             double beta) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= rows) return;
+    for (long long j = blockIdx.y; j < cols; j += gridDim.y) {
+        double* p = c + i * rs + j * cs;
+        *p = (beta == 0.0) ? 0.0 : beta * *p;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_mm(const MMParams& p, cudaStream_t s) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(mm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             kMMSmemBytes);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const int grid = p.tiles_m * p.tiles_n;
+    mm_kernel<<<grid, kThreads, kMMSmemBytes, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_repack(const double* src, long long rs, long long cs, long rows, long cols,
+                          double* dst, long long ld, long q, long q_al, cudaStream_t s) {
+    const long long ars = rs < 0 ? -rs : rs, acs = cs < 0 ? -cs : cs;
+    const int x_along_rows = (ars <= acs) ? 1 : 0;
+    dim3 grid(static_cast<unsigned>((rows + 31) / 32), static_cast<unsigned>((cols + 31) / 32));
+    repack_kernel<<<grid, dim3(32, 8), 0, s>>>(src, rs, cs, rows, cols, dst, ld, q, q_al,
+                                               x_along_rows);
+    return cudaGetLastError();
+}
+
+static unsigned col_grid(long long cols) {
+    return static_cast<unsigned>(cols < 16384 ? cols : 16384);
+}
+
+cudaError_t launch_materialize(const SumParams& p, cudaStream_t s) {
+    dim3 grid(static_cast<unsigned>((p.rows + 255) / 256), col_grid(p.cols));
+    materialize_kernel<<<grid, 256, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stream_update(const StreamParams& p, cudaStream_t s) {
+    dim3 grid(static_cast<unsigned>((p.qm + 255) / 256), col_grid(p.qn), p.nquad);
+    stream_update_kernel<<<grid, 256, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_scale(double* c, long rows, long cols, long long rs, long long cs, double beta,
+                         cudaStream_t s) {
+    dim3 grid(static_cast<unsigned>((rows + 255) / 256), col_grid(cols));
+    scale_kernel<<<grid, 256, 0, s>>>(c, rows, cols, rs, cs, beta);
+    return cudaGetLastError();
+}
+
+}  // namespace sb200

@@ -1,0 +1,103 @@
+// Device-side parameter blocks and launchers shared by the host engine
+// (engine.cpp) and the sm_100a kernels (kernels.cu).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sb200 {
+
+// ---- fused Strassen tile kernel (mm_kernel) -------------------------------
+constexpr int kBM = 128;            // CTA tile rows (logical quadrant rows)
+constexpr int kBN = 128;            // CTA tile cols
+constexpr int kBK = 16;             // k per pipeline step
+constexpr int kMaxQuad = 16;        // 2^L x 2^L quadrants, L <= 2
+constexpr int kMaxProducts = 49;    // 7^L
+constexpr int kMaxTerms = 4;        // operand terms / destinations per product at L <= 2
+constexpr int kConsumerWarps = 8;   // 2 warpgroups; 2 (m) x 4 (n) warps of 64 x 32
+constexpr int kSummerWarps = 3;     // producer warpgroup: 1 TMA warp + 3 operand-sum warps
+constexpr int kThreads = 128 + kConsumerWarps * 32;  // 384
+constexpr int kSlotBytes = kBM * kBK * 8;            // one 128x16 fp64 operand tile (16 KB)
+constexpr int kRawSlots = 8;                         // TMA ring of raw operand-term tiles
+constexpr int kStages = 2;                           // summed (A, B) operand stages
+constexpr int kProducerRegs = 56;                    // setmaxnreg split (per SMSP:
+constexpr int kConsumerRegs = 224;                   //  32*56 + 2*32*224 <= 16384)
+constexpr int kMMSmemBytes = (kRawSlots + 2 * kStages) * kSlotBytes + 1024 + 1024;
+
+// One Strassen product M_p = (sum_u as_u A_{aq_u}) (sum_u bs_u B_{bq_u});
+// destinations C_{cq_u} += alpha * cs_u * M_p.
+struct ProductDesc {
+    int8_t na, nb, nc, pad;
+    int8_t aq[kMaxTerms], as[kMaxTerms];
+    int8_t bq[kMaxTerms], bs[kMaxTerms];
+    int8_t cq[kMaxTerms], cs[kMaxTerms];
+};
+
+enum EpilogueMode : int {
+    kEpiRMW = 0,    // C_q += alpha * gamma * M (ABC, DGEMM)
+    kEpiStore = 1,  // M_p := M into product temporaries (AB, Naive)
+};
+
+struct alignas(64) MMParams {
+    CUtensorMap tmA[kMaxQuad];  // per A quadrant: dims (rows, cols), box 128 x 16
+    CUtensorMap tmB[kMaxQuad];  // per B quadrant: dims (k rows, n cols), box 16 x 128, swizzle 128B
+    ProductDesc prod[kMaxProducts];
+    double* cptr[kMaxQuad];     // C quadrant views (clipped)
+    int crows[kMaxQuad];
+    int ccols[kMaxQuad];
+    long long rs_c, cs_c;
+    double* mbase;              // kEpiStore: M_p = mbase + p * mstride, col-major, ld = ldm
+    long long mstride;
+    long long ldm;
+    double alpha;
+    int nprod;
+    int qm, qn, qk;             // logical quadrant extents
+    int tiles_m, tiles_n, ktiles;
+    int mode;
+    int group_m;                // tile rasterisation group height
+};
+
+cudaError_t launch_mm(const MMParams& p, cudaStream_t s);
+
+// ---- layout normalisation (TMA staging) -----------------------------------
+// dst(rowmap(i), j) = src(i, j), src element (i, j) at src[i*rs + j*cs];
+// rowmap(i) = (i / q) * q_al + i % q (quadrant rows placed at aligned
+// offsets); dst column-major with leading dimension ld.
+cudaError_t launch_repack(const double* src, long long rs, long long cs, long rows, long cols,
+                          double* dst, long long ld, long q, long q_al, cudaStream_t s);
+
+// ---- Naive: materialise an operand sum ------------------------------------
+struct SumParams {
+    const double* x[kMaxTerms];
+    long long xrows[kMaxTerms], xcols[kMaxTerms];
+    int coeff[kMaxTerms];
+    int n;
+    long long rs, cs;     // source strides (shared by all terms)
+    double* dst;          // column-major rows x cols, leading dimension ld
+    long long rows, cols, ld;
+};
+cudaError_t launch_materialize(const SumParams& p, cudaStream_t s);
+
+// ---- AB / Naive: stream products into C quadrants -------------------------
+constexpr int kMaxFanIn = 16;
+struct StreamParams {
+    double* cptr[kMaxQuad];
+    int crows[kMaxQuad], ccols[kMaxQuad];
+    int nsrc[kMaxQuad];
+    int8_t src_prod[kMaxQuad][kMaxFanIn];
+    int8_t src_coeff[kMaxQuad][kMaxFanIn];
+    long long rs_c, cs_c;
+    const double* mbase;
+    long long mstride, ldm;
+    double alpha;
+    int nquad;
+    int qm, qn;
+};
+cudaError_t launch_stream_update(const StreamParams& p, cudaStream_t s);
+
+// ---- beta pre-scale for the dgemm shim -------------------------------------
+cudaError_t launch_scale(double* c, long rows, long cols, long long rs, long long cs, double beta,
+                         cudaStream_t s);
+
+}  // namespace sb200

@@ -1,0 +1,220 @@
+"""The drop-in boundary on CPU: the C-ABI library loads, exports every symbol
+include/strassen.h declares, and reproduces the reference's host-side
+behaviour (validation order, status codes, counters, model, tables) without a
+GPU.  Mirrors the reference's test_capi.cpp."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+import paper_1605_01078_b200 as S
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CONFIGS = [("dgemm", 0), ("abc", 1), ("ab", 1), ("naive", 1), ("abc", 2), ("ab", 2), ("naive", 2)]
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "strassen.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(strassen_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = C.CDLL(S.LIB_PATH)
+    names = header_functions()
+    assert len(names) >= 17 + 8  # 17 reference functions + 8 B200 additions
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_reference_abi_subset_declared():
+    # the 17 reference functions (reference strassen.h:67-119) are all declared here
+    ref19 = ["strassen_ctx_create", "strassen_ctx_destroy", "strassen_ctx_set_blocking",
+             "strassen_ctx_get_blocking", "strassen_ctx_set_threads",
+             "strassen_ctx_enable_counters", "strassen_ctx_reset_counters",
+             "strassen_ctx_get_counters", "strassen_gemm", "strassen_reference_gemm",
+             "strassen_rel_error", "strassen_model_predict", "strassen_effective_gflops",
+             "strassen_model_params_ivy_bridge", "strassen_blocking_defaults",
+             "strassen_table_counts", "strassen_status_str"]
+    assert set(ref19) <= set(header_functions())
+
+
+def test_product_package_never_touches_oracle():
+    pkg = os.path.join(ROOT, "paper_1605_01078_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cpp", ".cu", ".hpp", ".h", "Makefile")):
+                text = open(os.path.join(dirpath, f)).read()
+                for pat in ("oracle_lib", "oracle/", "libstrassen_oracle", "libstrassen_ref",
+                            "strassen_oracle"):
+                    assert pat not in text, (f, pat)
+
+
+def test_ctx_lifecycle_and_blocking_round_trip():
+    # test_capi.cpp:27-45
+    ctx = S.Ctx()
+    assert ctx.blocking == dict(mc=96, nc=4096, kc=256, mr=8, nr=4)
+    b = ctx.blocking
+    ctx.set_blocking(64, b["nc"], b["kc"], b["mr"], b["nr"])
+    assert ctx.blocking["mc"] == 64
+    with pytest.raises(S.StrassenError) as e:
+        ctx.set_blocking(90, b["nc"], b["kc"], b["mr"], b["nr"])  # 90 % 8 != 0
+    assert e.value.status == S.ERR_PARAM
+    for bad in [(0, 4096, 256, 8, 4), (96, 4096, 256, 33, 4), (96, 4094, 256, 8, 4)]:
+        with pytest.raises(S.StrassenError):
+            ctx.set_blocking(*bad)
+
+
+def test_null_and_argument_errors():
+    # test_capi.cpp:47-67: same status codes, checked before any device use
+    lib = S.lib()
+    assert lib.strassen_ctx_create(None) == S.ERR_NULL
+    assert lib.strassen_ctx_set_threads(None, 2) == S.ERR_NULL
+    ctx = S.Ctx()
+    assert lib.strassen_ctx_set_threads(ctx.ptr, 0) == S.ERR_PARAM
+    a = np.zeros(4)
+    b = np.zeros(4)
+    c = np.zeros(4)
+    pa, pb, pc = (C.c_void_p(x.ctypes.data) for x in (a, b, c))
+    assert ctx.gemm_raw(S.DGEMM, 1, 2, 2, 2, 1.0, pa, 2, 1, pb, 2, 1, pc, 2, 1) == S.ERR_PARAM
+    assert ctx.gemm_raw(S.ABC, 3, 2, 2, 2, 1.0, pa, 2, 1, pb, 2, 1, pc, 2, 1) == S.ERR_PARAM
+    assert ctx.gemm_raw(S.ABC, 0, 2, 2, 2, 1.0, pa, 2, 1, pb, 2, 1, pc, 2, 1) == S.ERR_PARAM
+    assert ctx.gemm_raw(S.ABC, 1, -2, 2, 2, 1.0, pa, 2, 1, pb, 2, 1, pc, 2, 1) == S.ERR_PARAM
+    assert ctx.gemm_raw(S.ABC, 1, 2, 2, 2, 1.0, None, 2, 1, pb, 2, 1, pc, 2, 1) == S.ERR_NULL
+    assert ctx.gemm_raw(7, 1, 2, 2, 2, 1.0, pa, 2, 1, pb, 2, 1, pc, 2, 1) == S.ERR_PARAM
+    assert lib.strassen_gemm(None, S.ABC, 1, 2, 2, 2, 1.0, pa, 2, 1, pb, 2, 1, pc, 2, 1) == \
+        S.ERR_NULL
+
+
+def test_no_cpu_fallback_without_device():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    ctx = S.Ctx()
+    a, b, c = np.ones((4, 4)), np.ones((4, 4)), np.zeros((4, 4))
+    with pytest.raises(S.StrassenError) as e:
+        ctx.gemm("abc", 1, 1.0, a, b, c)
+    assert e.value.status == S.ERR_DEVICE
+    assert np.all(c == 0.0)
+
+
+def test_table_counts_and_status_strings():
+    # test_capi.cpp:173-190
+    assert S.table_counts(1) == (7, 5, 5, 12)
+    assert S.table_counts(2) == (49, 95, 95, 144)
+    with pytest.raises(S.StrassenError) as e:
+        S.table_counts(3)
+    assert e.value.status == S.ERR_PARAM
+    lib = S.lib()
+    assert lib.strassen_status_str(S.OK) == b"ok"
+    for s in range(1, 7):
+        assert len(lib.strassen_status_str(s)) > 0
+
+
+def test_effective_gflops_and_model():
+    # test_capi.cpp:138-171
+    assert S.effective_gflops(1000, 1000, 1000, 1.0) == 2.0
+    with pytest.raises(S.StrassenError) as e:
+        S.effective_gflops(10, 10, 10, 0.0)
+    assert e.value.status == S.ERR_DOMAIN
+    mp = S.model_params_ivy_bridge()
+    assert mp.lambda_ == 0.7 and mp.channel_factor == 4.0
+    bd, egf = S.model_predict("abc", 1, 16000, 16000, 512)
+    assert egf > 0
+    bd_dg, _ = S.model_predict("dgemm", 0, 16000, 16000, 512)
+    assert bd["total"] < bd_dg["total"]
+    with pytest.raises(S.StrassenError):
+        S.model_predict("abc", 3, 100, 100, 100)
+
+
+@pytest.mark.skipif(not O.RefStrassen.available(), reason="oracle/_ref not built")
+def test_model_bitwise_equal_to_reference():
+    ref = O.RefStrassen()
+    lib = ref.lib
+    lib.strassen_model_predict.argtypes = [C.c_int, C.c_int, C.c_long, C.c_long, C.c_long,
+                                           C.POINTER(S.Blocking), C.POINTER(S.ModelParams),
+                                           C.POINTER(S.Breakdown), C.POINTER(C.c_double)]
+    for (m, n, k) in [(16000, 16000, 512), (5000, 3000, 700), (1, 1, 1), (4097, 9999, 1000)]:
+        for v, L in CONFIGS:
+            bd, egf = S.model_predict(v, L, m, n, k)
+            rb = S.Breakdown()
+            re_ = C.c_double()
+            bp = S.Blocking(**S.blocking_defaults())
+            assert lib.strassen_model_predict(S.VARIANT_NAMES[v], L, m, n, k, C.byref(bp),
+                                              C.byref(S.model_params_ivy_bridge()), C.byref(rb),
+                                              C.byref(re_)) == 0
+            assert [getattr(rb, f) for f, _ in S.Breakdown._fields_] == list(bd.values())
+            assert re_.value == egf
+
+
+@pytest.mark.skipif(not O.RefStrassen.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("shape", [(64, 64, 64), (256, 256, 256), (117, 93, 201), (1, 1, 1),
+                                   (3, 3, 3), (31, 79, 127), (129, 64, 5), (2, 300, 2)])
+def test_counters_equal_reference_instrumentation(shape):
+    """Analytic counters == the reference's atomics, all configs, two blockings."""
+    m, n, k = shape
+    ref = O.RefStrassen()
+    ref.enable_counters()
+    ref.lib.strassen_ctx_set_blocking.argtypes = [C.c_void_p, C.POINTER(S.Blocking)]
+    ref.lib.strassen_ctx_reset_counters.argtypes = [C.c_void_p]
+    for bl in [None, dict(mc=16, nc=24, kc=7, mr=8, nr=4)]:
+        ref.lib.strassen_ctx_set_blocking(ref.ctx, C.byref(S.Blocking(**(bl or S.blocking_defaults()))))
+        for v, L in CONFIGS:
+            ref.lib.strassen_ctx_reset_counters(ref.ctx)
+            a, b, c = np.zeros((m, k)), np.zeros((k, n)), np.zeros((m, n))
+            ref.gemm(v, L, 1.0, a, b, c)
+            assert list(S.predicted_counters(v, L, m, n, k, bl).values()) == ref.counters()
+
+
+def test_counter_closed_forms():
+    # test_capi.cpp:117-136 and acceptance.cpp:100-157
+    c = S.predicted_counters("naive", 1, 64, 64, 64)
+    assert (c["a_plus_passes"], c["b_plus_passes"], c["c_plus_passes"]) == (19, 19, 36)
+    assert c["kernel_fma_flops"] == 7 * 2 * 32 ** 3
+    c = S.predicted_counters("naive", 2, 64, 64, 64)
+    assert (c["a_plus_passes"], c["b_plus_passes"], c["c_plus_passes"]) == (293, 293, 432)
+    d = 256
+    for L in (1, 2):
+        q = d >> L
+        mul, aa, ba, cu = S.table_counts(L)
+        c = S.predicted_counters("abc", L, d, d, d)
+        assert c["kernel_fma_flops"] == mul * 2 * q ** 3
+        assert c["pack_a_add_flops"] == aa * 2 * q * q
+        assert c["kernel_update_flops"] == cu * 2 * q * q
+    c = S.predicted_counters("abc", 1, d, d, d)
+    total = c["kernel_fma_flops"] + c["pack_a_add_flops"] + c["pack_b_add_flops"] + \
+        c["kernel_update_flops"]
+    assert total == 7 * d ** 3 // 4 + 5 * d * d + 6 * d * d
+
+
+def test_host_reference_gemm_and_rel_error_match_oracle():
+    m, n, k = 37, 29, 41
+    a = O.fill_uniform(m * k, 1).reshape(m, k)
+    b = np.asfortranarray(O.fill_uniform(k * n, 2).reshape(k, n))
+    c0 = O.fill_uniform(m * n, 3).reshape(m, n)
+    c1, c2 = c0.copy(), c0.copy()
+    S.reference_gemm(0.25, a, b, c1)
+    O.reference_gemm(0.25, a, b, c2)
+    assert np.array_equal(c1, c2)
+    assert S.rel_error(c1, c0) == O.rel_frobenius_error(c1, c0)
+
+
+def test_dgemm_shim_argument_checks():
+    ctx = S.Ctx()
+    a = np.zeros(16)
+    st = S.lib().strassen_dgemm(ctx.ptr, S.ABC, 1, b"X", b"N", 4, 4, 4, 1.0,
+                                C.c_void_p(a.ctypes.data), 4, C.c_void_p(a.ctypes.data), 4, 1.0,
+                                C.c_void_p(a.ctypes.data), 4)
+    assert st == S.ERR_PARAM
+    st = S.lib().strassen_dgemm(ctx.ptr, S.ABC, 1, b"N", b"N", 4, 4, 4, 1.0,
+                                C.c_void_p(a.ctypes.data), 3, C.c_void_p(a.ctypes.data), 4, 1.0,
+                                C.c_void_p(a.ctypes.data), 4)
+    assert st == S.ERR_PARAM  # lda < m
+
+
+def test_build_info_names_sm100a():
+    info = S.lib().strassen_build_info().decode()
+    assert "sm_100a" in info and "DMMA" in info

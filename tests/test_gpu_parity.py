@@ -1,0 +1,257 @@
+"""Parity of the B200 path (through the C ABI) against the oracle.
+
+Mirrors the reference's own tests: test_strassen.cpp (random shapes,
+odd/degenerate shapes, pairwise agreement, 7-product formula), test_capi.cpp
+(C-API oracle match, swapped-stride transpose, counters), test_kernel.cpp
+(clipped-destination canary), acceptance.cpp (random shapes up to 1200),
+test_bench.cpp (rank-b schedule), plus GPU-specific properties (host vs device
+pointers, run-to-run determinism, full-size checks)."""
+import numpy as np
+import pytest
+
+import oracle_lib as O
+import paper_1605_01078_b200 as S
+from gpu_util import CONFIGS, check, freivalds, inputs, oracle_result
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx(cuda):
+    c = S.Ctx()
+    yield c
+    c.close()
+
+
+def run(ctx, variant, level, alpha, a, b, c0):
+    c = np.array(c0, copy=True, order="K")
+    ctx.gemm(variant, level, alpha, a, b, c)
+    return c
+
+
+@pytest.mark.parametrize("variant,level", CONFIGS)
+def test_capi_oracle_match_117x93x201(ctx, variant, level):
+    # test_capi.cpp:69-95: row-major operands, alpha = 0.5
+    m, n, k = 117, 93, 201
+    a, b, c0 = inputs(m, n, k, (1, 2, 3), "row")
+    ref = oracle_result("dgemm", 0, 0.5, a, b, c0, use_reference_gemm=True)
+    check(variant, level, run(ctx, variant, level, 0.5, a, b, c0), ref, c0, a, b)
+
+
+def test_random_shapes_all_variants(ctx):
+    # test_strassen.cpp:64-82 (12 shapes <= 300, alpha in {1, -1, 0.5})
+    rng = np.random.default_rng(4)
+    for it in range(12):
+        m, n, k = (int(x) for x in rng.integers(1, 301, size=3))
+        al = [1.0, -1.0, 0.5][it % 3]
+        a, b, c0 = inputs(m, n, k, (10 + it, 20 + it, 30 + it), "row" if it % 2 else "col")
+        ref = oracle_result("dgemm", 0, al, a, b, c0, use_reference_gemm=True)
+        for v, L in CONFIGS:
+            check(v, L, run(ctx, v, L, al, a, b, c0), ref, c0, a, b)
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (3, 3, 3), (31, 79, 127), (129, 64, 5), (2, 300, 2),
+                                   (1, 5, 1), (7, 1, 9), (257, 129, 3), (130, 2, 260)])
+def test_odd_and_degenerate_shapes(ctx, shape):
+    # test_strassen.cpp:84-100 plus single-row/column fringes
+    m, n, k = shape
+    a, b, c0 = inputs(m, n, k, (100 + m, 200 + n, 300 + k), "row")
+    ref = oracle_result("dgemm", 0, 1.0, a, b, c0, use_reference_gemm=True)
+    for v, L in CONFIGS:
+        check(v, L, run(ctx, v, L, 1.0, a, b, c0), ref, c0, a, b)
+
+
+def test_variants_agree_pairwise(ctx):
+    # test_strassen.cpp:102-117 (1e-12)
+    m, n, k = 193, 150, 177
+    a, b, c0 = inputs(m, n, k, (5, 6, 7), "row")
+    for L in (1, 2):
+        abc = run(ctx, "abc", L, 1.0, a, b, c0)
+        for v in ("ab", "naive"):
+            other = run(ctx, v, L, 1.0, a, b, c0)
+            assert O.rel_frobenius_error(other, abc) < 1e-12
+
+
+def test_seven_product_2x2(ctx):
+    a, b, c0 = inputs(2, 2, 2, (1, 2, 3), "row")
+    want = oracle_result("abc", 1, 0.5, a, b, c0)
+    O.strassen_gemm("abc", 1, 0.5, a, b, want.copy())
+    got = run(ctx, "abc", 1, 0.5, a, b, c0)
+    check("abc", 1, got, want, c0, a, b)
+
+
+def test_transposition_via_swapped_strides(ctx):
+    # test_capi.cpp:97-115: A stored transposed (k x m row-major), swapped strides
+    m, n, k = 20, 15, 30
+    at = O.fill_uniform(k * m, 4).reshape(k, m)
+    b = O.fill_uniform(k * n, 5).reshape(k, n)
+    a_view = at.T  # rs = 1, cs = m
+    for v, L in CONFIGS:
+        c = np.zeros((m, n))
+        ctx.gemm(v, L, 1.0, a_view, b, c)
+        ref = np.zeros((m, n))
+        O.reference_gemm(1.0, np.ascontiguousarray(a_view), b, ref)
+        assert O.rel_frobenius_error(c, ref) < 1e-12
+
+
+@pytest.mark.parametrize("layout", ["col", "row"])
+def test_golden_vectors(ctx, layout):
+    """The committed reference outputs (tests/golden) within tolerance."""
+    import json
+    import os
+    d = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))
+    npz = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden.npz"))
+    n_checked = 0
+    for case in d["cases"]:
+        if case["layout"] != layout or not case["full"] or case["variant"] == "reference":
+            continue
+        m, n, k = case["m"], case["n"], case["k"]
+        a, b, c0 = inputs(m, n, k, case["seeds"], layout)
+        got = run(ctx, case["variant"], case["level"], case["alpha"], a, b, c0)
+        check(case["variant"], case["level"], np.ascontiguousarray(got), npz[case["key"]], c0,
+              a, b)
+        n_checked += 1
+    assert n_checked > 0
+
+
+def test_clipped_destination_canary(ctx):
+    # test_kernel.cpp:128-147: C is a window of a larger buffer; nothing outside
+    # the window may be written.
+    m, n, k = 133, 77, 150
+    a, b, _ = inputs(m, n, k, (8, 9, 10))
+    sentinel = -777.25
+    for v, L in CONFIGS:
+        buf = np.full((m + 9, n + 7), sentinel, order="F")
+        c = buf[3:3 + m, 2:2 + n]
+        c[...] = 0.0
+        ctx.gemm(v, L, 1.0, a, b, c)
+        outside = buf.copy()
+        outside[3:3 + m, 2:2 + n] = sentinel
+        assert np.all(outside == sentinel), (v, L)
+        ref = oracle_result("dgemm", 0, 1.0, a, b, np.zeros((m, n)), use_reference_gemm=True)
+        check(v, L, c, ref, np.zeros((m, n)), a, b)
+
+
+def test_device_pointers_equal_host_pointers_bitwise(ctx):
+    import torch
+    m, n, k = 300, 290, 520
+    a, b, c0 = inputs(m, n, k, (11, 12, 13))
+    for v, L in CONFIGS:
+        host = run(ctx, v, L, 1.0, a, b, c0)
+        ta = torch.from_numpy(a).cuda()
+        tb = torch.from_numpy(b).cuda()
+        tc = torch.from_numpy(np.array(c0, order="F")).cuda()
+        # torch .cuda() keeps strides for non-contiguous (Fortran) layouts? enforce explicitly
+        ta = torch.as_strided(ta.contiguous().t().contiguous().t(), (m, k), (1, m)) \
+            if ta.stride() != (1, m) else ta
+        ctx.gemm(v, L, 1.0, ta, tb, tc)
+        assert np.array_equal(tc.cpu().numpy(), host), (v, L)
+
+
+def test_run_to_run_bitwise_determinism(ctx):
+    # acceptance.cpp:202-217 analogue: tile ownership makes every C element's
+    # update order fixed, so repeated runs are bitwise identical.
+    m, n, k = 700, 650, 900
+    a, b, c0 = inputs(m, n, k, (21, 22, 23))
+    for v, L in CONFIGS:
+        r1 = run(ctx, v, L, 1.0, a, b, c0)
+        r2 = run(ctx, v, L, 1.0, a, b, c0)
+        assert np.array_equal(r1, r2), (v, L)
+
+
+def test_acceptance_random_shapes_up_to_1200(ctx):
+    # acceptance.cpp:52-80 (100 shapes in [1, 1200]; 24 here to bound CPU time),
+    # checked with the reference's 1e-10 criterion and the north-star normwise bound.
+    import random
+    for it in range(24):
+        rng = random.Random(1000 + it)
+        m, n, k = rng.randint(1, 1200), rng.randint(1, 1200), rng.randint(1, 1200)
+        al = [1.0, -1.0, 0.5][it % 3]
+        a, b, c0 = inputs(m, n, k, (3 * it + 1, 3 * it + 2, 3 * it + 3), "col")
+        ref = oracle_result("dgemm", 0, al, a, b, c0)
+        for v, L in CONFIGS:
+            got = run(ctx, v, L, al, a, b, c0)
+            assert O.rel_frobenius_error(np.ascontiguousarray(got), np.ascontiguousarray(ref)) \
+                <= 1e-10
+            check(v, L, got, ref, c0, a, b)
+
+
+def test_counters_through_the_abi(ctx):
+    # test_capi.cpp:117-136
+    c = S.Ctx()
+    c.enable_counters()
+    d = 64
+    a, b, _ = inputs(d, d, d, (6, 7, 8), "row")
+    out = np.zeros((d, d))
+    c.gemm("naive", 1, 1.0, a, b, out)
+    cv = c.counters()
+    assert (cv["a_plus_passes"], cv["b_plus_passes"], cv["c_plus_passes"]) == (19, 19, 36)
+    assert cv["kernel_fma_flops"] == 7 * 2 * 32 ** 3
+    c.reset_counters()
+    assert c.counters()["a_plus_passes"] == 0 and c.counters()["kernel_calls"] == 0
+
+
+def test_rank_b_schedule(ctx):
+    # test_bench.cpp:122-139 / bench_lib.cpp:56-71: C += sum_p A[:, p0:p0+b] B[p0:p0+b, :]
+    m = n = 160
+    k, bw = 256, 64
+    a, b, c0 = inputs(m, n, k, (31, 32, 33), "row")
+    ref = oracle_result("dgemm", 0, 1.0, a, b, c0, use_reference_gemm=True)
+    for v, L in [("abc", 1), ("abc", 2), ("ab", 2)]:
+        c = c0.copy()
+        for p0 in range(0, k, bw):
+            ctx.gemm(v, L, 1.0, a[:, p0:p0 + bw], b[p0:p0 + bw, :], c)
+        assert O.rel_frobenius_error(c, ref) < 1e-10
+
+
+def test_dgemm_shim_beta_and_transposes(ctx):
+    m, n, k = 90, 70, 110
+    a, b, c0 = inputs(m, n, k, (41, 42, 43))
+    for beta in (0.0, 1.0, 2.5):
+        for ta in ("N", "T"):
+            am = np.asfortranarray(a.T) if ta == "T" else a
+            c = np.array(c0, order="F")
+            ctx.dgemm("abc", 2, ta, "N", m, n, k, 0.75, am, am.shape[0], b, k, beta, c, m)
+            want = np.array(c0, order="F") * beta if beta != 0.0 else np.zeros((m, n), order="F")
+            O.reference_gemm(0.75, a, b, want)
+            assert O.rel_frobenius_error(c, want) < 1e-11
+
+
+def test_stream_ordered_device_entry(ctx):
+    import torch
+    m = n = k = 512
+    a, b, c0 = inputs(m, n, k, (51, 52, 53))
+    ta = torch.from_numpy(np.ascontiguousarray(a.T)).cuda().t()
+    tb = torch.from_numpy(np.ascontiguousarray(b.T)).cuda().t()
+    tc = torch.from_numpy(np.ascontiguousarray(c0.T)).cuda().t()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        ctx.gemm_device("abc", 2, 1.0, ta, tb, tc, stream=s)
+    s.synchronize()
+    ref = oracle_result("dgemm", 0, 1.0, a, b, c0)
+    check("abc", 2, tc.cpu().numpy(), ref, c0, a, b)
+
+
+@pytest.mark.parametrize("dim", [4096, 4097])
+def test_full_size_strassen_vs_classical(ctx, dim):
+    """Size-independent checks at sweep sizes: Strassen vs the GPU classical
+    kernel (normwise) and a long-double Freivalds check against the inputs."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(dim)
+    A = torch.rand(dim, dim, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    B = torch.rand(dim, dim, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    C0 = torch.rand(dim, dim, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
+    A, B, C0 = (x.t().contiguous().t() for x in (A, B, C0))  # column-major
+    base = C0.clone()
+    ctx.gemm_device("dgemm", 0, 1.0, A, B, base)
+    torch.cuda.synchronize()
+    an, bn = torch.linalg.norm(A).item(), torch.linalg.norm(B).item()
+    a_h, b_h, c0_h = A.cpu().numpy(), B.cpu().numpy(), C0.cpu().numpy()
+    assert freivalds(1.0, a_h, b_h, c0_h, base.cpu().numpy()) < 1e-15
+    for v, L in [("abc", 1), ("abc", 2), ("ab", 2)]:
+        C = C0.clone()
+        ctx.gemm_device(v, L, 1.0, A, B, C)
+        torch.cuda.synchronize()
+        nw = (torch.linalg.norm(C - base) / (an * bn)).item()
+        assert nw <= (1e-12 if L == 1 else 5e-12), (v, L, nw)
+        assert freivalds(1.0, a_h, b_h, c0_h, C.cpu().numpy()) < 1e-14
