@@ -157,7 +157,7 @@ const char* strassen_status_str(strassen_status s);  /* capi.cpp:225-235 */
 /* ============================ PART 2: B200 additions ======================= */
 
 /* Device-pointer entry on a caller-provided CUDA stream (cudaStream_t passed
- * as void*; NULL = the ctx stream).  A, B, C must be device (or managed)
+ * as void*, used exactly; NULL = the CUDA legacy default stream).  A, B, C must be device (or managed)
  * memory.  Asynchronous: returns after enqueueing; C is updated in stream
  * order.  Same validation and semantics as strassen_gemm. */
 strassen_status strassen_gemm_device(strassen_ctx* ctx, void* stream, strassen_variant variant,
@@ -175,7 +175,8 @@ strassen_status strassen_dgemm(strassen_ctx* ctx, strassen_variant variant, int 
                                long lda, const double* b, long ldb, double beta, double* c,
                                long ldc);
 
-/* Stream used by strassen_gemm / strassen_dgemm (cudaStream_t as void*). */
+/* Stream used by strassen_gemm / strassen_dgemm (cudaStream_t as void*);
+ * default (and NULL) = the CUDA legacy default stream. */
 strassen_status strassen_ctx_set_stream(strassen_ctx* ctx, void* stream);
 
 /* Number of CUDA kernels the last compute call on this ctx launched. */

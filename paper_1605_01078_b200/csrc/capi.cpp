@@ -107,7 +107,8 @@ sb200::DView stage_in(sb200::Engine& e, cudaStream_t s, const double* p, long ro
     return v;
 }
 
-strassen_status gemm_impl(strassen_ctx* ctx, cudaStream_t user_stream, bool device_only,
+strassen_status gemm_impl(strassen_ctx* ctx, bool explicit_stream, cudaStream_t user_stream,
+                          bool device_only,
                           strassen_variant variant, int level, long m, long n, long k,
                           double alpha, const double* a, long rs_a, long cs_a, const double* b,
                           long rs_b, long cs_b, double* c, long rs_c, long cs_c, bool has_beta,
@@ -118,7 +119,7 @@ strassen_status gemm_impl(strassen_ctx* ctx, cudaStream_t user_stream, bool devi
         validate_call(variant, m, n, k, ctx->blocking);
         sb200::Engine& e = ctx->engine;
         e.init();
-        cudaStream_t s = user_stream ? user_stream : e.stream();
+        cudaStream_t s = explicit_stream ? user_stream : e.stream();
         long launches = 0;
         bool sa = false, sb = false, sc = false;
         const sb200::DView A = stage_in(e, s, a, m, k, rs_a, cs_a, e.stage_a, true, sa);
@@ -201,16 +202,16 @@ strassen_status strassen_gemm(strassen_ctx* ctx, strassen_variant variant, int l
                               long n, long k, double alpha, const double* a, long rs_a, long cs_a,
                               const double* b, long rs_b, long cs_b, double* c, long rs_c,
                               long cs_c) {
-    return gemm_impl(ctx, nullptr, false, variant, level, m, n, k, alpha, a, rs_a, cs_a, b, rs_b,
-                     cs_b, c, rs_c, cs_c, false, 1.0);
+    return gemm_impl(ctx, false, nullptr, false, variant, level, m, n, k, alpha, a, rs_a, cs_a, b,
+                     rs_b, cs_b, c, rs_c, cs_c, false, 1.0);
 }
 
 strassen_status strassen_gemm_device(strassen_ctx* ctx, void* stream, strassen_variant variant,
                                      int level, long m, long n, long k, double alpha,
                                      const double* a, long rs_a, long cs_a, const double* b,
                                      long rs_b, long cs_b, double* c, long rs_c, long cs_c) {
-    return gemm_impl(ctx, static_cast<cudaStream_t>(stream), true, variant, level, m, n, k, alpha,
-                     a, rs_a, cs_a, b, rs_b, cs_b, c, rs_c, cs_c, false, 1.0);
+    return gemm_impl(ctx, true, static_cast<cudaStream_t>(stream), true, variant, level, m, n, k,
+                     alpha, a, rs_a, cs_a, b, rs_b, cs_b, c, rs_c, cs_c, false, 1.0);
 }
 
 strassen_status strassen_dgemm(strassen_ctx* ctx, strassen_variant variant, int level, char transa,
@@ -232,8 +233,8 @@ strassen_status strassen_dgemm(strassen_ctx* ctx, strassen_variant variant, int 
     // a transpose is the stride swap (reference strassen.h:1-6).
     const long rs_a = ta ? lda : 1, cs_a = ta ? 1 : lda;
     const long rs_b = tb ? ldb : 1, cs_b = tb ? 1 : ldb;
-    return gemm_impl(ctx, nullptr, false, variant, level, m, n, k, alpha, a, rs_a, cs_a, b, rs_b,
-                     cs_b, c, 1, ldc, true, beta);
+    return gemm_impl(ctx, false, nullptr, false, variant, level, m, n, k, alpha, a, rs_a, cs_a, b,
+                     rs_b, cs_b, c, 1, ldc, true, beta);
 }
 
 strassen_status strassen_ctx_set_stream(strassen_ctx* ctx, void* stream) {

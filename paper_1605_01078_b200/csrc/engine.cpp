@@ -169,7 +169,6 @@ Engine::~Engine() {
     if (!initialised) return;
     for (DeviceBuffer* b : {&stage_a, &stage_b, &stage_c, &pack_a, &pack_b, &mbuf, &tabuf, &tbbuf})
         if (b->ptr) cudaFree(b->ptr);
-    if (own_stream) cudaStreamDestroy(own_stream);
 }
 
 void Engine::init() {
@@ -178,11 +177,13 @@ void Engine::init() {
     if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
         throw Error(STRASSEN_ERR_DEVICE, "no CUDA device");
     ck(cudaGetDevice(&device), "cudaGetDevice");
-    ck(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
     initialised = true;
 }
 
-cudaStream_t Engine::stream() { return has_user_stream ? user_stream : own_stream; }
+// The synchronous entry points run on the ctx stream: the one set with
+// strassen_ctx_set_stream, else the CUDA legacy default stream (which orders
+// against the caller's work on other blocking streams).
+cudaStream_t Engine::stream() { return has_user_stream ? user_stream : nullptr; }
 
 double* Engine::ensure(DeviceBuffer& b, size_t bytes) {
     if (bytes == 0) bytes = 8;

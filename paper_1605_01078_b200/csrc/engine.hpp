@@ -32,7 +32,6 @@ struct DeviceBuffer {
 struct Engine {
     int device = -1;
     bool initialised = false;
-    cudaStream_t own_stream = nullptr;
     cudaStream_t user_stream = nullptr;
     bool has_user_stream = false;
     DeviceBuffer stage_a, stage_b, stage_c;   // host-operand staging

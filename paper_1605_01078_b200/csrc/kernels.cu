@@ -76,35 +76,60 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
+// Negate a double by flipping its sign bit with an integer op (keeps the
+// FP64 pipe, which DMMA saturates, free).
+__device__ __forceinline__ double flip_sign(double x, uint32_t neg) {
+    return __hiloint2double(__double2hiint(x) ^ static_cast<int>(neg << 31), __double2loint(x));
+}
+
 // Operand sum of one 2048-double tile into a stage buffer:
-// dst := sum_u c_u raw(slot_u), accumulated left to right like pack_a_sum /
-// pack_b_sum (blocking.cpp:24-28).  c_u = +-1 so fma(c, x, acc) rounds
-// exactly like acc + c*x; a single +1 term is a plain copy (no FP64 op).
-// All buffers are 1024-byte aligned and share the TMA box geometry, so the
-// elementwise sum at equal offsets preserves the (swizzled) layout.
-__device__ __forceinline__ const double2* raw_tile(const uint8_t* raw, uint32_t q) {
-    return reinterpret_cast<const double2*>(raw + (q % kRawSlots) * kSlotBytes);
+// dst := sum_u c_u raw(q0 + u), accumulated left to right like pack_a_sum /
+// pack_b_sum (blocking.cpp:24-28); c_u = +-1 is applied as a sign flip so
+// acc + c_u*x is one DADD, rounding exactly like the reference.  All buffers
+// are 1024-byte aligned and share the TMA box geometry, so the elementwise
+// sum at equal offsets preserves the (swizzled) layout.  N is the number of
+// terms (compile time), neg bit u = (c_u < 0).
+template <int N>
+__device__ __forceinline__ void sum_tile_n(const uint8_t* raw, uint32_t q0, uint32_t neg,
+                                           double2* __restrict__ dst, int t) {
+    constexpr int kVec = kSlotBytes / 16;           // 1024 double2 per tile
+    constexpr int kT = kSummerWarps * 32;           // 96 summing threads
+    constexpr int kIter = (kVec + kT - 1) / kT;     // 11
+    const double2* src[N];
+#pragma unroll
+    for (int u = 0; u < N; ++u)
+        src[u] = reinterpret_cast<const double2*>(raw + ((q0 + u) % kRawSlots) * kSlotBytes);
+#pragma unroll 4
+    for (int it = 0; it < kIter; ++it) {
+        const int idx = t + it * kT;
+        if (idx < kVec) {
+            double2 v = src[0][idx];
+            if (N == 1 && neg == 0) {
+                dst[idx] = v;
+                continue;
+            }
+            v.x = flip_sign(v.x, neg & 1);
+            v.y = flip_sign(v.y, neg & 1);
+#pragma unroll
+            for (int u = 1; u < N; ++u) {
+                const double2 w = src[u][idx];
+                v.x += flip_sign(w.x, (neg >> u) & 1);
+                v.y += flip_sign(w.y, (neg >> u) & 1);
+            }
+            dst[idx] = v;
+        }
+    }
 }
 
 __device__ __forceinline__ void sum_tile(const uint8_t* raw, uint32_t q0, int n,
                                          const int8_t* coef, double2* dst, int t) {
-    if (n == 1 && coef[0] == 1) {
-        const double2* src = raw_tile(raw, q0);
-        for (int idx = t; idx < kSlotBytes / 16; idx += kSummerWarps * 32) dst[idx] = src[idx];
-        return;
-    }
-    for (int idx = t; idx < kSlotBytes / 16; idx += kSummerWarps * 32) {
-        double2 v = raw_tile(raw, q0)[idx];
-        const double c0 = coef[0];
-        v.x *= c0;
-        v.y *= c0;
-        for (int u = 1; u < n; ++u) {
-            const double2 w = raw_tile(raw, q0 + u)[idx];
-            const double cu = coef[u];
-            v.x = fma(cu, w.x, v.x);
-            v.y = fma(cu, w.y, v.y);
-        }
-        dst[idx] = v;
+    uint32_t neg = 0;
+    for (int u = 0; u < n; ++u) neg |= (coef[u] < 0 ? 1u : 0u) << u;
+    switch (n) {
+        case 1: sum_tile_n<1>(raw, q0, neg, dst, t); break;
+        case 2: sum_tile_n<2>(raw, q0, neg, dst, t); break;
+        case 3: sum_tile_n<3>(raw, q0, neg, dst, t); break;
+        default: sum_tile_n<4>(raw, q0, neg, dst, t); break;
     }
 }
 
@@ -145,9 +170,10 @@ __device__ __forceinline__ void mma_step(const double* __restrict__ sA,
 }
 
 __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__ MMParams P) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* raw = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-byte alignment (128B-swizzle atoms) by offsetting the shared array
+    // itself, so every derived pointer stays in the shared address space (LDS/STS).
+    uint8_t* raw = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* stage = raw + kRawSlots * kSlotBytes;  // [kStages][A | B]
     uint64_t* raw_full = reinterpret_cast<uint64_t*>(stage + 2 * kStages * kSlotBytes);
     uint64_t* raw_empty = raw_full + kRawSlots;
@@ -181,10 +207,16 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     }
     __syncthreads();
 
-    if (warp < 4) {
+    // Warp roles: warps 0-7 (warpgroups 0-1) run the DMMA mainloop; warps
+    // 8-11 (warpgroup 2) are the producer (TMA) and operand-sum warps.  The
+    // sum warps get the highest warp ids because the SMSP issue arbiter is
+    // highest-warp-id first and their DFMAs share the FP64 pipe with DMMA:
+    // with lower ids they starve behind the DMMA warps (measured: ABC L1 ran
+    // at half speed).
+    if (warp >= kConsumerWarps) {
         // ================= producer warpgroup ================================
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
-        if (warp == 0) {
+        if (warp == kConsumerWarps) {
             // TMA issue: one elected lane walks products x k-steps x terms
             if (lane == 0) {
                 uint32_t q = 0;
@@ -209,7 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             }
         } else {
             // operand-sum warps: raw term tiles -> summed (A, B) stage
-            const int t = threadIdx.x - 32;
+            const int t = threadIdx.x - (kConsumerWarps + 1) * 32;
             uint32_t q = 0, T = 0;
             for (int p = 0; p < P.nprod; ++p) {
                 const ProductDesc& pd = P.prod[p];
@@ -238,7 +270,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
 
     // ================= consumer warpgroups: DMMA mainloop + epilogue =========
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kConsumerRegs));
-    const int cw = warp - 4;
+    const int cw = warp;
     const int wm = cw & 1, wn = cw >> 1;
     const int g = lane >> 2, j = lane & 3;
     uint32_t T = 0;

@@ -21,8 +21,13 @@ constexpr int kThreads = 128 + kConsumerWarps * 32;  // 384
 constexpr int kSlotBytes = kBM * kBK * 8;            // one 128x16 fp64 operand tile (16 KB)
 constexpr int kRawSlots = 8;                         // TMA ring of raw operand-term tiles
 constexpr int kStages = 2;                           // summed (A, B) operand stages
-constexpr int kProducerRegs = 56;                    // setmaxnreg split (per SMSP:
-constexpr int kConsumerRegs = 224;                   //  32*56 + 2*32*224 <= 16384)
+constexpr int kProducerRegs = 56;                    // setmaxnreg split
+constexpr int kConsumerRegs = 224;
+// setmaxnreg moves registers inside the CTA's launch allocation (384 threads x
+// 168 = 64512): the consumers' increase must be covered by the producers'
+// release or setmaxnreg.inc waits forever.
+static_assert(kProducerRegs * 128 + kConsumerRegs * kConsumerWarps * 32 <= kThreads * 168,
+              "setmaxnreg split exceeds the CTA register allocation");
 constexpr int kMMSmemBytes = (kRawSlots + 2 * kStages) * kSlotBytes + 1024 + 1024;
 
 // One Strassen product M_p = (sum_u as_u A_{aq_u}) (sum_u bs_u B_{bq_u});
