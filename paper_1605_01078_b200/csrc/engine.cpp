@@ -280,7 +280,13 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
     if (variant == STRASSEN_DGEMM || variant == STRASSEN_ABC) {
         P.mode = kEpiRMW;
         P.nprod = static_cast<int>(live.size());
-        for (size_t p = 0; p < live.size(); ++p) fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);
+        P.direct = 1;
+        for (size_t p = 0; p < live.size(); ++p) {
+            fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);
+            if (live[p].a.size() != 1 || live[p].b.size() != 1 || live[p].a[0].second != 1 ||
+                live[p].b[0].second != 1)
+                P.direct = 0;
+        }
         ck(launch_mm(P, s), "mm_kernel");
         return launches + 1;
     }
@@ -313,6 +319,7 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
         double* M = e.ensure(e.mbuf, static_cast<size_t>(mstride) * live.size() * 8);
         P.mbase = M;
         P.nprod = static_cast<int>(live.size());
+        P.direct = 0;
         for (size_t p = 0; p < live.size(); ++p) {
             fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);
             for (const auto& [q, g] : live[p].c) {
@@ -337,6 +344,7 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
     encode_map(&Q.tmA[0], TA, qm, qk, lda_t, kBM, kBK, false);
     encode_map(&Q.tmB[0], TB, qk, qn, ldb_t, kBK, kBN, true);
     Q.nprod = 1;
+    Q.direct = 1;
     Q.mbase = M;
     const Terms one = {{0, 1}};
     fill_desc(Q.prod[0], one, one, one);

@@ -65,6 +65,10 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+__device__ __forceinline__ void consumer_bar() {
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+}
+
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -82,90 +86,77 @@ __device__ __forceinline__ double flip_sign(double x, uint32_t neg) {
     return __hiloint2double(__double2hiint(x) ^ static_cast<int>(neg << 31), __double2loint(x));
 }
 
-// Operand sum of one 2048-double tile into a stage buffer:
-// dst := sum_u c_u raw(q0 + u), accumulated left to right like pack_a_sum /
-// pack_b_sum (blocking.cpp:24-28); c_u = +-1 is applied as a sign flip so
-// acc + c_u*x is one DADD, rounding exactly like the reference.  All buffers
-// are 1024-byte aligned and share the TMA box geometry, so the elementwise
-// sum at equal offsets preserves the (swizzled) layout.  N is the number of
-// terms (compile time), neg bit u = (c_u < 0).
-template <int N>
-__device__ __forceinline__ void sum_tile_n(const uint8_t* raw, uint32_t q0, uint32_t neg,
-                                           double2* __restrict__ dst, int t) {
-    constexpr int kVec = kSlotBytes / 16;           // 1024 double2 per tile
-    constexpr int kT = kSummerWarps * 32;           // 96 summing threads
-    constexpr int kIter = (kVec + kT - 1) / kT;     // 11
-    const double2* src[N];
-#pragma unroll
-    for (int u = 0; u < N; ++u)
-        src[u] = reinterpret_cast<const double2*>(raw + ((q0 + u) % kRawSlots) * kSlotBytes);
-#pragma unroll 4
-    for (int it = 0; it < kIter; ++it) {
-        const int idx = t + it * kT;
-        if (idx < kVec) {
-            double2 v = src[0][idx];
-            if (N == 1 && neg == 0) {
-                dst[idx] = v;
-                continue;
-            }
-            v.x = flip_sign(v.x, neg & 1);
-            v.y = flip_sign(v.y, neg & 1);
-#pragma unroll
-            for (int u = 1; u < N; ++u) {
-                const double2 w = src[u][idx];
-                v.x += flip_sign(w.x, (neg >> u) & 1);
-                v.y += flip_sign(w.y, (neg >> u) & 1);
-            }
-            dst[idx] = v;
-        }
-    }
-}
-
-__device__ __forceinline__ void sum_tile(const uint8_t* raw, uint32_t q0, int n,
-                                         const int8_t* coef, double2* dst, int t) {
-    uint32_t neg = 0;
-    for (int u = 0; u < n; ++u) neg |= (coef[u] < 0 ? 1u : 0u) << u;
-    switch (n) {
-        case 1: sum_tile_n<1>(raw, q0, neg, dst, t); break;
-        case 2: sum_tile_n<2>(raw, q0, neg, dst, t); break;
-        case 3: sum_tile_n<3>(raw, q0, neg, dst, t); break;
-        default: sum_tile_n<4>(raw, q0, neg, dst, t); break;
-    }
-}
-
-// One 128x128x16 step for a 64x32 warp tile.
-// A slot: TMA box {128 m, 16 k}, no swizzle: double (m, k) at k*128 + m.
-// B slot: TMA box {16 k, 128 n}, 128B swizzle: double (k, n) at byte
+// One DMMA k-substep s (of 4) of a 128x128x16 stage for a 64x32 warp tile:
+// 8 (m) x 4 (n) DMMA.8 = 32 instructions.
+// A tile: TMA box {128 m, 16 k}, no swizzle: double (m, k) at k*128 + m.
+// B tile: TMA box {16 k, 128 n}, 128B swizzle: double (k, n) at byte
 //         n*128 + (((k>>1) ^ (n&7)) << 4) + (k&1)*8.
-// The 16 k of the step are split over 4 DMMA k-steps s with physical
+// The 16 k of a stage are split over the 4 substeps with physical
 // k = 4*j + s for lane slot j = lane&3 (A and B agree, so the sum over k is
 // unchanged); A rows are permuted so lane group g = lane>>2 reads rows
 // 16h + 2g + {0,1} of fragments 2h, 2h+1 with one 16-byte load.  Both
 // patterns are bank-conflict free (4 wavefronts per 512-byte warp load).
-__device__ __forceinline__ void mma_step(const double* __restrict__ sA,
-                                         const uint8_t* __restrict__ sB, double (&acc)[8][4][2],
-                                         int wm, int wn, int g, int j) {
-    const double* pa = sA + 4 * j * kBM + wm * 64 + 2 * g;
-    const uint8_t* pb = sB + (wn * 32 + g) * 128;
+__device__ __forceinline__ void mma_substep(const double* __restrict__ sA,
+                                            const uint8_t* __restrict__ sB,
+                                            double (&acc)[8][4][2], int s, int wm, int wn, int g,
+                                            int j) {
+    const double* pa = sA + (4 * j + s) * kBM + wm * 64 + 2 * g;
+    const uint8_t* pb = sB + (wn * 32 + g) * 128 + (((2 * j + (s >> 1)) ^ g) << 4) + (s & 1) * 8;
+    double a[8], b[4];
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
-        double a[8], b[4];
+    for (int h = 0; h < 4; ++h) {
+        const double2 v = *reinterpret_cast<const double2*>(pa + 16 * h);
+        a[2 * h] = v.x;
+        a[2 * h + 1] = v.y;
+    }
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-            const double2 v = *reinterpret_cast<const double2*>(pa + s * kBM + 16 * h);
-            a[2 * h] = v.x;
-            a[2 * h + 1] = v.y;
-        }
+    for (int nf = 0; nf < 4; ++nf) b[nf] = *reinterpret_cast<const double*>(pb + nf * 8 * 128);
 #pragma unroll
-        for (int nf = 0; nf < 4; ++nf) {
-            // n = wn*32 + 8nf + g, so n & 7 == g; k = 4j + s
-            const int chunk = (2 * j + (s >> 1)) ^ g;
-            b[nf] = *reinterpret_cast<const double*>(pb + nf * 8 * 128 + chunk * 16 + (s & 1) * 8);
-        }
+    for (int mf = 0; mf < 8; ++mf)
 #pragma unroll
-        for (int mf = 0; mf < 8; ++mf)
+        for (int nf = 0; nf < 4; ++nf) dmma(acc[mf][nf][0], acc[mf][nf][1], a[mf], b[nf]);
+}
+
+// Operand staging job of one k-step: for each side (A, B), the raw TMA term
+// tiles (shared memory) and their signs; the result goes to a stage buffer.
+// The sum is formed by the 256 DMMA threads, one 16-byte vector per tile per
+// chunk (4 chunks per stage), left to right like pack_a_sum / pack_b_sum
+// (blocking.cpp:24-28): c_u = +-1 is a sign flip, so acc + c_u*x is one DADD
+// with exactly the reference's rounding.  A single +1 term is a copy.
+struct SumJob {
+    const double2* src[2][kMaxTerms];
+    double2* dst[2];
+    int n[2];
+    uint32_t neg[2];
+};
+
+__device__ __forceinline__ void sum_load(const SumJob& J, int chunk, int tid,
+                                         double2 (&v)[2][kMaxTerms]) {
+    const int idx = chunk * (kConsumerWarps * 32) + tid;
 #pragma unroll
-            for (int nf = 0; nf < 4; ++nf) dmma(acc[mf][nf][0], acc[mf][nf][1], a[mf], b[nf]);
+    for (int side = 0; side < 2; ++side)
+#pragma unroll
+        for (int u = 0; u < kMaxTerms; ++u)
+            if (u < J.n[side]) v[side][u] = J.src[side][u][idx];
+}
+
+__device__ __forceinline__ void sum_store(const SumJob& J, int chunk, int tid,
+                                          const double2 (&v)[2][kMaxTerms]) {
+    const int idx = chunk * (kConsumerWarps * 32) + tid;
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+        if (J.n[side] == 0) continue;
+        const uint32_t neg = J.neg[side];
+        double2 acc;
+        acc.x = flip_sign(v[side][0].x, neg & 1);
+        acc.y = flip_sign(v[side][0].y, neg & 1);
+#pragma unroll
+        for (int u = 1; u < kMaxTerms; ++u)
+            if (u < J.n[side]) {
+                acc.x += flip_sign(v[side][u].x, (neg >> u) & 1);
+                acc.y += flip_sign(v[side][u].y, (neg >> u) & 1);
+            }
+        J.dst[side][idx] = acc;
     }
 }
 
@@ -177,11 +168,12 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     uint8_t* stage = raw + kRawSlots * kSlotBytes;  // [kStages][A | B]
     uint64_t* raw_full = reinterpret_cast<uint64_t*>(stage + 2 * kStages * kSlotBytes);
     uint64_t* raw_empty = raw_full + kRawSlots;
-    uint64_t* st_full = raw_empty + kRawSlots;
-    uint64_t* st_empty = st_full + kStages;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    // direct: every product is a single +1 term on both sides (the classical
+    // DGEMM program): the mainloop reads the TMA slots in place.
+    const bool direct = P.direct != 0;
 
     // grouped rasterisation: group_m tile rows share B column panels in L2
     const int bid = blockIdx.x;
@@ -196,148 +188,211 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     if (threadIdx.x == 0) {
         for (int s = 0; s < kRawSlots; ++s) {
             mbar_init(&raw_full[s], 1);
-            mbar_init(&raw_empty[s], kSummerWarps);
-        }
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&st_full[s], kSummerWarps);
-            mbar_init(&st_empty[s], kConsumerWarps);
+            mbar_init(&raw_empty[s], direct ? kConsumerWarps : 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
     }
     __syncthreads();
 
-    // Warp roles: warps 0-7 (warpgroups 0-1) run the DMMA mainloop; warps
-    // 8-11 (warpgroup 2) are the producer (TMA) and operand-sum warps.  The
-    // sum warps get the highest warp ids because the SMSP issue arbiter is
-    // highest-warp-id first and their DFMAs share the FP64 pipe with DMMA:
-    // with lower ids they starve behind the DMMA warps (measured: ABC L1 ran
-    // at half speed).
     if (warp >= kConsumerWarps) {
-        // ================= producer warpgroup ================================
+        // ================= producer warpgroup (warps 8-11) ===================
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
-        if (warp == kConsumerWarps) {
+        if (warp == kConsumerWarps && lane == 0) {
             // TMA issue: one elected lane walks products x k-steps x terms
-            if (lane == 0) {
-                uint32_t q = 0;
-                const int m0 = tm * kBM, n0 = tn * kBN;
-                for (int p = 0; p < P.nprod; ++p) {
-                    const ProductDesc& pd = P.prod[p];
-                    for (int kt = 0; kt < P.ktiles; ++kt) {
-                        const int k0 = kt * kBK;
-                        for (int u = 0; u < pd.na + pd.nb; ++u, ++q) {
-                            const uint32_t s = q % kRawSlots;
-                            mbar_wait(&raw_empty[s], ((q / kRawSlots) & 1) ^ 1);
-                            mbar_expect_tx(&raw_full[s], kSlotBytes);
-                            if (u < pd.na)
-                                tma_load_2d(raw + s * kSlotBytes, &P.tmA[pd.aq[u]], m0, k0,
-                                            &raw_full[s]);
-                            else
-                                tma_load_2d(raw + s * kSlotBytes, &P.tmB[pd.bq[u - pd.na]], k0, n0,
-                                            &raw_full[s]);
-                        }
-                    }
-                }
-            }
-        } else {
-            // operand-sum warps: raw term tiles -> summed (A, B) stage
-            const int t = threadIdx.x - (kConsumerWarps + 1) * 32;
-            uint32_t q = 0, T = 0;
+            uint32_t q = 0;
+            const int m0 = tm * kBM, n0 = tn * kBN;
             for (int p = 0; p < P.nprod; ++p) {
                 const ProductDesc& pd = P.prod[p];
-                const int na = pd.na, nb = pd.nb;
-                for (int kt = 0; kt < P.ktiles; ++kt, ++T) {
-                    const uint32_t st = T % kStages;
-                    mbar_wait(&st_empty[st], ((T / kStages) & 1) ^ 1);
-                    for (uint32_t u = q; u < q + na + nb; ++u)
-                        mbar_wait(&raw_full[u % kRawSlots], (u / kRawSlots) & 1);
-                    double2* dA = reinterpret_cast<double2*>(stage + (2 * st) * kSlotBytes);
-                    double2* dB = reinterpret_cast<double2*>(stage + (2 * st + 1) * kSlotBytes);
-                    sum_tile(raw, q, na, pd.as, dA, t);
-                    sum_tile(raw, q + na, nb, pd.bs, dB, t);
-                    __syncwarp();
-                    if (lane == 0) {
-                        for (uint32_t u = q; u < q + na + nb; ++u)
-                            mbar_arrive(&raw_empty[u % kRawSlots]);
-                        mbar_arrive(&st_full[st]);
+                for (int kt = 0; kt < P.ktiles; ++kt) {
+                    const int k0 = kt * kBK;
+                    for (int u = 0; u < pd.na + pd.nb; ++u, ++q) {
+                        const uint32_t s = q % kRawSlots;
+                        mbar_wait(&raw_empty[s], ((q / kRawSlots) & 1) ^ 1);
+                        mbar_expect_tx(&raw_full[s], kSlotBytes);
+                        if (u < pd.na)
+                            tma_load_2d(raw + s * kSlotBytes, &P.tmA[pd.aq[u]], m0, k0,
+                                        &raw_full[s]);
+                        else
+                            tma_load_2d(raw + s * kSlotBytes, &P.tmB[pd.bq[u - pd.na]], k0, n0,
+                                        &raw_full[s]);
                     }
-                    q += na + nb;
                 }
             }
         }
         return;
     }
 
-    // ================= consumer warpgroups: DMMA mainloop + epilogue =========
+    // ================= DMMA warpgroups (warps 0-7) ==========================
+    // Software pipeline per k-step T: the operand sums of step T+1 (raw TMA
+    // term tiles -> stage[(T+1) % 2]) are formed in 4 chunks interleaved with
+    // the 4 DMMA substeps of step T (chunk loads before, adds/stores after
+    // the 32 DMMAs), so their shared-memory and FP64-pipe latency hides under
+    // DMMA work; one named barrier per step publishes the stage and retires
+    // the raw slots.
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kConsumerRegs));
-    const int cw = warp;
-    const int wm = cw & 1, wn = cw >> 1;
+    const int wm = warp & 1, wn = warp >> 1;
     const int g = lane >> 2, j = lane & 3;
-    uint32_t T = 0;
+    const int tid = threadIdx.x;
     double acc[8][4][2];
 
-    for (int p = 0; p < P.nprod; ++p) {
-        const ProductDesc& pd = P.prod[p];
+    auto make_job = [&](const ProductDesc& pd, uint32_t q, uint32_t st, SumJob& J) {
+        const int n[2] = {pd.na, pd.nb};
+        const int8_t* c[2] = {pd.as, pd.bs};
 #pragma unroll
-        for (int mf = 0; mf < 8; ++mf)
+        for (int side = 0; side < 2; ++side) {
+            J.n[side] = n[side];
+            J.neg[side] = 0;
+            const uint32_t q0 = q + (side ? pd.na : 0);
 #pragma unroll
-            for (int nf = 0; nf < 4; ++nf) acc[mf][nf][0] = acc[mf][nf][1] = 0.0;
+            for (int u = 0; u < kMaxTerms; ++u) {
+                J.src[side][u] = reinterpret_cast<const double2*>(
+                    raw + ((q0 + u) % kRawSlots) * kSlotBytes);
+                if (u < n[side]) J.neg[side] |= (c[side][u] < 0 ? 1u : 0u) << u;
+            }
+            J.dst[side] = reinterpret_cast<double2*>(stage + (2 * st + side) * kSlotBytes);
+        }
+    };
+    auto wait_full = [&](uint32_t q0, int n) {
+        for (uint32_t u = q0; u < q0 + n; ++u) mbar_wait(&raw_full[u % kRawSlots], (u / kRawSlots) & 1);
+    };
 
-        for (int kt = 0; kt < P.ktiles; ++kt, ++T) {
-            const uint32_t st = T % kStages;
-            mbar_wait(&st_full[st], (T / kStages) & 1);
-            mma_step(reinterpret_cast<const double*>(stage + (2 * st) * kSlotBytes),
-                     stage + (2 * st + 1) * kSlotBytes, acc, wm, wn, g, j);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&st_empty[st]);
+    int p = 0, kt = 0;
+    uint32_t q = 0, T = 0;
+    if (!direct) {  // prologue: stage step 0
+        const ProductDesc& pd = P.prod[0];
+        SumJob J;
+        make_job(pd, 0, 0, J);
+        wait_full(0, pd.na + pd.nb);
+        for (int c = 0; c < 4; ++c) {
+            double2 v[2][kMaxTerms];
+            sum_load(J, c, tid, v);
+            sum_store(J, c, tid, v);
+        }
+        consumer_bar();
+        if (tid == 0)
+            for (uint32_t u = 0; u < static_cast<uint32_t>(pd.na + pd.nb); ++u)
+                mbar_arrive(&raw_empty[u % kRawSlots]);
+    }
+
+    while (true) {
+        const ProductDesc& pd = P.prod[p];
+        const uint32_t nq = pd.na + pd.nb;
+        int p1 = p, kt1 = kt + 1;
+        if (kt1 == P.ktiles) {
+            ++p1;
+            kt1 = 0;
+        }
+        const bool has1 = p1 < P.nprod;
+        const uint32_t q1 = q + nq;
+        const uint32_t st = T % kStages, st1 = (T + 1) % kStages;
+
+        const double* sA;
+        const uint8_t* sB;
+        if (direct) {
+            wait_full(q, 2);
+            sA = reinterpret_cast<const double*>(raw + (q % kRawSlots) * kSlotBytes);
+            sB = raw + ((q + 1) % kRawSlots) * kSlotBytes;
+        } else {
+            sA = reinterpret_cast<const double*>(stage + (2 * st) * kSlotBytes);
+            sB = stage + (2 * st + 1) * kSlotBytes;
+        }
+        if (kt == 0) {
+#pragma unroll
+            for (int mf = 0; mf < 8; ++mf)
+#pragma unroll
+                for (int nf = 0; nf < 4; ++nf) acc[mf][nf][0] = acc[mf][nf][1] = 0.0;
         }
 
-        // ---- epilogue: rows/cols of this lane's accumulator fragments
-        const int mrow0 = tm * kBM + wm * 64 + 2 * g;
-        const int ncol0 = tn * kBN + wn * 32 + 2 * j;
-        if (P.mode == kEpiRMW) {
-            for (int u = 0; u < pd.nc; ++u) {
-                const int cq = pd.cq[u];
-                double* __restrict__ C = P.cptr[cq];
-                const int R = P.crows[cq], Cc = P.ccols[cq];
-                const double sc = P.alpha * static_cast<double>(pd.cs[u]);
+        const bool stage1 = !direct && has1;
+        if (stage1) {
+            const ProductDesc& pd1 = P.prod[p1];
+            SumJob J;
+            make_job(pd1, q1, st1, J);
+            wait_full(q1, pd1.na + pd1.nb);
 #pragma unroll
-                for (int nf = 0; nf < 4; ++nf) {
-                    double cv[8][2];
-#pragma unroll
-                    for (int mf = 0; mf < 8; ++mf)
-#pragma unroll
-                        for (int e = 0; e < 2; ++e) {
-                            const int row = mrow0 + 16 * (mf >> 1) + (mf & 1);
-                            const int col = ncol0 + 8 * nf + e;
-                            cv[mf][e] = (row < R && col < Cc)
-                                            ? C[row * P.rs_c + col * P.cs_c]
-                                            : 0.0;
-                        }
-#pragma unroll
-                    for (int mf = 0; mf < 8; ++mf)
-#pragma unroll
-                        for (int e = 0; e < 2; ++e) {
-                            const int row = mrow0 + 16 * (mf >> 1) + (mf & 1);
-                            const int col = ncol0 + 8 * nf + e;
-                            if (row < R && col < Cc)
-                                C[row * P.rs_c + col * P.cs_c] = fma(sc, acc[mf][nf][e], cv[mf][e]);
-                        }
-                }
+            for (int s = 0; s < 4; ++s) {
+                double2 v[2][kMaxTerms];
+                sum_load(J, s, tid, v);
+                mma_substep(sA, sB, acc, s, wm, wn, g, j);
+                sum_store(J, s, tid, v);
             }
         } else {
-            double* __restrict__ M = P.mbase + p * P.mstride;
 #pragma unroll
-            for (int nf = 0; nf < 4; ++nf)
-#pragma unroll
-                for (int mf = 0; mf < 8; ++mf)
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int row = mrow0 + 16 * (mf >> 1) + (mf & 1);
-                        const int col = ncol0 + 8 * nf + e;
-                        if (row < P.qm && col < P.qn) M[row + col * P.ldm] = acc[mf][nf][e];
-                    }
+            for (int s = 0; s < 4; ++s) mma_substep(sA, sB, acc, s, wm, wn, g, j);
         }
+
+        if (direct) {
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&raw_empty[q % kRawSlots]);
+                mbar_arrive(&raw_empty[(q + 1) % kRawSlots]);
+            }
+        }
+
+        if (kt == P.ktiles - 1) {
+            // ---- epilogue of product p: rows/cols of this lane's fragments
+            const int mrow0 = tm * kBM + wm * 64 + 2 * g;
+            const int ncol0 = tn * kBN + wn * 32 + 2 * j;
+            if (P.mode == kEpiRMW) {
+                for (int u = 0; u < pd.nc; ++u) {
+                    const int cq = pd.cq[u];
+                    double* __restrict__ C = P.cptr[cq];
+                    const int R = P.crows[cq], Cc = P.ccols[cq];
+                    const double sc = P.alpha * static_cast<double>(pd.cs[u]);
+#pragma unroll
+                    for (int nf = 0; nf < 4; ++nf) {
+                        double cv[8][2];
+#pragma unroll
+                        for (int mf = 0; mf < 8; ++mf)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                const int row = mrow0 + 16 * (mf >> 1) + (mf & 1);
+                                const int col = ncol0 + 8 * nf + e;
+                                cv[mf][e] = (row < R && col < Cc) ? C[row * P.rs_c + col * P.cs_c]
+                                                                  : 0.0;
+                            }
+#pragma unroll
+                        for (int mf = 0; mf < 8; ++mf)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                const int row = mrow0 + 16 * (mf >> 1) + (mf & 1);
+                                const int col = ncol0 + 8 * nf + e;
+                                if (row < R && col < Cc)
+                                    C[row * P.rs_c + col * P.cs_c] =
+                                        fma(sc, acc[mf][nf][e], cv[mf][e]);
+                            }
+                    }
+                }
+            } else {
+                double* __restrict__ M = P.mbase + p * P.mstride;
+#pragma unroll
+                for (int nf = 0; nf < 4; ++nf)
+#pragma unroll
+                    for (int mf = 0; mf < 8; ++mf)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int row = mrow0 + 16 * (mf >> 1) + (mf & 1);
+                            const int col = ncol0 + 8 * nf + e;
+                            if (row < P.qm && col < P.qn) M[row + col * P.ldm] = acc[mf][nf][e];
+                        }
+            }
+        }
+
+        if (stage1) {
+            // step T+1 is staged and every warp is done with step T
+            consumer_bar();
+            if (tid == 0) {
+                const ProductDesc& pd1 = P.prod[p1];
+                for (uint32_t u = q1; u < q1 + pd1.na + pd1.nb; ++u)
+                    mbar_arrive(&raw_empty[u % kRawSlots]);
+            }
+        }
+        if (!has1) break;
+        p = p1;
+        kt = kt1;
+        q = q1;
+        ++T;
     }
 }
 

@@ -16,19 +16,19 @@ constexpr int kMaxQuad = 16;        // 2^L x 2^L quadrants, L <= 2
 constexpr int kMaxProducts = 49;    // 7^L
 constexpr int kMaxTerms = 4;        // operand terms / destinations per product at L <= 2
 constexpr int kConsumerWarps = 8;   // 2 warpgroups; 2 (m) x 4 (n) warps of 64 x 32
-constexpr int kSummerWarps = 3;     // producer warpgroup: 1 TMA warp + 3 operand-sum warps
-constexpr int kThreads = 128 + kConsumerWarps * 32;  // 384
+constexpr int kThreads = 128 + kConsumerWarps * 32;  // 384: + TMA warpgroup (1 active warp)
 constexpr int kSlotBytes = kBM * kBK * 8;            // one 128x16 fp64 operand tile (16 KB)
-constexpr int kRawSlots = 8;                         // TMA ring of raw operand-term tiles
+constexpr int kRawSlots = 9;                         // TMA ring of raw operand-term tiles
 constexpr int kStages = 2;                           // summed (A, B) operand stages
-constexpr int kProducerRegs = 56;                    // setmaxnreg split
-constexpr int kConsumerRegs = 224;
+constexpr int kProducerRegs = 24;                    // setmaxnreg split
+constexpr int kConsumerRegs = 240;
 // setmaxnreg moves registers inside the CTA's launch allocation (384 threads x
 // 168 = 64512): the consumers' increase must be covered by the producers'
 // release or setmaxnreg.inc waits forever.
 static_assert(kProducerRegs * 128 + kConsumerRegs * kConsumerWarps * 32 <= kThreads * 168,
               "setmaxnreg split exceeds the CTA register allocation");
-constexpr int kMMSmemBytes = (kRawSlots + 2 * kStages) * kSlotBytes + 1024 + 1024;
+constexpr int kMMSmemBytes = (kRawSlots + 2 * kStages) * kSlotBytes + 1024 + 256;
+static_assert(kMMSmemBytes <= 227 * 1024, "shared memory budget");
 
 // One Strassen product M_p = (sum_u as_u A_{aq_u}) (sum_u bs_u B_{bq_u});
 // destinations C_{cq_u} += alpha * cs_u * M_p.
@@ -61,6 +61,7 @@ struct alignas(64) MMParams {
     int tiles_m, tiles_n, ktiles;
     int mode;
     int group_m;                // tile rasterisation group height
+    int direct;                 // every product is a single +1 term on both sides
 };
 
 cudaError_t launch_mm(const MMParams& p, cudaStream_t s);
