@@ -246,7 +246,7 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
             const int qi = I * side + J;
             if (a_live[qi])
                 encode_map(&P.tmA[qi], quad_origin(ta, I, J), quad_rows(ta, I), quad_cols(ta, J),
-                           ta.ld, kBM, kBK, false);
+                           ta.ld, 16, kBK, true);
             if (b_live[qi])
                 encode_map(&P.tmB[qi], quad_origin(tb, I, J), quad_rows(tb, I), quad_cols(tb, J),
                            tb.ld, kBK, kBN, true);
@@ -341,7 +341,7 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
     double* TB = e.ensure(e.tbbuf, static_cast<size_t>(ldb_t) * qn * 8);
     double* M = e.ensure(e.mbuf, static_cast<size_t>(mstride) * 8);
     MMParams Q = P;
-    encode_map(&Q.tmA[0], TA, qm, qk, lda_t, kBM, kBK, false);
+    encode_map(&Q.tmA[0], TA, qm, qk, lda_t, 16, kBK, true);
     encode_map(&Q.tmB[0], TB, qk, qn, ldb_t, kBK, kBN, true);
     Q.nprod = 1;
     Q.direct = 1;

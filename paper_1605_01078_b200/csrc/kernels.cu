@@ -86,35 +86,57 @@ __device__ __forceinline__ double flip_sign(double x, uint32_t neg) {
     return __hiloint2double(__double2hiint(x) ^ static_cast<int>(neg << 31), __double2loint(x));
 }
 
-// One DMMA k-substep s (of 4) of a 128x128x16 stage for a 64x32 warp tile:
-// 8 (m) x 4 (n) DMMA.8 = 32 instructions.
-// A tile: TMA box {128 m, 16 k}, no swizzle: double (m, k) at k*128 + m.
-// B tile: TMA box {16 k, 128 n}, 128B swizzle: double (k, n) at byte
-//         n*128 + (((k>>1) ^ (n&7)) << 4) + (k&1)*8.
-// The 16 k of a stage are split over the 4 substeps with physical
-// k = 4*j + s for lane slot j = lane&3 (A and B agree, so the sum over k is
-// unchanged); A rows are permuted so lane group g = lane>>2 reads rows
-// 16h + 2g + {0,1} of fragments 2h, 2h+1 with one 16-byte load.  Both
-// patterns are bank-conflict free (4 wavefronts per 512-byte warp load).
-__device__ __forceinline__ void mma_substep(const double* __restrict__ sA,
-                                            const uint8_t* __restrict__ sB,
-                                            double (&acc)[8][4][2], int s, int wm, int wn, int g,
-                                            int j) {
-    const double* pa = sA + (4 * j + s) * kBM + wm * 64 + 2 * g;
-    const uint8_t* pb = sB + (wn * 32 + g) * 128 + (((2 * j + (s >> 1)) ^ g) << 4) + (s & 1) * 8;
-    double a[8], b[4];
+// ---- shared-memory operand layouts and the DMMA fragment mapping ---------
+// A tile (128 m x 16 k): 8 TMA boxes of {16 m, 16 k} with the 128-byte
+// swizzle; double (m, k) at byte (m/16)*2048 + k*128 + (((m%16)/2 ^ k%8) << 4)
+// + (m%2)*8.
+// B tile (16 k x 128 n): one TMA box {16 k, 128 n}, 128-byte swizzle; double
+// (k, n) at byte n*128 + (((k/2) ^ n%8) << 4) + (k%2)*8.
+// A 16-k stage is 4 DMMA substeps s; lane (g = lane/4, j = lane%4) feeds
+// physical k = p(s, j) = 2j + (s%2) + 8(s/2) (A and B agree, so the sum over
+// k is unchanged).  Lane group g supplies A rows 16h + 2g + {0,1} of the
+// fragment pair (2h, 2h+1) with one 16-byte load and B column
+// nperm(g) = ((g%2)<<2) | (g/2) of each 8-column group, which also permutes
+// the accumulator columns the epilogue writes.  With these choices every
+// fragment load is a conflict-free 16-byte LDS (4 wavefronts per warp).
+__device__ __forceinline__ int nperm(int c) { return ((c & 1) << 2) | (c >> 1); }
+
+struct Frags {
+    double a[2][8];  // [substep in pair][m fragment]
+    double b[2][4];  // [substep in pair][n fragment]
+};
+
+// Fragments of substeps 2*sp and 2*sp+1.
+__device__ __forceinline__ void load_frags(const uint8_t* __restrict__ sA,
+                                           const uint8_t* __restrict__ sB, int sp, int wm, int wn,
+                                           int g, int j, Frags& f) {
 #pragma unroll
-    for (int h = 0; h < 4; ++h) {
-        const double2 v = *reinterpret_cast<const double2*>(pa + 16 * h);
-        a[2 * h] = v.x;
-        a[2 * h + 1] = v.y;
+    for (int ss = 0; ss < 2; ++ss) {
+        const int k = 2 * j + ss + 8 * sp;
+        const uint8_t* pa = sA + (wm * 4) * 2048 + k * 128 + ((g ^ (k & 7)) << 4);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const double2 v = *reinterpret_cast<const double2*>(pa + h * 2048);
+            f.a[ss][2 * h] = v.x;
+            f.a[ss][2 * h + 1] = v.y;
+        }
     }
+    const int nb = wn * 32 + nperm(g);  // n & 7 == nperm(g)
+    const uint8_t* pb = sB + nb * 128 + (((j + 4 * sp) ^ nperm(g)) << 4);
 #pragma unroll
-    for (int nf = 0; nf < 4; ++nf) b[nf] = *reinterpret_cast<const double*>(pb + nf * 8 * 128);
+    for (int nf = 0; nf < 4; ++nf) {
+        const double2 v = *reinterpret_cast<const double2*>(pb + nf * 8 * 128);
+        f.b[0][nf] = v.x;
+        f.b[1][nf] = v.y;
+    }
+}
+
+__device__ __forceinline__ void dmma_substep(const Frags& f, int ss, double (&acc)[8][4][2]) {
 #pragma unroll
     for (int mf = 0; mf < 8; ++mf)
 #pragma unroll
-        for (int nf = 0; nf < 4; ++nf) dmma(acc[mf][nf][0], acc[mf][nf][1], a[mf], b[nf]);
+        for (int nf = 0; nf < 4; ++nf)
+            dmma(acc[mf][nf][0], acc[mf][nf][1], f.a[ss][mf], f.b[ss][nf]);
 }
 
 // Operand staging job of one k-step: for each side (A, B), the raw TMA term
@@ -123,35 +145,37 @@ __device__ __forceinline__ void mma_substep(const double* __restrict__ sA,
 // chunk (4 chunks per stage), left to right like pack_a_sum / pack_b_sum
 // (blocking.cpp:24-28): c_u = +-1 is a sign flip, so acc + c_u*x is one DADD
 // with exactly the reference's rounding.  A single +1 term is a copy.
+template <int MAXT>
 struct SumJob {
-    const double2* src[2][kMaxTerms];
+    const double2* src[2][MAXT];
     double2* dst[2];
     int n[2];
     uint32_t neg[2];
 };
 
-__device__ __forceinline__ void sum_load(const SumJob& J, int chunk, int tid,
-                                         double2 (&v)[2][kMaxTerms]) {
+template <int MAXT>
+__device__ __forceinline__ void sum_load(const SumJob<MAXT>& J, int chunk, int tid,
+                                         double2 (&v)[2][MAXT]) {
     const int idx = chunk * (kConsumerWarps * 32) + tid;
 #pragma unroll
     for (int side = 0; side < 2; ++side)
 #pragma unroll
-        for (int u = 0; u < kMaxTerms; ++u)
+        for (int u = 0; u < MAXT; ++u)
             if (u < J.n[side]) v[side][u] = J.src[side][u][idx];
 }
 
-__device__ __forceinline__ void sum_store(const SumJob& J, int chunk, int tid,
-                                          const double2 (&v)[2][kMaxTerms]) {
+template <int MAXT>
+__device__ __forceinline__ void sum_store(const SumJob<MAXT>& J, int chunk, int tid,
+                                          const double2 (&v)[2][MAXT]) {
     const int idx = chunk * (kConsumerWarps * 32) + tid;
 #pragma unroll
     for (int side = 0; side < 2; ++side) {
-        if (J.n[side] == 0) continue;
         const uint32_t neg = J.neg[side];
         double2 acc;
         acc.x = flip_sign(v[side][0].x, neg & 1);
         acc.y = flip_sign(v[side][0].y, neg & 1);
 #pragma unroll
-        for (int u = 1; u < kMaxTerms; ++u)
+        for (int u = 1; u < MAXT; ++u)
             if (u < J.n[side]) {
                 acc.x += flip_sign(v[side][u].x, (neg >> u) & 1);
                 acc.y += flip_sign(v[side][u].y, (neg >> u) & 1);
@@ -160,6 +184,7 @@ __device__ __forceinline__ void sum_store(const SumJob& J, int chunk, int tid,
     }
 }
 
+template <int MAXT>
 __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__ MMParams P) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment (128B-swizzle atoms) by offsetting the shared array
@@ -210,12 +235,15 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                         const uint32_t s = q % kRawSlots;
                         mbar_wait(&raw_empty[s], ((q / kRawSlots) & 1) ^ 1);
                         mbar_expect_tx(&raw_full[s], kSlotBytes);
-                        if (u < pd.na)
-                            tma_load_2d(raw + s * kSlotBytes, &P.tmA[pd.aq[u]], m0, k0,
-                                        &raw_full[s]);
-                        else
-                            tma_load_2d(raw + s * kSlotBytes, &P.tmB[pd.bq[u - pd.na]], k0, n0,
-                                        &raw_full[s]);
+                        uint8_t* dst = raw + s * kSlotBytes;
+                        if (u < pd.na) {
+                            const CUtensorMap* map = &P.tmA[pd.aq[u]];
+#pragma unroll
+                            for (int box = 0; box < kBM / 16; ++box)
+                                tma_load_2d(dst + box * 2048, map, m0 + 16 * box, k0, &raw_full[s]);
+                        } else {
+                            tma_load_2d(dst, &P.tmB[pd.bq[u - pd.na]], k0, n0, &raw_full[s]);
+                        }
                     }
                 }
             }
@@ -236,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     const int tid = threadIdx.x;
     double acc[8][4][2];
 
-    auto make_job = [&](const ProductDesc& pd, uint32_t q, uint32_t st, SumJob& J) {
+    auto make_job = [&](const ProductDesc& pd, uint32_t q, uint32_t st, SumJob<MAXT>& J) {
         const int n[2] = {pd.na, pd.nb};
         const int8_t* c[2] = {pd.as, pd.bs};
 #pragma unroll
@@ -245,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             J.neg[side] = 0;
             const uint32_t q0 = q + (side ? pd.na : 0);
 #pragma unroll
-            for (int u = 0; u < kMaxTerms; ++u) {
+            for (int u = 0; u < MAXT; ++u) {
                 J.src[side][u] = reinterpret_cast<const double2*>(
                     raw + ((q0 + u) % kRawSlots) * kSlotBytes);
                 if (u < n[side]) J.neg[side] |= (c[side][u] < 0 ? 1u : 0u) << u;
@@ -254,18 +282,19 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         }
     };
     auto wait_full = [&](uint32_t q0, int n) {
-        for (uint32_t u = q0; u < q0 + n; ++u) mbar_wait(&raw_full[u % kRawSlots], (u / kRawSlots) & 1);
+        for (uint32_t u = q0; u < q0 + n; ++u)
+            mbar_wait(&raw_full[u % kRawSlots], (u / kRawSlots) & 1);
     };
 
     int p = 0, kt = 0;
     uint32_t q = 0, T = 0;
     if (!direct) {  // prologue: stage step 0
         const ProductDesc& pd = P.prod[0];
-        SumJob J;
+        SumJob<MAXT> J;
         make_job(pd, 0, 0, J);
         wait_full(0, pd.na + pd.nb);
         for (int c = 0; c < 4; ++c) {
-            double2 v[2][kMaxTerms];
+            double2 v[2][MAXT];
             sum_load(J, c, tid, v);
             sum_store(J, c, tid, v);
         }
@@ -287,14 +316,13 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         const uint32_t q1 = q + nq;
         const uint32_t st = T % kStages, st1 = (T + 1) % kStages;
 
-        const double* sA;
-        const uint8_t* sB;
+        const uint8_t *sA, *sB;
         if (direct) {
             wait_full(q, 2);
-            sA = reinterpret_cast<const double*>(raw + (q % kRawSlots) * kSlotBytes);
+            sA = raw + (q % kRawSlots) * kSlotBytes;
             sB = raw + ((q + 1) % kRawSlots) * kSlotBytes;
         } else {
-            sA = reinterpret_cast<const double*>(stage + (2 * st) * kSlotBytes);
+            sA = stage + (2 * st) * kSlotBytes;
             sB = stage + (2 * st + 1) * kSlotBytes;
         }
         if (kt == 0) {
@@ -307,19 +335,29 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         const bool stage1 = !direct && has1;
         if (stage1) {
             const ProductDesc& pd1 = P.prod[p1];
-            SumJob J;
+            SumJob<MAXT> J;
             make_job(pd1, q1, st1, J);
             wait_full(q1, pd1.na + pd1.nb);
 #pragma unroll
-            for (int s = 0; s < 4; ++s) {
-                double2 v[2][kMaxTerms];
-                sum_load(J, s, tid, v);
-                mma_substep(sA, sB, acc, s, wm, wn, g, j);
-                sum_store(J, s, tid, v);
+            for (int sp = 0; sp < 2; ++sp) {
+                Frags f;
+                load_frags(sA, sB, sp, wm, wn, g, j, f);
+#pragma unroll
+                for (int ss = 0; ss < 2; ++ss) {
+                    double2 v[2][MAXT];
+                    sum_load(J, 2 * sp + ss, tid, v);
+                    dmma_substep(f, ss, acc);
+                    sum_store(J, 2 * sp + ss, tid, v);
+                }
             }
         } else {
 #pragma unroll
-            for (int s = 0; s < 4; ++s) mma_substep(sA, sB, acc, s, wm, wn, g, j);
+            for (int sp = 0; sp < 2; ++sp) {
+                Frags f;
+                load_frags(sA, sB, sp, wm, wn, g, j, f);
+                dmma_substep(f, 0, acc);
+                dmma_substep(f, 1, acc);
+            }
         }
 
         if (direct) {
@@ -331,9 +369,12 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         }
 
         if (kt == P.ktiles - 1) {
-            // ---- epilogue of product p: rows/cols of this lane's fragments
+            // ---- epilogue of product p.  Accumulator (mf, nf, e) of lane
+            // (g, j) is row 16(mf/2) + 2g + mf%2 and column 8nf + nperm(2j + e)
+            // of this warp's 64 x 32 tile.
             const int mrow0 = tm * kBM + wm * 64 + 2 * g;
-            const int ncol0 = tn * kBN + wn * 32 + 2 * j;
+            const int ncol0 = tn * kBN + wn * 32;
+            const int c0 = nperm(2 * j), c1 = nperm(2 * j + 1);
             if (P.mode == kEpiRMW) {
                 for (int u = 0; u < pd.nc; ++u) {
                     const int cq = pd.cq[u];
@@ -348,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
 #pragma unroll
                             for (int e = 0; e < 2; ++e) {
                                 const int row = mrow0 + 16 * (mf >> 1) + (mf & 1);
-                                const int col = ncol0 + 8 * nf + e;
+                                const int col = ncol0 + 8 * nf + (e ? c1 : c0);
                                 cv[mf][e] = (row < R && col < Cc) ? C[row * P.rs_c + col * P.cs_c]
                                                                   : 0.0;
                             }
@@ -357,7 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
 #pragma unroll
                             for (int e = 0; e < 2; ++e) {
                                 const int row = mrow0 + 16 * (mf >> 1) + (mf & 1);
-                                const int col = ncol0 + 8 * nf + e;
+                                const int col = ncol0 + 8 * nf + (e ? c1 : c0);
                                 if (row < R && col < Cc)
                                     C[row * P.rs_c + col * P.cs_c] =
                                         fma(sc, acc[mf][nf][e], cv[mf][e]);
@@ -373,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
 #pragma unroll
                         for (int e = 0; e < 2; ++e) {
                             const int row = mrow0 + 16 * (mf >> 1) + (mf & 1);
-                            const int col = ncol0 + 8 * nf + e;
+                            const int col = ncol0 + 8 * nf + (e ? c1 : c0);
                             if (row < P.qm && col < P.qn) M[row + col * P.ldm] = acc[mf][nf][e];
                         }
             }
@@ -475,17 +516,28 @@ __global__ void scale_kernel(double* c, long rows, long cols, long long rs, long
 
 }  // namespace
 
-cudaError_t launch_mm(const MMParams& p, cudaStream_t s) {
+template <int MAXT>
+static cudaError_t launch_mm_t(const MMParams& p, cudaStream_t s) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(mm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(mm_kernel<MAXT>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              kMMSmemBytes);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     const int grid = p.tiles_m * p.tiles_n;
-    mm_kernel<<<grid, kThreads, kMMSmemBytes, s>>>(p);
+    mm_kernel<MAXT><<<grid, kThreads, kMMSmemBytes, s>>>(p);
     return cudaGetLastError();
+}
+
+cudaError_t launch_mm(const MMParams& p, cudaStream_t s) {
+    int maxt = 1;
+    for (int i = 0; i < p.nprod; ++i) {
+        maxt = p.prod[i].na > maxt ? p.prod[i].na : maxt;
+        maxt = p.prod[i].nb > maxt ? p.prod[i].nb : maxt;
+    }
+    return maxt <= 2 ? launch_mm_t<2>(p, s) : launch_mm_t<kMaxTerms>(p, s);
 }
 
 cudaError_t launch_repack(const double* src, long long rs, long long cs, long rows, long cols,
