@@ -139,49 +139,58 @@ __device__ __forceinline__ void dmma_substep(const Frags& f, int ss, double (&ac
             dmma(acc[mf][nf][0], acc[mf][nf][1], f.a[ss][mf], f.b[ss][nf]);
 }
 
-// Operand staging job of one k-step: for each side (A, B), the raw TMA term
-// tiles (shared memory) and their signs; the result goes to a stage buffer.
-// The sum is formed by the 256 DMMA threads, one 16-byte vector per tile per
-// chunk (4 chunks per stage), left to right like pack_a_sum / pack_b_sum
-// (blocking.cpp:24-28): c_u = +-1 is a sign flip, so acc + c_u*x is one DADD
-// with exactly the reference's rounding.  A single +1 term is a copy.
-template <int MAXT>
-struct SumJob {
-    const double2* src[2][MAXT];
-    double2* dst[2];
-    int n[2];
-    uint32_t neg[2];
-};
-
-template <int MAXT>
-__device__ __forceinline__ void sum_load(const SumJob<MAXT>& J, int chunk, int tid,
-                                         double2 (&v)[2][MAXT]) {
-    const int idx = chunk * (kConsumerWarps * 32) + tid;
+// Operand sum of one k-step, formed by the sum warps: for each side (A, B)
+// stage := sum_u c_u raw(q0 + u), left to right like pack_a_sum /
+// pack_b_sum (blocking.cpp:24-28).  c_u = +-1 is a sign flip, so acc + c_u*x
+// is one DADD with exactly the reference's rounding; a single +1 term is a
+// copy.  All loads of a batch are issued before any add or store.
+template <int N>
+__device__ __forceinline__ void sum_side(const uint8_t* raw, uint32_t q0, uint32_t neg,
+                                         double2* __restrict__ dst, int t) {
+    constexpr int kVec = kSlotBytes / 16;       // 1024 double2 per tile
+    constexpr int kT = kSummerWarps * 32;       // 224 summing threads
+    constexpr int U = (N <= 2) ? 3 : 2;         // vectors per thread per batch
+    const double2* src[N];
 #pragma unroll
-    for (int side = 0; side < 2; ++side)
+    for (int u = 0; u < N; ++u)
+        src[u] = reinterpret_cast<const double2*>(raw + ((q0 + u) % kRawSlots) * kSlotBytes);
+#pragma unroll 1
+    for (int base = t; base < kVec; base += U * kT) {
+        double2 v[U][N];
 #pragma unroll
-        for (int u = 0; u < MAXT; ++u)
-            if (u < J.n[side]) v[side][u] = J.src[side][u][idx];
+        for (int b = 0; b < U; ++b) {
+            const int idx = base + b * kT;
+#pragma unroll
+            for (int u = 0; u < N; ++u)
+                v[b][u] = idx < kVec ? src[u][idx] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int b = 0; b < U; ++b) {
+            const int idx = base + b * kT;
+            double2 acc = v[b][0];
+            if (!(N == 1 && neg == 0)) {
+                acc.x = flip_sign(acc.x, neg & 1);
+                acc.y = flip_sign(acc.y, neg & 1);
+#pragma unroll
+                for (int u = 1; u < N; ++u) {
+                    acc.x += flip_sign(v[b][u].x, (neg >> u) & 1);
+                    acc.y += flip_sign(v[b][u].y, (neg >> u) & 1);
+                }
+            }
+            if (idx < kVec) dst[idx] = acc;
+        }
+    }
 }
 
 template <int MAXT>
-__device__ __forceinline__ void sum_store(const SumJob<MAXT>& J, int chunk, int tid,
-                                          const double2 (&v)[2][MAXT]) {
-    const int idx = chunk * (kConsumerWarps * 32) + tid;
-#pragma unroll
-    for (int side = 0; side < 2; ++side) {
-        const uint32_t neg = J.neg[side];
-        double2 acc;
-        acc.x = flip_sign(v[side][0].x, neg & 1);
-        acc.y = flip_sign(v[side][0].y, neg & 1);
-#pragma unroll
-        for (int u = 1; u < MAXT; ++u)
-            if (u < J.n[side]) {
-                acc.x += flip_sign(v[side][u].x, (neg >> u) & 1);
-                acc.y += flip_sign(v[side][u].y, (neg >> u) & 1);
-            }
-        J.dst[side][idx] = acc;
-    }
+__device__ __forceinline__ void sum_side_n(const uint8_t* raw, uint32_t q0, int n,
+                                           const int8_t* coef, double2* dst, int t) {
+    uint32_t neg = 0;
+    for (int u = 0; u < n; ++u) neg |= (coef[u] < 0 ? 1u : 0u) << u;
+    if (n == 1) sum_side<1>(raw, q0, neg, dst, t);
+    else if (MAXT <= 2 || n == 2) sum_side<2>(raw, q0, neg, dst, t);
+    else if (n == 3) sum_side<(MAXT > 2 ? 3 : 2)>(raw, q0, neg, dst, t);
+    else sum_side<(MAXT > 2 ? 4 : 2)>(raw, q0, neg, dst, t);
 }
 
 template <int MAXT>
@@ -193,11 +202,14 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     uint8_t* stage = raw + kRawSlots * kSlotBytes;  // [kStages][A | B]
     uint64_t* raw_full = reinterpret_cast<uint64_t*>(stage + 2 * kStages * kSlotBytes);
     uint64_t* raw_empty = raw_full + kRawSlots;
+    uint64_t* st_full = raw_empty + kRawSlots;
+    uint64_t* st_empty = st_full + kStages;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     // direct: every product is a single +1 term on both sides (the classical
-    // DGEMM program): the mainloop reads the TMA slots in place.
+    // DGEMM program): the DMMA warps read the TMA slots in place and the sum
+    // warps idle.
     const bool direct = P.direct != 0;
 
     // grouped rasterisation: group_m tile rows share B column panels in L2
@@ -213,18 +225,27 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     if (threadIdx.x == 0) {
         for (int s = 0; s < kRawSlots; ++s) {
             mbar_init(&raw_full[s], 1);
-            mbar_init(&raw_empty[s], direct ? kConsumerWarps : 1);
+            mbar_init(&raw_empty[s], direct ? kConsumerWarps : kSummerWarps);
+        }
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&st_full[s], kSummerWarps);
+            mbar_init(&st_empty[s], kConsumerWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
     }
     __syncthreads();
 
+    // Warp roles: warps 0-7 (warpgroups 0-1) run the DMMA mainloop; warp 8
+    // issues TMA; warps 9-15 form the operand sums.  The sum warps have the
+    // highest warp ids (the SMSP issue arbiter favours them) and never touch
+    // the DMMA warps' instruction stream: measured, sums interleaved into the
+    // DMMA warps cost ~30% of DMMA issue (profiles/r01_notes.md).
     if (warp >= kConsumerWarps) {
-        // ================= producer warpgroup (warps 8-11) ===================
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
-        if (warp == kConsumerWarps && lane == 0) {
-            // TMA issue: one elected lane walks products x k-steps x terms
+        if (warp == kConsumerWarps) {
+            if (lane != 0) return;
+            // ===== TMA issue: one lane walks products x k-steps x terms
             uint32_t q = 0;
             const int m0 = tm * kBM, n0 = tn * kBN;
             for (int p = 0; p < P.nprod; ++p) {
@@ -247,110 +268,62 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                     }
                 }
             }
+            return;
+        }
+        if (direct) return;
+        // ===== operand-sum warps: raw term tiles -> summed (A, B) stage
+        const int t = threadIdx.x - (kConsumerWarps + 1) * 32;
+        uint32_t q = 0, T = 0;
+        for (int p = 0; p < P.nprod; ++p) {
+            const ProductDesc& pd = P.prod[p];
+            const int na = pd.na, nb = pd.nb;
+            for (int kt = 0; kt < P.ktiles; ++kt, ++T) {
+                const uint32_t st = T % kStages;
+                mbar_wait(&st_empty[st], ((T / kStages) & 1) ^ 1);
+                for (uint32_t u = q; u < q + na + nb; ++u)
+                    mbar_wait(&raw_full[u % kRawSlots], (u / kRawSlots) & 1);
+                sum_side_n<MAXT>(raw, q, na, pd.as,
+                                 reinterpret_cast<double2*>(stage + (2 * st) * kSlotBytes), t);
+                sum_side_n<MAXT>(raw, q + na, nb, pd.bs,
+                                 reinterpret_cast<double2*>(stage + (2 * st + 1) * kSlotBytes), t);
+                __syncwarp();
+                if (lane == 0) {
+                    for (uint32_t u = q; u < q + na + nb; ++u) mbar_arrive(&raw_empty[u % kRawSlots]);
+                    mbar_arrive(&st_full[st]);
+                }
+                q += na + nb;
+            }
         }
         return;
     }
 
     // ================= DMMA warpgroups (warps 0-7) ==========================
-    // Software pipeline per k-step T: the operand sums of step T+1 (raw TMA
-    // term tiles -> stage[(T+1) % 2]) are formed in 4 chunks interleaved with
-    // the 4 DMMA substeps of step T (chunk loads before, adds/stores after
-    // the 32 DMMAs), so their shared-memory and FP64-pipe latency hides under
-    // DMMA work; one named barrier per step publishes the stage and retires
-    // the raw slots.
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kConsumerRegs));
     const int wm = warp & 1, wn = warp >> 1;
     const int g = lane >> 2, j = lane & 3;
-    const int tid = threadIdx.x;
     double acc[8][4][2];
-
-    auto make_job = [&](const ProductDesc& pd, uint32_t q, uint32_t st, SumJob<MAXT>& J) {
-        const int n[2] = {pd.na, pd.nb};
-        const int8_t* c[2] = {pd.as, pd.bs};
-#pragma unroll
-        for (int side = 0; side < 2; ++side) {
-            J.n[side] = n[side];
-            J.neg[side] = 0;
-            const uint32_t q0 = q + (side ? pd.na : 0);
-#pragma unroll
-            for (int u = 0; u < MAXT; ++u) {
-                J.src[side][u] = reinterpret_cast<const double2*>(
-                    raw + ((q0 + u) % kRawSlots) * kSlotBytes);
-                if (u < n[side]) J.neg[side] |= (c[side][u] < 0 ? 1u : 0u) << u;
-            }
-            J.dst[side] = reinterpret_cast<double2*>(stage + (2 * st + side) * kSlotBytes);
-        }
-    };
-    auto wait_full = [&](uint32_t q0, int n) {
-        for (uint32_t u = q0; u < q0 + n; ++u)
-            mbar_wait(&raw_full[u % kRawSlots], (u / kRawSlots) & 1);
-    };
-
-    int p = 0, kt = 0;
     uint32_t q = 0, T = 0;
-    if (!direct) {  // prologue: stage step 0
-        const ProductDesc& pd = P.prod[0];
-        SumJob<MAXT> J;
-        make_job(pd, 0, 0, J);
-        wait_full(0, pd.na + pd.nb);
-        for (int c = 0; c < 4; ++c) {
-            double2 v[2][MAXT];
-            sum_load(J, c, tid, v);
-            sum_store(J, c, tid, v);
-        }
-        consumer_bar();
-        if (tid == 0)
-            for (uint32_t u = 0; u < static_cast<uint32_t>(pd.na + pd.nb); ++u)
-                mbar_arrive(&raw_empty[u % kRawSlots]);
-    }
 
-    while (true) {
+    for (int p = 0; p < P.nprod; ++p) {
         const ProductDesc& pd = P.prod[p];
-        const uint32_t nq = pd.na + pd.nb;
-        int p1 = p, kt1 = kt + 1;
-        if (kt1 == P.ktiles) {
-            ++p1;
-            kt1 = 0;
-        }
-        const bool has1 = p1 < P.nprod;
-        const uint32_t q1 = q + nq;
-        const uint32_t st = T % kStages, st1 = (T + 1) % kStages;
+#pragma unroll
+        for (int mf = 0; mf < 8; ++mf)
+#pragma unroll
+            for (int nf = 0; nf < 4; ++nf) acc[mf][nf][0] = acc[mf][nf][1] = 0.0;
 
-        const uint8_t *sA, *sB;
-        if (direct) {
-            wait_full(q, 2);
-            sA = raw + (q % kRawSlots) * kSlotBytes;
-            sB = raw + ((q + 1) % kRawSlots) * kSlotBytes;
-        } else {
-            sA = stage + (2 * st) * kSlotBytes;
-            sB = stage + (2 * st + 1) * kSlotBytes;
-        }
-        if (kt == 0) {
-#pragma unroll
-            for (int mf = 0; mf < 8; ++mf)
-#pragma unroll
-                for (int nf = 0; nf < 4; ++nf) acc[mf][nf][0] = acc[mf][nf][1] = 0.0;
-        }
-
-        const bool stage1 = !direct && has1;
-        if (stage1) {
-            const ProductDesc& pd1 = P.prod[p1];
-            SumJob<MAXT> J;
-            make_job(pd1, q1, st1, J);
-            wait_full(q1, pd1.na + pd1.nb);
-#pragma unroll
-            for (int sp = 0; sp < 2; ++sp) {
-                Frags f;
-                load_frags(sA, sB, sp, wm, wn, g, j, f);
-#pragma unroll
-                for (int ss = 0; ss < 2; ++ss) {
-                    double2 v[2][MAXT];
-                    sum_load(J, 2 * sp + ss, tid, v);
-                    dmma_substep(f, ss, acc);
-                    sum_store(J, 2 * sp + ss, tid, v);
-                }
+        for (int kt = 0; kt < P.ktiles; ++kt, ++T) {
+            const uint8_t *sA, *sB;
+            const uint32_t st = T % kStages;
+            if (direct) {
+                mbar_wait(&raw_full[q % kRawSlots], (q / kRawSlots) & 1);
+                mbar_wait(&raw_full[(q + 1) % kRawSlots], ((q + 1) / kRawSlots) & 1);
+                sA = raw + (q % kRawSlots) * kSlotBytes;
+                sB = raw + ((q + 1) % kRawSlots) * kSlotBytes;
+            } else {
+                mbar_wait(&st_full[st], (T / kStages) & 1);
+                sA = stage + (2 * st) * kSlotBytes;
+                sB = stage + (2 * st + 1) * kSlotBytes;
             }
-        } else {
 #pragma unroll
             for (int sp = 0; sp < 2; ++sp) {
                 Frags f;
@@ -358,82 +331,66 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                 dmma_substep(f, 0, acc);
                 dmma_substep(f, 1, acc);
             }
-        }
-
-        if (direct) {
             __syncwarp();
             if (lane == 0) {
-                mbar_arrive(&raw_empty[q % kRawSlots]);
-                mbar_arrive(&raw_empty[(q + 1) % kRawSlots]);
+                if (direct) {
+                    mbar_arrive(&raw_empty[q % kRawSlots]);
+                    mbar_arrive(&raw_empty[(q + 1) % kRawSlots]);
+                } else {
+                    mbar_arrive(&st_empty[st]);
+                }
             }
+            q += pd.na + pd.nb;
         }
 
-        if (kt == P.ktiles - 1) {
-            // ---- epilogue of product p.  Accumulator (mf, nf, e) of lane
-            // (g, j) is row 16(mf/2) + 2g + mf%2 and column 8nf + nperm(2j + e)
-            // of this warp's 64 x 32 tile.
-            const int mrow0 = tm * kBM + wm * 64 + 2 * g;
-            const int ncol0 = tn * kBN + wn * 32;
-            const int c0 = nperm(2 * j), c1 = nperm(2 * j + 1);
-            if (P.mode == kEpiRMW) {
-                for (int u = 0; u < pd.nc; ++u) {
-                    const int cq = pd.cq[u];
-                    double* __restrict__ C = P.cptr[cq];
-                    const int R = P.crows[cq], Cc = P.ccols[cq];
-                    const double sc = P.alpha * static_cast<double>(pd.cs[u]);
+        // ---- epilogue of product p.  Accumulator (mf, nf, e) of lane (g, j)
+        // is row 16(mf/2) + 2g + mf%2 and column 8nf + nperm(2j + e) of this
+        // warp's 64 x 32 tile.
+        const int mrow0 = tm * kBM + wm * 64 + 2 * g;
+        const int ncol0 = tn * kBN + wn * 32;
+        const int c0 = nperm(2 * j), c1 = nperm(2 * j + 1);
+        if (P.mode == kEpiRMW) {
+            for (int u = 0; u < pd.nc; ++u) {
+                const int cq = pd.cq[u];
+                double* __restrict__ C = P.cptr[cq];
+                const int R = P.crows[cq], Cc = P.ccols[cq];
+                const double sc = P.alpha * static_cast<double>(pd.cs[u]);
 #pragma unroll
-                    for (int nf = 0; nf < 4; ++nf) {
-                        double cv[8][2];
-#pragma unroll
-                        for (int mf = 0; mf < 8; ++mf)
-#pragma unroll
-                            for (int e = 0; e < 2; ++e) {
-                                const int row = mrow0 + 16 * (mf >> 1) + (mf & 1);
-                                const int col = ncol0 + 8 * nf + (e ? c1 : c0);
-                                cv[mf][e] = (row < R && col < Cc) ? C[row * P.rs_c + col * P.cs_c]
-                                                                  : 0.0;
-                            }
-#pragma unroll
-                        for (int mf = 0; mf < 8; ++mf)
-#pragma unroll
-                            for (int e = 0; e < 2; ++e) {
-                                const int row = mrow0 + 16 * (mf >> 1) + (mf & 1);
-                                const int col = ncol0 + 8 * nf + (e ? c1 : c0);
-                                if (row < R && col < Cc)
-                                    C[row * P.rs_c + col * P.cs_c] =
-                                        fma(sc, acc[mf][nf][e], cv[mf][e]);
-                            }
-                    }
-                }
-            } else {
-                double* __restrict__ M = P.mbase + p * P.mstride;
-#pragma unroll
-                for (int nf = 0; nf < 4; ++nf)
+                for (int nf = 0; nf < 4; ++nf) {
+                    double cv[8][2];
 #pragma unroll
                     for (int mf = 0; mf < 8; ++mf)
 #pragma unroll
                         for (int e = 0; e < 2; ++e) {
                             const int row = mrow0 + 16 * (mf >> 1) + (mf & 1);
                             const int col = ncol0 + 8 * nf + (e ? c1 : c0);
-                            if (row < P.qm && col < P.qn) M[row + col * P.ldm] = acc[mf][nf][e];
+                            cv[mf][e] =
+                                (row < R && col < Cc) ? C[row * P.rs_c + col * P.cs_c] : 0.0;
                         }
+#pragma unroll
+                    for (int mf = 0; mf < 8; ++mf)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int row = mrow0 + 16 * (mf >> 1) + (mf & 1);
+                            const int col = ncol0 + 8 * nf + (e ? c1 : c0);
+                            if (row < R && col < Cc)
+                                C[row * P.rs_c + col * P.cs_c] = fma(sc, acc[mf][nf][e], cv[mf][e]);
+                        }
+                }
             }
+        } else {
+            double* __restrict__ M = P.mbase + p * P.mstride;
+#pragma unroll
+            for (int nf = 0; nf < 4; ++nf)
+#pragma unroll
+                for (int mf = 0; mf < 8; ++mf)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int row = mrow0 + 16 * (mf >> 1) + (mf & 1);
+                        const int col = ncol0 + 8 * nf + (e ? c1 : c0);
+                        if (row < P.qm && col < P.qn) M[row + col * P.ldm] = acc[mf][nf][e];
+                    }
         }
-
-        if (stage1) {
-            // step T+1 is staged and every warp is done with step T
-            consumer_bar();
-            if (tid == 0) {
-                const ProductDesc& pd1 = P.prod[p1];
-                for (uint32_t u = q1; u < q1 + pd1.na + pd1.nb; ++u)
-                    mbar_arrive(&raw_empty[u % kRawSlots]);
-            }
-        }
-        if (!has1) break;
-        p = p1;
-        kt = kt1;
-        q = q1;
-        ++T;
     }
 }
 
