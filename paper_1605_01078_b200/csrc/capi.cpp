@@ -366,9 +366,8 @@ const char* strassen_build_info(void) {
         return std::string("libstrassen_b200 sm_100a; mm_kernel tile ") + std::to_string(sb200::kBM) +
                "x" + std::to_string(sb200::kBN) + "x" + std::to_string(sb200::kBK) +
                " DMMA.8 (mma.sync m8n8k4 f64); TMA ring " + std::to_string(sb200::kRawSlots) +
-               " x 16 KB, " + std::to_string(sb200::kStages) + " summed stages; 1 TMA + " +
-               std::to_string(sb200::kSummerWarps) + " sum + " +
-               std::to_string(sb200::kConsumerWarps) + " DMMA warps";
+               " x 16 KB of operand-term tiles; operand sums formed in registers by the " +
+               std::to_string(sb200::kConsumerWarps) + " DMMA warps; 1 TMA warp";
     }();
     return info.c_str();
 }

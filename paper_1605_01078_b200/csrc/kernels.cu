@@ -106,28 +106,54 @@ struct Frags {
     double b[2][4];  // [substep in pair][n fragment]
 };
 
-// Fragments of substeps 2*sp and 2*sp+1.
-__device__ __forceinline__ void load_frags(const uint8_t* __restrict__ sA,
-                                           const uint8_t* __restrict__ sB, int sp, int wm, int wn,
-                                           int g, int j, Frags& f) {
+// Fragment addresses of substeps 2*sp and 2*sp+1 inside an A / B tile.
+__device__ __forceinline__ const uint8_t* frag_a_ptr(const uint8_t* sA, int ss, int sp, int wm,
+                                                     int g, int j) {
+    const int k = 2 * j + ss + 8 * sp;
+    return sA + (wm * 4) * 2048 + k * 128 + ((g ^ (k & 7)) << 4);
+}
+__device__ __forceinline__ const uint8_t* frag_b_ptr(const uint8_t* sB, int sp, int wn, int g,
+                                                     int j) {
+    return sB + (wn * 32 + nperm(g)) * 128 + (((j + 4 * sp) ^ nperm(g)) << 4);
+}
+
+// Operand term u of one side, loaded and added into the fragments:
+// acc (+)= c_u * x, c_u = +-1 applied as a sign flip so each add is one DADD
+// rounding exactly like the reference's pack_a_sum / pack_b_sum accumulation
+// (blocking.cpp:24-28; terms in listed order, the first one copied).
+template <bool FIRST>
+__device__ __forceinline__ void frag_a_term(const uint8_t* sA, int sp, int wm, int g, int j,
+                                            uint32_t neg, Frags& f) {
 #pragma unroll
     for (int ss = 0; ss < 2; ++ss) {
-        const int k = 2 * j + ss + 8 * sp;
-        const uint8_t* pa = sA + (wm * 4) * 2048 + k * 128 + ((g ^ (k & 7)) << 4);
+        const uint8_t* pa = frag_a_ptr(sA, ss, sp, wm, g, j);
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
             const double2 v = *reinterpret_cast<const double2*>(pa + h * 2048);
-            f.a[ss][2 * h] = v.x;
-            f.a[ss][2 * h + 1] = v.y;
+            if (FIRST) {
+                f.a[ss][2 * h] = flip_sign(v.x, neg);
+                f.a[ss][2 * h + 1] = flip_sign(v.y, neg);
+            } else {
+                f.a[ss][2 * h] += flip_sign(v.x, neg);
+                f.a[ss][2 * h + 1] += flip_sign(v.y, neg);
+            }
         }
     }
-    const int nb = wn * 32 + nperm(g);  // n & 7 == nperm(g)
-    const uint8_t* pb = sB + nb * 128 + (((j + 4 * sp) ^ nperm(g)) << 4);
+}
+template <bool FIRST>
+__device__ __forceinline__ void frag_b_term(const uint8_t* sB, int sp, int wn, int g, int j,
+                                            uint32_t neg, Frags& f) {
+    const uint8_t* pb = frag_b_ptr(sB, sp, wn, g, j);
 #pragma unroll
     for (int nf = 0; nf < 4; ++nf) {
         const double2 v = *reinterpret_cast<const double2*>(pb + nf * 8 * 128);
-        f.b[0][nf] = v.x;
-        f.b[1][nf] = v.y;
+        if (FIRST) {
+            f.b[0][nf] = flip_sign(v.x, neg);
+            f.b[1][nf] = flip_sign(v.y, neg);
+        } else {
+            f.b[0][nf] += flip_sign(v.x, neg);
+            f.b[1][nf] += flip_sign(v.y, neg);
+        }
     }
 }
 
@@ -139,78 +165,17 @@ __device__ __forceinline__ void dmma_substep(const Frags& f, int ss, double (&ac
             dmma(acc[mf][nf][0], acc[mf][nf][1], f.a[ss][mf], f.b[ss][nf]);
 }
 
-// Operand sum of one k-step, formed by the sum warps: for each side (A, B)
-// stage := sum_u c_u raw(q0 + u), left to right like pack_a_sum /
-// pack_b_sum (blocking.cpp:24-28).  c_u = +-1 is a sign flip, so acc + c_u*x
-// is one DADD with exactly the reference's rounding; a single +1 term is a
-// copy.  All loads of a batch are issued before any add or store.
-template <int N>
-__device__ __forceinline__ void sum_side(const uint8_t* raw, uint32_t q0, uint32_t neg,
-                                         double2* __restrict__ dst, int t) {
-    constexpr int kVec = kSlotBytes / 16;       // 1024 double2 per tile
-    constexpr int kT = kSummerWarps * 32;       // 224 summing threads
-    constexpr int U = (N <= 2) ? 3 : 2;         // vectors per thread per batch
-    const double2* src[N];
-#pragma unroll
-    for (int u = 0; u < N; ++u)
-        src[u] = reinterpret_cast<const double2*>(raw + ((q0 + u) % kRawSlots) * kSlotBytes);
-#pragma unroll 1
-    for (int base = t; base < kVec; base += U * kT) {
-        double2 v[U][N];
-#pragma unroll
-        for (int b = 0; b < U; ++b) {
-            const int idx = base + b * kT;
-#pragma unroll
-            for (int u = 0; u < N; ++u)
-                v[b][u] = idx < kVec ? src[u][idx] : make_double2(0.0, 0.0);
-        }
-#pragma unroll
-        for (int b = 0; b < U; ++b) {
-            const int idx = base + b * kT;
-            double2 acc = v[b][0];
-            if (!(N == 1 && neg == 0)) {
-                acc.x = flip_sign(acc.x, neg & 1);
-                acc.y = flip_sign(acc.y, neg & 1);
-#pragma unroll
-                for (int u = 1; u < N; ++u) {
-                    acc.x += flip_sign(v[b][u].x, (neg >> u) & 1);
-                    acc.y += flip_sign(v[b][u].y, (neg >> u) & 1);
-                }
-            }
-            if (idx < kVec) dst[idx] = acc;
-        }
-    }
-}
-
-template <int MAXT>
-__device__ __forceinline__ void sum_side_n(const uint8_t* raw, uint32_t q0, int n,
-                                           const int8_t* coef, double2* dst, int t) {
-    uint32_t neg = 0;
-    for (int u = 0; u < n; ++u) neg |= (coef[u] < 0 ? 1u : 0u) << u;
-    if (n == 1) sum_side<1>(raw, q0, neg, dst, t);
-    else if (MAXT <= 2 || n == 2) sum_side<2>(raw, q0, neg, dst, t);
-    else if (n == 3) sum_side<(MAXT > 2 ? 3 : 2)>(raw, q0, neg, dst, t);
-    else sum_side<(MAXT > 2 ? 4 : 2)>(raw, q0, neg, dst, t);
-}
-
 template <int MAXT>
 __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__ MMParams P) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment (128B-swizzle atoms) by offsetting the shared array
     // itself, so every derived pointer stays in the shared address space (LDS/STS).
     uint8_t* raw = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint8_t* stage = raw + kRawSlots * kSlotBytes;  // [kStages][A | B]
-    uint64_t* raw_full = reinterpret_cast<uint64_t*>(stage + 2 * kStages * kSlotBytes);
+    uint64_t* raw_full = reinterpret_cast<uint64_t*>(raw + kRawSlots * kSlotBytes);
     uint64_t* raw_empty = raw_full + kRawSlots;
-    uint64_t* st_full = raw_empty + kRawSlots;
-    uint64_t* st_empty = st_full + kStages;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    // direct: every product is a single +1 term on both sides (the classical
-    // DGEMM program): the DMMA warps read the TMA slots in place and the sum
-    // warps idle.
-    const bool direct = P.direct != 0;
 
     // grouped rasterisation: group_m tile rows share B column panels in L2
     const int bid = blockIdx.x;
@@ -225,122 +190,94 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     if (threadIdx.x == 0) {
         for (int s = 0; s < kRawSlots; ++s) {
             mbar_init(&raw_full[s], 1);
-            mbar_init(&raw_empty[s], direct ? kConsumerWarps : kSummerWarps);
-        }
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&st_full[s], kSummerWarps);
-            mbar_init(&st_empty[s], kConsumerWarps);
+            mbar_init(&raw_empty[s], kConsumerWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
     }
     __syncthreads();
 
-    // Warp roles: warps 0-7 (warpgroups 0-1) run the DMMA mainloop; warp 8
-    // issues TMA; warps 9-15 form the operand sums.  The sum warps have the
-    // highest warp ids (the SMSP issue arbiter favours them) and never touch
-    // the DMMA warps' instruction stream: measured, sums interleaved into the
-    // DMMA warps cost ~30% of DMMA issue (profiles/r01_notes.md).
     if (warp >= kConsumerWarps) {
+        // ================= TMA warpgroup (warps 8-11; one lane issues) =======
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
-        if (warp == kConsumerWarps) {
-            if (lane != 0) return;
-            // ===== TMA issue: one lane walks products x k-steps x terms
-            uint32_t q = 0;
-            const int m0 = tm * kBM, n0 = tn * kBN;
-            for (int p = 0; p < P.nprod; ++p) {
-                const ProductDesc& pd = P.prod[p];
-                for (int kt = 0; kt < P.ktiles; ++kt) {
-                    const int k0 = kt * kBK;
-                    for (int u = 0; u < pd.na + pd.nb; ++u, ++q) {
-                        const uint32_t s = q % kRawSlots;
-                        mbar_wait(&raw_empty[s], ((q / kRawSlots) & 1) ^ 1);
-                        mbar_expect_tx(&raw_full[s], kSlotBytes);
-                        uint8_t* dst = raw + s * kSlotBytes;
-                        if (u < pd.na) {
-                            const CUtensorMap* map = &P.tmA[pd.aq[u]];
-#pragma unroll
-                            for (int box = 0; box < kBM / 16; ++box)
-                                tma_load_2d(dst + box * 2048, map, m0 + 16 * box, k0, &raw_full[s]);
-                        } else {
-                            tma_load_2d(dst, &P.tmB[pd.bq[u - pd.na]], k0, n0, &raw_full[s]);
-                        }
-                    }
-                }
-            }
-            return;
-        }
-        if (direct) return;
-        // ===== operand-sum warps: raw term tiles -> summed (A, B) stage
-        const int t = threadIdx.x - (kConsumerWarps + 1) * 32;
-        uint32_t q = 0, T = 0;
+        if (warp != kConsumerWarps || lane != 0) return;
+        uint32_t q = 0;
+        const int m0 = tm * kBM, n0 = tn * kBN;
         for (int p = 0; p < P.nprod; ++p) {
             const ProductDesc& pd = P.prod[p];
-            const int na = pd.na, nb = pd.nb;
-            for (int kt = 0; kt < P.ktiles; ++kt, ++T) {
-                const uint32_t st = T % kStages;
-                mbar_wait(&st_empty[st], ((T / kStages) & 1) ^ 1);
-                for (uint32_t u = q; u < q + na + nb; ++u)
-                    mbar_wait(&raw_full[u % kRawSlots], (u / kRawSlots) & 1);
-                sum_side_n<MAXT>(raw, q, na, pd.as,
-                                 reinterpret_cast<double2*>(stage + (2 * st) * kSlotBytes), t);
-                sum_side_n<MAXT>(raw, q + na, nb, pd.bs,
-                                 reinterpret_cast<double2*>(stage + (2 * st + 1) * kSlotBytes), t);
-                __syncwarp();
-                if (lane == 0) {
-                    for (uint32_t u = q; u < q + na + nb; ++u) mbar_arrive(&raw_empty[u % kRawSlots]);
-                    mbar_arrive(&st_full[st]);
+            for (int kt = 0; kt < P.ktiles; ++kt) {
+                const int k0 = kt * kBK;
+                for (int u = 0; u < pd.na + pd.nb; ++u, ++q) {
+                    const uint32_t s = q % kRawSlots;
+                    mbar_wait(&raw_empty[s], ((q / kRawSlots) & 1) ^ 1);
+                    mbar_expect_tx(&raw_full[s], kSlotBytes);
+                    uint8_t* dst = raw + s * kSlotBytes;
+                    if (u < pd.na) {
+                        const CUtensorMap* map = &P.tmA[pd.aq[u]];
+#pragma unroll
+                        for (int box = 0; box < kBM / 16; ++box)
+                            tma_load_2d(dst + box * 2048, map, m0 + 16 * box, k0, &raw_full[s]);
+                    } else {
+                        tma_load_2d(dst, &P.tmB[pd.bq[u - pd.na]], k0, n0, &raw_full[s]);
+                    }
                 }
-                q += na + nb;
             }
         }
         return;
     }
 
     // ================= DMMA warpgroups (warps 0-7) ==========================
+    // Each warp forms the Strassen operand sums of exactly the fragments it
+    // multiplies, in registers, straight from the TMA term tiles: the sums'
+    // DADDs sit in the DMMA warp's own instruction stream (DADDs issued by
+    // other warps are starved while DMMA saturates the FP64 pipe, measured in
+    // microbench/fp64_contend.cu), and no stage buffer, barrier or
+    // cross-warp handoff is needed.
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kConsumerRegs));
     const int wm = warp & 1, wn = warp >> 1;
     const int g = lane >> 2, j = lane & 3;
     double acc[8][4][2];
-    uint32_t q = 0, T = 0;
+    uint32_t q = 0;
 
     for (int p = 0; p < P.nprod; ++p) {
         const ProductDesc& pd = P.prod[p];
+        const int na = pd.na, nb = pd.nb;
+        uint32_t nega = 0, negb = 0;
+        for (int u = 0; u < na; ++u) nega |= (pd.as[u] < 0 ? 1u : 0u) << u;
+        for (int u = 0; u < nb; ++u) negb |= (pd.bs[u] < 0 ? 1u : 0u) << u;
 #pragma unroll
         for (int mf = 0; mf < 8; ++mf)
 #pragma unroll
             for (int nf = 0; nf < 4; ++nf) acc[mf][nf][0] = acc[mf][nf][1] = 0.0;
 
-        for (int kt = 0; kt < P.ktiles; ++kt, ++T) {
-            const uint8_t *sA, *sB;
-            const uint32_t st = T % kStages;
-            if (direct) {
-                mbar_wait(&raw_full[q % kRawSlots], (q / kRawSlots) & 1);
-                mbar_wait(&raw_full[(q + 1) % kRawSlots], ((q + 1) / kRawSlots) & 1);
-                sA = raw + (q % kRawSlots) * kSlotBytes;
-                sB = raw + ((q + 1) % kRawSlots) * kSlotBytes;
-            } else {
-                mbar_wait(&st_full[st], (T / kStages) & 1);
-                sA = stage + (2 * st) * kSlotBytes;
-                sB = stage + (2 * st + 1) * kSlotBytes;
+        for (int kt = 0; kt < P.ktiles; ++kt) {
+            const uint32_t nq = na + nb;
+            for (uint32_t u = q; u < q + nq; ++u)
+                mbar_wait(&raw_full[u % kRawSlots], (u / kRawSlots) & 1);
+            const uint8_t* sA[MAXT];
+            const uint8_t* sB[MAXT];
+#pragma unroll
+            for (int u = 0; u < MAXT; ++u) {
+                sA[u] = raw + ((q + u) % kRawSlots) * kSlotBytes;
+                sB[u] = raw + ((q + na + u) % kRawSlots) * kSlotBytes;
             }
 #pragma unroll
             for (int sp = 0; sp < 2; ++sp) {
                 Frags f;
-                load_frags(sA, sB, sp, wm, wn, g, j, f);
+                frag_a_term<true>(sA[0], sp, wm, g, j, nega & 1, f);
+                frag_b_term<true>(sB[0], sp, wn, g, j, negb & 1, f);
+#pragma unroll
+                for (int u = 1; u < MAXT; ++u) {
+                    if (u < na) frag_a_term<false>(sA[u], sp, wm, g, j, (nega >> u) & 1, f);
+                    if (u < nb) frag_b_term<false>(sB[u], sp, wn, g, j, (negb >> u) & 1, f);
+                }
                 dmma_substep(f, 0, acc);
                 dmma_substep(f, 1, acc);
             }
             __syncwarp();
-            if (lane == 0) {
-                if (direct) {
-                    mbar_arrive(&raw_empty[q % kRawSlots]);
-                    mbar_arrive(&raw_empty[(q + 1) % kRawSlots]);
-                } else {
-                    mbar_arrive(&st_empty[st]);
-                }
-            }
-            q += pd.na + pd.nb;
+            if (lane == 0)
+                for (uint32_t u = q; u < q + nq; ++u) mbar_arrive(&raw_empty[u % kRawSlots]);
+            q += nq;
         }
 
         // ---- epilogue of product p.  Accumulator (mf, nf, e) of lane (g, j)

@@ -16,20 +16,17 @@ constexpr int kMaxQuad = 16;        // 2^L x 2^L quadrants, L <= 2
 constexpr int kMaxProducts = 49;    // 7^L
 constexpr int kMaxTerms = 4;        // operand terms / destinations per product at L <= 2
 constexpr int kConsumerWarps = 8;   // 2 warpgroups; 2 (m) x 4 (n) warps of 64 x 32
-constexpr int kSummerWarps = 7;     // producer warpgroups: 1 TMA warp + 7 operand-sum warps
-constexpr int kThreads = (kConsumerWarps + 1 + kSummerWarps) * 32;  // 512
+constexpr int kThreads = 128 + kConsumerWarps * 32;  // 384: + TMA warpgroup (1 active warp)
 constexpr int kSlotBytes = kBM * kBK * 8;            // one 128x16 fp64 operand tile (16 KB)
-constexpr int kRawSlots = 8;                         // TMA ring of raw operand-term tiles
-constexpr int kStages = 3;                           // summed (A, B) operand stages
-constexpr int kProducerRegs = 48;                    // setmaxnreg split
-constexpr int kConsumerRegs = 208;
-// setmaxnreg moves registers inside the CTA's launch allocation (512 threads x
-// 128 = 65536): the consumers' increase must be covered by the producers'
-// release, or setmaxnreg.inc waits forever.
-static_assert(kProducerRegs * (kThreads - kConsumerWarps * 32) + kConsumerRegs * kConsumerWarps * 32 <=
-                  kThreads * (65536 / kThreads),
+constexpr int kRawSlots = 13;                        // TMA ring of operand-term tiles (208 KB)
+constexpr int kProducerRegs = 24;                    // setmaxnreg split
+constexpr int kConsumerRegs = 240;
+// setmaxnreg moves registers inside the CTA's launch allocation (384 threads x
+// 168 = 64512): the DMMA warps' increase must be covered by the producer
+// warpgroup's release, or setmaxnreg.inc waits forever.
+static_assert(kProducerRegs * 128 + kConsumerRegs * kConsumerWarps * 32 <= kThreads * 168,
               "setmaxnreg split exceeds the CTA register allocation");
-constexpr int kMMSmemBytes = (kRawSlots + 2 * kStages) * kSlotBytes + 1024 + 256;
+constexpr int kMMSmemBytes = kRawSlots * kSlotBytes + 1024 + 256;
 static_assert(kMMSmemBytes <= 227 * 1024, "shared memory budget");
 
 // One Strassen product M_p = (sum_u as_u A_{aq_u}) (sum_u bs_u B_{bq_u});
