@@ -121,9 +121,12 @@ __device__ __forceinline__ const uint8_t* frag_b_ptr(const uint8_t* sB, int sp, 
 // acc (+)= c_u * x, c_u = +-1 applied as a sign flip so each add is one DADD
 // rounding exactly like the reference's pack_a_sum / pack_b_sum accumulation
 // (blocking.cpp:24-28; terms in listed order, the first one copied).
+// FIRST: plain load (the caller negates afterwards in the rare -1 case);
+// otherwise acc = fma(c, x, acc) with c = +-1, which rounds exactly like
+// acc + c*x (c*x is exact) and needs no separate negation.
 template <bool FIRST>
 __device__ __forceinline__ void frag_a_term(const uint8_t* sA, int sp, int wm, int g, int j,
-                                            uint32_t neg, Frags& f) {
+                                            double c, Frags& f) {
 #pragma unroll
     for (int ss = 0; ss < 2; ++ss) {
         const uint8_t* pa = frag_a_ptr(sA, ss, sp, wm, g, j);
@@ -131,28 +134,28 @@ __device__ __forceinline__ void frag_a_term(const uint8_t* sA, int sp, int wm, i
         for (int h = 0; h < 4; ++h) {
             const double2 v = *reinterpret_cast<const double2*>(pa + h * 2048);
             if (FIRST) {
-                f.a[ss][2 * h] = flip_sign(v.x, neg);
-                f.a[ss][2 * h + 1] = flip_sign(v.y, neg);
+                f.a[ss][2 * h] = v.x;
+                f.a[ss][2 * h + 1] = v.y;
             } else {
-                f.a[ss][2 * h] += flip_sign(v.x, neg);
-                f.a[ss][2 * h + 1] += flip_sign(v.y, neg);
+                f.a[ss][2 * h] = fma(c, v.x, f.a[ss][2 * h]);
+                f.a[ss][2 * h + 1] = fma(c, v.y, f.a[ss][2 * h + 1]);
             }
         }
     }
 }
 template <bool FIRST>
 __device__ __forceinline__ void frag_b_term(const uint8_t* sB, int sp, int wn, int g, int j,
-                                            uint32_t neg, Frags& f) {
+                                            double c, Frags& f) {
     const uint8_t* pb = frag_b_ptr(sB, sp, wn, g, j);
 #pragma unroll
     for (int nf = 0; nf < 4; ++nf) {
         const double2 v = *reinterpret_cast<const double2*>(pb + nf * 8 * 128);
         if (FIRST) {
-            f.b[0][nf] = flip_sign(v.x, neg);
-            f.b[1][nf] = flip_sign(v.y, neg);
+            f.b[0][nf] = v.x;
+            f.b[1][nf] = v.y;
         } else {
-            f.b[0][nf] += flip_sign(v.x, neg);
-            f.b[1][nf] += flip_sign(v.y, neg);
+            f.b[0][nf] = fma(c, v.x, f.b[0][nf]);
+            f.b[1][nf] = fma(c, v.y, f.b[1][nf]);
         }
     }
 }
@@ -201,15 +204,14 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         // ================= TMA warpgroup (warps 8-11; one lane issues) =======
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
         if (warp != kConsumerWarps || lane != 0) return;
-        uint32_t q = 0;
+        uint32_t s = 0, phase = 0;
         const int m0 = tm * kBM, n0 = tn * kBN;
         for (int p = 0; p < P.nprod; ++p) {
             const ProductDesc& pd = P.prod[p];
             for (int kt = 0; kt < P.ktiles; ++kt) {
                 const int k0 = kt * kBK;
-                for (int u = 0; u < pd.na + pd.nb; ++u, ++q) {
-                    const uint32_t s = q % kRawSlots;
-                    mbar_wait(&raw_empty[s], ((q / kRawSlots) & 1) ^ 1);
+                for (int u = 0; u < pd.na + pd.nb; ++u) {
+                    mbar_wait(&raw_empty[s], phase ^ 1);
                     mbar_expect_tx(&raw_full[s], kSlotBytes);
                     uint8_t* dst = raw + s * kSlotBytes;
                     if (u < pd.na) {
@@ -219,6 +221,10 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                             tma_load_2d(dst + box * 2048, map, m0 + 16 * box, k0, &raw_full[s]);
                     } else {
                         tma_load_2d(dst, &P.tmB[pd.bq[u - pd.na]], k0, n0, &raw_full[s]);
+                    }
+                    if (++s == kRawSlots) {
+                        s = 0;
+                        phase ^= 1;
                     }
                 }
             }
@@ -237,47 +243,80 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     const int wm = warp & 1, wn = warp >> 1;
     const int g = lane >> 2, j = lane & 3;
     double acc[8][4][2];
-    uint32_t q = 0;
+    // ring position of the next term tile: slot index and its fill parity
+    uint32_t slot = 0, phase = 0;
 
     for (int p = 0; p < P.nprod; ++p) {
         const ProductDesc& pd = P.prod[p];
         const int na = pd.na, nb = pd.nb;
-        uint32_t nega = 0, negb = 0;
-        for (int u = 0; u < na; ++u) nega |= (pd.as[u] < 0 ? 1u : 0u) << u;
-        for (int u = 0; u < nb; ++u) negb |= (pd.bs[u] < 0 ? 1u : 0u) << u;
+        const bool neg_a0 = pd.as[0] < 0, neg_b0 = pd.bs[0] < 0;  // warp-uniform
+        double ca[MAXT], cb[MAXT];
+#pragma unroll
+        for (int u = 0; u < MAXT; ++u) {
+            ca[u] = u < na ? static_cast<double>(pd.as[u]) : 0.0;
+            cb[u] = u < nb ? static_cast<double>(pd.bs[u]) : 0.0;
+        }
 #pragma unroll
         for (int mf = 0; mf < 8; ++mf)
 #pragma unroll
             for (int nf = 0; nf < 4; ++nf) acc[mf][nf][0] = acc[mf][nf][1] = 0.0;
 
         for (int kt = 0; kt < P.ktiles; ++kt) {
-            const uint32_t nq = na + nb;
-            for (uint32_t u = q; u < q + nq; ++u)
-                mbar_wait(&raw_full[u % kRawSlots], (u / kRawSlots) & 1);
+            // term tiles of this k-step: A terms, then B terms, in ring order
+            // (a k-step uses at most 2*MAXT <= 8 < kRawSlots slots: one wrap at most)
             const uint8_t* sA[MAXT];
             const uint8_t* sB[MAXT];
+            const uint32_t slot0 = slot;
 #pragma unroll
             for (int u = 0; u < MAXT; ++u) {
-                sA[u] = raw + ((q + u) % kRawSlots) * kSlotBytes;
-                sB[u] = raw + ((q + na + u) % kRawSlots) * kSlotBytes;
+                uint32_t sa = slot0 + u, sb = slot0 + na + u;
+                const uint32_t pa = (sa >= kRawSlots) ? phase ^ 1 : phase;
+                const uint32_t pb = (sb >= kRawSlots) ? phase ^ 1 : phase;
+                sa = (sa >= kRawSlots) ? sa - kRawSlots : sa;
+                sb = (sb >= kRawSlots) ? sb - kRawSlots : sb;
+                sA[u] = raw + sa * kSlotBytes;
+                sB[u] = raw + sb * kSlotBytes;
+                if (u < na) mbar_wait(&raw_full[sa], pa);
+                if (u < nb) mbar_wait(&raw_full[sb], pb);
+            }
+            slot += na + nb;
+            if (slot >= kRawSlots) {
+                slot -= kRawSlots;
+                phase ^= 1;
             }
 #pragma unroll
             for (int sp = 0; sp < 2; ++sp) {
                 Frags f;
-                frag_a_term<true>(sA[0], sp, wm, g, j, nega & 1, f);
-                frag_b_term<true>(sB[0], sp, wn, g, j, negb & 1, f);
+                frag_a_term<true>(sA[0], sp, wm, g, j, 1.0, f);
+                frag_b_term<true>(sB[0], sp, wn, g, j, 1.0, f);
+                if (neg_a0) {
+#pragma unroll
+                    for (int ss = 0; ss < 2; ++ss)
+#pragma unroll
+                        for (int mf = 0; mf < 8; ++mf) f.a[ss][mf] = -f.a[ss][mf];
+                }
+                if (neg_b0) {
+#pragma unroll
+                    for (int ss = 0; ss < 2; ++ss)
+#pragma unroll
+                        for (int nf = 0; nf < 4; ++nf) f.b[ss][nf] = -f.b[ss][nf];
+                }
 #pragma unroll
                 for (int u = 1; u < MAXT; ++u) {
-                    if (u < na) frag_a_term<false>(sA[u], sp, wm, g, j, (nega >> u) & 1, f);
-                    if (u < nb) frag_b_term<false>(sB[u], sp, wn, g, j, (negb >> u) & 1, f);
+                    if (u < na) frag_a_term<false>(sA[u], sp, wm, g, j, ca[u], f);
+                    if (u < nb) frag_b_term<false>(sB[u], sp, wn, g, j, cb[u], f);
                 }
                 dmma_substep(f, 0, acc);
                 dmma_substep(f, 1, acc);
             }
             __syncwarp();
-            if (lane == 0)
-                for (uint32_t u = q; u < q + nq; ++u) mbar_arrive(&raw_empty[u % kRawSlots]);
-            q += nq;
+            if (lane == 0) {
+                uint32_t s2 = slot0;
+                for (int u = 0; u < na + nb; ++u) {
+                    mbar_arrive(&raw_empty[s2]);
+                    if (++s2 == kRawSlots) s2 = 0;
+                }
+            }
         }
 
         // ---- epilogue of product p.  Accumulator (mf, nf, e) of lane (g, j)
