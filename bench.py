@@ -4,7 +4,7 @@
 One step = one strassen_gemm call (C := alpha A B + C) on the workload
 m = n = k = 16384, column-major fp64, uniform[-1, 1) synthetic inputs
 (BASELINE.json configs[1], top of the square sweep; it fits one GPU).
-Default variant: ABC, two levels.  Prints ONE JSON line on rank 0.
+Default variant: ABC, one level.  Prints ONE JSON line on rank 0.
 
   value     effective FP64 TFLOP/s (2mnk / t, summed over ranks), device
             pointers, inputs resident in HBM, CUDA events on the launch stream
@@ -42,7 +42,7 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
     p.add_argument("--variant", default="abc", choices=["dgemm", "abc", "ab", "naive"])
-    p.add_argument("--level", type=int, default=2)
+    p.add_argument("--level", type=int, default=1)
     p.add_argument("--dim", type=int, default=16384)
     p.add_argument("--m", type=int, default=0)
     p.add_argument("--n", type=int, default=0)
