@@ -50,7 +50,12 @@ typedef enum strassen_variant {
     STRASSEN_DGEMM = 0, /* classical gemm; level must be 0 */
     STRASSEN_ABC = 1,   /* operand sums formed on chip, multi-destination epilogue */
     STRASSEN_AB = 2,    /* operand sums on chip, products to temporaries, streamed C */
-    STRASSEN_NAIVE = 3  /* operand sums and products materialised */
+    STRASSEN_NAIVE = 3, /* operand sums and products materialised */
+    /* B200 addition (not in the reference): operand sums materialised by one
+     * batched HBM pass, C updates fused in the epilogue (no product
+     * temporaries) -- the fourth point of the paper's fusion design space,
+     * and the fastest two-level form on B200. */
+    STRASSEN_C = 4
 } strassen_variant;
 
 /* reference strassen.h:32-35.  Kept for ABI parity: validated exactly like the

@@ -26,8 +26,8 @@ __all__ = [
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libstrassen_b200.so")
 
-DGEMM, ABC, AB, NAIVE = 0, 1, 2, 3
-VARIANT_NAMES = {"dgemm": DGEMM, "abc": ABC, "ab": AB, "naive": NAIVE}
+DGEMM, ABC, AB, NAIVE, C_VARIANT = 0, 1, 2, 3, 4
+VARIANT_NAMES = {"dgemm": DGEMM, "abc": ABC, "ab": AB, "naive": NAIVE, "c": C_VARIANT}
 
 OK, ERR_DIMENSION, ERR_PARAM, ERR_DOMAIN, ERR_ALLOC, ERR_NULL, ERR_DEVICE = range(7)
 

@@ -141,6 +141,15 @@ void count_call(strassen_variant variant, int level, long m, long n, long k,
             five_loop(qm, qn, qk, a, b, d, bp, c);
             continue;
         }
+        if (variant == STRASSEN_C) {  // B200 addition: Naive's sums, ABC's fused C
+            if (e.a.size() > 1)
+                materialize(e.a.size(), qm, qk, c.a_plus_passes, c.a_plus_elems, c.a_plus_flops);
+            if (e.b.size() > 1)
+                materialize(e.b.size(), qk, qn, c.b_plus_passes, c.b_plus_elems, c.b_plus_flops);
+            five_loop(qm, qn, qk, {e.a.size() > 1 ? Ext{qm, qk} : a[0]},
+                      {e.b.size() > 1 ? Ext{qk, qn} : b[0]}, d, bp, c);
+            continue;
+        }
         if (variant == STRASSEN_AB) {
             five_loop(qm, qn, qk, a, b, {{qm, qn}}, bp, c);
         } else {

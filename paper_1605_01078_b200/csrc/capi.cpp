@@ -62,7 +62,7 @@ strassen_status check_variant_level(strassen_variant variant, int level) {
 
 void validate_call(strassen_variant variant, long m, long n, long k, const strassen_blocking& bp) {
     if (variant != STRASSEN_DGEMM && variant != STRASSEN_ABC && variant != STRASSEN_AB &&
-        variant != STRASSEN_NAIVE)
+        variant != STRASSEN_NAIVE && variant != STRASSEN_C)
         throw std::invalid_argument("unknown variant");
     if (m < 1 || n < 1 || k < 1) throw std::invalid_argument("gemm: dimensions must be >= 1");
     sb200::validate_blocking(bp);

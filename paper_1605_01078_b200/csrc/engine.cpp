@@ -128,6 +128,8 @@ QuadView c_quad(const DView& C, long qm, long qn, long I, long J) {
     return q;
 }
 
+int side_of(int level) { return 1 << level; }
+
 const Program& program(int level) {
     static const Program p0 = identity_program();
     return level == 0 ? p0 : program_for_level(level);
@@ -276,6 +278,63 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
         live.push_back(std::move(l));
     }
     if (live.empty()) return launches;
+
+    if (variant == STRASSEN_C) {
+        // C variant (B200 addition): every multi-term operand sum materialised
+        // by one batched HBM pass, then one mm_kernel over all 7^L products
+        // with single-term operands and the fused multi-destination epilogue.
+        const long long lda_t = ((qm + 3) / 4) * 4, ldb_t = ((qk + 3) / 4) * 4;
+        int na_sums = 0, nb_sums = 0;
+        for (const Live& l : live) {
+            na_sums += l.a.size() > 1;
+            nb_sums += l.b.size() > 1;
+        }
+        double* TA = e.ensure(e.tabuf, static_cast<size_t>(std::max(na_sums, 1)) * lda_t * qk * 8);
+        double* TB = e.ensure(e.tbbuf, static_cast<size_t>(std::max(nb_sums, 1)) * ldb_t * qn * 8);
+        for (int side = 0; side < 2; ++side) {
+            SumBatchParams* SB = new SumBatchParams;  // ~10 KB: keep off the stack
+            std::memset(SB, 0, sizeof(*SB));
+            const TmaOperand& t = side == 0 ? ta : tb;
+            SB->rows = side == 0 ? qm : qk;
+            SB->cols = side == 0 ? qk : qn;
+            SB->ld = side == 0 ? lda_t : ldb_t;
+            int next_map = kMaxQuad;
+            for (size_t p = 0; p < live.size(); ++p) {
+                Terms& terms = side == 0 ? live[p].a : live[p].b;
+                if (terms.size() <= 1) continue;  // single term: the quadrant map, sign in-kernel
+                const int z = SB->njobs++;
+                double* dst = (side == 0 ? TA : TB) + static_cast<size_t>(z) * SB->ld * SB->cols;
+                SB->dst[z] = dst;
+                SB->nterms[z] = static_cast<int>(terms.size());
+                for (size_t u = 0; u < terms.size(); ++u) {
+                    const int qi = terms[u].first;
+                    SumTerm& st = SB->t[z][u];
+                    st.x = quad_origin(t, qi / side_of(L), qi % side_of(L));
+                    st.rows = static_cast<int>(quad_rows(t, qi / side_of(L)));
+                    st.cols = static_cast<int>(quad_cols(t, qi % side_of(L)));
+                    st.ld = t.ld;
+                    st.coeff = terms[u].second;
+                }
+                const int mi = next_map++;
+                if (side == 0)
+                    encode_map(&P.tmA[mi], dst, qm, qk, lda_t, 16, kBK, true);
+                else
+                    encode_map(&P.tmB[mi], dst, qk, qn, ldb_t, kBK, kBN, true);
+                terms = {{mi, 1}};
+            }
+            cudaError_t err = launch_sum_batch(*SB, s);
+            const int njobs = SB->njobs;
+            delete SB;
+            ck(err, "sum_batch");
+            if (njobs) ++launches;
+        }
+        P.mode = kEpiRMW;
+        P.nprod = static_cast<int>(live.size());
+        P.direct = 1;
+        for (size_t p = 0; p < live.size(); ++p) fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);
+        ck(launch_mm(P, s), "mm_kernel (C)");
+        return launches + 1;
+    }
 
     if (variant == STRASSEN_DGEMM || variant == STRASSEN_ABC) {
         P.mode = kEpiRMW;

@@ -417,6 +417,29 @@ __global__ void materialize_kernel(const SumParams P) {
     }
 }
 
+// -------------------------------------------------------------- sum batch ---
+// C variant: all multi-term operand sums of a launch, one job per blockIdx.z.
+// Same arithmetic as materialize_kernel (variants.cpp:53-96 order).
+__global__ void sum_batch_kernel(const __grid_constant__ SumBatchParams P) {
+    const int z = blockIdx.z;
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= P.rows) return;
+    const int n = P.nterms[z];
+    double* dst = P.dst[z];
+    for (long long j = blockIdx.y; j < P.cols; j += gridDim.y) {
+        double v = 0.0;
+#pragma unroll
+        for (int u = 0; u < kMaxTerms; ++u) {
+            if (u >= n) break;
+            const SumTerm& t = P.t[z][u];
+            const double x = (i < t.rows && j < t.cols) ? t.x[i + j * t.ld] : 0.0;
+            const double c = t.coeff;
+            v = (u == 0) ? c * x : fma(c, x, v);
+        }
+        dst[i + j * P.ld] = v;
+    }
+}
+
 // --------------------------------------------------------- stream update ---
 // C_q(i, j) += sum over (p, gamma) feeding q, in table order, of
 // (alpha * gamma) * M_p(i, j)  (variants.cpp:99-109, applied entry by entry).
@@ -490,6 +513,14 @@ static unsigned col_grid(long long cols) {
 cudaError_t launch_materialize(const SumParams& p, cudaStream_t s) {
     dim3 grid(static_cast<unsigned>((p.rows + 255) / 256), col_grid(p.cols));
     materialize_kernel<<<grid, 256, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sum_batch(const SumBatchParams& p, cudaStream_t s) {
+    if (p.njobs == 0) return cudaSuccess;
+    dim3 grid(static_cast<unsigned>((p.rows + 255) / 256),
+              static_cast<unsigned>(p.cols < 2048 ? p.cols : 2048), p.njobs);
+    sum_batch_kernel<<<grid, 256, 0, s>>>(p);
     return cudaGetLastError();
 }
 

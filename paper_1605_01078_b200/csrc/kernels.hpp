@@ -13,6 +13,7 @@ constexpr int kBM = 128;            // CTA tile rows (logical quadrant rows)
 constexpr int kBN = 128;            // CTA tile cols
 constexpr int kBK = 16;             // k per pipeline step
 constexpr int kMaxQuad = 16;        // 2^L x 2^L quadrants, L <= 2
+constexpr int kMaxMaps = 64;        // tensor maps per side: 16 quadrants + materialised sums
 constexpr int kMaxProducts = 49;    // 7^L
 constexpr int kMaxTerms = 4;        // operand terms / destinations per product at L <= 2
 constexpr int kConsumerWarps = 8;   // 2 warpgroups; 2 (m) x 4 (n) warps of 64 x 32
@@ -44,8 +45,8 @@ enum EpilogueMode : int {
 };
 
 struct alignas(64) MMParams {
-    CUtensorMap tmA[kMaxQuad];  // per A quadrant: dims (rows, cols), box 128 x 16
-    CUtensorMap tmB[kMaxQuad];  // per B quadrant: dims (k rows, n cols), box 16 x 128, swizzle 128B
+    CUtensorMap tmA[kMaxMaps];  // A operands: dims (rows, cols), box 16 x 16, swizzle 128B
+    CUtensorMap tmB[kMaxMaps];  // B operands: dims (k rows, n cols), box 16 x 128, swizzle 128B
     ProductDesc prod[kMaxProducts];
     double* cptr[kMaxQuad];     // C quadrant views (clipped)
     int crows[kMaxQuad];
@@ -71,6 +72,25 @@ cudaError_t launch_mm(const MMParams& p, cudaStream_t s);
 // offsets); dst column-major with leading dimension ld.
 cudaError_t launch_repack(const double* src, long long rs, long long cs, long rows, long cols,
                           double* dst, long long ld, long q, long q_al, cudaStream_t s);
+
+// ---- C variant: materialise many operand sums in one launch ----------------
+// job z: dst_z(i, j) = sum_u c_u X_{z,u}(i, j) over a rows x cols logical extent,
+// zero outside each term's clipped view; sources column-major (rs = 1).
+constexpr int kMaxSumJobs = 98;
+struct SumTerm {
+    const double* x;
+    int rows, cols;
+    long long ld;
+    int coeff;
+};
+struct SumBatchParams {
+    SumTerm t[kMaxSumJobs][kMaxTerms];
+    double* dst[kMaxSumJobs];
+    int nterms[kMaxSumJobs];
+    int njobs;
+    long long rows, cols, ld;
+};
+cudaError_t launch_sum_batch(const SumBatchParams& p, cudaStream_t s);
 
 // ---- Naive: materialise an operand sum ------------------------------------
 struct SumParams {

@@ -3,7 +3,9 @@ import numpy as np
 
 import oracle_lib as O
 
-CONFIGS = [("dgemm", 0), ("abc", 1), ("ab", 1), ("naive", 1), ("abc", 2), ("ab", 2), ("naive", 2)]
+# the reference's seven configurations plus the B200 "C" variant at both levels
+CONFIGS = [("dgemm", 0), ("abc", 1), ("ab", 1), ("naive", 1), ("abc", 2), ("ab", 2), ("naive", 2),
+           ("c", 1), ("c", 2)]
 # BASELINE.json north star: normwise ||C - C_ref||_F / (||A||_F ||B||_F)
 NORMWISE_TOL = {0: 1e-12, 1: 1e-12, 2: 5e-12}
 # the reference's own tolerance on rel_frobenius_error (test_capi.cpp:92, test_strassen.cpp:79)

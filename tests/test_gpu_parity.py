@@ -67,7 +67,7 @@ def test_variants_agree_pairwise(ctx):
     a, b, c0 = inputs(m, n, k, (5, 6, 7), "row")
     for L in (1, 2):
         abc = run(ctx, "abc", L, 1.0, a, b, c0)
-        for v in ("ab", "naive"):
+        for v in ("ab", "naive", "c"):
             other = run(ctx, v, L, 1.0, a, b, c0)
             assert O.rel_frobenius_error(other, abc) < 1e-12
 
@@ -197,7 +197,7 @@ def test_rank_b_schedule(ctx):
     k, bw = 256, 64
     a, b, c0 = inputs(m, n, k, (31, 32, 33), "row")
     ref = oracle_result("dgemm", 0, 1.0, a, b, c0, use_reference_gemm=True)
-    for v, L in [("abc", 1), ("abc", 2), ("ab", 2)]:
+    for v, L in [("abc", 1), ("abc", 2), ("ab", 2), ("c", 2)]:
         c = c0.copy()
         for p0 in range(0, k, bw):
             ctx.gemm(v, L, 1.0, a[:, p0:p0 + bw], b[p0:p0 + bw, :], c)
@@ -248,7 +248,7 @@ def test_full_size_strassen_vs_classical(ctx, dim):
     an, bn = torch.linalg.norm(A).item(), torch.linalg.norm(B).item()
     a_h, b_h, c0_h = A.cpu().numpy(), B.cpu().numpy(), C0.cpu().numpy()
     assert freivalds(1.0, a_h, b_h, c0_h, base.cpu().numpy()) < 1e-15
-    for v, L in [("abc", 1), ("abc", 2), ("ab", 2)]:
+    for v, L in [("abc", 1), ("abc", 2), ("ab", 2), ("c", 1), ("c", 2), ("naive", 2)]:
         C = C0.clone()
         ctx.gemm_device(v, L, 1.0, A, B, C)
         torch.cuda.synchronize()
