@@ -16,9 +16,12 @@ Default variant: ABC, one level.  Prints ONE JSON line on rank 0.
             reference sources with its own flags) on a bounded sample
   --impl reference  times that reference CPU path alone (rank 0).
 
-Multi-GPU (torchrun, N > 1): every rank runs its own 16384^3 instance
-("replicas", weak scaling); time = max over ranks.  The SUMMA distributed
-layer is benchmarked separately.
+Multi-GPU (torchrun, N > 1): SUMMA over NCCL (paper_1605_01078_b200/summa.py),
+weak scaling.  The pr x pc grid comes from grid_for(N) (1x2, 2x2, 2x4).  Rank
+(i, j) owns a 16384 x 16384 block of C, and the global problem is
+m = 16384*pr, n = 16384*pc, k = 16384.  A panels are broadcast along rows and
+B panels along columns, overlapped with the local Strassen rank-b updates.
+Every rank therefore does one 16384^3 of work per step; time = max over ranks.
 """
 import argparse
 import json
@@ -218,9 +221,11 @@ def main():
         x.uniform_(-1.0, 1.0, generator=g)
         return x.t()  # (r, c) with strides (1, r)
 
-    A, B, C = colmajor(m, k), colmajor(k, n), colmajor(m, n)
     ctx = S.Ctx()
     stream = torch.cuda.current_stream()
+    if world > 1:
+        return run_summa(args, rank, world, local, colmajor, barrier, max_over_ranks)
+    A, B, C = colmajor(m, k), colmajor(k, n), colmajor(m, n)
 
     def time_device(variant, level, steps, warmup):
         for _ in range(warmup):
@@ -330,6 +335,65 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_summa(args, rank, world, local, colmajor, barrier, max_over_ranks):
+    """N > 1: SUMMA weak scaling with 16384^2 C blocks per rank (see module doc)."""
+    import torch
+
+    from paper_1605_01078_b200 import summa as SU
+    L = SU.make_layout(args.m * SU.grid_for(world)[0], args.n * SU.grid_for(world)[1], args.k,
+                       world)
+    comm = SU.TorchComm(L)
+    A_l, B_l, C_l = colmajor(L.m_l, L.k_c), colmajor(L.k_r, L.n_l), colmajor(L.m_l, L.n_l)
+    step = lambda: SU.summa(L, comm, A_l, B_l, C_l, 1.0, args.variant, args.level)  # noqa: E731
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    flops = 2.0 * L.m * L.n * L.k
+    line = {
+        "metric": "effective FP64 TFLOPS (2mnk/t)", "value": flops / (ms * 1e-3) / 1e12,
+        "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic uniform[-1,1) (torch generator, column-major)",
+        "config": {"workload": f"SUMMA m={L.m} n={L.n} k={L.k} on {L.pr}x{L.pc} GPUs "
+                               f"(16384^2 C block per rank)", "variant": args.variant,
+                   "level": args.level, "m": L.m, "n": L.n, "k": L.k, "panel_b": L.b,
+                   "grid": [L.pr, L.pc], "parallelism": f"summa{L.pr}x{L.pc}",
+                   "l2": "inputs larger than the 126 MB L2"},
+        "clocks": clk.summary(),
+        "gpu_launches": L.panels * args.steps,
+    }
+    if not args.no_e2e:
+        # end to end: pinned host blocks in, C block out, around one SUMMA step
+        Ah, Bh, Ch = (x.t().cpu().pin_memory().t() for x in (A_l, B_l, C_l))
+        barrier()
+        t0 = time.perf_counter()
+        A_l.copy_(Ah, non_blocking=True)
+        B_l.copy_(Bh, non_blocking=True)
+        C_l.copy_(Ch, non_blocking=True)
+        step()
+        Ch.copy_(C_l)
+        torch.cuda.synchronize()
+        dt = max_over_ranks(time.perf_counter() - t0)
+        line["e2e"] = {"value": flops / dt / 1e12, "unit": "TFLOP/s",
+                       "h2d_bytes_per_step": world * 8 * (L.m_l * L.k_c + L.k_r * L.n_l + L.m_l * L.n_l),
+                       "d2h_bytes_per_step": world * 8 * L.m_l * L.n_l, "ms_per_step": dt * 1e3,
+                       "api": "summa() over strassen_gemm_device, pinned host blocks"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    import torch.distributed as dist
+    dist.destroy_process_group()
 
 
 if __name__ == "__main__":

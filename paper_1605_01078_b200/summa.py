@@ -1,0 +1,221 @@
+"""SUMMA distributed layer: Strassen DGEMM sharded over the GPUs of one node.
+
+The paper's distributed experiment runs SUMMA on a 2-D process grid,
+with local one/two-level ABC Strassen as the rank-b update. The reference stops at an
+in-process rank-b schedule (tools/bench_lib.cpp:56-71). SURVEY.md §8(e) is the
+design followed here.
+
+* Process grid pr x pc, chosen by :func:`grid_for` (P=2 -> 1x2, 4 -> 2x2, 8 -> 2x4).
+  Rank r sits at (r // pc, r % pc).
+* 2-D block distribution. Rank (i, j) owns
+  A_ij = A[i*m_l:(i+1)*m_l, j*k_c:(j+1)*k_c]   (m_l = m/pr, k_c = k/pc)
+  B_ij = B[i*k_r:(i+1)*k_r, j*n_l:(j+1)*n_l]   (k_r = k/pr, n_l = n/pc)
+  C_ij = C[i*m_l:(i+1)*m_l, j*n_l:(j+1)*n_l]
+* One exchange step per k-panel p of width b:
+  * the rank in process row i owning A columns [p*b, (p+1)*b) broadcasts that
+    m_l x b slice along row i;
+  * the rank in process column j owning B rows [p*b, (p+1)*b) broadcasts that
+    b x n_l slice along column j.
+  Then every rank runs C_ij += alpha * A_panel @ B_panel locally, with the chosen variant
+  and level (strassen_gemm_device on the current CUDA stream).
+* Broadcasts for panel p+1 are issued asynchronously before the local update of panel p,
+  into the other of two panel buffers, so communication overlaps compute.
+
+Communicators:
+
+* :class:`TorchComm` uses torch.distributed with one process per GPU. Row and column
+  groups come from ``new_group``. NCCL runs over NVLink/NVSwitch; gloo runs on CPU for the
+  tests.
+* :func:`summa_loopback` runs P virtual ranks in ONE process. Each "broadcast" is a device
+  copy and the ranks execute one after another. It exercises the full data path and the
+  real kernels on a single GPU; nothing waits on another launch.
+
+The local update is pluggable (``local_gemm``), so the host-side distribution logic can be
+checked on CPU against a dense product.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Callable, List, Optional
+
+import torch
+
+
+def grid_for(p: int):
+    """Most-square pr x pc grid with pr <= pc (1x2, 2x2, 2x4)."""
+    pr = int(math.isqrt(p))
+    while p % pr:
+        pr -= 1
+    return pr, p // pr
+
+
+@dataclass
+class Layout:
+    m: int
+    n: int
+    k: int
+    pr: int
+    pc: int
+    b: int  # panel width
+
+    @property
+    def m_l(self):
+        return self.m // self.pr
+
+    @property
+    def n_l(self):
+        return self.n // self.pc
+
+    @property
+    def k_c(self):  # A columns per rank
+        return self.k // self.pc
+
+    @property
+    def k_r(self):  # B rows per rank
+        return self.k // self.pr
+
+    @property
+    def panels(self):
+        return self.k // self.b
+
+    def a_owner_col(self, p):
+        """Process column owning A panel p, and the local column offset."""
+        g = p * self.b
+        return g // self.k_c, g % self.k_c
+
+    def b_owner_row(self, p):
+        g = p * self.b
+        return g // self.k_r, g % self.k_r
+
+
+def make_layout(m, n, k, p, b=None):
+    pr, pc = grid_for(p)
+    if m % pr or n % pc or k % pr or k % pc:
+        raise ValueError(f"m={m}, n={n}, k={k} must divide the {pr}x{pc} grid")
+    step = math.gcd(k // pr, k // pc)  # a panel must not straddle an owner boundary
+    if b is None:
+        b = step
+        while b > 4096 and b % 2 == 0:  # bound the panel buffers
+            b //= 2
+    if step % b:
+        raise ValueError(f"panel width {b} must divide gcd(k/pr, k/pc) = {step}")
+    return Layout(m, n, k, pr, pc, b)
+
+
+def local_blocks(layout: Layout, rank: int, A: torch.Tensor, B: torch.Tensor, C: torch.Tensor):
+    """Slices of global A, B, C owned by `rank` (for tests and data set-up)."""
+    i, j = divmod(rank, layout.pc)
+    a = A[i * layout.m_l:(i + 1) * layout.m_l, j * layout.k_c:(j + 1) * layout.k_c]
+    b = B[i * layout.k_r:(i + 1) * layout.k_r, j * layout.n_l:(j + 1) * layout.n_l]
+    c = C[i * layout.m_l:(i + 1) * layout.m_l, j * layout.n_l:(j + 1) * layout.n_l]
+    return a, b, c
+
+
+# ------------------------------------------------------------- communicators
+class TorchComm:
+    """torch.distributed (NCCL on GPUs, gloo on CPU) with row/column groups."""
+
+    def __init__(self, layout: Layout):
+        import torch.distributed as dist
+        self.dist = dist
+        self.rank = dist.get_rank()
+        self.world = dist.get_world_size()
+        if self.world != layout.pr * layout.pc:
+            raise ValueError("world size does not match the process grid")
+        self.layout = layout
+        self.i, self.j = divmod(self.rank, layout.pc)
+        # every rank must create every group, in the same order
+        self.row_groups = [dist.new_group([r * layout.pc + c for c in range(layout.pc)])
+                           for r in range(layout.pr)]
+        self.col_groups = [dist.new_group([r * layout.pc + c for r in range(layout.pr)])
+                           for c in range(layout.pc)]
+
+    def bcast_row(self, t: torch.Tensor, src_col: int):
+        """Broadcast along this rank's process row from column src_col (async)."""
+        if self.layout.pc == 1:
+            return None
+        return self.dist.broadcast(t, src=self.i * self.layout.pc + src_col,
+                                   group=self.row_groups[self.i], async_op=True)
+
+    def bcast_col(self, t: torch.Tensor, src_row: int):
+        if self.layout.pr == 1:
+            return None
+        return self.dist.broadcast(t, src=src_row * self.layout.pc + self.j,
+                                   group=self.col_groups[self.j], async_op=True)
+
+
+def _default_local_gemm(variant, level):
+    import paper_1605_01078_b200 as S
+    ctx = S.Ctx()
+
+    def run(alpha, a, b, c):
+        if c.is_cuda:
+            ctx.gemm_device(variant, level, alpha, a, b, c)
+        else:
+            ctx.gemm(variant, level, alpha, a, b, c)
+    return run
+
+
+def summa(layout: Layout, comm: TorchComm, A_l: torch.Tensor, B_l: torch.Tensor,
+          C_l: torch.Tensor, alpha: float = 1.0, variant="abc", level=1,
+          local_gemm: Optional[Callable] = None) -> int:
+    """C_l += alpha * (A @ B)_ij on rank (i, j) of a torch.distributed job.
+
+    A_l (m_l x k_c), B_l (k_r x n_l), C_l (m_l x n_l) are the rank's blocks. The panel
+    buffers are column-major, so the local Strassen call reads them through TMA without a
+    repack. Returns the number of local updates.
+    """
+    L = layout
+    gemm = local_gemm or _default_local_gemm(variant, level)
+    dev = C_l.device
+
+    # contiguous storage for the collectives, column-major views for the kernels
+    abase = [torch.empty((L.b, L.m_l), dtype=torch.float64, device=dev) for _ in range(2)]
+    bbase = [torch.empty((L.n_l, L.b), dtype=torch.float64, device=dev) for _ in range(2)]
+    abuf = [t.t() for t in abase]
+    bbuf = [t.t() for t in bbase]
+
+    def post(p):
+        s = p % 2
+        ac, aoff = L.a_owner_col(p)
+        br, boff = L.b_owner_row(p)
+        if comm.j == ac:
+            abuf[s].copy_(A_l[:, aoff:aoff + L.b])
+        if comm.i == br:
+            bbuf[s].copy_(B_l[boff:boff + L.b, :])
+        return [w for w in (comm.bcast_row(abase[s], ac), comm.bcast_col(bbase[s], br)) if w]
+
+    pending = post(0)
+    for p in range(L.panels):
+        nxt = post(p + 1) if p + 1 < L.panels else []
+        for w in pending:
+            w.wait()
+        gemm(alpha, abuf[p % 2], bbuf[p % 2], C_l)
+        pending = nxt
+    return L.panels
+
+
+def summa_loopback(layout: Layout, A_blocks: List[torch.Tensor], B_blocks: List[torch.Tensor],
+                   C_blocks: List[torch.Tensor], alpha: float = 1.0, variant="abc", level=1,
+                   local_gemm: Optional[Callable] = None) -> int:
+    """The same schedule with P virtual ranks in one process.
+
+    Each "broadcast" is a copy from the owner's block, and ranks run one after another on
+    one device. Nothing waits on another launch, so a single GPU can run it safely.
+    """
+    L = layout
+    gemm = local_gemm or _default_local_gemm(variant, level)
+    P = L.pr * L.pc
+    dev = C_blocks[0].device
+    abuf = torch.empty((L.b, L.m_l), dtype=torch.float64, device=dev).t()
+    bbuf = torch.empty((L.n_l, L.b), dtype=torch.float64, device=dev).t()
+    for p in range(L.panels):
+        ac, aoff = L.a_owner_col(p)
+        br, boff = L.b_owner_row(p)
+        for r in range(P):
+            i, j = divmod(r, L.pc)
+            abuf.copy_(A_blocks[i * L.pc + ac][:, aoff:aoff + L.b])   # row-i broadcast
+            bbuf.copy_(B_blocks[br * L.pc + j][boff:boff + L.b, :])   # column-j broadcast
+            gemm(alpha, abuf, bbuf, C_blocks[r])
+    return L.panels

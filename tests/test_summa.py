@@ -1,0 +1,118 @@
+"""SUMMA distributed layer: host-side logic on CPU (gloo, world sizes 2/4) and
+a single-process loopback; the GPU loopback with the real kernels is -m gpu."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1605_01078_b200 import summa as SU
+
+
+def dense(m, n, k, seed):
+    g = torch.Generator().manual_seed(seed)
+    A = torch.rand(m, k, dtype=torch.float64, generator=g) * 2 - 1
+    B = torch.rand(k, n, dtype=torch.float64, generator=g) * 2 - 1
+    C = torch.rand(m, n, dtype=torch.float64, generator=g) * 2 - 1
+    return A, B, C
+
+
+def matmul_update(alpha, a, b, c):
+    c.add_(alpha * (a @ b))
+
+
+def test_grids_and_layout():
+    assert SU.grid_for(1) == (1, 1)
+    assert SU.grid_for(2) == (1, 2)
+    assert SU.grid_for(4) == (2, 2)
+    assert SU.grid_for(8) == (2, 4)
+    L = SU.make_layout(64, 96, 48, 8, b=4)
+    assert (L.pr, L.pc, L.m_l, L.n_l, L.k_c, L.k_r, L.panels) == (2, 4, 32, 24, 12, 24, 12)
+    assert L.a_owner_col(5) == (1, 8)   # k columns 20..23 live on process column 1
+    assert L.b_owner_row(7) == (1, 4)   # k rows 28..31 live on process row 1
+    with pytest.raises(ValueError):
+        SU.make_layout(64, 96, 48, 8, b=5)
+    with pytest.raises(ValueError):
+        SU.make_layout(63, 96, 48, 8)
+
+
+@pytest.mark.parametrize("P", [1, 2, 4, 8])
+def test_loopback_schedule_matches_dense(P):
+    m, n, k = 48, 40, 64
+    A, B, C = dense(m, n, k, 7)
+    want = C + 0.5 * (A @ B)
+    L = SU.make_layout(m, n, k, P, b=4)
+    blocks = [SU.local_blocks(L, r, A, B, C) for r in range(P)]
+    Cb = [c.clone() for _, _, c in blocks]
+    SU.summa_loopback(L, [a for a, _, _ in blocks], [b for _, b, _ in blocks], Cb, alpha=0.5,
+                      local_gemm=matmul_update)
+    for r in range(P):
+        _, _, wc = SU.local_blocks(L, r, A, B, want)
+        assert torch.allclose(Cb[r], wc, rtol=0, atol=1e-12)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, m, n, k, b, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A, B, C = dense(m, n, k, 11)
+        L = SU.make_layout(m, n, k, world, b=b)
+        comm = SU.TorchComm(L)
+        a, bb, c = SU.local_blocks(L, rank, A, B, C)
+        c = c.clone()
+        panels = SU.summa(L, comm, a.contiguous(), bb.contiguous(), c, alpha=-1.0,
+                          local_gemm=matmul_update)
+        want = C - A @ B
+        _, _, wc = SU.local_blocks(L, rank, A, B, want)
+        q.put((rank, panels, float((c - wc).abs().max())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,b", [(2, 8), (4, 4), (4, 16)])
+def test_summa_gloo_matches_dense(world, b):
+    m, n, k = 32, 48, 64
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, m, n, k, b, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(world))
+    assert [r for r, _, _ in res] == list(range(world))
+    for _, panels, err in res:
+        assert panels == k // b
+        assert err < 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P,variant,level", [(2, "abc", 1), (4, "abc", 2), (8, "c", 2)])
+def test_loopback_on_gpu_with_strassen_kernels(cuda, P, variant, level):
+    """Full SUMMA data path with the real sm_100a kernels (virtual ranks, one GPU)."""
+    m, n, k = 1024, 2048, 2048
+    A, B, C = (x.to(cuda) for x in dense(m, n, k, 3))
+    L = SU.make_layout(m, n, k, P, b=256)
+    blocks = [SU.local_blocks(L, r, A, B, C) for r in range(P)]
+    Cb = [c.t().contiguous().t() for _, _, c in blocks]  # column-major C blocks
+    SU.summa_loopback(L, [a for a, _, _ in blocks], [b for _, b, _ in blocks], Cb,
+                      variant=variant, level=level)
+    torch.cuda.synchronize()
+    want = C + A @ B
+    an, bn = torch.linalg.norm(A).item(), torch.linalg.norm(B).item()
+    for r in range(P):
+        _, _, wc = SU.local_blocks(L, r, A, B, want)
+        nw = (torch.linalg.norm(Cb[r] - wc) / (an * bn)).item()
+        assert nw <= (1e-12 if level == 1 else 5e-12), (r, nw)

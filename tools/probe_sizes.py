@@ -19,12 +19,14 @@ proc = subprocess.Popen(["nvidia-smi", "--query-gpu=clocks.sm,power.draw,clocks_
                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=subprocess.PIPE,
                         stderr=subprocess.DEVNULL, text=True)
 threading.Thread(target=lambda: [clk.append(l.strip()) for l in proc.stdout], daemon=True).start()
-for dim in [int(x) for x in sys.argv[1].split(",")]:
-    g = torch.Generator(device="cuda").manual_seed(dim)
-    A = (torch.rand(dim, dim, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
-    B = (torch.rand(dim, dim, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
-    C0 = (torch.rand(dim, dim, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
-    x = torch.rand(dim, 1, dtype=torch.float64, device="cuda", generator=g)
+for spec in sys.argv[1].split(","):
+    m, n, k = (int(v) for v in spec.split("x")) if "x" in spec else (int(spec),) * 3
+    dim = spec
+    g = torch.Generator(device="cuda").manual_seed(m + n + k)
+    A = (torch.rand(k, m, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    B = (torch.rand(n, k, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    C0 = (torch.rand(n, m, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    x = torch.rand(n, 1, dtype=torch.float64, device="cuda", generator=g)
     want = C0 @ x + A @ (B @ x)
     for vl in variants:
         v, L = vl[:-1], int(vl[-1])
@@ -42,7 +44,7 @@ for dim in [int(x) for x in sys.argv[1].split(",")]:
         ms = statistics.median(times)
         err = (torch.linalg.norm(C @ x - want) /
                (torch.linalg.norm(A) * torch.linalg.norm(B) * torch.linalg.norm(x))).item()
-        print(f"{dim} {vl}: {ms:.3f} ms  {2*dim**3/ms/1e9:.2f} TF/s  (min {min(times):.3f})  "
+        print(f"{dim} {vl}: {ms:.3f} ms  {2*m*n*k/ms/1e9:.2f} TF/s  (min {min(times):.3f})  "
               f"freivalds {err:.2e}  launches {ctx.last_launches()}", flush=True)
 proc.terminate()
 sm = [float(l.split(",")[0]) for l in clk if l and l.split(",")[0].strip().replace(".", "").isdigit()]
