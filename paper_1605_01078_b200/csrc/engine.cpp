@@ -179,6 +179,7 @@ void Engine::init() {
     if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
         throw Error(STRASSEN_ERR_DEVICE, "no CUDA device");
     ck(cudaGetDevice(&device), "cudaGetDevice");
+    ck(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device), "SM count");
     initialised = true;
 }
 
@@ -216,6 +217,63 @@ bool is_device_pointer(const void* p) {
         return false;
     }
     return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+// Fused launch of P (ABC / DGEMM / C): tile ownership with the multi-destination
+// epilogue, or -- when the output has fewer than two waves of tiles -- split
+// mode: one CTA per (tile, product, k-chunk) into L2-resident partials M_{p,s},
+// then one deterministic stream pass (partials summed in s order, destinations
+// applied in table order).
+long launch_fused(Engine& e, cudaStream_t s, MMParams& P, const std::vector<Terms>& dests,
+                  const std::vector<QuadView>& cq, const DView& C, double alpha) {
+    const int ntiles = P.tiles_m * P.tiles_n;
+    const int sms = e.num_sms > 0 ? e.num_sms : 148;
+    if (ntiles >= 2 * sms) {
+        P.mode = kEpiRMW;
+        P.split = 0;
+        ck(launch_mm(P, s), "mm_kernel");
+        return 1;
+    }
+    int ksplit = 1;
+    const long base = static_cast<long>(ntiles) * P.nprod;
+    while (base * ksplit < 4L * sms && P.ktiles / (ksplit + 1) >= 4) ++ksplit;
+    const int per = (P.ktiles + ksplit - 1) / ksplit;
+    ksplit = (P.ktiles + per - 1) / per;
+    const long long ldm = P.qm, mstride = ldm * P.qn;
+    double* M = e.ensure(e.mbuf, static_cast<size_t>(mstride) * P.nprod * ksplit * 8);
+    P.mode = kEpiStore;
+    P.split = 1;
+    P.ksplit = ksplit;
+    P.kt_per_split = per;
+    P.mbase = M;
+    P.ldm = ldm;
+    P.mstride = mstride;
+    ck(launch_mm(P, s), "mm_kernel (split)");
+    StreamParams S;
+    std::memset(&S, 0, sizeof(S));
+    S.rs_c = C.rs;
+    S.cs_c = C.cs;
+    S.alpha = alpha;
+    S.ldm = ldm;
+    S.mstride = mstride;
+    S.ksplit = ksplit;
+    S.nquad = static_cast<int>(cq.size());
+    S.qm = P.qm;
+    S.qn = P.qn;
+    S.mbase = M;
+    for (size_t qi = 0; qi < cq.size(); ++qi) {
+        S.cptr[qi] = cq[qi].p;
+        S.crows[qi] = static_cast<int>(cq[qi].rows);
+        S.ccols[qi] = static_cast<int>(cq[qi].cols);
+    }
+    for (size_t p = 0; p < dests.size(); ++p)
+        for (const auto& [q, g] : dests[p]) {
+            S.src_prod[q][S.nsrc[q]] = static_cast<int8_t>(p);
+            S.src_coeff[q][S.nsrc[q]] = static_cast<int8_t>(g);
+            ++S.nsrc[q];
+        }
+    ck(launch_stream_update(S, s), "stream_update (split)");
+    return 2;
 }
 
 // ------------------------------------------------------------- run_device --
@@ -328,26 +386,28 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
             ck(err, "sum_batch");
             if (njobs) ++launches;
         }
-        P.mode = kEpiRMW;
         P.nprod = static_cast<int>(live.size());
         P.direct = 1;
-        for (size_t p = 0; p < live.size(); ++p) fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);
-        ck(launch_mm(P, s), "mm_kernel (C)");
-        return launches + 1;
+        std::vector<Terms> dests;
+        for (size_t p = 0; p < live.size(); ++p) {
+            fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);
+            dests.push_back(live[p].c);
+        }
+        return launches + launch_fused(e, s, P, dests, cq, C, alpha);
     }
 
     if (variant == STRASSEN_DGEMM || variant == STRASSEN_ABC) {
-        P.mode = kEpiRMW;
         P.nprod = static_cast<int>(live.size());
         P.direct = 1;
+        std::vector<Terms> dests;
         for (size_t p = 0; p < live.size(); ++p) {
             fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);
+            dests.push_back(live[p].c);
             if (live[p].a.size() != 1 || live[p].b.size() != 1 || live[p].a[0].second != 1 ||
                 live[p].b[0].second != 1)
                 P.direct = 0;
         }
-        ck(launch_mm(P, s), "mm_kernel");
-        return launches + 1;
+        return launches + launch_fused(e, s, P, dests, cq, C, alpha);
     }
 
     // AB / Naive: products to quadrant-sized temporaries, then streamed into C.
@@ -363,6 +423,7 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
     S.nquad = nq;
     S.qm = static_cast<int>(qm);
     S.qn = static_cast<int>(qn);
+    S.ksplit = 1;
     for (int qi = 0; qi < nq; ++qi) {
         S.cptr[qi] = cq[qi].p;
         S.crows[qi] = static_cast<int>(cq[qi].rows);
@@ -372,6 +433,18 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
     P.ldm = ldm;
     P.mstride = mstride;
 
+    const bool few_tiles = P.tiles_m * P.tiles_n < 2 * (e.num_sms > 0 ? e.num_sms : 148);
+    if (variant == STRASSEN_AB && few_tiles) {
+        // few output tiles: product/k-split partials + stream (AB semantics:
+        // products to temporaries, streamed into C in table order)
+        P.nprod = static_cast<int>(live.size());
+        std::vector<Terms> dests;
+        for (size_t p = 0; p < live.size(); ++p) {
+            fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);
+            dests.push_back(live[p].c);
+        }
+        return launches + launch_fused(e, s, P, dests, cq, C, alpha);
+    }
     if (variant == STRASSEN_AB) {
         // One launch computes every product into its own temporary (all 7^L
         // batched); one launch streams them into C in table order.
@@ -429,6 +502,11 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
             sp.ld = side_ab == 0 ? lda_t : ldb_t;
             ck(launch_materialize(sp, s), "materialize");
             ++launches;
+        }
+        if (few_tiles) {  // split-K partials + stream, same Naive semantics
+            MMParams R = Q;
+            launches += launch_fused(e, s, R, {l.c}, cq, C, alpha);
+            continue;
         }
         ck(launch_mm(Q, s), "mm_kernel (Naive)");
         ++launches;

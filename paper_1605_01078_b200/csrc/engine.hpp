@@ -31,6 +31,7 @@ struct DeviceBuffer {
 // blocking.hpp:33-42): grow-only buffers reused across calls.
 struct Engine {
     int device = -1;
+    int num_sms = 0;
     bool initialised = false;
     cudaStream_t user_stream = nullptr;
     bool has_user_stream = false;

@@ -180,8 +180,19 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
 
+    // split mode: blockIdx -> (tile, product, k-chunk)
+    int bid = blockIdx.x;
+    int p_lo = 0, p_hi = P.nprod, kt_lo = 0, kt_hi = P.ktiles;
+    if (P.split) {
+        const int ntiles = P.tiles_m * P.tiles_n;
+        const int s_idx = (bid / ntiles) % P.ksplit;
+        p_lo = bid / (ntiles * P.ksplit);
+        p_hi = p_lo + 1;
+        kt_lo = s_idx * P.kt_per_split;
+        kt_hi = min(P.ktiles, kt_lo + P.kt_per_split);
+        bid %= ntiles;
+    }
     // grouped rasterisation: group_m tile rows share B column panels in L2
-    const int bid = blockIdx.x;
     const int per_group = P.group_m * P.tiles_n;
     const int grp = bid / per_group;
     const int first_m = grp * P.group_m;
@@ -206,9 +217,9 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         if (warp != kConsumerWarps || lane != 0) return;
         uint32_t s = 0, phase = 0;
         const int m0 = tm * kBM, n0 = tn * kBN;
-        for (int p = 0; p < P.nprod; ++p) {
+        for (int p = p_lo; p < p_hi; ++p) {
             const ProductDesc& pd = P.prod[p];
-            for (int kt = 0; kt < P.ktiles; ++kt) {
+            for (int kt = kt_lo; kt < kt_hi; ++kt) {
                 const int k0 = kt * kBK;
                 for (int u = 0; u < pd.na + pd.nb; ++u) {
                     mbar_wait(&raw_empty[s], phase ^ 1);
@@ -246,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     // ring position of the next term tile: slot index and its fill parity
     uint32_t slot = 0, phase = 0;
 
-    for (int p = 0; p < P.nprod; ++p) {
+    for (int p = p_lo; p < p_hi; ++p) {
         const ProductDesc& pd = P.prod[p];
         const int na = pd.na, nb = pd.nb;
         const bool neg_a0 = pd.as[0] < 0, neg_b0 = pd.bs[0] < 0;  // warp-uniform
@@ -261,7 +272,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
 #pragma unroll
             for (int nf = 0; nf < 4; ++nf) acc[mf][nf][0] = acc[mf][nf][1] = 0.0;
 
-        for (int kt = 0; kt < P.ktiles; ++kt) {
+        for (int kt = kt_lo; kt < kt_hi; ++kt) {
             // term tiles of this k-step: A terms, then B terms, in ring order
             // (a k-step uses at most 2*MAXT <= 8 < kRawSlots slots: one wrap at most)
             const uint8_t* sA[MAXT];
@@ -355,7 +366,8 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                 }
             }
         } else {
-            double* __restrict__ M = P.mbase + p * P.mstride;
+            const int mi = P.split ? p * P.ksplit + (kt_lo / P.kt_per_split) : p;
+            double* __restrict__ M = P.mbase + mi * P.mstride;
 #pragma unroll
             for (int nf = 0; nf < 4; ++nf)
 #pragma unroll
@@ -453,8 +465,10 @@ __global__ void stream_update_kernel(const StreamParams P) {
         double* cp = C + i * P.rs_c + j * P.cs_c;
         double c = *cp;
         for (int u = 0; u < ns; ++u) {
-            const double* M = P.mbase + P.src_prod[quad][u] * P.mstride;
-            c = fma(P.alpha * static_cast<double>(P.src_coeff[quad][u]), M[i + j * P.ldm], c);
+            const double* M = P.mbase + P.src_prod[quad][u] * P.ksplit * P.mstride;
+            double v = M[i + j * P.ldm];
+            for (int sp = 1; sp < P.ksplit; ++sp) v += M[sp * P.mstride + i + j * P.ldm];
+            c = fma(P.alpha * static_cast<double>(P.src_coeff[quad][u]), v, c);
         }
         *cp = c;
     }
@@ -482,7 +496,7 @@ static cudaError_t launch_mm_t(const MMParams& p, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    const int grid = p.tiles_m * p.tiles_n;
+    const int grid = p.tiles_m * p.tiles_n * (p.split ? p.nprod * p.ksplit : 1);
     mm_kernel<MAXT><<<grid, kThreads, kMMSmemBytes, s>>>(p);
     return cudaGetLastError();
 }

@@ -62,6 +62,10 @@ struct alignas(64) MMParams {
     int mode;
     int group_m;                // tile rasterisation group height
     int direct;                 // every product is a single +1 term on both sides
+    // split mode (few output tiles): blockIdx -> (tile, product, k-chunk); each
+    // CTA stores its partial product to M_{p*ksplit+s} (kEpiStore)
+    int split;
+    int ksplit, kt_per_split;
 };
 
 cudaError_t launch_mm(const MMParams& p, cudaStream_t s);
@@ -118,6 +122,7 @@ struct StreamParams {
     double alpha;
     int nquad;
     int qm, qn;
+    int ksplit;  // M_p = sum_{s < ksplit} mbase[(p*ksplit + s) * mstride], s ascending
 };
 cudaError_t launch_stream_update(const StreamParams& p, cudaStream_t s);
 
