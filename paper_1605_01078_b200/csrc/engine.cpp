@@ -337,10 +337,13 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
     }
     if (live.empty()) return launches;
 
-    if (variant == STRASSEN_C) {
-        // C variant (B200 addition): every multi-term operand sum materialised
-        // by one batched HBM pass, then one mm_kernel over all 7^L products
-        // with single-term operands and the fused multi-destination epilogue.
+    if (variant == STRASSEN_C || variant == STRASSEN_NAIVE) {
+        // Every multi-term operand sum materialised by one batched HBM pass
+        // (materialize_sum, variants.cpp:53-96, for all entries at once), then
+        // one mm_kernel over all 7^L products with single-term operands.
+        //   C variant (B200 addition): fused multi-destination epilogue.
+        //   Naive: products to temporaries M_p, then one stream pass applying
+        //          C_r += alpha*gamma*M_p in table order (variants.cpp:99-109).
         const long long lda_t = ((qm + 3) / 4) * 4, ldb_t = ((qk + 3) / 4) * 4;
         int na_sums = 0, nb_sums = 0;
         for (const Live& l : live) {
@@ -393,7 +396,41 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
             fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);
             dests.push_back(live[p].c);
         }
-        return launches + launch_fused(e, s, P, dests, cq, C, alpha);
+        if (variant == STRASSEN_C || P.tiles_m * P.tiles_n < 2 * std::max(e.num_sms, 1))
+            return launches + launch_fused(e, s, P, dests, cq, C, alpha);  // (split when small)
+        // Naive, batched: M_p for every product in one launch, one stream pass
+        const long long ldm = qm, mstride = ldm * qn;
+        double* M = e.ensure(e.mbuf, static_cast<size_t>(mstride) * live.size() * 8);
+        P.mode = kEpiStore;
+        P.mbase = M;
+        P.ldm = ldm;
+        P.mstride = mstride;
+        ck(launch_mm(P, s), "mm_kernel (Naive)");
+        StreamParams S;
+        std::memset(&S, 0, sizeof(S));
+        S.rs_c = C.rs;
+        S.cs_c = C.cs;
+        S.alpha = alpha;
+        S.ldm = ldm;
+        S.mstride = mstride;
+        S.ksplit = 1;
+        S.nquad = nq;
+        S.qm = static_cast<int>(qm);
+        S.qn = static_cast<int>(qn);
+        S.mbase = M;
+        for (int qi = 0; qi < nq; ++qi) {
+            S.cptr[qi] = cq[qi].p;
+            S.crows[qi] = static_cast<int>(cq[qi].rows);
+            S.ccols[qi] = static_cast<int>(cq[qi].cols);
+        }
+        for (size_t p = 0; p < dests.size(); ++p)
+            for (const auto& [q, g] : dests[p]) {
+                S.src_prod[q][S.nsrc[q]] = static_cast<int8_t>(p);
+                S.src_coeff[q][S.nsrc[q]] = static_cast<int8_t>(g);
+                ++S.nsrc[q];
+            }
+        ck(launch_stream_update(S, s), "stream_update (Naive)");
+        return launches + 2;
     }
 
     if (variant == STRASSEN_DGEMM || variant == STRASSEN_ABC) {
@@ -410,7 +447,7 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
         return launches + launch_fused(e, s, P, dests, cq, C, alpha);
     }
 
-    // AB / Naive: products to quadrant-sized temporaries, then streamed into C.
+    // AB: products to quadrant-sized temporaries, then streamed into C.
     const long long ldm = qm;
     const long long mstride = ldm * qn;
     StreamParams S;
@@ -466,62 +503,7 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
         return launches + 2;
     }
 
-    // Naive: per product, materialise T_A (qm x qk) and T_B (qk x qn) with
-    // zero padding, multiply them as single terms, stream M into C.
-    const long long lda_t = ((qm + 3) / 4) * 4, ldb_t = ((qk + 3) / 4) * 4;
-    double* TA = e.ensure(e.tabuf, static_cast<size_t>(lda_t) * qk * 8);
-    double* TB = e.ensure(e.tbbuf, static_cast<size_t>(ldb_t) * qn * 8);
-    double* M = e.ensure(e.mbuf, static_cast<size_t>(mstride) * 8);
-    MMParams Q = P;
-    encode_map(&Q.tmA[0], TA, qm, qk, lda_t, 16, kBK, true);
-    encode_map(&Q.tmB[0], TB, qk, qn, ldb_t, kBK, kBN, true);
-    Q.nprod = 1;
-    Q.direct = 1;
-    Q.mbase = M;
-    const Terms one = {{0, 1}};
-    fill_desc(Q.prod[0], one, one, one);
-    for (const Live& l : live) {
-        for (int side_ab = 0; side_ab < 2; ++side_ab) {
-            const Terms& terms = side_ab == 0 ? l.a : l.b;
-            const TmaOperand& t = side_ab == 0 ? ta : tb;
-            SumParams sp;
-            std::memset(&sp, 0, sizeof(sp));
-            sp.n = static_cast<int>(terms.size());
-            for (size_t u = 0; u < terms.size(); ++u) {
-                const int qi = terms[u].first;
-                sp.x[u] = quad_origin(t, qi / side, qi % side);
-                sp.xrows[u] = quad_rows(t, qi / side);
-                sp.xcols[u] = quad_cols(t, qi % side);
-                sp.coeff[u] = terms[u].second;
-            }
-            sp.rs = 1;
-            sp.cs = t.ld;
-            sp.dst = side_ab == 0 ? TA : TB;
-            sp.rows = side_ab == 0 ? qm : qk;
-            sp.cols = side_ab == 0 ? qk : qn;
-            sp.ld = side_ab == 0 ? lda_t : ldb_t;
-            ck(launch_materialize(sp, s), "materialize");
-            ++launches;
-        }
-        if (few_tiles) {  // split-K partials + stream, same Naive semantics
-            MMParams R = Q;
-            launches += launch_fused(e, s, R, {l.c}, cq, C, alpha);
-            continue;
-        }
-        ck(launch_mm(Q, s), "mm_kernel (Naive)");
-        ++launches;
-        StreamParams T = S;
-        std::memset(T.nsrc, 0, sizeof(T.nsrc));
-        for (const auto& [q, g] : l.c) {
-            T.src_prod[q][0] = 0;
-            T.src_coeff[q][0] = static_cast<int8_t>(g);
-            T.nsrc[q] = 1;
-        }
-        T.mbase = M;
-        ck(launch_stream_update(T, s), "stream_update");
-        ++launches;
-    }
-    return launches;
+    throw Error(STRASSEN_ERR_PARAM, "unhandled variant");
 }
 
 long scale_device(Engine& e, cudaStream_t s, const DView& C, double beta) {

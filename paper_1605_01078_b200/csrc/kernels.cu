@@ -411,24 +411,6 @@ __global__ void repack_kernel(const double* __restrict__ src, long long rs, long
     }
 }
 
-// ------------------------------------------------------------ materialise ---
-// dst(i, j) = sum_u c_u X_u(i, j), zero outside each clipped view
-// (variants.cpp:53-96: first pass d0*x0 [+ d1*x1], then += ds*xs).
-__global__ void materialize_kernel(const SumParams P) {
-    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const long long jj = blockIdx.y;
-    if (i >= P.rows) return;
-    for (long long j = jj; j < P.cols; j += gridDim.y) {
-        double v = 0.0;
-        for (int u = 0; u < P.n; ++u) {
-            const double x = (i < P.xrows[u] && j < P.xcols[u]) ? P.x[u][i * P.rs + j * P.cs] : 0.0;
-            const double c = P.coeff[u];
-            v = (u == 0) ? c * x : fma(c, x, v);
-        }
-        P.dst[i + j * P.ld] = v;
-    }
-}
-
 // -------------------------------------------------------------- sum batch ---
 // C variant: all multi-term operand sums of a launch, one job per blockIdx.z.
 // Same arithmetic as materialize_kernel (variants.cpp:53-96 order).
@@ -522,12 +504,6 @@ cudaError_t launch_repack(const double* src, long long rs, long long cs, long ro
 
 static unsigned col_grid(long long cols) {
     return static_cast<unsigned>(cols < 16384 ? cols : 16384);
-}
-
-cudaError_t launch_materialize(const SumParams& p, cudaStream_t s) {
-    dim3 grid(static_cast<unsigned>((p.rows + 255) / 256), col_grid(p.cols));
-    materialize_kernel<<<grid, 256, 0, s>>>(p);
-    return cudaGetLastError();
 }
 
 cudaError_t launch_sum_batch(const SumBatchParams& p, cudaStream_t s) {

@@ -96,18 +96,6 @@ struct SumBatchParams {
 };
 cudaError_t launch_sum_batch(const SumBatchParams& p, cudaStream_t s);
 
-// ---- Naive: materialise an operand sum ------------------------------------
-struct SumParams {
-    const double* x[kMaxTerms];
-    long long xrows[kMaxTerms], xcols[kMaxTerms];
-    int coeff[kMaxTerms];
-    int n;
-    long long rs, cs;     // source strides (shared by all terms)
-    double* dst;          // column-major rows x cols, leading dimension ld
-    long long rows, cols, ld;
-};
-cudaError_t launch_materialize(const SumParams& p, cudaStream_t s);
-
 // ---- AB / Naive: stream products into C quadrants -------------------------
 constexpr int kMaxFanIn = 16;
 struct StreamParams {
