@@ -4,7 +4,11 @@
 One step = one strassen_gemm call (C := alpha A B + C) on the workload
 m = n = k = 16384, column-major fp64, uniform[-1, 1) synthetic inputs
 (BASELINE.json configs[1], top of the square sweep; it fits one GPU).
-Default variant: ABC, one level.  Prints ONE JSON line on rank 0.
+Default: two-level Strassen, Naive variant (batched: all operand sums in one
+HBM pass, all 49 products in one launch, one stream pass) -- the fastest
+configuration measured on B200 (profiles/r01_notes.md).  Every other
+variant/level is timed on the same inputs and reported under "variants".
+Prints ONE JSON line on rank 0.
 
   value     effective FP64 TFLOP/s (2mnk / t, summed over ranks), device
             pointers, inputs resident in HBM, CUDA events on the launch stream
@@ -44,8 +48,9 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--variant", default="abc", choices=["dgemm", "abc", "ab", "naive"])
-    p.add_argument("--level", type=int, default=1)
+    p.add_argument("--variant", default="naive", choices=["dgemm", "abc", "ab", "naive", "c"])
+    p.add_argument("--level", type=int, default=2)
+    p.add_argument("--no-variants", action="store_true")
     p.add_argument("--dim", type=int, default=16384)
     p.add_argument("--m", type=int, default=0)
     p.add_argument("--n", type=int, default=0)
@@ -67,14 +72,39 @@ def table_counts(level):
     return {0: (1, 0, 0, 1), 1: (7, 5, 5, 12), 2: (49, 95, 95, 144)}[level]
 
 
-def executed_flops(m, n, k, level):
-    """F_exec (implementation counts, 144 C updates at L2)."""
+def executed_flops(m, n, k, level, variant="abc"):
+    """Flops the mm_kernel launch executes (implementation
+    counts, 144 C updates at level 2).  abc: products + fused operand sums +
+    fused C updates; ab: no C updates (streamed); c: no operand sums
+    (materialised); naive: products only."""
     if level == 0:
         return 2.0 * m * n * k
     s = 1 << level
     qm, qn, qk = -(-m // s), -(-n // s), -(-k // s)
     mul, aa, ba, cu = table_counts(level)
-    return mul * 2.0 * qm * qn * qk + 2.0 * (aa * qm * qk + ba * qk * qn + cu * qm * qn)
+    f = mul * 2.0 * qm * qn * qk
+    if variant in ("abc", "ab"):
+        f += 2.0 * (aa * qm * qk + ba * qk * qn)
+    if variant in ("abc", "c"):
+        f += 2.0 * cu * qm * qn
+    return f
+
+
+# sum over multi-term operands of (terms + 1): read every term, write the sum
+# (per side; L1 term histogram {1: 2, 2: 5}, L2 {1: 4, 2: 20, 4: 25})
+SUM_PASSES = {1: 5 * 3, 2: 20 * 3 + 25 * 5}
+
+
+def hbm_bytes(kernel, m, n, k, level, ordinal=0):
+    """Algorithmic HBM bytes of the auxiliary launches."""
+    s = 1 << level
+    qm, qn, qk = -(-m // s), -(-n // s), -(-k // s)
+    mul, aa, ba, cu = table_counts(level)
+    if kernel == "sum_batch_kernel" and level > 0:  # ordinal 0: A side, 1: B side
+        return 8.0 * SUM_PASSES[level] * (qm * qk if ordinal == 0 else qk * qn)
+    if kernel == "stream_update_kernel":  # read M_p per update, RMW each C element once
+        return 8.0 * (cu * qm * qn + 2 * m * n)
+    return None
 
 
 class ClockSampler:
@@ -255,10 +285,17 @@ def main():
     flops = 2.0 * m * n * k
     value = world * flops / (ms_per_step * 1e-3) / 1e12
 
-    # roofline of the dominant kernel (the only launch of an aligned ABC/DGEMM call)
+    # roofline of the dominant kernel (mm_kernel), timed by the library's own
+    # per-launch CUDA events on the launch stream (one extra profiled step)
     peaks = json.load(open(os.path.join(ROOT, "profiles", "fp64_peaks.json")))
-    kern_ms = statistics.mean(per_ms)
-    f_exec = executed_flops(m, n, k, args.level)
+    ctx.enable_profiling(True)
+    ctx.gemm_device(args.variant, args.level, 1.0, A, B, C, stream)
+    torch.cuda.synchronize()
+    prof = ctx.last_profile()
+    ctx.enable_profiling(False)
+    mm_ms = [x["ms"] for x in prof if x["kernel"] == "mm_kernel"]
+    kern_ms = sum(mm_ms) if mm_ms else statistics.mean(per_ms)
+    f_exec = executed_flops(m, n, k, args.level, args.variant)
     achieved = f_exec / (kern_ms * 1e-3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -269,9 +306,23 @@ def main():
             traffic = t[key]
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["dmma_tflops"],
                 "unit": "TFLOP/s", "frac": achieved / peaks["dmma_tflops"], "traffic": traffic,
-                "flops_per_launch": f_exec, "kernel_ms": kern_ms, "launches_per_step": launches,
+                "flops_per_launch": f_exec, "kernel_ms": kern_ms, "kernel": "mm_kernel",
+                "launches_per_step": launches, "step_profile_ms": prof,
                 "peak_source": "measured FP64 DMMA peak, profiles/fp64_peaks.json "
                                "(MEASURED_PEAKS.json has bf16/HBM only)"}
+    hbm_peak = None
+    try:
+        hbm_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    except Exception:
+        hbm_peak = 6442.2
+    seen = {}
+    for x in prof:
+        nb = hbm_bytes(x["kernel"], m, n, k, args.level, seen.get(x["kernel"], 0))
+        seen[x["kernel"]] = seen.get(x["kernel"], 0) + 1
+        if nb and x["ms"] > 0:
+            roofline.setdefault("aux_hbm", []).append(
+                {"kernel": x["kernel"], "achieved_gbs": nb / (x["ms"] * 1e-3) / 1e9,
+                 "peak_gbs": hbm_peak, "frac": nb / (x["ms"] * 1e-3) / 1e9 / hbm_peak})
 
     line = {
         "metric": "effective FP64 TFLOPS (2mnk/t)", "value": value, "unit": "TFLOP/s",
@@ -286,6 +337,15 @@ def main():
         "roofline": roofline, "clocks": clk.summary(),
         "gpu_launches": launches * args.steps,
     }
+
+    if not args.no_variants:
+        table = {}
+        for v, lv in [("dgemm", 0), ("abc", 1), ("ab", 1), ("naive", 1), ("c", 1), ("abc", 2),
+                      ("ab", 2), ("naive", 2), ("c", 2)]:
+            tt, _, _ = time_device(v, lv, 2, 1)
+            t_ms = max_over_ranks(tt) / 2
+            table[f"{v}{lv}"] = {"value": world * flops / (t_ms * 1e-3) / 1e12, "ms": t_ms}
+        line["variants"] = table
 
     if not args.no_classical and args.variant != "dgemm":
         c_total, c_per, _ = time_device("dgemm", 0, max(2, args.steps // 2), 1)

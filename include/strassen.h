@@ -187,6 +187,13 @@ strassen_status strassen_ctx_set_stream(strassen_ctx* ctx, void* stream);
 /* Number of CUDA kernels the last compute call on this ctx launched. */
 strassen_status strassen_ctx_last_launches(const strassen_ctx* ctx, long* out);
 
+/* Per-launch CUDA-event timing of the calls on this ctx (off by default).
+ * strassen_ctx_last_profile writes a JSON list [{"kernel": name, "ms": t}, ...]
+ * for the last compute call into buf (NUL-terminated; STRASSEN_ERR_ALLOC if
+ * it did not fit).  Synchronises with the recorded events. */
+strassen_status strassen_ctx_enable_profiling(strassen_ctx* ctx, int enabled);
+strassen_status strassen_ctx_last_profile(strassen_ctx* ctx, char* buf, long size);
+
 /* Device memory currently held by the ctx workspace, in bytes. */
 strassen_status strassen_ctx_workspace_bytes(const strassen_ctx* ctx, long* out);
 

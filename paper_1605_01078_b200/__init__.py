@@ -116,6 +116,8 @@ def _declare(lib):
         "strassen_ctx_workspace_bytes": (_ST, [vp, C.POINTER(_L)]),
         "strassen_count_call": (_ST, [C.c_int, C.c_int, _L, _L, _L, C.POINTER(Blocking),
                                       C.POINTER(Counters)]),
+        "strassen_ctx_enable_profiling": (_ST, [vp, C.c_int]),
+        "strassen_ctx_last_profile": (_ST, [vp, C.c_char_p, _L]),
         "strassen_build_info": (C.c_char_p, []),
         "strassen_last_error": (C.c_char_p, []),
     }
@@ -227,6 +229,16 @@ class Ctx:
         n = C.c_long()
         _check(self._l.strassen_ctx_last_launches(self.ptr, C.byref(n)), "last_launches")
         return n.value
+
+    def enable_profiling(self, on=True):
+        _check(self._l.strassen_ctx_enable_profiling(self.ptr, int(bool(on))), "enable_profiling")
+
+    def last_profile(self):
+        """[{'kernel': name, 'ms': t}, ...] for the last compute call (profiling on)."""
+        import json
+        buf = C.create_string_buffer(1 << 16)
+        _check(self._l.strassen_ctx_last_profile(self.ptr, buf, len(buf)), "last_profile")
+        return json.loads(buf.value.decode())
 
     def workspace_bytes(self):
         n = C.c_long()

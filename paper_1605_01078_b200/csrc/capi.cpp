@@ -127,6 +127,11 @@ strassen_status gemm_impl(strassen_ctx* ctx, bool explicit_stream, cudaStream_t 
         const sb200::DView C = stage_in(e, s, c, m, n, rs_c, cs_c, e.stage_c, true, sc);
         if (device_only && (sa || sb || sc))
             throw std::invalid_argument("strassen_gemm_device: operands must be device memory");
+        for (auto& t : e.timed) {
+            cudaEventDestroy(t.start);
+            cudaEventDestroy(t.stop);
+        }
+        e.timed.clear();
         if (has_beta && beta != 1.0) launches += sb200::scale_device(e, s, C, beta);
         launches += sb200::run_device(e, s, variant, level, alpha, A, B, C);
         if (sc) {
@@ -248,6 +253,21 @@ strassen_status strassen_ctx_last_launches(const strassen_ctx* ctx, long* out) {
     if (!ctx || !out) return STRASSEN_ERR_NULL;
     *out = ctx->engine.last_launches;
     return STRASSEN_OK;
+}
+
+strassen_status strassen_ctx_enable_profiling(strassen_ctx* ctx, int enabled) {
+    if (!ctx) return STRASSEN_ERR_NULL;
+    ctx->engine.profiling = enabled != 0;
+    return STRASSEN_OK;
+}
+
+strassen_status strassen_ctx_last_profile(strassen_ctx* ctx, char* buf, long size) {
+    if (!ctx || !buf) return STRASSEN_ERR_NULL;
+    if (size < 1) return STRASSEN_ERR_PARAM;
+    const std::string j = ctx->engine.last_profile();
+    std::strncpy(buf, j.c_str(), static_cast<size_t>(size - 1));
+    buf[size - 1] = 0;
+    return static_cast<long>(j.size()) < size ? STRASSEN_OK : STRASSEN_ERR_ALLOC;
 }
 
 strassen_status strassen_ctx_workspace_bytes(const strassen_ctx* ctx, long* out) {

@@ -98,9 +98,11 @@ TmaOperand prepare(Engine& e, cudaStream_t s, const DView& v, long q_rows, long 
     long long ld = static_cast<long long>(side > 1 ? q_al * side : v.rows);
     ld = std::max<long long>(((ld + 3) / 4) * 4, 4);
     double* dst = e.ensure(scratch, static_cast<size_t>(ld) * v.cols * 8);
+    e.prof_begin("repack_kernel", s);
     ck(launch_repack(v.p, v.rs, v.cs, v.rows, v.cols, dst, ld, side > 1 ? q_rows : v.rows + 1,
                      side > 1 ? q_al : v.rows + 1, s),
        "repack");
+    e.prof_end(s);
     ++launches;
     t.base = dst;
     t.ld = ld;
@@ -183,6 +185,32 @@ void Engine::init() {
     initialised = true;
 }
 
+void Engine::prof_begin(const char* name, cudaStream_t s) {
+    if (!profiling) return;
+    Timed t{name, nullptr, nullptr};
+    cudaEventCreate(&t.start);
+    cudaEventCreate(&t.stop);
+    cudaEventRecord(t.start, s);
+    timed.push_back(t);
+}
+
+void Engine::prof_end(cudaStream_t s) {
+    if (!profiling || timed.empty()) return;
+    cudaEventRecord(timed.back().stop, s);
+}
+
+std::string Engine::last_profile() {
+    std::string out = "[";
+    for (size_t i = 0; i < timed.size(); ++i) {
+        float ms = -1.0f;
+        if (cudaEventSynchronize(timed[i].stop) == cudaSuccess)
+            cudaEventElapsedTime(&ms, timed[i].start, timed[i].stop);
+        out += (i ? ", " : "") + std::string("{\"kernel\": \"") + timed[i].name +
+               "\", \"ms\": " + std::to_string(ms) + "}";
+    }
+    return out + "]";
+}
+
 // The synchronous entry points run on the ctx stream: the one set with
 // strassen_ctx_set_stream, else the CUDA legacy default stream (which orders
 // against the caller's work on other blocking streams).
@@ -231,7 +259,9 @@ long launch_fused(Engine& e, cudaStream_t s, MMParams& P, const std::vector<Term
     if (ntiles >= 2 * sms) {
         P.mode = kEpiRMW;
         P.split = 0;
+        e.prof_begin("mm_kernel", s);
         ck(launch_mm(P, s), "mm_kernel");
+        e.prof_end(s);
         return 1;
     }
     int ksplit = 1;
@@ -248,7 +278,9 @@ long launch_fused(Engine& e, cudaStream_t s, MMParams& P, const std::vector<Term
     P.mbase = M;
     P.ldm = ldm;
     P.mstride = mstride;
+    e.prof_begin("mm_kernel", s);
     ck(launch_mm(P, s), "mm_kernel (split)");
+    e.prof_end(s);
     StreamParams S;
     std::memset(&S, 0, sizeof(S));
     S.rs_c = C.rs;
@@ -272,7 +304,9 @@ long launch_fused(Engine& e, cudaStream_t s, MMParams& P, const std::vector<Term
             S.src_coeff[q][S.nsrc[q]] = static_cast<int8_t>(g);
             ++S.nsrc[q];
         }
+    e.prof_begin("stream_update_kernel", s);
     ck(launch_stream_update(S, s), "stream_update (split)");
+    e.prof_end(s);
     return 2;
 }
 
@@ -383,7 +417,9 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
                     encode_map(&P.tmB[mi], dst, qk, qn, ldb_t, kBK, kBN, true);
                 terms = {{mi, 1}};
             }
+            e.prof_begin("sum_batch_kernel", s);
             cudaError_t err = launch_sum_batch(*SB, s);
+            e.prof_end(s);
             const int njobs = SB->njobs;
             delete SB;
             ck(err, "sum_batch");
@@ -405,7 +441,9 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
         P.mbase = M;
         P.ldm = ldm;
         P.mstride = mstride;
+        e.prof_begin("mm_kernel", s);
         ck(launch_mm(P, s), "mm_kernel (Naive)");
+        e.prof_end(s);
         StreamParams S;
         std::memset(&S, 0, sizeof(S));
         S.rs_c = C.rs;
@@ -429,7 +467,9 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
                 S.src_coeff[q][S.nsrc[q]] = static_cast<int8_t>(g);
                 ++S.nsrc[q];
             }
+        e.prof_begin("stream_update_kernel", s);
         ck(launch_stream_update(S, s), "stream_update (Naive)");
+        e.prof_end(s);
         return launches + 2;
     }
 
@@ -497,9 +537,13 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
                 ++S.nsrc[q];
             }
         }
+        e.prof_begin("mm_kernel", s);
         ck(launch_mm(P, s), "mm_kernel (AB)");
+        e.prof_end(s);
         S.mbase = M;
+        e.prof_begin("stream_update_kernel", s);
         ck(launch_stream_update(S, s), "stream_update");
+        e.prof_end(s);
         return launches + 2;
     }
 

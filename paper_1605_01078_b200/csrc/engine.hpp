@@ -10,6 +10,7 @@
 #include <stdexcept>
 #include <string>
 #include <vector>
+#include <string>
 
 #include "strassen.h"
 
@@ -39,6 +40,16 @@ struct Engine {
     DeviceBuffer pack_a, pack_b;              // TMA layout normalisation
     DeviceBuffer mbuf, tabuf, tbbuf;          // AB / Naive temporaries
     long last_launches = 0;
+    // optional per-launch timing of the last call (strassen_ctx_enable_profiling)
+    bool profiling = false;
+    struct Timed {
+        const char* name;
+        cudaEvent_t start, stop;
+    };
+    std::vector<Timed> timed;
+    void prof_begin(const char* name, cudaStream_t s);
+    void prof_end(cudaStream_t s);
+    std::string last_profile();  // JSON list of {"kernel": name, "ms": t}
 
     ~Engine();
     void init();
