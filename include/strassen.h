@@ -187,6 +187,11 @@ strassen_status strassen_ctx_set_stream(strassen_ctx* ctx, void* stream);
 /* Number of CUDA kernels the last compute call on this ctx launched. */
 strassen_status strassen_ctx_last_launches(const strassen_ctx* ctx, long* out);
 
+/* Fringe handling for m, n or k not divisible by 2^level: 1 (default) =
+ * dynamic peeling (Strassen on the even core + classical fringe updates);
+ * 0 = the reference's zero padding of clipped quadrants (matrix.cpp:14-22). */
+strassen_status strassen_ctx_set_peeling(strassen_ctx* ctx, int enabled);
+
 /* Per-launch CUDA-event timing of the calls on this ctx (off by default).
  * strassen_ctx_last_profile writes a JSON list [{"kernel": name, "ms": t}, ...]
  * for the last compute call into buf (NUL-terminated; STRASSEN_ERR_ALLOC if

@@ -117,6 +117,7 @@ def _declare(lib):
         "strassen_count_call": (_ST, [C.c_int, C.c_int, _L, _L, _L, C.POINTER(Blocking),
                                       C.POINTER(Counters)]),
         "strassen_ctx_enable_profiling": (_ST, [vp, C.c_int]),
+        "strassen_ctx_set_peeling": (_ST, [vp, C.c_int]),
         "strassen_ctx_last_profile": (_ST, [vp, C.c_char_p, _L]),
         "strassen_build_info": (C.c_char_p, []),
         "strassen_last_error": (C.c_char_p, []),
@@ -229,6 +230,10 @@ class Ctx:
         n = C.c_long()
         _check(self._l.strassen_ctx_last_launches(self.ptr, C.byref(n)), "last_launches")
         return n.value
+
+    def set_peeling(self, on=True):
+        """Odd fringes: dynamic peeling (default) or the reference's zero padding."""
+        _check(self._l.strassen_ctx_set_peeling(self.ptr, int(bool(on))), "set_peeling")
 
     def enable_profiling(self, on=True):
         _check(self._l.strassen_ctx_enable_profiling(self.ptr, int(bool(on))), "enable_profiling")

@@ -255,6 +255,12 @@ strassen_status strassen_ctx_last_launches(const strassen_ctx* ctx, long* out) {
     return STRASSEN_OK;
 }
 
+strassen_status strassen_ctx_set_peeling(strassen_ctx* ctx, int enabled) {
+    if (!ctx) return STRASSEN_ERR_NULL;
+    ctx->engine.peeling = enabled != 0;
+    return STRASSEN_OK;
+}
+
 strassen_status strassen_ctx_enable_profiling(strassen_ctx* ctx, int enabled) {
     if (!ctx) return STRASSEN_ERR_NULL;
     ctx->engine.profiling = enabled != 0;

@@ -220,7 +220,8 @@ double* Engine::ensure(DeviceBuffer& b, size_t bytes) {
     if (bytes == 0) bytes = 8;
     if (b.bytes < bytes) {
         if (b.ptr) {
-            ck(cudaStreamSynchronize(stream()), "sync before realloc");
+            // earlier launches (on any stream) may still read it
+            ck(cudaDeviceSynchronize(), "sync before realloc");
             cudaFree(b.ptr);
             b.ptr = nullptr;
             b.bytes = 0;
@@ -311,8 +312,59 @@ long launch_fused(Engine& e, cudaStream_t s, MMParams& P, const std::vector<Term
 }
 
 // ------------------------------------------------------------- run_device --
+namespace {
+long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level, double alpha,
+                  const DView& A, const DView& B, const DView& C);
+
+DView sub(const DView& v, long r0, long c0, long rows, long cols) {
+    DView o = v;
+    o.p = v.p + r0 * v.rs + c0 * v.cs;
+    o.rows = rows;
+    o.cols = cols;
+    return o;
+}
+}  // namespace
+
+// Dynamic peeling (north star; the reference pads instead, matrix.cpp:14-22):
+// when m, n or k is not a multiple of 2^L, Strassen runs on the even core
+// m_e x n_e x k_e (every quadrant full, no padded tiles) and three classical
+// fringe updates finish the product:
+//   C[0:m_e, 0:n_e] += alpha A[0:m_e, k_e:k] B[k_e:k, 0:n_e]   (rank-k_r)
+//   C[m_e:m, 0:n]   += alpha A[m_e:m, 0:k]   B                  (bottom rows)
+//   C[0:m_e, n_e:n] += alpha A[0:m_e, 0:k]   B[0:k, n_e:n]      (right columns)
+// Tiny problems (core below one 128-tile per quadrant) keep the padded path.
 long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, double alpha,
                 const DView& A, const DView& B, const DView& C) {
+    const int L = (variant == STRASSEN_DGEMM) ? 0 : level;
+    const long S = 1L << L;
+    const long m = A.rows, k = A.cols, n = B.cols;
+    const long me = m & ~(S - 1), ne = n & ~(S - 1), ke = k & ~(S - 1);
+    const bool ragged = me != m || ne != n || ke != k;
+    // peel only when it removes padded work: compare output-tile x k-step counts
+    auto work = [&](long mm, long nn, long kk) {
+        return ceil_div(ceil_div(mm, S), kBM) * ceil_div(ceil_div(nn, S), kBN) *
+               ceil_div(ceil_div(kk, S), kBK);
+    };
+    if (!(L > 0 && ragged && e.peeling && me >= S * kBM && ne >= S * kBN && ke >= S * kBK &&
+          work(me, ne, ke) < work(m, n, k)))
+        return run_strassen(e, s, variant, level, alpha, A, B, C);
+    long launches = run_strassen(e, s, variant, level, alpha, sub(A, 0, 0, me, ke),
+                                 sub(B, 0, 0, ke, ne), sub(C, 0, 0, me, ne));
+    if (ke < k)
+        launches += run_strassen(e, s, STRASSEN_DGEMM, 0, alpha, sub(A, 0, ke, me, k - ke),
+                                 sub(B, ke, 0, k - ke, ne), sub(C, 0, 0, me, ne));
+    if (me < m)
+        launches += run_strassen(e, s, STRASSEN_DGEMM, 0, alpha, sub(A, me, 0, m - me, k), B,
+                                 sub(C, me, 0, m - me, n));
+    if (ne < n)
+        launches += run_strassen(e, s, STRASSEN_DGEMM, 0, alpha, sub(A, 0, 0, me, k),
+                                 sub(B, 0, ne, k, n - ne), sub(C, 0, ne, me, n - ne));
+    return launches;
+}
+
+namespace {
+long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level, double alpha,
+                  const DView& A, const DView& B, const DView& C) {
     const int L = (variant == STRASSEN_DGEMM) ? 0 : level;
     const int side = 1 << L;
     const long m = A.rows, k = A.cols, n = B.cols;
@@ -549,6 +601,7 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
 
     throw Error(STRASSEN_ERR_PARAM, "unhandled variant");
 }
+}  // namespace
 
 long scale_device(Engine& e, cudaStream_t s, const DView& C, double beta) {
     (void)e;

@@ -255,3 +255,17 @@ def test_full_size_strassen_vs_classical(ctx, dim):
         nw = (torch.linalg.norm(C - base) / (an * bn)).item()
         assert nw <= (1e-12 if L == 1 else 5e-12), (v, L, nw)
         assert freivalds(1.0, a_h, b_h, c0_h, C.cpu().numpy()) < 1e-14
+
+
+@pytest.mark.parametrize("shape", [(4097, 4097, 4097), (1027, 2053, 1541), (2050, 1025, 4099)])
+def test_dynamic_peeling_vs_padding(ctx, shape):
+    """Odd sizes: the peeled path (even core + classical fringes) and the
+    reference's padded path both match the oracle's blocked DGEMM."""
+    m, n, k = shape
+    a, b, c0 = inputs(m, n, k, (61, 62, 63))
+    ref = oracle_result("dgemm", 0, 1.0, a, b, c0, use_reference_gemm=False)
+    for peel in (True, False):
+        ctx.set_peeling(peel)
+        for v, L in [("abc", 1), ("abc", 2), ("naive", 2), ("c", 2)]:
+            check(v, L, run(ctx, v, L, 1.0, a, b, c0), ref, c0, a, b)
+    ctx.set_peeling(True)
