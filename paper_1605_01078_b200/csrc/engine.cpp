@@ -254,10 +254,11 @@ bool is_device_pointer(const void* p) {
 // then one deterministic stream pass (partials summed in s order, destinations
 // applied in table order).
 long launch_fused(Engine& e, cudaStream_t s, MMParams& P, const std::vector<Terms>& dests,
-                  const std::vector<QuadView>& cq, const DView& C, double alpha) {
+                  const std::vector<QuadView>& cq, const DView& C, double alpha,
+                  bool force_split = false) {
     const int ntiles = P.tiles_m * P.tiles_n;
     const int sms = e.num_sms > 0 ? e.num_sms : 148;
-    if (ntiles >= 2 * sms) {
+    if (ntiles >= 2 * sms && !force_split) {
         P.mode = kEpiRMW;
         P.split = 0;
         e.prof_begin("mm_kernel", s);
@@ -484,8 +485,10 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
             fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);
             dests.push_back(live[p].c);
         }
-        if (variant == STRASSEN_C || P.tiles_m * P.tiles_n < 2 * std::max(e.num_sms, 1))
-            return launches + launch_fused(e, s, P, dests, cq, C, alpha);  // (split when small)
+        // C: fused epilogue (split only when few tiles).  Naive: products to
+        // temporaries on a product-parallel grid (one CTA per tile x product:
+        // balanced waves at every size), then one stream pass.
+        return launches + launch_fused(e, s, P, dests, cq, C, alpha, variant == STRASSEN_NAIVE);
         // Naive, batched: M_p for every product in one launch, one stream pass
         const long long ldm = qm, mstride = ldm * qn;
         double* M = e.ensure(e.mbuf, static_cast<size_t>(mstride) * live.size() * 8);
@@ -539,66 +542,19 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
         return launches + launch_fused(e, s, P, dests, cq, C, alpha);
     }
 
-    // AB: products to quadrant-sized temporaries, then streamed into C.
-    const long long ldm = qm;
-    const long long mstride = ldm * qn;
-    StreamParams S;
-    std::memset(&S, 0, sizeof(S));
-    S.rs_c = C.rs;
-    S.cs_c = C.cs;
-    S.alpha = alpha;
-    S.ldm = ldm;
-    S.mstride = mstride;
-    S.nquad = nq;
-    S.qm = static_cast<int>(qm);
-    S.qn = static_cast<int>(qn);
-    S.ksplit = 1;
-    for (int qi = 0; qi < nq; ++qi) {
-        S.cptr[qi] = cq[qi].p;
-        S.crows[qi] = static_cast<int>(cq[qi].rows);
-        S.ccols[qi] = static_cast<int>(cq[qi].cols);
-    }
-    P.mode = kEpiStore;
-    P.ldm = ldm;
-    P.mstride = mstride;
-
-    const bool few_tiles = P.tiles_m * P.tiles_n < 2 * (e.num_sms > 0 ? e.num_sms : 148);
-    if (variant == STRASSEN_AB && few_tiles) {
-        // few output tiles: product/k-split partials + stream (AB semantics:
-        // products to temporaries, streamed into C in table order)
+    if (variant == STRASSEN_AB) {
+        // AB (variants.cpp:142-168): fused operand sums, products to
+        // temporaries on a product-parallel grid (k-split too when few tiles),
+        // streamed into C in table order.
         P.nprod = static_cast<int>(live.size());
+        P.direct = 0;
         std::vector<Terms> dests;
         for (size_t p = 0; p < live.size(); ++p) {
             fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);
             dests.push_back(live[p].c);
         }
-        return launches + launch_fused(e, s, P, dests, cq, C, alpha);
+        return launches + launch_fused(e, s, P, dests, cq, C, alpha, true);
     }
-    if (variant == STRASSEN_AB) {
-        // One launch computes every product into its own temporary (all 7^L
-        // batched); one launch streams them into C in table order.
-        double* M = e.ensure(e.mbuf, static_cast<size_t>(mstride) * live.size() * 8);
-        P.mbase = M;
-        P.nprod = static_cast<int>(live.size());
-        P.direct = 0;
-        for (size_t p = 0; p < live.size(); ++p) {
-            fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);
-            for (const auto& [q, g] : live[p].c) {
-                S.src_prod[q][S.nsrc[q]] = static_cast<int8_t>(p);
-                S.src_coeff[q][S.nsrc[q]] = static_cast<int8_t>(g);
-                ++S.nsrc[q];
-            }
-        }
-        e.prof_begin("mm_kernel", s);
-        ck(launch_mm(P, s), "mm_kernel (AB)");
-        e.prof_end(s);
-        S.mbase = M;
-        e.prof_begin("stream_update_kernel", s);
-        ck(launch_stream_update(S, s), "stream_update");
-        e.prof_end(s);
-        return launches + 2;
-    }
-
     throw Error(STRASSEN_ERR_PARAM, "unhandled variant");
 }
 }  // namespace

@@ -1,0 +1,96 @@
+"""BASELINE.json sweeps on one B200, CSV in the reference bench schema
+(tools/bench_lib.cpp:138-157: m,n,k,variant,level,threads,reps,time_s,
+egf_measured,egf_modeled,rel_err) plus the executed-flop fraction of the
+measured DMMA peak.  rel_err is a Freivalds estimate
+||C x - C0 x - A(B x)|| / (||A||_F ||B||_F ||x||) of the Strassen result.
+
+usage: python tools/sweep.py square|rankk|fixedk out.csv [reps]
+"""
+import csv
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import paper_1605_01078_b200 as S
+
+PEAK = 37.05
+CFG = {"dgemm": 0}
+ALL = [("dgemm", 0), ("abc", 1), ("ab", 1), ("naive", 1), ("c", 1), ("abc", 2), ("ab", 2),
+       ("naive", 2), ("c", 2)]
+
+
+def table(level):
+    return {0: (1, 0, 0, 1), 1: (7, 5, 5, 12), 2: (49, 95, 95, 144)}[level]
+
+
+def shapes(family):
+    if family == "square":  # configs[1]
+        return [(d, d, d) for d in range(1024, 16385, 1024)] + [(1000,) * 3, (4097,) * 3, (9999,) * 3]
+    if family == "rankk":   # configs[2]: m = n = 16384, k = 256..16384 step 256
+        return [(16384, 16384, k) for k in range(256, 16385, 256)]
+    if family == "fixedk":  # configs[3]: k = 1024, m = n = 2048..32768
+        return [(d, d, 1024) for d in range(2048, 32769, 2048)]
+    raise SystemExit(f"unknown family {family}")
+
+
+def variants(family):
+    if family == "rankk":
+        return [("dgemm", 0), ("abc", 1), ("ab", 1), ("abc", 2), ("ab", 2), ("naive", 2), ("c", 2)]
+    if family == "fixedk":
+        return [("dgemm", 0), ("abc", 2), ("ab", 2), ("naive", 2), ("c", 2), ("c", 1)]
+    return ALL
+
+
+def main():
+    family, out = sys.argv[1], sys.argv[2]
+    reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
+    ctx = S.Ctx()
+    rows = []
+    for (m, n, k) in shapes(family):
+        g = torch.Generator(device="cuda").manual_seed(m * 7 + n * 3 + k)
+        dist = torch.randn if family == "fixedk" else None  # configs[3]: normal(0, 1)
+        def mk(r, c):
+            x = torch.empty((c, r), dtype=torch.float64, device="cuda")
+            if dist:
+                x.normal_(0.0, 1.0, generator=g)
+            else:
+                x.uniform_(-1.0, 1.0, generator=g)
+            return x.t()
+        A, B, C0 = mk(m, k), mk(k, n), mk(m, n)
+        x = torch.rand(n, 1, dtype=torch.float64, device="cuda", generator=g)
+        want = C0 @ x + A @ (B @ x)
+        den = (torch.linalg.norm(A) * torch.linalg.norm(B) * torch.linalg.norm(x)).item()
+        for v, L in variants(family):
+            best = None
+            for r in range(reps + 1):
+                C = C0.clone().t().contiguous().t()  # fresh column-major copy of C0
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                ctx.gemm_device(v, L, 1.0, A, B, C)
+                e1.record()
+                torch.cuda.synchronize()
+                t = e0.elapsed_time(e1) * 1e-3
+                if r > 0:
+                    best = t if best is None else min(best, t)
+            err = (torch.linalg.norm(C @ x - want).item()) / den
+            egf = 2.0 * m * n * k / best * 1e-9
+            s = 1 << L
+            qm, qn, qk = -(-m // s), -(-n // s), -(-k // s)
+            mul, aa, ba, cu = table(L)
+            fexec = mul * 2.0 * qm * qn * qk if L else 2.0 * m * n * k
+            rows.append(dict(m=m, n=n, k=k, variant=v, level=L, threads=1, reps=reps, time_s=best,
+                             egf_measured=egf, egf_modeled="", rel_err=err,
+                             exec_frac_of_dmma_peak=fexec / best / 1e12 / PEAK))
+            print(f"{m}x{n}x{k} {v}{L}: {egf / 1e3:.2f} TF/s err {err:.1e}", flush=True)
+        del A, B, C0, C
+    with open(out, "w", newline="") as f:
+        w = csv.DictWriter(f, fieldnames=list(rows[0].keys()))
+        w.writeheader()
+        w.writerows(rows)
+
+
+if __name__ == "__main__":
+    main()
