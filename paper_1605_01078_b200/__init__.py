@@ -24,7 +24,8 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libstrassen_b200.so")
+# STRASSEN_B200_LIB: alternative in-tree build (A/B experiments, tools/ab.sh)
+LIB_PATH = os.path.join(HERE, os.environ.get("STRASSEN_B200_LIB", "libstrassen_b200.so"))
 
 DGEMM, ABC, AB, NAIVE, C_VARIANT = 0, 1, 2, 3, 4
 VARIANT_NAMES = {"dgemm": DGEMM, "abc": ABC, "ab": AB, "naive": NAIVE, "c": C_VARIANT}

@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstring>
 #include <mutex>
+#include <cstdlib>
 
 #include "kernels.hpp"
 #include "table.hpp"
@@ -271,7 +272,7 @@ long launch_fused(Engine& e, cudaStream_t s, MMParams& P, const std::vector<Term
     while (base * ksplit < 4L * sms && P.ktiles / (ksplit + 1) >= 4) ++ksplit;
     const int per = (P.ktiles + ksplit - 1) / ksplit;
     ksplit = (P.ktiles + per - 1) / per;
-    const long long ldm = P.qm, mstride = ldm * P.qn;
+    const long long ldm = (P.qm + 1) / 2 * 2, mstride = ldm * P.qn;  // even: 16-B stores
     double* M = e.ensure(e.mbuf, static_cast<size_t>(mstride) * P.nprod * ksplit * 8);
     P.mode = kEpiStore;
     P.split = 1;

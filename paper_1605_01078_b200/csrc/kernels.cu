@@ -367,16 +367,27 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             }
         } else {
             const int mi = P.split ? p * P.ksplit + (kt_lo / P.kt_per_split) : p;
+            // product temporaries: rows 2g, 2g+1 of fragment pair (2h, 2h+1)
+            // are adjacent (ldm even) -> one 16-byte streaming store
+            // (st.global.cs: evict-first, keeps operand panels in L2)
             double* __restrict__ M = P.mbase + mi * P.mstride;
 #pragma unroll
             for (int nf = 0; nf < 4; ++nf)
 #pragma unroll
-                for (int mf = 0; mf < 8; ++mf)
+                for (int h = 0; h < 4; ++h)
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
-                        const int row = mrow0 + 16 * (mf >> 1) + (mf & 1);
+                        const int row = mrow0 + 16 * h;
                         const int col = ncol0 + 8 * nf + (e ? c1 : c0);
-                        if (row < P.qm && col < P.qn) M[row + col * P.ldm] = acc[mf][nf][e];
+                        if (col >= P.qn) continue;
+                        double* dst = M + row + static_cast<long long>(col) * P.ldm;
+                        if (row + 1 < P.qm) {
+                            asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(dst),
+                                         "d"(acc[2 * h][nf][e]), "d"(acc[2 * h + 1][nf][e])
+                                         : "memory");
+                        } else if (row < P.qm) {
+                            dst[0] = acc[2 * h][nf][e];
+                        }
                     }
         }
     }
