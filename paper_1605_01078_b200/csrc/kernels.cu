@@ -500,6 +500,7 @@ cudaError_t launch_mm(const MMParams& p, cudaStream_t s) {
         maxt = p.prod[i].na > maxt ? p.prod[i].na : maxt;
         maxt = p.prod[i].nb > maxt ? p.prod[i].nb : maxt;
     }
+    if (maxt == 1) return launch_mm_t<1>(p, s);  // single-term programs: no sum code at all
     return maxt <= 2 ? launch_mm_t<2>(p, s) : launch_mm_t<kMaxTerms>(p, s);
 }
 
