@@ -426,22 +426,51 @@ __global__ void repack_kernel(const double* __restrict__ src, long long rs, long
 // C variant: all multi-term operand sums of a launch, one job per blockIdx.z.
 // Same arithmetic as materialize_kernel (variants.cpp:53-96 order).
 __global__ void sum_batch_kernel(const __grid_constant__ SumBatchParams P) {
+    // one thread = rows (2r, 2r+1) of two columns: 16-byte loads/stores
+    // (sources are TMA-ready quadrants: 16-byte aligned, even leading dims)
     const int z = blockIdx.z;
-    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const long long i = 2 * (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x);
     if (i >= P.rows) return;
     const int n = P.nterms[z];
     double* dst = P.dst[z];
-    for (long long j = blockIdx.y; j < P.cols; j += gridDim.y) {
-        double v = 0.0;
+    for (long long j = 2 * blockIdx.y; j < P.cols; j += 2 * gridDim.y) {
+        double2 v[2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) v[c] = make_double2(0.0, 0.0);
 #pragma unroll
         for (int u = 0; u < kMaxTerms; ++u) {
             if (u >= n) break;
             const SumTerm& t = P.t[z][u];
-            const double x = (i < t.rows && j < t.cols) ? t.x[i + j * t.ld] : 0.0;
-            const double c = t.coeff;
-            v = (u == 0) ? c * x : fma(c, x, v);
+            const double cu = t.coeff;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const long long jj = j + c;
+                double2 x = make_double2(0.0, 0.0);
+                if (jj < t.cols) {
+                    if (i + 1 < t.rows) {
+                        x = *reinterpret_cast<const double2*>(t.x + i + jj * t.ld);
+                    } else if (i < t.rows) {
+                        x.x = t.x[i + jj * t.ld];
+                    }
+                }
+                if (u == 0) {
+                    v[c].x = cu * x.x;
+                    v[c].y = cu * x.y;
+                } else {
+                    v[c].x = fma(cu, x.x, v[c].x);
+                    v[c].y = fma(cu, x.y, v[c].y);
+                }
+            }
         }
-        dst[i + j * P.ld] = v;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const long long jj = j + c;
+            if (jj >= P.cols) continue;
+            if (i + 1 < P.rows)
+                *reinterpret_cast<double2*>(dst + i + jj * P.ld) = v[c];
+            else
+                dst[i + jj * P.ld] = v[c].x;
+        }
     }
 }
 
@@ -520,9 +549,10 @@ static unsigned col_grid(long long cols) {
 
 cudaError_t launch_sum_batch(const SumBatchParams& p, cudaStream_t s) {
     if (p.njobs == 0) return cudaSuccess;
-    dim3 grid(static_cast<unsigned>((p.rows + 255) / 256),
-              static_cast<unsigned>(p.cols < 2048 ? p.cols : 2048), p.njobs);
-    sum_batch_kernel<<<grid, 256, 0, s>>>(p);
+    const long long pairs = (p.rows + 1) / 2, cpairs = (p.cols + 1) / 2;
+    dim3 grid(static_cast<unsigned>((pairs + 127) / 128),
+              static_cast<unsigned>(cpairs < 1024 ? cpairs : 1024), p.njobs);
+    sum_batch_kernel<<<grid, 128, 0, s>>>(p);
     return cudaGetLastError();
 }
 
