@@ -85,8 +85,12 @@ void cuda_ck(cudaError_t e, const char* what) {
 }
 
 // Host operand -> device view (copy of the view's span); device -> as is.
+// Host operands are copied on the engine's copy stream (in call order A, B, C)
+// and each gets a ready event; kernels wait on it right before their first
+// read, so B's and C's transfers overlap the work that does not need them.
 sb200::DView stage_in(sb200::Engine& e, cudaStream_t s, const double* p, long rows, long cols,
-                      long rs, long cs, sb200::DeviceBuffer& buf, bool copy, bool& staged) {
+                      long rs, long cs, sb200::DeviceBuffer& buf, bool copy, bool& staged,
+                      cudaEvent_t ready_ev) {
     sb200::DView v;
     v.rows = rows;
     v.cols = cols;
@@ -101,8 +105,13 @@ sb200::DView stage_in(sb200::Engine& e, cudaStream_t s, const double* p, long ro
     span_of(rows, cols, rs, cs, lo, hi);
     const size_t count = static_cast<size_t>(hi - lo + 1);
     double* d = e.ensure(buf, count * 8);
-    if (copy)
-        cuda_ck(cudaMemcpyAsync(d, p + lo, count * 8, cudaMemcpyHostToDevice, s), "H2D operand");
+    (void)s;
+    if (copy) {
+        cuda_ck(cudaMemcpyAsync(d, p + lo, count * 8, cudaMemcpyHostToDevice, e.copy_stream),
+                "H2D operand");
+        cuda_ck(cudaEventRecord(ready_ev, e.copy_stream), "ready event");
+        v.ready = ready_ev;
+    }
     v.p = d - lo;
     return v;
 }
@@ -122,9 +131,12 @@ strassen_status gemm_impl(strassen_ctx* ctx, bool explicit_stream, cudaStream_t 
         cudaStream_t s = explicit_stream ? user_stream : e.stream();
         long launches = 0;
         bool sa = false, sb = false, sc = false;
-        const sb200::DView A = stage_in(e, s, a, m, k, rs_a, cs_a, e.stage_a, true, sa);
-        const sb200::DView B = stage_in(e, s, b, k, n, rs_b, cs_b, e.stage_b, true, sb);
-        const sb200::DView C = stage_in(e, s, c, m, n, rs_c, cs_c, e.stage_c, true, sc);
+        // the copy stream may only overwrite staging buffers once earlier work on s is done
+        cuda_ck(cudaEventRecord(e.ev_call, s), "call event");
+        cuda_ck(cudaStreamWaitEvent(e.copy_stream, e.ev_call, 0), "copy stream order");
+        const sb200::DView A = stage_in(e, s, a, m, k, rs_a, cs_a, e.stage_a, true, sa, e.ev_ready[0]);
+        const sb200::DView B = stage_in(e, s, b, k, n, rs_b, cs_b, e.stage_b, true, sb, e.ev_ready[1]);
+        const sb200::DView C = stage_in(e, s, c, m, n, rs_c, cs_c, e.stage_c, true, sc, e.ev_ready[2]);
         if (device_only && (sa || sb || sc))
             throw std::invalid_argument("strassen_gemm_device: operands must be device memory");
         for (auto& t : e.timed) {
@@ -137,6 +149,7 @@ strassen_status gemm_impl(strassen_ctx* ctx, bool explicit_stream, cudaStream_t 
         if (sc) {
             long lo, hi;
             span_of(m, n, rs_c, cs_c, lo, hi);
+            sb200::wait_ready(s, C);  // even if no kernel touched C
             cuda_ck(cudaMemcpyAsync(c + lo, C.p + lo, static_cast<size_t>(hi - lo + 1) * 8,
                                     cudaMemcpyDeviceToHost, s),
                     "D2H result");

@@ -64,6 +64,7 @@ long clip(long v, long lo, long hi) { return std::max(lo, std::min(hi, v)); }
 // An operand prepared for TMA: column-major, 16-byte aligned quadrant origins.
 struct TmaOperand {
     const double* base = nullptr;
+    cudaEvent_t ready = nullptr;  // pending copy-in of the operand (read in place)
     long long ld = 0;
     long q_rows_al = 0;  // row offset between quadrant rows (>= logical q rows)
     long rows = 0, cols = 0;
@@ -88,6 +89,7 @@ TmaOperand prepare(Engine& e, cudaStream_t s, const DView& v, long q_rows, long 
     t.q_rows = q_rows;
     t.q_cols = q_cols;
     if (tma_ready(v, q_rows, side)) {
+        t.ready = v.ready;
         t.base = v.p;
         t.ld = v.cs;
         t.q_rows_al = q_rows;
@@ -99,6 +101,7 @@ TmaOperand prepare(Engine& e, cudaStream_t s, const DView& v, long q_rows, long 
     long long ld = static_cast<long long>(side > 1 ? q_al * side : v.rows);
     ld = std::max<long long>(((ld + 3) / 4) * 4, 4);
     double* dst = e.ensure(scratch, static_cast<size_t>(ld) * v.cols * 8);
+    wait_ready(s, v);
     e.prof_begin("repack_kernel", s);
     ck(launch_repack(v.p, v.rs, v.cs, v.rows, v.cols, dst, ld, side > 1 ? q_rows : v.rows + 1,
                      side > 1 ? q_al : v.rows + 1, s),
@@ -172,6 +175,10 @@ void fill_desc(ProductDesc& d, const Terms& a, const Terms& b, const Terms& c) {
 // ------------------------------------------------------------------ Engine --
 Engine::~Engine() {
     if (!initialised) return;
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+    if (ev_call) cudaEventDestroy(ev_call);
+    for (auto ev : ev_ready)
+        if (ev) cudaEventDestroy(ev);
     for (DeviceBuffer* b : {&stage_a, &stage_b, &stage_c, &pack_a, &pack_b, &mbuf, &tabuf, &tbbuf})
         if (b->ptr) cudaFree(b->ptr);
 }
@@ -183,6 +190,9 @@ void Engine::init() {
         throw Error(STRASSEN_ERR_DEVICE, "no CUDA device");
     ck(cudaGetDevice(&device), "cudaGetDevice");
     ck(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device), "SM count");
+    ck(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking), "copy stream");
+    ck(cudaEventCreateWithFlags(&ev_call, cudaEventDisableTiming), "event");
+    for (auto& ev : ev_ready) ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
     initialised = true;
 }
 
@@ -260,6 +270,7 @@ long launch_fused(Engine& e, cudaStream_t s, MMParams& P, const std::vector<Term
     const int ntiles = P.tiles_m * P.tiles_n;
     const int sms = e.num_sms > 0 ? e.num_sms : 148;
     if (ntiles >= 2 * sms && !force_split) {
+        wait_ready(s, C);  // fused epilogue reads C
         P.mode = kEpiRMW;
         P.split = 0;
         e.prof_begin("mm_kernel", s);
@@ -307,6 +318,7 @@ long launch_fused(Engine& e, cudaStream_t s, MMParams& P, const std::vector<Term
             S.src_coeff[q][S.nsrc[q]] = static_cast<int8_t>(g);
             ++S.nsrc[q];
         }
+    wait_ready(s, C);  // first reader of C: its copy-in overlapped the products
     e.prof_begin("stream_update_kernel", s);
     ck(launch_stream_update(S, s), "stream_update (split)");
     e.prof_end(s);
@@ -424,6 +436,10 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
         live.push_back(std::move(l));
     }
     if (live.empty()) return launches;
+    if (variant != STRASSEN_C && variant != STRASSEN_NAIVE) {  // mm_kernel reads A and B
+        if (ta.ready) cudaStreamWaitEvent(s, ta.ready, 0);
+        if (tb.ready) cudaStreamWaitEvent(s, tb.ready, 0);
+    }
 
     if (variant == STRASSEN_C || variant == STRASSEN_NAIVE) {
         // Every multi-term operand sum materialised by one batched HBM pass
@@ -470,6 +486,11 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
                 else
                     encode_map(&P.tmB[mi], dst, qk, qn, ldb_t, kBK, kBN, true);
                 terms = {{mi, 1}};
+            }
+            if (side == 0) {
+                if (ta.ready) cudaStreamWaitEvent(s, ta.ready, 0);
+            } else if (tb.ready) {
+                cudaStreamWaitEvent(s, tb.ready, 0);
             }
             e.prof_begin("sum_batch_kernel", s);
             cudaError_t err = launch_sum_batch(*SB, s);
@@ -562,6 +583,7 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
 
 long scale_device(Engine& e, cudaStream_t s, const DView& C, double beta) {
     (void)e;
+    wait_ready(s, C);
     ck(launch_scale(C.p, C.rows, C.cols, C.rs, C.cs, beta, s), "scale");
     return 1;
 }

@@ -55,6 +55,9 @@ struct Engine {
     ~Engine();
     void init();
     cudaStream_t stream();
+    // host-operand staging: copies run on their own stream, one event each
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_call = nullptr, ev_ready[3] = {nullptr, nullptr, nullptr};
     double* ensure(DeviceBuffer& b, size_t bytes);
     size_t workspace_bytes() const;
 };
@@ -63,7 +66,15 @@ struct DView {  // a strided matrix view in device memory
     double* p = nullptr;
     long rows = 0, cols = 0;
     long long rs = 0, cs = 0;
+    // set when the view is still being copied in (host operand on the copy
+    // stream): kernels that read it wait on this event right before launch
+    cudaEvent_t ready = nullptr;
 };
+
+// Make stream s wait until view v has landed (no-op for resident operands).
+inline void wait_ready(cudaStream_t s, const DView& v) {
+    if (v.ready) cudaStreamWaitEvent(s, v.ready, 0);
+}
 
 // C := alpha A B + C on device views, enqueued on `s` (no synchronisation).
 // variant/level already validated.  Returns the number of kernel launches.

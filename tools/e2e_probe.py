@@ -1,0 +1,16 @@
+"""e2e probe: strassen_gemm through the C ABI with pinned host buffers."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_1605_01078_b200 as S
+dim = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+ctx = S.Ctx()
+g = torch.Generator().manual_seed(0)
+A, B, C = ((torch.rand(dim, dim, dtype=torch.float64, generator=g) * 2 - 1).pin_memory().t() for _ in range(3))
+for v in (sys.argv[2].split(",") if len(sys.argv) > 2 else ["naive2", "abc1", "dgemm0"]):
+    ctx.gemm(v[:-1], int(v[-1]), 1.0, A, B, C)
+    t0 = time.perf_counter()
+    for _ in range(2):
+        ctx.gemm(v[:-1], int(v[-1]), 1.0, A, B, C)
+    dt = (time.perf_counter() - t0) / 2
+    print(f"{dim} {v}: e2e {dt*1e3:.1f} ms  {2*dim**3/dt/1e12:.2f} TF/s", flush=True)
