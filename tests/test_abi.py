@@ -218,3 +218,29 @@ def test_dgemm_shim_argument_checks():
 def test_build_info_names_sm100a():
     info = S.lib().strassen_build_info().decode()
     assert "sm_100a" in info and "DMMA" in info
+
+
+def test_b200_ctx_setters_without_device():
+    ctx = S.Ctx()
+    ctx.set_peeling(False)
+    ctx.set_peeling(True)
+    ctx.enable_profiling(True)
+    assert ctx.last_profile() == []
+    ctx.set_stream(None)
+    assert ctx.workspace_bytes() == 0
+    assert S.lib().strassen_ctx_set_peeling(None, 1) == S.ERR_NULL
+    assert S.lib().strassen_ctx_last_profile(ctx.ptr, None, 10) == S.ERR_NULL
+
+
+def test_c_variant_counters_and_validation():
+    # B200 addition: Naive's materialised sums (multi-term operands only), ABC's fused C
+    c = S.predicted_counters("c", 1, 64, 64, 64)
+    assert c["a_plus_passes"] == 5 * 3 and c["b_plus_passes"] == 5 * 3
+    assert c["c_plus_passes"] == 0
+    assert c["kernel_fma_flops"] == 7 * 2 * 32 ** 3
+    assert c["kernel_update_flops"] == 12 * 2 * 32 * 32
+    ctx = S.Ctx()
+    a = np.zeros(16)
+    pa = C.c_void_p(a.ctypes.data)
+    assert ctx.gemm_raw(S.C_VARIANT, 0, 4, 4, 4, 1.0, pa, 4, 1, pa, 4, 1, pa, 4, 1) == S.ERR_PARAM
+    assert ctx.gemm_raw(S.C_VARIANT, 3, 4, 4, 4, 1.0, pa, 4, 1, pa, 4, 1, pa, 4, 1) == S.ERR_PARAM

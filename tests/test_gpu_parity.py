@@ -269,3 +269,34 @@ def test_dynamic_peeling_vs_padding(ctx, shape):
         for v, L in [("abc", 1), ("abc", 2), ("naive", 2), ("c", 2)]:
             check(v, L, run(ctx, v, L, 1.0, a, b, c0), ref, c0, a, b)
     ctx.set_peeling(True)
+
+
+def test_profiling_reports_each_launch(ctx):
+    m = n = k = 2048
+    a, b, c0 = inputs(m, n, k, (71, 72, 73))
+    c = S.Ctx()
+    c.enable_profiling(True)
+    out = np.array(c0, order="F")
+    c.gemm("naive", 2, 1.0, a, b, out)
+    prof = c.last_profile()
+    names = [p["kernel"] for p in prof]
+    assert names.count("mm_kernel") == 1 and "stream_update_kernel" in names
+    assert all(p["ms"] > 0 for p in prof)
+    assert c.last_launches() == len(prof)
+
+
+def test_host_staging_overlap_each_variant_and_operand_kind(ctx):
+    """Copy-stream staging: host A/B/C in every combination with device ones."""
+    import torch
+    m, n, k = 700, 900, 800
+    a, b, c0 = inputs(m, n, k, (81, 82, 83))
+    ref = oracle_result("dgemm", 0, 0.5, a, b, c0, use_reference_gemm=False)
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x.T)).cuda().t()  # noqa: E731
+    for host_mask in range(8):
+        for v, L in [("naive", 2), ("abc", 1), ("c", 2)]:
+            A = a if host_mask & 1 else dev(a)
+            B = b if host_mask & 2 else dev(b)
+            C = np.array(c0, order="F") if host_mask & 4 else dev(c0)
+            ctx.gemm(v, L, 0.5, A, B, C)
+            got = C if isinstance(C, np.ndarray) else C.cpu().numpy()
+            check(v, L, got, ref, c0, a, b)
