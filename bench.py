@@ -39,7 +39,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CPU_SAMPLE = 4096  # bounded reference sample: m = n = k = 4096
+CPU_SAMPLE = 0  # bounded reference sample edge; 0 = adaptive (about 3 s per call, <= 4096)
 
 
 def parse():
@@ -163,8 +163,17 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def reference_cpu(dim, variant, level, reps=2, warmup=1):
-    """The reference library itself on the host cores (bounded sample)."""
+def ref_variant(variant):
+    """The reference has no "c" variant (a B200 addition): its arm runs ABC."""
+    return "abc" if variant == "c" else variant
+
+
+def reference_cpu(dim, variant, level, reps=2, warmup=1, target_s=3.0):
+    """The reference library itself on the host cores (bounded sample).
+
+    dim = 0 picks the sample edge adaptively: time one 1024^3 call, then scale
+    (O(n^3)) to about target_s per call, rounded to 256 and capped at 4096.
+    """
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import numpy as np
 
@@ -176,6 +185,16 @@ def reference_cpu(dim, variant, level, reps=2, warmup=1):
         raise RuntimeError("oracle/_ref/libstrassen_ref.so missing (make -C oracle ref)")
     ref = O.RefStrassen(path)
     ref.set_threads(cores)
+    variant = ref_variant(variant)
+    if not dim:
+        rng = np.random.default_rng(1)
+        x = np.asfortranarray(rng.uniform(-1, 1, (1024, 1024)))
+        y = x.copy(order="F")
+        t0 = time.perf_counter()
+        ref.gemm(variant, level, 1.0, x, x, y)
+        t1 = time.perf_counter() - t0
+        dim = int(1024 * (target_s / max(t1, 1e-3)) ** (1.0 / 3.0)) // 256 * 256
+        dim = max(1024, min(4096, dim))
     rng = np.random.default_rng(0)
     a = np.asfortranarray(rng.uniform(-1, 1, (dim, dim)))
     b = np.asfortranarray(rng.uniform(-1, 1, (dim, dim)))
@@ -187,7 +206,7 @@ def reference_cpu(dim, variant, level, reps=2, warmup=1):
         dt = time.perf_counter() - t0
         if i >= warmup:
             times.append(dt)
-    return {"kind": kind, "cores": cores, "times": times,
+    return {"kind": kind, "cores": cores, "times": times, "dim": dim,
             "sample": f"m=n=k={dim} {variant}{level} via the reference C ABI "
                       f"(oracle/_ref, -O3 -DNDEBUG -fopenmp, threads={cores}), column-major, "
                       f"uniform[-1,1); best of {reps} after {warmup} warm-up"}
@@ -196,8 +215,9 @@ def reference_cpu(dim, variant, level, reps=2, warmup=1):
 def run_reference(args, rank):
     if rank != 0:
         return
-    dim = args.cpu_sample
-    r = reference_cpu(dim, args.variant, args.level, reps=args.steps, warmup=args.warmup)
+    r = reference_cpu(args.cpu_sample, args.variant, args.level, reps=args.steps,
+                      warmup=args.warmup)
+    dim = r["dim"]
     t = sum(r["times"]) / len(r["times"])
     tf = 2.0 * dim ** 3 / t / 1e12
     line = {
@@ -206,7 +226,8 @@ def run_reference(args, rank):
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic uniform[-1,1)",
         "config": {"workload": f"square m=n=k={args.m} {args.variant} level {args.level} "
-                   f"(bounded CPU sample m=n=k={dim})", "variant": args.variant,
+                   f"(bounded CPU sample m=n=k={dim}; reference variant "
+                   f"{ref_variant(args.variant)})", "variant": args.variant,
                    "level": args.level, "m": dim, "n": dim, "k": dim},
         "cpu_baseline": {"value": tf, "unit": "TFLOP/s", "cores": r["cores"], "kind": r["kind"],
                          "sample": r["sample"]},
@@ -388,7 +409,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         r = reference_cpu(args.cpu_sample, args.variant, args.level)
         t = min(r["times"])
-        line["cpu_baseline"] = {"value": 2.0 * args.cpu_sample ** 3 / t / 1e12, "unit": "TFLOP/s",
+        line["cpu_baseline"] = {"value": 2.0 * r["dim"] ** 3 / t / 1e12, "unit": "TFLOP/s",
                                 "cores": r["cores"], "kind": r["kind"], "sample": r["sample"]}
 
     if rank == 0:
