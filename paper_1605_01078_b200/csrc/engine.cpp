@@ -417,6 +417,12 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
     P.rs_c = C.rs;
     P.cs_c = C.cs;
     P.alpha = alpha;
+    {   // 16-byte epilogue: C column-major, even ldc, every quadrant origin aligned
+        bool vec = C.rs == 1 && C.cs % 2 == 0 && (reinterpret_cast<uintptr_t>(C.p) % 16) == 0;
+        for (int qi = 0; qi < side * side && vec; ++qi)
+            vec = (reinterpret_cast<uintptr_t>(cq[qi].p) % 16) == 0;
+        P.c_vec = vec ? 1 : 0;
+    }
     P.qm = static_cast<int>(qm);
     P.qn = static_cast<int>(qn);
     P.qk = static_cast<int>(qk);

@@ -337,11 +337,54 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         const int ncol0 = tn * kBN + wn * 32;
         const int c0 = nperm(2 * j), c1 = nperm(2 * j + 1);
         if (P.mode == kEpiRMW) {
+            // 16-byte path: C column-major with rows (2g, 2g+1) of the fragment
+            // pair (2h, 2h+1) adjacent and 16-byte aligned (checked on the host)
             for (int u = 0; u < pd.nc; ++u) {
                 const int cq = pd.cq[u];
                 double* __restrict__ C = P.cptr[cq];
                 const int R = P.crows[cq], Cc = P.ccols[cq];
                 const double sc = P.alpha * static_cast<double>(pd.cs[u]);
+                if (P.c_vec) {
+#pragma unroll
+                    for (int nh = 0; nh < 2; ++nh) {  // two rounds of 16 loads in flight
+                        double2 cv[2][4][2];
+#pragma unroll
+                        for (int n2 = 0; n2 < 2; ++n2)
+#pragma unroll
+                            for (int h = 0; h < 4; ++h)
+#pragma unroll
+                                for (int e = 0; e < 2; ++e) {
+                                    const int nf = 2 * nh + n2;
+                                    const int row = mrow0 + 16 * h;
+                                    const int col = ncol0 + 8 * nf + (e ? c1 : c0);
+                                    double2 v = make_double2(0.0, 0.0);
+                                    if (col < Cc) {
+                                        const double* src = C + row + static_cast<long long>(col) * P.cs_c;
+                                        if (row + 1 < R) v = *reinterpret_cast<const double2*>(src);
+                                        else if (row < R) v.x = *src;
+                                    }
+                                    cv[n2][h][e] = v;
+                                }
+#pragma unroll
+                        for (int n2 = 0; n2 < 2; ++n2)
+#pragma unroll
+                            for (int h = 0; h < 4; ++h)
+#pragma unroll
+                                for (int e = 0; e < 2; ++e) {
+                                    const int nf = 2 * nh + n2;
+                                    const int row = mrow0 + 16 * h;
+                                    const int col = ncol0 + 8 * nf + (e ? c1 : c0);
+                                    if (col >= Cc) continue;
+                                    double* dst = C + row + static_cast<long long>(col) * P.cs_c;
+                                    double2 v = cv[n2][h][e];
+                                    v.x = fma(sc, acc[2 * h][nf][e], v.x);
+                                    v.y = fma(sc, acc[2 * h + 1][nf][e], v.y);
+                                    if (row + 1 < R) *reinterpret_cast<double2*>(dst) = v;
+                                    else if (row < R) *dst = v.x;
+                                }
+                    }
+                    continue;
+                }
 #pragma unroll
                 for (int nf = 0; nf < 4; ++nf) {
                     double cv[8][2];
