@@ -202,6 +202,13 @@ strassen_status strassen_ctx_last_profile(strassen_ctx* ctx, char* buf, long siz
 /* Device memory currently held by the ctx workspace, in bytes. */
 strassen_status strassen_ctx_workspace_bytes(const strassen_ctx* ctx, long* out);
 
+/* Model-guided dispatch (the paper's use of its model,
+ * PAPER.md:894-895): the variant and level a B200 cost model, fitted to the
+ * measured kernel efficiencies, predicts fastest for an m x n x k multiply,
+ * and the predicted seconds (may be NULL).  No device needed. */
+strassen_status strassen_select(long m, long n, long k, strassen_variant* variant_out,
+                                int* level_out, double* seconds_out);
+
 /* Counter values one strassen_gemm(variant, level, m, n, k) call adds under
  * blocking *bp (the analytic instrumentation; no device needed).  Same
  * validation as strassen_gemm for variant / level / dimensions / blocking. */

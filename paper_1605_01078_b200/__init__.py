@@ -21,6 +21,7 @@ __all__ = [
     "DGEMM", "ABC", "AB", "NAIVE", "StrassenError", "Ctx", "build", "lib", "gemm", "gemm_device",
     "dgemm", "reference_gemm", "rel_error", "table_counts", "effective_gflops", "model_predict",
     "blocking_defaults", "model_params_ivy_bridge", "predicted_counters", "COUNTER_FIELDS",
+    "select",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -120,6 +121,7 @@ def _declare(lib):
         "strassen_ctx_enable_profiling": (_ST, [vp, C.c_int]),
         "strassen_ctx_set_peeling": (_ST, [vp, C.c_int]),
         "strassen_ctx_last_profile": (_ST, [vp, C.c_char_p, _L]),
+        "strassen_select": (_ST, [_L, _L, _L, C.POINTER(C.c_int), C.POINTER(C.c_int), _dp]),
         "strassen_build_info": (C.c_char_p, []),
         "strassen_last_error": (C.c_char_p, []),
     }
@@ -384,3 +386,11 @@ def predicted_counters(variant, level, m, n, k, blocking=None):
     _check(lib().strassen_count_call(_variant(variant), int(level), m, n, k, C.byref(bp),
                                      C.byref(c)), "count_call")
     return {f: getattr(c, f) for f in COUNTER_FIELDS}
+
+
+def select(m, n, k):
+    """(variant name, level, predicted seconds) the B200 cost model picks for a shape."""
+    v, lv, t = C.c_int(), C.c_int(), C.c_double()
+    _check(lib().strassen_select(m, n, k, C.byref(v), C.byref(lv), C.byref(t)), "select")
+    name = {val: key for key, val in VARIANT_NAMES.items()}[v.value]
+    return name, lv.value, t.value

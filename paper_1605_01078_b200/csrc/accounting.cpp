@@ -13,6 +13,7 @@
 #include "accounting.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <stdexcept>
 
 #include "table.hpp"
@@ -257,6 +258,84 @@ void model_predict(strassen_variant v, int level, long m, long n, long k,
               (t.tm_a_mul + t.tm_b_mul + t.tm_c_mul + t.tm_a_add + t.tm_b_add + t.tm_c_add);
     out = t;
     egf = effective_gflops(m, n, k, t.total);
+}
+
+
+// ------------------------------------------------------- B200 dispatch model --
+// The paper's purpose for its model is choosing the family member per shape
+// (reference model.cpp).  This is the same T = T_a + T_m split
+// re-fitted to B200 with the round-1 measurements (profiles/r01_notes.md,
+// profiles/r01_sweep_*.csv):
+//   T_a: executed mm_kernel flops / (37.05 TF/s * e_mm * wave efficiency), with
+//        e_mm = 0.96 for single-term programs (DGEMM, Naive, C), 0.86 / 0.62 for
+//        the fused two- / four-term sums (ABC, AB at level 1 / 2);
+//   T_m: HBM bytes of the sum / stream / C-update traffic at 5.5 TB/s;
+//   + 6 us per launch and the split-mode partials for outputs under two waves.
+namespace {
+double waves_eff(double ctas, double sms) {
+    const double w = std::ceil(ctas / sms);
+    return ctas / (w * sms);
+}
+}  // namespace
+
+double b200_predict_seconds(strassen_variant v, int level, long m, long n, long k, int sms) {
+    const double P = 37.05e12, BW = 5.5e12, launch = 6e-6;
+    const int L = (v == STRASSEN_DGEMM) ? 0 : level;
+    const long S = 1L << L;
+    const double qm = static_cast<double>(ceil_div(m, S)), qn = static_cast<double>(ceil_div(n, S)),
+                 qk = static_cast<double>(ceil_div(k, S));
+    static const double tc[3][4] = {{1, 0, 0, 1}, {7, 5, 5, 12}, {49, 95, 95, 144}};
+    const double mul = tc[L][0], aa = tc[L][1], ba = tc[L][2], cu = tc[L][3];
+    const double tiles = std::ceil(qm / 128.0) * std::ceil(qn / 128.0);
+    double e_mm = 0.96;
+    if (v == STRASSEN_ABC || v == STRASSEN_AB) e_mm = (L == 1) ? 0.86 : 0.62;
+    const bool per_product_grid = (v == STRASSEN_AB || v == STRASSEN_NAIVE);
+    const bool split = tiles < 2.0 * sms;
+    double ctas = (per_product_grid || split) ? tiles * mul : tiles;
+    double ks = 1;
+    if (split) {  // k-chunks as engine.cpp launch_fused picks them
+        const double ktiles = std::ceil(qk / 16.0);
+        while (tiles * mul * ks < 4.0 * sms && std::floor(ktiles / (ks + 1)) >= 4) ks += 1;
+        ctas *= ks;
+    }
+    // per-CTA fixed cost (barrier init, pipeline fill, epilogue): ~4 us per wave
+    double t = mul * 2.0 * qm * qn * qk / (P * e_mm * waves_eff(ctas, sms)) +
+               4e-6 * std::ceil(ctas / sms);
+    double bytes = 0.0;
+    int launches = 1;
+    if (v == STRASSEN_NAIVE || v == STRASSEN_C) {  // materialised sums, both sides
+        bytes += 8.0 * ((aa + mul) * qm * qk + (ba + mul) * qk * qn);
+        launches += 2;
+    }
+    if (per_product_grid || split || v == STRASSEN_NAIVE) {  // M_{p,s} + stream pass
+        // write every partial M_{p,s}; each C update reads its product's partials
+        bytes += 8.0 * (ks * mul * qm * qn + ks * cu * qm * qn + 2.0 * m * n);
+        launches += 1;
+    } else {  // fused epilogue: C read + write per C update
+        bytes += 16.0 * cu * qm * qn;
+    }
+    t += bytes / BW + launches * launch;
+    return t;
+}
+
+void b200_select(long m, long n, long k, int sms, strassen_variant& v_out, int& l_out,
+                 double& t_out) {
+    const struct {
+        strassen_variant v;
+        int l;
+    } cand[] = {{STRASSEN_DGEMM, 0}, {STRASSEN_ABC, 1}, {STRASSEN_AB, 1}, {STRASSEN_NAIVE, 1},
+                {STRASSEN_C, 1},     {STRASSEN_ABC, 2}, {STRASSEN_AB, 2}, {STRASSEN_NAIVE, 2},
+                {STRASSEN_C, 2}};
+    t_out = 1e300;
+    for (const auto& c : cand) {
+        if (c.l > 0 && (m < (1L << c.l) || n < (1L << c.l) || k < (1L << c.l))) continue;
+        const double t = b200_predict_seconds(c.v, c.l, m, n, k, sms);
+        if (t < t_out) {
+            t_out = t;
+            v_out = c.v;
+            l_out = c.l;
+        }
+    }
 }
 
 }  // namespace sb200

@@ -21,4 +21,10 @@ void model_predict(strassen_variant v, int level, long m, long n, long k,
                    const strassen_blocking& bp, const strassen_model_params& mp,
                    strassen_breakdown& out, double& egf);
 
+// B200 cost model (strassen_select): predicted seconds of
+// one strassen_gemm call, and the fastest (variant, level) for a shape.
+double b200_predict_seconds(strassen_variant v, int level, long m, long n, long k, int sms);
+void b200_select(long m, long n, long k, int sms, strassen_variant& v_out, int& l_out,
+                 double& t_out);
+
 }  // namespace sb200

@@ -388,6 +388,22 @@ const char* strassen_status_str(strassen_status s) {
     return "unknown";
 }
 
+strassen_status strassen_select(long m, long n, long k, strassen_variant* variant_out,
+                                int* level_out, double* seconds_out) {
+    if (!variant_out || !level_out) return STRASSEN_ERR_NULL;
+    if (m < 1 || n < 1 || k < 1) return STRASSEN_ERR_PARAM;
+    int sms = 148;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    else
+        cudaGetLastError();
+    double t = 0.0;
+    sb200::b200_select(m, n, k, sms > 0 ? sms : 148, *variant_out, *level_out, t);
+    if (seconds_out) *seconds_out = t;
+    return STRASSEN_OK;
+}
+
 strassen_status strassen_count_call(strassen_variant variant, int level, long m, long n, long k,
                                     const strassen_blocking* bp, strassen_counter_values* out) {
     if (!bp || !out) return STRASSEN_ERR_NULL;

@@ -244,3 +244,27 @@ def test_c_variant_counters_and_validation():
     pa = C.c_void_p(a.ctypes.data)
     assert ctx.gemm_raw(S.C_VARIANT, 0, 4, 4, 4, 1.0, pa, 4, 1, pa, 4, 1, pa, 4, 1) == S.ERR_PARAM
     assert ctx.gemm_raw(S.C_VARIANT, 3, 4, 4, 4, 1.0, pa, 4, 1, pa, 4, 1, pa, 4, 1) == S.ERR_PARAM
+
+
+def test_model_guided_selection_against_measured_sweeps():
+    """strassen_select (B200 cost model) vs the committed round-1 sweeps:
+    its pick must be within 3% of the fastest measured configuration."""
+    import collections
+    import csv
+    misses = []
+    for fam in ("square", "rankk", "fixedk"):
+        path = os.path.join(ROOT, "profiles", f"r01_sweep_{fam}.csv")
+        by = collections.defaultdict(dict)
+        for r in csv.DictReader(open(path)):
+            by[(int(r["m"]), int(r["n"]), int(r["k"]))][r["variant"] + r["level"]] = float(r["time_s"])
+        for shape, times in by.items():
+            v, lv, t = S.select(*shape)
+            key = f"{v}{lv}"
+            if key in times and times[key] > 1.03 * min(times.values()):
+                misses.append((shape, key, times[key] / min(times.values())))
+            assert t > 0
+    assert not misses, misses
+    assert S.select(16384, 16384, 16384)[:2] == ("naive", 2)
+    assert S.select(1024, 1024, 1024)[:2] == ("dgemm", 0)
+    with pytest.raises(S.StrassenError):
+        S.select(0, 4, 4)
