@@ -507,7 +507,6 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
             if (njobs) ++launches;
         }
         P.nprod = static_cast<int>(live.size());
-        P.direct = 1;
         std::vector<Terms> dests;
         for (size_t p = 0; p < live.size(); ++p) {
             fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);
@@ -558,14 +557,10 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
 
     if (variant == STRASSEN_DGEMM || variant == STRASSEN_ABC) {
         P.nprod = static_cast<int>(live.size());
-        P.direct = 1;
         std::vector<Terms> dests;
         for (size_t p = 0; p < live.size(); ++p) {
             fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);
             dests.push_back(live[p].c);
-            if (live[p].a.size() != 1 || live[p].b.size() != 1 || live[p].a[0].second != 1 ||
-                live[p].b[0].second != 1)
-                P.direct = 0;
         }
         return launches + launch_fused(e, s, P, dests, cq, C, alpha);
     }
@@ -575,7 +570,6 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
         // temporaries on a product-parallel grid (k-split too when few tiles),
         // streamed into C in table order.
         P.nprod = static_cast<int>(live.size());
-        P.direct = 0;
         std::vector<Terms> dests;
         for (size_t p = 0; p < live.size(); ++p) {
             fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);

@@ -65,10 +65,6 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
-__device__ __forceinline__ void consumer_bar() {
-    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
-}
-
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -78,12 +74,6 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(d0), "+d"(d1)
                  : "d"(a), "d"(b));
-}
-
-// Negate a double by flipping its sign bit with an integer op (keeps the
-// FP64 pipe, which DMMA saturates, free).
-__device__ __forceinline__ double flip_sign(double x, uint32_t neg) {
-    return __hiloint2double(__double2hiint(x) ^ static_cast<int>(neg << 31), __double2loint(x));
 }
 
 // ---- shared-memory operand layouts and the DMMA fragment mapping ---------
@@ -467,7 +457,7 @@ __global__ void repack_kernel(const double* __restrict__ src, long long rs, long
 
 // -------------------------------------------------------------- sum batch ---
 // C variant: all multi-term operand sums of a launch, one job per blockIdx.z.
-// Same arithmetic as materialize_kernel (variants.cpp:53-96 order).
+// Arithmetic of materialize_sum (variants.cpp:53-96): d0*x0, then += ds*xs in order.
 __global__ void sum_batch_kernel(const __grid_constant__ SumBatchParams P) {
     // one thread = rows (2r, 2r+1) of two columns: 16-byte loads/stores
     // (sources are TMA-ready quadrants: 16-byte aligned, even leading dims)

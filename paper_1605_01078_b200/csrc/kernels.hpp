@@ -61,7 +61,6 @@ struct alignas(64) MMParams {
     int tiles_m, tiles_n, ktiles;
     int mode;
     int group_m;                // tile rasterisation group height
-    int direct;                 // every product is a single +1 term on both sides
     int c_vec;                  // C column-major, even ldc, 16-byte aligned quadrants
     // split mode (few output tiles): blockIdx -> (tile, product, k-chunk); each
     // CTA stores its partial product to M_{p*ksplit+s} (kEpiStore)
