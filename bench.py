@@ -92,18 +92,24 @@ def executed_flops(m, n, k, level, variant="abc"):
 
 # sum over multi-term operands of (terms + 1): read every term, write the sum
 # (per side; L1 term histogram {1: 2, 2: 5}, L2 {1: 4, 2: 20, 4: 25})
-SUM_PASSES = {1: 5 * 3, 2: 20 * 3 + 25 * 5}
+# multi-term operand sums per side (= materialised outputs of one sum pass)
+MULTI_TERM_SUMS = {1: 5, 2: 45}
 
 
 def hbm_bytes(kernel, m, n, k, level, ordinal=0):
-    """Algorithmic HBM bytes of the auxiliary launches."""
+    """Algorithmic HBM bytes of the auxiliary launches.
+
+    sum pass (gather form): every source quadrant read once + every sum written once;
+    stream pass: every M_p read once + each C element read and written once.
+    """
     s = 1 << level
     qm, qn, qk = -(-m // s), -(-n // s), -(-k // s)
     mul, aa, ba, cu = table_counts(level)
     if kernel == "sum_batch_kernel" and level > 0:  # ordinal 0: A side, 1: B side
-        return 8.0 * SUM_PASSES[level] * (qm * qk if ordinal == 0 else qk * qn)
-    if kernel == "stream_update_kernel":  # read M_p per update, RMW each C element once
-        return 8.0 * (cu * qm * qn + 2 * m * n)
+        quads = s * s + MULTI_TERM_SUMS[level]
+        return 8.0 * quads * (qm * qk if ordinal == 0 else qk * qn)
+    if kernel == "stream_update_kernel":
+        return 8.0 * (mul * qm * qn + 2 * m * n)
     return None
 
 

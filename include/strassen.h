@@ -192,6 +192,13 @@ strassen_status strassen_ctx_last_launches(const strassen_ctx* ctx, long* out);
  * 0 = the reference's zero padding of clipped quadrants (matrix.cpp:14-22). */
 strassen_status strassen_ctx_set_peeling(strassen_ctx* ctx, int enabled);
 
+/* Host-pointer calls (strassen_gemm / strassen_dgemm with beta == 1) with
+ * column-major B and C: 1 (default) = pipeline the call in column windows of
+ * the quadrant partition, so B's and C's transfers and C's copy-back overlap
+ * the kernels of other windows; 0 = copy everything in, compute, copy out.
+ * Results are bitwise identical either way. */
+strassen_status strassen_ctx_set_pipelining(strassen_ctx* ctx, int enabled);
+
 /* Per-launch CUDA-event timing of the calls on this ctx (off by default).
  * strassen_ctx_last_profile writes a JSON list [{"kernel": name, "ms": t}, ...]
  * for the last compute call into buf (NUL-terminated; STRASSEN_ERR_ALLOC if

@@ -120,6 +120,7 @@ def _declare(lib):
                                       C.POINTER(Counters)]),
         "strassen_ctx_enable_profiling": (_ST, [vp, C.c_int]),
         "strassen_ctx_set_peeling": (_ST, [vp, C.c_int]),
+        "strassen_ctx_set_pipelining": (_ST, [vp, C.c_int]),
         "strassen_ctx_last_profile": (_ST, [vp, C.c_char_p, _L]),
         "strassen_select": (_ST, [_L, _L, _L, C.POINTER(C.c_int), C.POINTER(C.c_int), _dp]),
         "strassen_build_info": (C.c_char_p, []),
@@ -237,6 +238,10 @@ class Ctx:
     def set_peeling(self, on=True):
         """Odd fringes: dynamic peeling (default) or the reference's zero padding."""
         _check(self._l.strassen_ctx_set_peeling(self.ptr, int(bool(on))), "set_peeling")
+
+    def set_pipelining(self, on=True):
+        """Host calls: column-window pipelining of transfers and kernels (default on)."""
+        _check(self._l.strassen_ctx_set_pipelining(self.ptr, int(bool(on))), "set_pipelining")
 
     def enable_profiling(self, on=True):
         _check(self._l.strassen_ctx_enable_profiling(self.ptr, int(bool(on))), "enable_profiling")

@@ -134,9 +134,18 @@ strassen_status gemm_impl(strassen_ctx* ctx, bool explicit_stream, cudaStream_t 
         // the copy stream may only overwrite staging buffers once earlier work on s is done
         cuda_ck(cudaEventRecord(e.ev_call, s), "call event");
         cuda_ck(cudaStreamWaitEvent(e.copy_stream, e.ev_call, 0), "copy stream order");
+        // Host B and C in column-major layouts: pipeline the call in column
+        // windows (engine.hpp ColumnWindows) when the problem is large enough.
+        long qcols = 0;
+        const int nwin =
+            (!device_only && e.pipelining && !(has_beta && beta != 1.0) && rs_b == 1 &&
+             rs_c == 1 && cs_b >= k && cs_c >= m && !sb200::is_device_pointer(b) &&
+             !sb200::is_device_pointer(c))
+                ? sb200::plan_windows(e, variant, level, m, n, k, qcols)
+                : 0;
         const sb200::DView A = stage_in(e, s, a, m, k, rs_a, cs_a, e.stage_a, true, sa, e.ev_ready[0]);
-        const sb200::DView B = stage_in(e, s, b, k, n, rs_b, cs_b, e.stage_b, true, sb, e.ev_ready[1]);
-        const sb200::DView C = stage_in(e, s, c, m, n, rs_c, cs_c, e.stage_c, true, sc, e.ev_ready[2]);
+        const sb200::DView B = stage_in(e, s, b, k, n, rs_b, cs_b, e.stage_b, nwin == 0, sb, e.ev_ready[1]);
+        const sb200::DView C = stage_in(e, s, c, m, n, rs_c, cs_c, e.stage_c, nwin == 0, sc, e.ev_ready[2]);
         if (device_only && (sa || sb || sc))
             throw std::invalid_argument("strassen_gemm_device: operands must be device memory");
         for (auto& t : e.timed) {
@@ -144,15 +153,63 @@ strassen_status gemm_impl(strassen_ctx* ctx, bool explicit_stream, cudaStream_t 
             cudaEventDestroy(t.stop);
         }
         e.timed.clear();
-        if (has_beta && beta != 1.0) launches += sb200::scale_device(e, s, C, beta);
-        launches += sb200::run_device(e, s, variant, level, alpha, A, B, C);
-        if (sc) {
-            long lo, hi;
-            span_of(m, n, rs_c, cs_c, lo, hi);
-            sb200::wait_ready(s, C);  // even if no kernel touched C
-            cuda_ck(cudaMemcpyAsync(c + lo, C.p + lo, static_cast<size_t>(hi - lo + 1) * 8,
-                                    cudaMemcpyDeviceToHost, s),
-                    "D2H result");
+        if (nwin > 0) {
+            const int L = (variant == STRASSEN_DGEMM) ? 0 : level;
+            const long side = 1L << L, qn = (n + side - 1) / side;
+            // global column range of window w inside quadrant column block J
+            auto cols_of = [&](int w, long J, long& j0, long& j1) {
+                j0 = std::min(n, J * qn + w * qcols);
+                j1 = std::min(n, J * qn + std::min(qn, (w + 1) * qcols));
+            };
+            // column-major spans: columns [j0, j1) of a rows x n view with ld cs
+            auto copy_cols = [&](double* dst, const double* src, long j0, long j1, long rows,
+                                 long cs, cudaMemcpyKind kind, cudaStream_t st) {
+                if (j0 >= j1) return;
+                const size_t count = static_cast<size_t>((j1 - 1 - j0) * cs + rows);
+                cuda_ck(cudaMemcpyAsync(dst + j0 * cs, src + j0 * cs, count * 8, kind, st),
+                        kind == cudaMemcpyHostToDevice ? "H2D window" : "D2H window");
+            };
+            sb200::ColumnWindows W;
+            W.count = nwin;
+            W.qcols = qcols;
+            W.b_ready = e.ev_win_b;
+            W.c_ready = e.ev_win_c;
+            W.done = e.ev_win_done;
+            W.issue_in = [&](int w) {
+                long j0, j1;
+                for (long J = 0; J < side; ++J) {
+                    cols_of(w, J, j0, j1);
+                    copy_cols(B.p, b, j0, j1, k, cs_b, cudaMemcpyHostToDevice, e.copy_stream);
+                }
+                cuda_ck(cudaEventRecord(e.ev_win_b[w], e.copy_stream), "window event");
+                for (long J = 0; J < side; ++J) {
+                    cols_of(w, J, j0, j1);
+                    copy_cols(C.p, c, j0, j1, m, cs_c, cudaMemcpyHostToDevice, e.copy_stream);
+                }
+                cuda_ck(cudaEventRecord(e.ev_win_c[w], e.copy_stream), "window event");
+            };
+            W.issue_out = [&](int w) {
+                cuda_ck(cudaStreamWaitEvent(e.d2h_stream, e.ev_win_done[w], 0), "window wait");
+                long j0, j1;
+                for (long J = 0; J < side; ++J) {
+                    cols_of(w, J, j0, j1);
+                    copy_cols(c, C.p, j0, j1, m, cs_c, cudaMemcpyDeviceToHost, e.d2h_stream);
+                }
+            };
+            launches += sb200::run_device(e, s, variant, level, alpha, A, B, C, &W);
+            cuda_ck(cudaEventRecord(e.ev_d2h, e.d2h_stream), "d2h event");
+            cuda_ck(cudaStreamWaitEvent(s, e.ev_d2h, 0), "d2h wait");
+        } else {
+            if (has_beta && beta != 1.0) launches += sb200::scale_device(e, s, C, beta);
+            launches += sb200::run_device(e, s, variant, level, alpha, A, B, C);
+            if (sc) {
+                long lo, hi;
+                span_of(m, n, rs_c, cs_c, lo, hi);
+                sb200::wait_ready(s, C);  // even if no kernel touched C
+                cuda_ck(cudaMemcpyAsync(c + lo, C.p + lo, static_cast<size_t>(hi - lo + 1) * 8,
+                                        cudaMemcpyDeviceToHost, s),
+                        "D2H result");
+            }
         }
         if (!device_only) cuda_ck(cudaStreamSynchronize(s), "kernel execution");
         else cuda_ck(cudaGetLastError(), "kernel launch");
@@ -271,6 +328,12 @@ strassen_status strassen_ctx_last_launches(const strassen_ctx* ctx, long* out) {
 strassen_status strassen_ctx_set_peeling(strassen_ctx* ctx, int enabled) {
     if (!ctx) return STRASSEN_ERR_NULL;
     ctx->engine.peeling = enabled != 0;
+    return STRASSEN_OK;
+}
+
+strassen_status strassen_ctx_set_pipelining(strassen_ctx* ctx, int enabled) {
+    if (!ctx) return STRASSEN_ERR_NULL;
+    ctx->engine.pipelining = enabled != 0;
     return STRASSEN_OK;
 }
 

@@ -134,8 +134,6 @@ QuadView c_quad(const DView& C, long qm, long qn, long I, long J) {
     return q;
 }
 
-int side_of(int level) { return 1 << level; }
-
 const Program& program(int level) {
     static const Program p0 = identity_program();
     return level == 0 ? p0 : program_for_level(level);
@@ -177,8 +175,13 @@ Engine::~Engine() {
     if (!initialised) return;
     if (copy_stream) cudaStreamDestroy(copy_stream);
     if (ev_call) cudaEventDestroy(ev_call);
+    if (d2h_stream) cudaStreamDestroy(d2h_stream);
     for (auto ev : ev_ready)
         if (ev) cudaEventDestroy(ev);
+    for (cudaEvent_t* arr : {ev_win_b, ev_win_c, ev_win_done})
+        for (int w = 0; w < kMaxWindows; ++w)
+            if (arr[w]) cudaEventDestroy(arr[w]);
+    if (ev_d2h) cudaEventDestroy(ev_d2h);
     for (DeviceBuffer* b : {&stage_a, &stage_b, &stage_c, &pack_a, &pack_b, &mbuf, &tabuf, &tbbuf})
         if (b->ptr) cudaFree(b->ptr);
 }
@@ -193,6 +196,11 @@ void Engine::init() {
     ck(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking), "copy stream");
     ck(cudaEventCreateWithFlags(&ev_call, cudaEventDisableTiming), "event");
     for (auto& ev : ev_ready) ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
+    ck(cudaStreamCreateWithFlags(&d2h_stream, cudaStreamNonBlocking), "d2h stream");
+    ck(cudaEventCreateWithFlags(&ev_d2h, cudaEventDisableTiming), "event");
+    for (cudaEvent_t* arr : {ev_win_b, ev_win_c, ev_win_done})
+        for (int w = 0; w < kMaxWindows; ++w)
+            ck(cudaEventCreateWithFlags(&arr[w], cudaEventDisableTiming), "event");
     initialised = true;
 }
 
@@ -259,18 +267,48 @@ bool is_device_pointer(const void* p) {
     return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
 }
 
-// Fused launch of P (ABC / DGEMM / C): tile ownership with the multi-destination
-// epilogue, or -- when the output has fewer than two waves of tiles -- split
-// mode: one CTA per (tile, product, k-chunk) into L2-resident partials M_{p,s},
-// then one deterministic stream pass (partials summed in s order, destinations
+// Launch plan of P (ABC / DGEMM / C / AB / Naive), decided on the WHOLE problem
+// so that a column window computes exactly what the unwindowed call does:
+// tile ownership with the multi-destination epilogue, or -- when the output has
+// fewer than two waves of tiles, or the variant stores products (AB, Naive) --
+// split mode: one CTA per (tile, product, k-chunk) into partials M_{p,s}, then
+// one deterministic stream pass (partials summed in s order, destinations
 // applied in table order).
-long launch_fused(Engine& e, cudaStream_t s, MMParams& P, const std::vector<Terms>& dests,
-                  const std::vector<QuadView>& cq, const DView& C, double alpha,
-                  bool force_split = false) {
+struct FusedPlan {
+    bool split = false;
+    int ksplit = 1, per = 0;
+    long long ldm = 0, mstride = 0;
+    double* M = nullptr;
+};
+
+FusedPlan plan_fused(Engine& e, const MMParams& P, bool force_split) {
+    FusedPlan F;
     const int ntiles = P.tiles_m * P.tiles_n;
     const int sms = e.num_sms > 0 ? e.num_sms : 148;
-    if (ntiles >= 2 * sms && !force_split) {
-        wait_ready(s, C);  // fused epilogue reads C
+    if (ntiles >= 2 * sms && !force_split) return F;
+    int ksplit = 1;
+    const long base = static_cast<long>(ntiles) * P.nprod;
+    while (base * ksplit < 4L * sms && P.ktiles / (ksplit + 1) >= 4) ++ksplit;
+    F.per = (P.ktiles + ksplit - 1) / ksplit;
+    F.ksplit = (P.ktiles + F.per - 1) / F.per;
+    F.split = true;
+    F.ldm = (P.qm + 1) / 2 * 2;  // even: 16-B stores
+    F.mstride = F.ldm * P.qn;
+    F.M = e.ensure(e.mbuf, static_cast<size_t>(F.mstride) * P.nprod * F.ksplit * 8);
+    return F;
+}
+
+// Quadrant columns [c0, c1) of the plan: the mm launch over those tile columns
+// (c0 a multiple of kBN) and, in split mode, the stream pass over them.
+// wait_c() is called right before the first launch that touches C.
+long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
+                      const std::vector<Terms>& dests, const std::vector<QuadView>& cq,
+                      const DView& C, double alpha, long c0, long c1,
+                      const std::function<void()>& wait_c) {
+    P.tn0 = static_cast<int>(c0 / kBN);
+    P.tiles_n = static_cast<int>(ceil_div(c1 - c0, kBN));
+    if (!F.split) {
+        wait_c();  // fused epilogue reads C
         P.mode = kEpiRMW;
         P.split = 0;
         e.prof_begin("mm_kernel", s);
@@ -278,20 +316,13 @@ long launch_fused(Engine& e, cudaStream_t s, MMParams& P, const std::vector<Term
         e.prof_end(s);
         return 1;
     }
-    int ksplit = 1;
-    const long base = static_cast<long>(ntiles) * P.nprod;
-    while (base * ksplit < 4L * sms && P.ktiles / (ksplit + 1) >= 4) ++ksplit;
-    const int per = (P.ktiles + ksplit - 1) / ksplit;
-    ksplit = (P.ktiles + per - 1) / per;
-    const long long ldm = (P.qm + 1) / 2 * 2, mstride = ldm * P.qn;  // even: 16-B stores
-    double* M = e.ensure(e.mbuf, static_cast<size_t>(mstride) * P.nprod * ksplit * 8);
     P.mode = kEpiStore;
     P.split = 1;
-    P.ksplit = ksplit;
-    P.kt_per_split = per;
-    P.mbase = M;
-    P.ldm = ldm;
-    P.mstride = mstride;
+    P.ksplit = F.ksplit;
+    P.kt_per_split = F.per;
+    P.mbase = F.M;
+    P.ldm = F.ldm;
+    P.mstride = F.mstride;
     e.prof_begin("mm_kernel", s);
     ck(launch_mm(P, s), "mm_kernel (split)");
     e.prof_end(s);
@@ -300,13 +331,15 @@ long launch_fused(Engine& e, cudaStream_t s, MMParams& P, const std::vector<Term
     S.rs_c = C.rs;
     S.cs_c = C.cs;
     S.alpha = alpha;
-    S.ldm = ldm;
-    S.mstride = mstride;
-    S.ksplit = ksplit;
+    S.ldm = F.ldm;
+    S.mstride = F.mstride;
+    S.ksplit = F.ksplit;
     S.nquad = static_cast<int>(cq.size());
     S.qm = P.qm;
     S.qn = P.qn;
-    S.mbase = M;
+    S.c0 = static_cast<int>(c0);
+    S.c1 = static_cast<int>(c1);
+    S.mbase = F.M;
     for (size_t qi = 0; qi < cq.size(); ++qi) {
         S.cptr[qi] = cq[qi].p;
         S.crows[qi] = static_cast<int>(cq[qi].rows);
@@ -318,9 +351,9 @@ long launch_fused(Engine& e, cudaStream_t s, MMParams& P, const std::vector<Term
             S.src_coeff[q][S.nsrc[q]] = static_cast<int8_t>(g);
             ++S.nsrc[q];
         }
-    wait_ready(s, C);  // first reader of C: its copy-in overlapped the products
+    wait_c();  // first reader of C: its copy-in overlapped the products
     e.prof_begin("stream_update_kernel", s);
-    ck(launch_stream_update(S, s), "stream_update (split)");
+    ck(launch_stream_update(S, s), "stream_update");
     e.prof_end(s);
     return 2;
 }
@@ -328,7 +361,7 @@ long launch_fused(Engine& e, cudaStream_t s, MMParams& P, const std::vector<Term
 // ------------------------------------------------------------- run_device --
 namespace {
 long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level, double alpha,
-                  const DView& A, const DView& B, const DView& C);
+                  const DView& A, const DView& B, const DView& C, const ColumnWindows* win);
 
 DView sub(const DView& v, long r0, long c0, long rows, long cols) {
     DView o = v;
@@ -339,6 +372,28 @@ DView sub(const DView& v, long r0, long c0, long rows, long cols) {
 }
 }  // namespace
 
+int plan_windows(const Engine& e, strassen_variant variant, int level, long m, long n, long k,
+                 long& qcols) {
+    (void)k;
+    const int L = (variant == STRASSEN_DGEMM) ? 0 : level;
+    const long side = 1L << L;
+    const long qm = ceil_div(m, side), qn = ceil_div(n, side);
+    const long tiles_m = ceil_div(qm, kBM), tiles_n = ceil_div(qn, kBN);
+    const long sms = e.num_sms > 0 ? e.num_sms : 148;
+    long per_col = tiles_m;  // CTAs per tile column
+    if (variant == STRASSEN_NAIVE || variant == STRASSEN_AB) {
+        for (int l = 0; l < L; ++l) per_col *= 7;
+    } else if (tiles_m * tiles_n < 2 * sms) {
+        return 0;  // split-mode sizes: a few milliseconds, nothing to overlap
+    }
+    // at least 4 waves of CTAs per window keeps the per-window tail small
+    long count = std::min<long>(Engine::kMaxWindows / 2, tiles_n * per_col / (4 * sms));
+    count = std::min(count, tiles_n);
+    if (count < 2) return 0;
+    qcols = ceil_div(tiles_n, count) * kBN;
+    return static_cast<int>(ceil_div(qn, qcols));
+}
+
 // Dynamic peeling (north star; the reference pads instead, matrix.cpp:14-22):
 // when m, n or k is not a multiple of 2^L, Strassen runs on the even core
 // m_e x n_e x k_e (every quadrant full, no padded tiles) and three classical
@@ -348,7 +403,7 @@ DView sub(const DView& v, long r0, long c0, long rows, long cols) {
 //   C[0:m_e, n_e:n] += alpha A[0:m_e, 0:k]   B[0:k, n_e:n]      (right columns)
 // Tiny problems (core below one 128-tile per quadrant) keep the padded path.
 long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, double alpha,
-                const DView& A, const DView& B, const DView& C) {
+                const DView& A, const DView& B, const DView& C, const ColumnWindows* win) {
     const int L = (variant == STRASSEN_DGEMM) ? 0 : level;
     const long S = 1L << L;
     const long m = A.rows, k = A.cols, n = B.cols;
@@ -359,35 +414,59 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
         return ceil_div(ceil_div(mm, S), kBM) * ceil_div(ceil_div(nn, S), kBN) *
                ceil_div(ceil_div(kk, S), kBK);
     };
-    if (!(L > 0 && ragged && e.peeling && me >= S * kBM && ne >= S * kBN && ke >= S * kBK &&
-          work(me, ne, ke) < work(m, n, k)))
-        return run_strassen(e, s, variant, level, alpha, A, B, C);
+    const bool peel = L > 0 && ragged && e.peeling && me >= S * kBM && ne >= S * kBN &&
+                      ke >= S * kBK && work(me, ne, ke) < work(m, n, k);
+    if (win && win->count > 0 && (peel || !tma_ready(B, ceil_div(k, S), static_cast<int>(S)))) {
+        // not windowable: everything in first, everything out last
+        for (int w = 0; w < win->count; ++w) {
+            win->issue_in(w);
+            ck(cudaStreamWaitEvent(s, win->b_ready[w], 0), "window wait");
+            ck(cudaStreamWaitEvent(s, win->c_ready[w], 0), "window wait");
+        }
+        const long launches = run_device(e, s, variant, level, alpha, A, B, C, nullptr);
+        for (int w = 0; w < win->count; ++w) {
+            ck(cudaEventRecord(win->done[w], s), "window done");
+            win->issue_out(w);
+        }
+        return launches;
+    }
+    if (!peel) return run_strassen(e, s, variant, level, alpha, A, B, C, win);
     long launches = run_strassen(e, s, variant, level, alpha, sub(A, 0, 0, me, ke),
-                                 sub(B, 0, 0, ke, ne), sub(C, 0, 0, me, ne));
+                                 sub(B, 0, 0, ke, ne), sub(C, 0, 0, me, ne), nullptr);
     if (ke < k)
         launches += run_strassen(e, s, STRASSEN_DGEMM, 0, alpha, sub(A, 0, ke, me, k - ke),
-                                 sub(B, ke, 0, k - ke, ne), sub(C, 0, 0, me, ne));
+                                 sub(B, ke, 0, k - ke, ne), sub(C, 0, 0, me, ne), nullptr);
     if (me < m)
         launches += run_strassen(e, s, STRASSEN_DGEMM, 0, alpha, sub(A, me, 0, m - me, k), B,
-                                 sub(C, me, 0, m - me, n));
+                                 sub(C, me, 0, m - me, n), nullptr);
     if (ne < n)
         launches += run_strassen(e, s, STRASSEN_DGEMM, 0, alpha, sub(A, 0, 0, me, k),
-                                 sub(B, 0, ne, k, n - ne), sub(C, 0, ne, me, n - ne));
+                                 sub(B, 0, ne, k, n - ne), sub(C, 0, ne, me, n - ne), nullptr);
     return launches;
 }
 
 namespace {
 long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level, double alpha,
-                  const DView& A, const DView& B, const DView& C) {
+                  const DView& A, const DView& B, const DView& C, const ColumnWindows* win) {
     const int L = (variant == STRASSEN_DGEMM) ? 0 : level;
     const int side = 1 << L;
     const long m = A.rows, k = A.cols, n = B.cols;
     const long qm = ceil_div(m, side), qk = ceil_div(k, side), qn = ceil_div(n, side);
     long launches = 0;
+    const int nwin = win ? win->count : 1;
+    const long wcols = win ? win->qcols : qn;
+    if (win) win->issue_in(0);
+    // window w's B columns / C columns have landed (whole operands without windows)
+    auto wait_b = [&](int w) {
+        if (win) ck(cudaStreamWaitEvent(s, win->b_ready[w], 0), "window wait");
+    };
+    auto wait_c = [&](int w) {
+        if (win) ck(cudaStreamWaitEvent(s, win->c_ready[w], 0), "window wait");
+        else wait_ready(s, C);
+    };
 
     const TmaOperand ta = prepare(e, s, A, qm, qk, side, e.pack_a, launches);
     const TmaOperand tb = prepare(e, s, B, qk, qn, side, e.pack_b, launches);
-
     const int nq = side * side;
     std::vector<bool> a_live(nq), b_live(nq), c_live(nq);
     std::vector<QuadView> cq(nq);
@@ -441,16 +520,25 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
         if (l.a.empty() || l.b.empty() || l.c.empty()) continue;
         live.push_back(std::move(l));
     }
-    if (live.empty()) return launches;
-    if (variant != STRASSEN_C && variant != STRASSEN_NAIVE) {  // mm_kernel reads A and B
-        if (ta.ready) cudaStreamWaitEvent(s, ta.ready, 0);
-        if (tb.ready) cudaStreamWaitEvent(s, tb.ready, 0);
+    if (live.empty()) {
+        if (win)
+            for (int w = 0; w < nwin; ++w) {
+                if (w + 1 < nwin) win->issue_in(w + 1);
+                wait_b(w);
+                wait_c(w);
+                ck(cudaEventRecord(win->done[w], s), "window done");
+                win->issue_out(w);
+            }
+        return launches;
     }
+    if (ta.ready) cudaStreamWaitEvent(s, ta.ready, 0);  // every path reads A first
 
-    if (variant == STRASSEN_C || variant == STRASSEN_NAIVE) {
-        // Every multi-term operand sum materialised by one batched HBM pass
-        // (materialize_sum, variants.cpp:53-96, for all entries at once), then
-        // one mm_kernel over all 7^L products with single-term operands.
+    const bool sums = variant == STRASSEN_C || variant == STRASSEN_NAIVE;
+    std::vector<SumBatchParams*> side_sums(2, nullptr);
+    if (sums) {
+        // Every multi-term operand sum materialised by one HBM pass per side
+        // (materialize_sum, variants.cpp:53-96, for all entries at once); the
+        // mm launch then runs all 7^L products with single-term operands.
         //   C variant (B200 addition): fused multi-destination epilogue.
         //   Naive: products to temporaries M_p, then one stream pass applying
         //          C_r += alpha*gamma*M_p in table order (variants.cpp:99-109).
@@ -462,122 +550,93 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
         }
         double* TA = e.ensure(e.tabuf, static_cast<size_t>(std::max(na_sums, 1)) * lda_t * qk * 8);
         double* TB = e.ensure(e.tbbuf, static_cast<size_t>(std::max(nb_sums, 1)) * ldb_t * qn * 8);
-        for (int side = 0; side < 2; ++side) {
+        for (int sd = 0; sd < 2; ++sd) {
+            int next_map = kMaxQuad;  // tmA / tmB: 16 quadrant maps, then the sums
             SumBatchParams* SB = new SumBatchParams;  // ~10 KB: keep off the stack
             std::memset(SB, 0, sizeof(*SB));
-            const TmaOperand& t = side == 0 ? ta : tb;
-            SB->rows = side == 0 ? qm : qk;
-            SB->cols = side == 0 ? qk : qn;
-            SB->ld = side == 0 ? lda_t : ldb_t;
-            int next_map = kMaxQuad;
+            side_sums[sd] = SB;
+            const TmaOperand& t = sd == 0 ? ta : tb;
+            SB->rows = sd == 0 ? qm : qk;
+            SB->cols = sd == 0 ? qk : qn;
+            SB->ld = sd == 0 ? lda_t : ldb_t;
             for (size_t p = 0; p < live.size(); ++p) {
-                Terms& terms = side == 0 ? live[p].a : live[p].b;
+                Terms& terms = sd == 0 ? live[p].a : live[p].b;
                 if (terms.size() <= 1) continue;  // single term: the quadrant map, sign in-kernel
                 const int z = SB->njobs++;
-                double* dst = (side == 0 ? TA : TB) + static_cast<size_t>(z) * SB->ld * SB->cols;
+                double* dst = (sd == 0 ? TA : TB) + static_cast<size_t>(z) * SB->ld * SB->cols;
                 SB->dst[z] = dst;
                 SB->nterms[z] = static_cast<int>(terms.size());
                 for (size_t u = 0; u < terms.size(); ++u) {
                     const int qi = terms[u].first;
                     SumTerm& st = SB->t[z][u];
-                    st.x = quad_origin(t, qi / side_of(L), qi % side_of(L));
-                    st.rows = static_cast<int>(quad_rows(t, qi / side_of(L)));
-                    st.cols = static_cast<int>(quad_cols(t, qi % side_of(L)));
+                    st.x = quad_origin(t, qi / side, qi % side);
+                    st.rows = static_cast<int>(quad_rows(t, qi / side));
+                    st.cols = static_cast<int>(quad_cols(t, qi % side));
                     st.ld = t.ld;
                     st.coeff = terms[u].second;
                 }
                 const int mi = next_map++;
-                if (side == 0)
+                if (mi >= kMaxMaps) throw Error(STRASSEN_ERR_PARAM, "too many operand maps");
+                if (sd == 0)
                     encode_map(&P.tmA[mi], dst, qm, qk, lda_t, 16, kBK, true);
                 else
                     encode_map(&P.tmB[mi], dst, qk, qn, ldb_t, kBK, kBN, true);
                 terms = {{mi, 1}};
             }
-            if (side == 0) {
-                if (ta.ready) cudaStreamWaitEvent(s, ta.ready, 0);
-            } else if (tb.ready) {
-                cudaStreamWaitEvent(s, tb.ready, 0);
-            }
-            e.prof_begin("sum_batch_kernel", s);
-            cudaError_t err = launch_sum_batch(*SB, s);
-            e.prof_end(s);
-            const int njobs = SB->njobs;
-            delete SB;
-            ck(err, "sum_batch");
-            if (njobs) ++launches;
         }
-        P.nprod = static_cast<int>(live.size());
-        std::vector<Terms> dests;
-        for (size_t p = 0; p < live.size(); ++p) {
-            fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);
-            dests.push_back(live[p].c);
-        }
-        // C: fused epilogue (split only when few tiles).  Naive: products to
-        // temporaries on a product-parallel grid (one CTA per tile x product:
-        // balanced waves at every size), then one stream pass.
-        return launches + launch_fused(e, s, P, dests, cq, C, alpha, variant == STRASSEN_NAIVE);
-        // Naive, batched: M_p for every product in one launch, one stream pass
-        const long long ldm = qm, mstride = ldm * qn;
-        double* M = e.ensure(e.mbuf, static_cast<size_t>(mstride) * live.size() * 8);
-        P.mode = kEpiStore;
-        P.mbase = M;
-        P.ldm = ldm;
-        P.mstride = mstride;
-        e.prof_begin("mm_kernel", s);
-        ck(launch_mm(P, s), "mm_kernel (Naive)");
+        e.prof_begin("sum_batch_kernel", s);
+        cudaError_t err = launch_sum_batch(*side_sums[0], s);
         e.prof_end(s);
-        StreamParams S;
-        std::memset(&S, 0, sizeof(S));
-        S.rs_c = C.rs;
-        S.cs_c = C.cs;
-        S.alpha = alpha;
-        S.ldm = ldm;
-        S.mstride = mstride;
-        S.ksplit = 1;
-        S.nquad = nq;
-        S.qm = static_cast<int>(qm);
-        S.qn = static_cast<int>(qn);
-        S.mbase = M;
-        for (int qi = 0; qi < nq; ++qi) {
-            S.cptr[qi] = cq[qi].p;
-            S.crows[qi] = static_cast<int>(cq[qi].rows);
-            S.ccols[qi] = static_cast<int>(cq[qi].cols);
+        if (side_sums[0]->njobs) ++launches;
+        if (err != cudaSuccess) {
+            delete side_sums[0];
+            delete side_sums[1];
+            ck(err, "sum_batch (A)");
         }
-        for (size_t p = 0; p < dests.size(); ++p)
-            for (const auto& [q, g] : dests[p]) {
-                S.src_prod[q][S.nsrc[q]] = static_cast<int8_t>(p);
-                S.src_coeff[q][S.nsrc[q]] = static_cast<int8_t>(g);
-                ++S.nsrc[q];
-            }
-        e.prof_begin("stream_update_kernel", s);
-        ck(launch_stream_update(S, s), "stream_update (Naive)");
-        e.prof_end(s);
-        return launches + 2;
     }
 
-    if (variant == STRASSEN_DGEMM || variant == STRASSEN_ABC) {
-        P.nprod = static_cast<int>(live.size());
-        std::vector<Terms> dests;
-        for (size_t p = 0; p < live.size(); ++p) {
-            fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);
-            dests.push_back(live[p].c);
-        }
-        return launches + launch_fused(e, s, P, dests, cq, C, alpha);
+    P.nprod = static_cast<int>(live.size());
+    std::vector<Terms> dests;
+    for (size_t p = 0; p < live.size(); ++p) {
+        fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);
+        dests.push_back(live[p].c);
     }
+    // C / ABC / DGEMM: fused epilogue (split only when few tiles).  AB, Naive:
+    // products to temporaries on a product-parallel grid (one CTA per tile x
+    // product: balanced waves at every size), then one stream pass
+    // (AB: variants.cpp:142-168).
+    const bool store_products = variant == STRASSEN_NAIVE || variant == STRASSEN_AB;
+    const FusedPlan F = plan_fused(e, P, store_products);
 
-    if (variant == STRASSEN_AB) {
-        // AB (variants.cpp:142-168): fused operand sums, products to
-        // temporaries on a product-parallel grid (k-split too when few tiles),
-        // streamed into C in table order.
-        P.nprod = static_cast<int>(live.size());
-        std::vector<Terms> dests;
-        for (size_t p = 0; p < live.size(); ++p) {
-            fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);
-            dests.push_back(live[p].c);
+    try {
+        for (int w = 0; w < nwin; ++w) {
+            if (win && w + 1 < nwin) win->issue_in(w + 1);  // prefetch the next window
+            const long c0 = w * wcols, c1 = std::min(qn, c0 + wcols);
+            wait_b(w);
+            if (!win && tb.ready) cudaStreamWaitEvent(s, tb.ready, 0);
+            if (sums && side_sums[1]->njobs) {
+                side_sums[1]->c0 = c0;
+                side_sums[1]->cols = c1;
+                e.prof_begin("sum_batch_kernel", s);
+                ck(launch_sum_batch(*side_sums[1], s), "sum_batch (B)");
+                e.prof_end(s);
+                ++launches;
+            }
+            launches += run_fused_window(e, s, P, F, dests, cq, C, alpha, c0, c1,
+                                         [&] { wait_c(w); });
+            if (win) {
+                ck(cudaEventRecord(win->done[w], s), "window done");
+                win->issue_out(w);
+            }
         }
-        return launches + launch_fused(e, s, P, dests, cq, C, alpha, true);
+    } catch (...) {
+        delete side_sums[0];
+        delete side_sums[1];
+        throw;
     }
-    throw Error(STRASSEN_ERR_PARAM, "unhandled variant");
+    delete side_sums[0];
+    delete side_sums[1];
+    return launches;
 }
 }  // namespace
 

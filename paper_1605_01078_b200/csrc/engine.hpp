@@ -7,6 +7,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -58,6 +59,13 @@ struct Engine {
     // host-operand staging: copies run on their own stream, one event each
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_call = nullptr, ev_ready[3] = {nullptr, nullptr, nullptr};
+    // column-window pipeline of host calls (ColumnWindows): results leave on
+    // their own stream so they overlap the next window's transfers and kernels
+    bool pipelining = true;  // strassen_ctx_set_pipelining
+    cudaStream_t d2h_stream = nullptr;
+    cudaEvent_t ev_d2h = nullptr;
+    static constexpr int kMaxWindows = 8;
+    cudaEvent_t ev_win_b[kMaxWindows] = {}, ev_win_c[kMaxWindows] = {}, ev_win_done[kMaxWindows] = {};
     double* ensure(DeviceBuffer& b, size_t bytes);
     size_t workspace_bytes() const;
 };
@@ -76,10 +84,33 @@ inline void wait_ready(cudaStream_t s, const DView& v) {
     if (v.ready) cudaStreamWaitEvent(s, v.ready, 0);
 }
 
+// Host-call pipeline: B and C arrive (and C leaves) in column windows of the
+// quadrant partition -- window w is quadrant columns [w*qcols, (w+1)*qcols) of
+// every quadrant column block -- so the transfers of one window overlap the
+// kernels of the others.  Per element the arithmetic is exactly that of the
+// unwindowed call (same partition, same launch modes, same k order).
+struct ColumnWindows {
+    int count = 0;
+    long qcols = 0;                       // multiple of the 128-column tile
+    std::function<void(int)> issue_in;   // enqueue window w's B and C copies, record b/c_ready[w]
+    std::function<void(int)> issue_out;  // enqueue window w's result copy after done[w]
+    cudaEvent_t* b_ready = nullptr;
+    cudaEvent_t* c_ready = nullptr;
+    cudaEvent_t* done = nullptr;         // recorded on s after window w's last kernel
+};
+
+// Number of column windows worth pipelining a host call into (0: none) and
+// their width in quadrant columns.
+int plan_windows(const Engine& e, strassen_variant variant, int level, long m, long n, long k,
+                 long& qcols);
+
 // C := alpha A B + C on device views, enqueued on `s` (no synchronisation).
 // variant/level already validated.  Returns the number of kernel launches.
+// With `win`, B's and C's windows are copied in by win->issue_in (their views
+// carry no ready event) and every window is handed to win->issue_out.
 long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, double alpha,
-                const DView& A, const DView& B, const DView& C);
+                const DView& A, const DView& B, const DView& C,
+                const ColumnWindows* win = nullptr);
 
 // C := beta C on a device view.
 long scale_device(Engine& e, cudaStream_t s, const DView& C, double beta);

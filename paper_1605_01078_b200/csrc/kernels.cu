@@ -18,6 +18,8 @@
 // Why DMMA, and why sums are formed once per CTA: DESIGN.md section 3
 // (profiles/r01_fp64_peak.log: DMMA 37.1 TF/s vs DFMA 34.2; DADD shares the
 // FP64 pipe with DMMA).
+#include <cstring>
+
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -189,7 +191,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     const int gsz = min(P.tiles_m - first_m, P.group_m);
     const int rr = bid - grp * per_group;
     const int tm = first_m + rr % gsz;
-    const int tn = rr / gsz;
+    const int tn = rr / gsz + P.tn0;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kRawSlots; ++s) {
@@ -466,7 +468,7 @@ __global__ void sum_batch_kernel(const __grid_constant__ SumBatchParams P) {
     if (i >= P.rows) return;
     const int n = P.nterms[z];
     double* dst = P.dst[z];
-    for (long long j = 2 * blockIdx.y; j < P.cols; j += 2 * gridDim.y) {
+    for (long long j = P.c0 + 2 * blockIdx.y; j < P.cols; j += 2 * gridDim.y) {
         double2 v[2];
 #pragma unroll
         for (int c = 0; c < 2; ++c) v[c] = make_double2(0.0, 0.0);
@@ -516,7 +518,8 @@ __global__ void stream_update_kernel(const StreamParams P) {
     if (i >= P.crows[quad]) return;
     double* C = P.cptr[quad];
     const int ns = P.nsrc[quad];
-    for (long long j = blockIdx.y; j < P.ccols[quad]; j += gridDim.y) {
+    const long long jend = P.ccols[quad] < P.c1 ? P.ccols[quad] : P.c1;
+    for (long long j = P.c0 + blockIdx.y; j < jend; j += gridDim.y) {
         double* cp = C + i * P.rs_c + j * P.cs_c;
         double c = *cp;
         for (int u = 0; u < ns; ++u) {
@@ -526,6 +529,130 @@ __global__ void stream_update_kernel(const StreamParams P) {
             c = fma(P.alpha * static_cast<double>(P.src_coeff[quad][u]), v, c);
         }
         *cp = c;
+    }
+}
+
+// ------------------------------------------------- gather forms (one pass) ---
+// The batched passes above read each source once per use: a level-2 side has 16
+// quadrants feeding 45 sums through 185 term reads.  The gather forms read every
+// source ONCE per position, keep the values in shared memory (indexable, each
+// thread touches only its own slots, so no barrier), and emit every output:
+// HBM traffic = sources + outputs.  Per element the arithmetic and its order
+// are exactly those of sum_batch_kernel / stream_update_kernel.
+struct SumGatherParams {
+    const double* src[kMaxQuad];
+    int srows[kMaxQuad], scols[kMaxQuad];
+    long long sld[kMaxQuad];
+    int nsrc;
+    double* dst[kMaxSumJobs];
+    int8_t nterms[kMaxSumJobs];
+    int8_t tsrc[kMaxSumJobs][kMaxTerms];
+    int8_t tcoeff[kMaxSumJobs][kMaxTerms];
+    int njobs;
+    long long rows, cols, ld;
+    long long c0;
+};
+constexpr int kGatherThreads = 128;
+
+__global__ void __launch_bounds__(kGatherThreads)
+sum_gather_kernel(const __grid_constant__ SumGatherParams P) {
+    __shared__ double2 xs[kMaxQuad][kGatherThreads];  // 32 KB
+    const int tid = threadIdx.x;
+    const long long i = 2 * (static_cast<long long>(blockIdx.x) * kGatherThreads + tid);
+    if (i >= P.rows) return;
+    const bool pair = i + 1 < P.rows;
+    for (long long j = P.c0 + blockIdx.y; j < P.cols; j += gridDim.y) {
+#pragma unroll
+        for (int q = 0; q < kMaxQuad; ++q) {
+            if (q < P.nsrc) {
+                double2 x = make_double2(0.0, 0.0);
+                if (j < P.scols[q]) {
+                    const double* px = P.src[q] + i + j * P.sld[q];
+                    if (i + 1 < P.srows[q])
+                        x = *reinterpret_cast<const double2*>(px);
+                    else if (i < P.srows[q])
+                        x.x = *px;
+                }
+                xs[q][tid] = x;
+            }
+        }
+        for (int z = 0; z < P.njobs; ++z) {
+            const int n = P.nterms[z];
+            const double c0 = P.tcoeff[z][0];
+            const double2 x0 = xs[P.tsrc[z][0]][tid];
+            double2 v = make_double2(c0 * x0.x, c0 * x0.y);
+            for (int u = 1; u < n; ++u) {
+                const double cu = P.tcoeff[z][u];
+                const double2 x = xs[P.tsrc[z][u]][tid];
+                v.x = fma(cu, x.x, v.x);
+                v.y = fma(cu, x.y, v.y);
+            }
+            double* pd = P.dst[z] + i + j * P.ld;
+            if (pair)
+                *reinterpret_cast<double2*>(pd) = v;
+            else
+                *pd = v.x;
+        }
+    }
+}
+
+struct StreamGatherParams {
+    double* cptr[kMaxQuad];
+    int crows[kMaxQuad], ccols[kMaxQuad];
+    long long rs_c, cs_c;
+    int nquad;
+    const double* mbase;
+    long long mstride, ldm;
+    int ksplit;
+    int nprod;
+    int8_t ndest[kMaxProducts];
+    int8_t dq[kMaxProducts][kMaxQuad];
+    int8_t dcoeff[kMaxProducts][kMaxQuad];
+    double alpha;
+    int qm, qn;
+    int c0, c1;
+};
+constexpr int kStreamThreads = 256;
+constexpr int kStreamBatch = 8;  // M loads in flight per thread
+
+__global__ void __launch_bounds__(kStreamThreads)
+stream_gather_kernel(const __grid_constant__ StreamGatherParams P) {
+    __shared__ double cs[kMaxQuad][kStreamThreads];  // 32 KB
+    const int tid = threadIdx.x;
+    const long long i = static_cast<long long>(blockIdx.x) * kStreamThreads + tid;
+    if (i >= P.qm) return;
+    for (long long j = P.c0 + blockIdx.y; j < P.c1; j += gridDim.y) {
+#pragma unroll
+        for (int q = 0; q < kMaxQuad; ++q)
+            if (q < P.nquad)
+                cs[q][tid] = (i < P.crows[q] && j < P.ccols[q])
+                                 ? P.cptr[q][i * P.rs_c + j * P.cs_c] : 0.0;
+        const double* Mij = P.mbase + i + j * P.ldm;
+        for (int p0 = 0; p0 < P.nprod; p0 += kStreamBatch) {
+            double v[kStreamBatch];
+#pragma unroll
+            for (int t = 0; t < kStreamBatch; ++t) {
+                if (p0 + t < P.nprod) {
+                    const double* M = Mij + static_cast<long long>(p0 + t) * P.ksplit * P.mstride;
+                    v[t] = M[0];
+                    for (int sp = 1; sp < P.ksplit; ++sp) v[t] += M[sp * P.mstride];
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < kStreamBatch; ++t) {
+                if (p0 + t >= P.nprod) break;
+                const int nd = P.ndest[p0 + t];
+                for (int d = 0; d < nd; ++d) {
+                    const int q = P.dq[p0 + t][d];
+                    cs[q][tid] = fma(P.alpha * static_cast<double>(P.dcoeff[p0 + t][d]), v[t],
+                                     cs[q][tid]);
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kMaxQuad; ++q)
+            if (q < P.nquad && i < P.crows[q] && j < P.ccols[q])
+                P.cptr[q][i * P.rs_c + j * P.cs_c] = cs[q][tid];
     }
 }
 
@@ -580,17 +707,102 @@ static unsigned col_grid(long long cols) {
     return static_cast<unsigned>(cols < 16384 ? cols : 16384);
 }
 
+// Gather form when the jobs draw on at most kMaxQuad distinct sources (every
+// level-1/2 side); otherwise the per-job form.
+static bool to_gather(const SumBatchParams& p, SumGatherParams& g) {
+    std::memset(&g, 0, sizeof(g));
+    for (int z = 0; z < p.njobs; ++z) {
+        g.dst[z] = p.dst[z];
+        g.nterms[z] = static_cast<int8_t>(p.nterms[z]);
+        for (int u = 0; u < p.nterms[z]; ++u) {
+            const SumTerm& t = p.t[z][u];
+            int q = 0;
+            while (q < g.nsrc && !(g.src[q] == t.x && g.srows[q] == t.rows &&
+                                   g.scols[q] == t.cols && g.sld[q] == t.ld))
+                ++q;
+            if (q == g.nsrc) {
+                if (g.nsrc == kMaxQuad) return false;
+                g.src[q] = t.x;
+                g.srows[q] = t.rows;
+                g.scols[q] = t.cols;
+                g.sld[q] = t.ld;
+                ++g.nsrc;
+            }
+            g.tsrc[z][u] = static_cast<int8_t>(q);
+            g.tcoeff[z][u] = static_cast<int8_t>(t.coeff);
+        }
+    }
+    g.njobs = p.njobs;
+    g.rows = p.rows;
+    g.cols = p.cols;
+    g.ld = p.ld;
+    g.c0 = p.c0;
+    return true;
+}
+
 cudaError_t launch_sum_batch(const SumBatchParams& p, cudaStream_t s) {
     if (p.njobs == 0) return cudaSuccess;
-    const long long pairs = (p.rows + 1) / 2, cpairs = (p.cols + 1) / 2;
+    static thread_local SumGatherParams g;  // host staging; copied at launch
+    if (to_gather(p, g)) {
+        const long long pairs = (p.rows + 1) / 2;
+        const long long w = p.cols - p.c0;
+        dim3 grid(static_cast<unsigned>((pairs + kGatherThreads - 1) / kGatherThreads),
+                  static_cast<unsigned>(w < 2048 ? w : 2048));
+        sum_gather_kernel<<<grid, kGatherThreads, 0, s>>>(g);
+        return cudaGetLastError();
+    }
+    const long long pairs = (p.rows + 1) / 2, cpairs = (p.cols - p.c0 + 1) / 2;
     dim3 grid(static_cast<unsigned>((pairs + 127) / 128),
               static_cast<unsigned>(cpairs < 1024 ? cpairs : 1024), p.njobs);
     sum_batch_kernel<<<grid, 128, 0, s>>>(p);
     return cudaGetLastError();
 }
 
+// Product-major gather form: valid when every quadrant's sources are in
+// ascending product order (table order), so visiting products in order applies
+// each quadrant's updates in the same order as the per-quadrant form.
+static bool to_gather(const StreamParams& p, StreamGatherParams& g) {
+    std::memset(&g, 0, sizeof(g));
+    for (int q = 0; q < p.nquad; ++q)
+        for (int u = 0; u < p.nsrc[q]; ++u) {
+            const int pr = p.src_prod[q][u];
+            if (pr < 0 || pr >= kMaxProducts) return false;
+            if (u > 0 && pr <= p.src_prod[q][u - 1]) return false;
+            g.nprod = pr + 1 > g.nprod ? pr + 1 : g.nprod;
+            g.dq[pr][g.ndest[pr]] = static_cast<int8_t>(q);
+            g.dcoeff[pr][g.ndest[pr]] = p.src_coeff[q][u];
+            ++g.ndest[pr];
+        }
+    for (int q = 0; q < kMaxQuad; ++q) {
+        g.cptr[q] = p.cptr[q];
+        g.crows[q] = p.crows[q];
+        g.ccols[q] = p.ccols[q];
+    }
+    g.rs_c = p.rs_c;
+    g.cs_c = p.cs_c;
+    g.nquad = p.nquad;
+    g.mbase = p.mbase;
+    g.mstride = p.mstride;
+    g.ldm = p.ldm;
+    g.ksplit = p.ksplit;
+    g.alpha = p.alpha;
+    g.qm = p.qm;
+    g.qn = p.qn;
+    g.c0 = p.c0;
+    g.c1 = p.c1;
+    return true;
+}
+
 cudaError_t launch_stream_update(const StreamParams& p, cudaStream_t s) {
-    dim3 grid(static_cast<unsigned>((p.qm + 255) / 256), col_grid(p.qn), p.nquad);
+    static thread_local StreamGatherParams g;
+    if (to_gather(p, g)) {
+        const int w = p.c1 - p.c0;
+        dim3 grid(static_cast<unsigned>((p.qm + kStreamThreads - 1) / kStreamThreads),
+                  static_cast<unsigned>(w < 4096 ? w : 4096));
+        stream_gather_kernel<<<grid, kStreamThreads, 0, s>>>(g);
+        return cudaGetLastError();
+    }
+    dim3 grid(static_cast<unsigned>((p.qm + 255) / 256), col_grid(p.c1 - p.c0), p.nquad);
     stream_update_kernel<<<grid, 256, 0, s>>>(p);
     return cudaGetLastError();
 }

@@ -224,6 +224,8 @@ def test_b200_ctx_setters_without_device():
     ctx = S.Ctx()
     ctx.set_peeling(False)
     ctx.set_peeling(True)
+    ctx.set_pipelining(False)
+    ctx.set_pipelining(True)
     ctx.enable_profiling(True)
     assert ctx.last_profile() == []
     ctx.set_stream(None)

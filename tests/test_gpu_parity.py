@@ -300,3 +300,39 @@ def test_host_staging_overlap_each_variant_and_operand_kind(ctx):
             ctx.gemm(v, L, 0.5, A, B, C)
             got = C if isinstance(C, np.ndarray) else C.cpu().numpy()
             check(v, L, got, ref, c0, a, b)
+
+
+@pytest.mark.parametrize("v,L,m,n,k", [
+    ("naive", 2, 4096, 4096, 1024),   # 4 windows
+    ("c", 2, 4096, 4000, 768),        # last window partial, clipped quadrant columns
+    ("ab", 2, 4096, 4352, 512),
+    ("naive", 1, 4096, 6144, 640),
+    ("abc", 1, 10240, 10240, 256),    # RMW epilogue per window
+    ("dgemm", 0, 10240, 10240, 256),
+    ("naive", 2, 4097, 4099, 1030),   # ragged: peeled, windows fall back to whole-operand order
+])
+def test_host_pipeline_bitwise_equal_to_unpipelined(v, L, m, n, k):
+    """Host calls in column windows (strassen_ctx_set_pipelining) compute exactly the
+    unwindowed result; ldc > m exercises strided window spans."""
+    import torch
+    g = torch.Generator().manual_seed(m + n + k)
+    a = np.asfortranarray((torch.rand(m, k, dtype=torch.float64, generator=g) * 2 - 1).numpy())
+    b = np.asfortranarray((torch.rand(k, n, dtype=torch.float64, generator=g) * 2 - 1).numpy())
+    cbig = np.asfortranarray((torch.rand(m + 3, n, dtype=torch.float64, generator=g) * 2 - 1).numpy())
+    c0 = cbig[:m, :]  # column-major view with ldc = m + 3
+    assert c0.strides == (8, 8 * (m + 3))
+    outs = []
+    for pipe in (True, False):
+        c = S.Ctx()
+        c.set_pipelining(pipe)
+        buf = np.array(cbig, order="F")
+        view = buf[:m, :]
+        c.gemm(v, L, 1.0, a, b, view)
+        assert np.array_equal(buf[m:, :], cbig[m:, :])  # ld padding untouched
+        outs.append(view.copy())
+        c.close()
+    assert np.array_equal(outs[0], outs[1]), (v, L)
+    C0 = torch.from_numpy(np.array(c0, order="F")).cuda()
+    S.Ctx().gemm(v, L, 1.0, torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), C0)
+    assert np.array_equal(C0.cpu().numpy(), outs[0]), (v, L)
+    assert freivalds(1.0, a, b, c0, outs[0]) < 1e-14
