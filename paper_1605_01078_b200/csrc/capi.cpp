@@ -134,18 +134,20 @@ strassen_status gemm_impl(strassen_ctx* ctx, bool explicit_stream, cudaStream_t 
         // the copy stream may only overwrite staging buffers once earlier work on s is done
         cuda_ck(cudaEventRecord(e.ev_call, s), "call event");
         cuda_ck(cudaStreamWaitEvent(e.copy_stream, e.ev_call, 0), "copy stream order");
-        // Host B and C in column-major layouts: pipeline the call in column
-        // windows (engine.hpp ColumnWindows) when the problem is large enough.
-        long qcols = 0;
-        const int nwin =
-            (!device_only && e.pipelining && !(has_beta && beta != 1.0) && rs_b == 1 &&
-             rs_c == 1 && cs_b >= k && cs_c >= m && !sb200::is_device_pointer(b) &&
-             !sb200::is_device_pointer(c))
-                ? sb200::plan_windows(e, variant, level, m, n, k, qcols)
-                : 0;
-        const sb200::DView A = stage_in(e, s, a, m, k, rs_a, cs_a, e.stage_a, true, sa, e.ev_ready[0]);
-        const sb200::DView B = stage_in(e, s, b, k, n, rs_b, cs_b, e.stage_b, nwin == 0, sb, e.ev_ready[1]);
-        const sb200::DView C = stage_in(e, s, c, m, n, rs_c, cs_c, e.stage_c, nwin == 0, sc, e.ev_ready[2]);
+        // Host B and C in column-major layouts: pipeline the call in windows
+        // (engine.hpp Windows) when the problem is large enough; A arrives in
+        // row strips when it is host column-major too.
+        sb200::Windows W;
+        const bool a_strips = rs_a == 1 && cs_a >= m && !sb200::is_device_pointer(a);
+        if (!device_only && e.pipelining && !(has_beta && beta != 1.0) && rs_b == 1 &&
+            rs_c == 1 && cs_b >= k && cs_c >= m && !sb200::is_device_pointer(b) &&
+            !sb200::is_device_pointer(c))
+            sb200::plan_windows(e, variant, level, m, n, k, a_strips, W);
+        const bool windowed = W.count() > 0;
+        const bool a_windowed = windowed && W.rows > 1;
+        const sb200::DView A = stage_in(e, s, a, m, k, rs_a, cs_a, e.stage_a, !a_windowed, sa, e.ev_ready[0]);
+        const sb200::DView B = stage_in(e, s, b, k, n, rs_b, cs_b, e.stage_b, !windowed, sb, e.ev_ready[1]);
+        const sb200::DView C = stage_in(e, s, c, m, n, rs_c, cs_c, e.stage_c, !windowed, sc, e.ev_ready[2]);
         if (device_only && (sa || sb || sc))
             throw std::invalid_argument("strassen_gemm_device: operands must be device memory");
         for (auto& t : e.timed) {
@@ -153,48 +155,64 @@ strassen_status gemm_impl(strassen_ctx* ctx, bool explicit_stream, cudaStream_t 
             cudaEventDestroy(t.stop);
         }
         e.timed.clear();
-        if (nwin > 0) {
+        if (windowed) {
             const int L = (variant == STRASSEN_DGEMM) ? 0 : level;
-            const long side = 1L << L, qn = (n + side - 1) / side;
-            // global column range of window w inside quadrant column block J
-            auto cols_of = [&](int w, long J, long& j0, long& j1) {
-                j0 = std::min(n, J * qn + w * qcols);
-                j1 = std::min(n, J * qn + std::min(qn, (w + 1) * qcols));
+            const long side = 1L << L, qm = (m + side - 1) / side, qn = (n + side - 1) / side;
+            // global index ranges of strip w (width q_w) inside every quadrant
+            // block of extent q, clipped to [0, total) and merged when adjacent
+            auto ranges = [&](long total, long q, long q_w, int w) {
+                std::vector<std::pair<long, long>> out;
+                for (long I = 0; I < side; ++I) {
+                    const long lo = std::min(total, I * q + w * q_w);
+                    const long hi = std::min(total, I * q + std::min(q, (w + 1) * q_w));
+                    if (lo >= hi) continue;
+                    if (!out.empty() && out.back().second == lo) out.back().second = hi;
+                    else out.emplace_back(lo, hi);
+                }
+                return out;
             };
-            // column-major spans: columns [j0, j1) of a rows x n view with ld cs
-            auto copy_cols = [&](double* dst, const double* src, long j0, long j1, long rows,
-                                 long cs, cudaMemcpyKind kind, cudaStream_t st) {
-                if (j0 >= j1) return;
-                const size_t count = static_cast<size_t>((j1 - 1 - j0) * cs + rows);
-                cuda_ck(cudaMemcpyAsync(dst + j0 * cs, src + j0 * cs, count * 8, kind, st),
+            // rows [i0, i1) x columns [j0, j1) of a column-major view (ld) as one 2-D copy
+            auto copy_block = [&](double* dst, const double* src, long ld, long i0, long i1,
+                                  long j0, long j1, cudaMemcpyKind kind, cudaStream_t st) {
+                const size_t off = static_cast<size_t>(i0 + j0 * ld);
+                cuda_ck(cudaMemcpy2DAsync(dst + off, ld * 8, src + off, ld * 8, (i1 - i0) * 8,
+                                          j1 - j0, kind, st),
                         kind == cudaMemcpyHostToDevice ? "H2D window" : "D2H window");
             };
-            sb200::ColumnWindows W;
-            W.count = nwin;
-            W.qcols = qcols;
+            W.a_ready = e.ev_win_a;
             W.b_ready = e.ev_win_b;
             W.c_ready = e.ev_win_c;
             W.done = e.ev_win_done;
-            W.issue_in = [&](int w) {
-                long j0, j1;
-                for (long J = 0; J < side; ++J) {
-                    cols_of(w, J, j0, j1);
-                    copy_cols(B.p, b, j0, j1, k, cs_b, cudaMemcpyHostToDevice, e.copy_stream);
-                }
-                cuda_ck(cudaEventRecord(e.ev_win_b[w], e.copy_stream), "window event");
-                for (long J = 0; J < side; ++J) {
-                    cols_of(w, J, j0, j1);
-                    copy_cols(C.p, c, j0, j1, m, cs_c, cudaMemcpyHostToDevice, e.copy_stream);
-                }
+            W.issue_a = [&](int r) {
+                if (a_windowed)
+                    for (auto [i0, i1] : ranges(m, qm, W.qrows, r))
+                        copy_block(A.p, a, cs_a, i0, i1, 0, k, cudaMemcpyHostToDevice,
+                                   e.copy_stream);
+                // otherwise A was staged whole (or is resident): the event follows it
+                cuda_ck(cudaEventRecord(e.ev_win_a[r], e.copy_stream), "window event");
+            };
+            W.issue_b = [&](int cw) {
+                for (auto [j0, j1] : ranges(n, qn, W.qcols, cw))
+                    copy_block(B.p, b, cs_b, 0, k, j0, j1, cudaMemcpyHostToDevice, e.copy_stream);
+                cuda_ck(cudaEventRecord(e.ev_win_b[cw], e.copy_stream), "window event");
+            };
+            auto c_blocks = [&](int w, cudaMemcpyKind kind, cudaStream_t st) {
+                const auto rr = ranges(m, qm, W.qrows, w / W.cols);
+                const auto cc = ranges(n, qn, W.qcols, w % W.cols);
+                for (auto [i0, i1] : rr)
+                    for (auto [j0, j1] : cc)
+                        if (kind == cudaMemcpyHostToDevice)
+                            copy_block(C.p, c, cs_c, i0, i1, j0, j1, kind, st);
+                        else
+                            copy_block(c, C.p, cs_c, i0, i1, j0, j1, kind, st);
+            };
+            W.issue_c = [&](int w) {
+                c_blocks(w, cudaMemcpyHostToDevice, e.copy_stream);
                 cuda_ck(cudaEventRecord(e.ev_win_c[w], e.copy_stream), "window event");
             };
             W.issue_out = [&](int w) {
                 cuda_ck(cudaStreamWaitEvent(e.d2h_stream, e.ev_win_done[w], 0), "window wait");
-                long j0, j1;
-                for (long J = 0; J < side; ++J) {
-                    cols_of(w, J, j0, j1);
-                    copy_cols(c, C.p, j0, j1, m, cs_c, cudaMemcpyDeviceToHost, e.d2h_stream);
-                }
+                c_blocks(w, cudaMemcpyDeviceToHost, e.d2h_stream);
             };
             launches += sb200::run_device(e, s, variant, level, alpha, A, B, C, &W);
             cuda_ck(cudaEventRecord(e.ev_d2h, e.d2h_stream), "d2h event");

@@ -5,7 +5,9 @@
 
 #include <algorithm>
 #include <cstring>
+#include <memory>
 #include <mutex>
+#include <cstdio>
 #include <cstdlib>
 
 #include "kernels.hpp"
@@ -178,10 +180,15 @@ Engine::~Engine() {
     if (d2h_stream) cudaStreamDestroy(d2h_stream);
     for (auto ev : ev_ready)
         if (ev) cudaEventDestroy(ev);
-    for (cudaEvent_t* arr : {ev_win_b, ev_win_c, ev_win_done})
+    if (aux_stream) cudaStreamDestroy(aux_stream);
+    for (cudaEvent_t* arr : {ev_win_a, ev_win_b, ev_sum_a, ev_sum_b})
+        for (int w = 0; w < kMaxStrips; ++w)
+            if (arr[w]) cudaEventDestroy(arr[w]);
+    for (cudaEvent_t* arr : {ev_win_c, ev_win_done})
         for (int w = 0; w < kMaxWindows; ++w)
             if (arr[w]) cudaEventDestroy(arr[w]);
-    if (ev_d2h) cudaEventDestroy(ev_d2h);
+    for (cudaEvent_t ev : {ev_d2h, ev_fork, ev_join})
+        if (ev) cudaEventDestroy(ev);
     for (DeviceBuffer* b : {&stage_a, &stage_b, &stage_c, &pack_a, &pack_b, &mbuf, &tabuf, &tbbuf})
         if (b->ptr) cudaFree(b->ptr);
 }
@@ -197,8 +204,13 @@ void Engine::init() {
     ck(cudaEventCreateWithFlags(&ev_call, cudaEventDisableTiming), "event");
     for (auto& ev : ev_ready) ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
     ck(cudaStreamCreateWithFlags(&d2h_stream, cudaStreamNonBlocking), "d2h stream");
-    ck(cudaEventCreateWithFlags(&ev_d2h, cudaEventDisableTiming), "event");
-    for (cudaEvent_t* arr : {ev_win_b, ev_win_c, ev_win_done})
+    ck(cudaStreamCreateWithFlags(&aux_stream, cudaStreamNonBlocking), "aux stream");
+    for (cudaEvent_t* ev : {&ev_d2h, &ev_fork, &ev_join})
+        ck(cudaEventCreateWithFlags(ev, cudaEventDisableTiming), "event");
+    for (cudaEvent_t* arr : {ev_win_a, ev_win_b, ev_sum_a, ev_sum_b})
+        for (int w = 0; w < kMaxStrips; ++w)
+            ck(cudaEventCreateWithFlags(&arr[w], cudaEventDisableTiming), "event");
+    for (cudaEvent_t* arr : {ev_win_c, ev_win_done})
         for (int w = 0; w < kMaxWindows; ++w)
             ck(cudaEventCreateWithFlags(&arr[w], cudaEventDisableTiming), "event");
     initialised = true;
@@ -298,13 +310,15 @@ FusedPlan plan_fused(Engine& e, const MMParams& P, bool force_split) {
     return F;
 }
 
-// Quadrant columns [c0, c1) of the plan: the mm launch over those tile columns
-// (c0 a multiple of kBN) and, in split mode, the stream pass over them.
+// Window [r0, r1) x [c0, c1) (quadrant coordinates, r0 / c0 tile multiples) of
+// the plan: the mm launch over those tiles and, in split mode, the stream pass.
 // wait_c() is called right before the first launch that touches C.
 long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
                       const std::vector<Terms>& dests, const std::vector<QuadView>& cq,
-                      const DView& C, double alpha, long c0, long c1,
+                      const DView& C, double alpha, long r0, long r1, long c0, long c1,
                       const std::function<void()>& wait_c) {
+    P.tm0 = static_cast<int>(r0 / kBM);
+    P.tiles_m = static_cast<int>(ceil_div(r1 - r0, kBM));
     P.tn0 = static_cast<int>(c0 / kBN);
     P.tiles_n = static_cast<int>(ceil_div(c1 - c0, kBN));
     if (!F.split) {
@@ -337,6 +351,8 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
     S.nquad = static_cast<int>(cq.size());
     S.qm = P.qm;
     S.qn = P.qn;
+    S.r0 = static_cast<int>(r0);
+    S.r1 = static_cast<int>(r1);
     S.c0 = static_cast<int>(c0);
     S.c1 = static_cast<int>(c1);
     S.mbase = F.M;
@@ -361,7 +377,7 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
 // ------------------------------------------------------------- run_device --
 namespace {
 long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level, double alpha,
-                  const DView& A, const DView& B, const DView& C, const ColumnWindows* win);
+                  const DView& A, const DView& B, const DView& C, const Windows* win);
 
 DView sub(const DView& v, long r0, long c0, long rows, long cols) {
     DView o = v;
@@ -372,26 +388,56 @@ DView sub(const DView& v, long r0, long c0, long rows, long cols) {
 }
 }  // namespace
 
-int plan_windows(const Engine& e, strassen_variant variant, int level, long m, long n, long k,
-                 long& qcols) {
+std::vector<int> window_order(int rows, int cols) {
+    std::vector<int> order;
+    for (int sh = 0; sh < std::max(rows, cols); ++sh) {
+        if (sh < cols)
+            for (int r = 0; r < std::min(sh, rows); ++r) order.push_back(r * cols + sh);
+        if (sh < rows)
+            for (int c = 0; c <= std::min(sh, cols - 1); ++c) order.push_back(sh * cols + c);
+    }
+    return order;
+}
+
+void plan_windows(const Engine& e, strassen_variant variant, int level, long m, long n, long k,
+                  bool row_windows, Windows& w) {
     (void)k;
+    w.rows = w.cols = 0;
     const int L = (variant == STRASSEN_DGEMM) ? 0 : level;
     const long side = 1L << L;
     const long qm = ceil_div(m, side), qn = ceil_div(n, side);
     const long tiles_m = ceil_div(qm, kBM), tiles_n = ceil_div(qn, kBN);
     const long sms = e.num_sms > 0 ? e.num_sms : 148;
-    long per_col = tiles_m;  // CTAs per tile column
+    long per_tile = 1;  // CTAs per output tile
     if (variant == STRASSEN_NAIVE || variant == STRASSEN_AB) {
-        for (int l = 0; l < L; ++l) per_col *= 7;
+        for (int l = 0; l < L; ++l) per_tile *= 7;
     } else if (tiles_m * tiles_n < 2 * sms) {
-        return 0;  // split-mode sizes: a few milliseconds, nothing to overlap
+        return;  // split-mode sizes: a few milliseconds, nothing to overlap
     }
-    // at least 4 waves of CTAs per window keeps the per-window tail small
-    long count = std::min<long>(Engine::kMaxWindows / 2, tiles_n * per_col / (4 * sms));
-    count = std::min(count, tiles_n);
-    if (count < 2) return 0;
-    qcols = ceil_div(tiles_n, count) * kBN;
-    return static_cast<int>(ceil_div(qn, qcols));
+    // windows of >= 2 waves each (consecutive windows overlap on two streams);
+    // grow the grid keeping it square-ish
+    const long max_w = tiles_m * tiles_n * per_tile / (2 * sms);
+    long R = 1, Cn = 1;
+    for (;;) {
+        const bool grow_c = Cn < Engine::kMaxStrips && Cn < tiles_n && R * (Cn + 1) <= max_w;
+        const bool grow_r = row_windows && R < Engine::kMaxStrips && R < tiles_m &&
+                            (R + 1) * Cn <= max_w;
+        if (grow_c && (Cn <= R || !grow_r)) ++Cn;
+        else if (grow_r) ++R;
+        else break;
+    }
+    if (const char* env = std::getenv("STRASSEN_B200_WINDOWS")) {  // "RxC" (experiments)
+        long r = 0, c = 0;
+        if (std::sscanf(env, "%ldx%ld", &r, &c) == 2) {
+            R = clip(r, 1, row_windows ? std::min<long>(Engine::kMaxStrips, tiles_m) : 1);
+            Cn = clip(c, 1, std::min<long>(Engine::kMaxStrips, tiles_n));
+        }
+    }
+    if (R * Cn < 2) return;
+    w.qrows = ceil_div(tiles_m, R) * kBM;
+    w.qcols = ceil_div(tiles_n, Cn) * kBN;
+    w.rows = static_cast<int>(ceil_div(qm, w.qrows));
+    w.cols = static_cast<int>(ceil_div(qn, w.qcols));
 }
 
 // Dynamic peeling (north star; the reference pads instead, matrix.cpp:14-22):
@@ -403,7 +449,7 @@ int plan_windows(const Engine& e, strassen_variant variant, int level, long m, l
 //   C[0:m_e, n_e:n] += alpha A[0:m_e, 0:k]   B[0:k, n_e:n]      (right columns)
 // Tiny problems (core below one 128-tile per quadrant) keep the padded path.
 long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, double alpha,
-                const DView& A, const DView& B, const DView& C, const ColumnWindows* win) {
+                const DView& A, const DView& B, const DView& C, const Windows* win) {
     const int L = (variant == STRASSEN_DGEMM) ? 0 : level;
     const long S = 1L << L;
     const long m = A.rows, k = A.cols, n = B.cols;
@@ -416,15 +462,19 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
     };
     const bool peel = L > 0 && ragged && e.peeling && me >= S * kBM && ne >= S * kBN &&
                       ke >= S * kBK && work(me, ne, ke) < work(m, n, k);
-    if (win && win->count > 0 && (peel || !tma_ready(B, ceil_div(k, S), static_cast<int>(S)))) {
+    if (win && win->count() > 0 &&
+        (peel || !tma_ready(A, ceil_div(m, S), static_cast<int>(S)) ||
+         !tma_ready(B, ceil_div(k, S), static_cast<int>(S)))) {
         // not windowable: everything in first, everything out last
-        for (int w = 0; w < win->count; ++w) {
-            win->issue_in(w);
-            ck(cudaStreamWaitEvent(s, win->b_ready[w], 0), "window wait");
-            ck(cudaStreamWaitEvent(s, win->c_ready[w], 0), "window wait");
-        }
+        for (int r = 0; r < win->rows; ++r) win->issue_a(r);
+        for (int c = 0; c < win->cols; ++c) win->issue_b(c);
+        for (int w = 0; w < win->count(); ++w) win->issue_c(w);
+        for (int r = 0; r < win->rows; ++r) ck(cudaStreamWaitEvent(s, win->a_ready[r], 0), "wait");
+        for (int c = 0; c < win->cols; ++c) ck(cudaStreamWaitEvent(s, win->b_ready[c], 0), "wait");
+        for (int w = 0; w < win->count(); ++w)
+            ck(cudaStreamWaitEvent(s, win->c_ready[w], 0), "wait");
         const long launches = run_device(e, s, variant, level, alpha, A, B, C, nullptr);
-        for (int w = 0; w < win->count; ++w) {
+        for (int w = 0; w < win->count(); ++w) {
             ck(cudaEventRecord(win->done[w], s), "window done");
             win->issue_out(w);
         }
@@ -447,24 +497,12 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
 
 namespace {
 long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level, double alpha,
-                  const DView& A, const DView& B, const DView& C, const ColumnWindows* win) {
+                  const DView& A, const DView& B, const DView& C, const Windows* win) {
     const int L = (variant == STRASSEN_DGEMM) ? 0 : level;
     const int side = 1 << L;
     const long m = A.rows, k = A.cols, n = B.cols;
     const long qm = ceil_div(m, side), qk = ceil_div(k, side), qn = ceil_div(n, side);
     long launches = 0;
-    const int nwin = win ? win->count : 1;
-    const long wcols = win ? win->qcols : qn;
-    if (win) win->issue_in(0);
-    // window w's B columns / C columns have landed (whole operands without windows)
-    auto wait_b = [&](int w) {
-        if (win) ck(cudaStreamWaitEvent(s, win->b_ready[w], 0), "window wait");
-    };
-    auto wait_c = [&](int w) {
-        if (win) ck(cudaStreamWaitEvent(s, win->c_ready[w], 0), "window wait");
-        else wait_ready(s, C);
-    };
-
     const TmaOperand ta = prepare(e, s, A, qm, qk, side, e.pack_a, launches);
     const TmaOperand tb = prepare(e, s, B, qk, qn, side, e.pack_b, launches);
     const int nq = side * side;
@@ -520,21 +558,65 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
         if (l.a.empty() || l.b.empty() || l.c.empty()) continue;
         live.push_back(std::move(l));
     }
+    // Windows (r, c) in row-major order; without `win` one window covers all.
+    const int nr = win ? win->rows : 1, nc = win ? win->cols : 1, nw = nr * nc;
+    const long wrows = win ? win->qrows : qm, wcols = win ? win->qcols : qn;
+    // Windows alternate between s and the aux stream (ordered after s's work so
+    // far); s joins the aux stream at the end.
+    cudaStream_t ws[2] = {s, nw > 1 ? e.aux_stream : s};
+    if (nw > 1) {
+        ck(cudaEventRecord(e.ev_fork, s), "fork");
+        ck(cudaStreamWaitEvent(e.aux_stream, e.ev_fork, 0), "fork");
+    }
+    auto wait_ev = [&](cudaStream_t st, cudaEvent_t ev) {
+        if (ev) ck(cudaStreamWaitEvent(st, ev, 0), "wait");
+    };
+    auto wait_a = [&](cudaStream_t st, int r) { wait_ev(st, win ? win->a_ready[r] : ta.ready); };
+    auto wait_b = [&](cudaStream_t st, int c) { wait_ev(st, win ? win->b_ready[c] : tb.ready); };
+    auto wait_c = [&](cudaStream_t st, int w) {
+        if (win) wait_ev(st, win->c_ready[w]);
+        else wait_ready(st, C);
+    };
+    auto finish = [&](cudaStream_t st, int w) {
+        if (!win) return;
+        ck(cudaEventRecord(win->done[w], st), "window done");
+        win->issue_out(w);
+    };
+    // processing order; the first window of each row strip computes its A
+    // sums (and triggers its copy), likewise for column strips and B
+    const std::vector<int> order = win ? window_order(nr, nc) : std::vector<int>{0};
+    std::vector<int> first_r(nr, -1), first_c(nc, -1);
+    for (int i = 0; i < nw; ++i) {
+        if (first_r[order[i] / nc] < 0) first_r[order[i] / nc] = order[i];
+        if (first_c[order[i] % nc] < 0) first_c[order[i] % nc] = order[i];
+    }
+    auto prefetch = [&](int i) {  // copies of the i-th window, issued one window ahead
+        if (!win || i >= nw) return;
+        const int w = order[i], r = w / nc, c = w % nc;
+        if (first_r[r] == w) win->issue_a(r);
+        if (first_c[c] == w) win->issue_b(c);
+        win->issue_c(w);
+    };
+    auto join = [&] {
+        if (nw > 1) {
+            ck(cudaEventRecord(e.ev_join, e.aux_stream), "join");
+            ck(cudaStreamWaitEvent(s, e.ev_join, 0), "join");
+        }
+    };
+
+    prefetch(0);
     if (live.empty()) {
-        if (win)
-            for (int w = 0; w < nwin; ++w) {
-                if (w + 1 < nwin) win->issue_in(w + 1);
-                wait_b(w);
-                wait_c(w);
-                ck(cudaEventRecord(win->done[w], s), "window done");
-                win->issue_out(w);
-            }
+        for (int i = 0; i < nw; ++i) {
+            prefetch(i + 1);
+            wait_c(s, order[i]);
+            finish(s, order[i]);
+        }
+        join();
         return launches;
     }
-    if (ta.ready) cudaStreamWaitEvent(s, ta.ready, 0);  // every path reads A first
 
     const bool sums = variant == STRASSEN_C || variant == STRASSEN_NAIVE;
-    std::vector<SumBatchParams*> side_sums(2, nullptr);
+    std::unique_ptr<SumBatchParams> side_sums[2];
     if (sums) {
         // Every multi-term operand sum materialised by one HBM pass per side
         // (materialize_sum, variants.cpp:53-96, for all entries at once); the
@@ -551,10 +633,10 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
         double* TA = e.ensure(e.tabuf, static_cast<size_t>(std::max(na_sums, 1)) * lda_t * qk * 8);
         double* TB = e.ensure(e.tbbuf, static_cast<size_t>(std::max(nb_sums, 1)) * ldb_t * qn * 8);
         for (int sd = 0; sd < 2; ++sd) {
-            int next_map = kMaxQuad;  // tmA / tmB: 16 quadrant maps, then the sums
-            SumBatchParams* SB = new SumBatchParams;  // ~10 KB: keep off the stack
+            side_sums[sd].reset(new SumBatchParams);  // ~10 KB: keep off the stack
+            SumBatchParams* SB = side_sums[sd].get();
             std::memset(SB, 0, sizeof(*SB));
-            side_sums[sd] = SB;
+            int next_map = kMaxQuad;  // tmA / tmB: 16 quadrant maps, then the sums
             const TmaOperand& t = sd == 0 ? ta : tb;
             SB->rows = sd == 0 ? qm : qk;
             SB->cols = sd == 0 ? qk : qn;
@@ -584,15 +666,6 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
                 terms = {{mi, 1}};
             }
         }
-        e.prof_begin("sum_batch_kernel", s);
-        cudaError_t err = launch_sum_batch(*side_sums[0], s);
-        e.prof_end(s);
-        if (side_sums[0]->njobs) ++launches;
-        if (err != cudaSuccess) {
-            delete side_sums[0];
-            delete side_sums[1];
-            ck(err, "sum_batch (A)");
-        }
     }
 
     P.nprod = static_cast<int>(live.size());
@@ -608,34 +681,45 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
     const bool store_products = variant == STRASSEN_NAIVE || variant == STRASSEN_AB;
     const FusedPlan F = plan_fused(e, P, store_products);
 
-    try {
-        for (int w = 0; w < nwin; ++w) {
-            if (win && w + 1 < nwin) win->issue_in(w + 1);  // prefetch the next window
-            const long c0 = w * wcols, c1 = std::min(qn, c0 + wcols);
-            wait_b(w);
-            if (!win && tb.ready) cudaStreamWaitEvent(s, tb.ready, 0);
-            if (sums && side_sums[1]->njobs) {
-                side_sums[1]->c0 = c0;
-                side_sums[1]->cols = c1;
-                e.prof_begin("sum_batch_kernel", s);
-                ck(launch_sum_batch(*side_sums[1], s), "sum_batch (B)");
-                e.prof_end(s);
+    for (int i = 0; i < nw; ++i) {
+        prefetch(i + 1);
+        const int w = order[i], r = w / nc, c = w % nc;
+        cudaStream_t st = ws[i % 2];
+        const long r0 = r * wrows, r1 = std::min(qm, r0 + wrows);
+        const long c0 = c * wcols, c1 = std::min(qn, c0 + wcols);
+        wait_a(st, r);
+        wait_b(st, c);
+        if (sums) {
+            // A sums of row strip r in its first window, B sums of column strip c
+            // in row 0; later windows wait on them
+            for (int sd = 0; sd < 2; ++sd) {
+                SumBatchParams& SB = *side_sums[sd];
+                const bool owner = sd == 0 ? first_r[r] == w : first_c[c] == w;
+                cudaEvent_t ev = sd == 0 ? e.ev_sum_a[r] : e.ev_sum_b[c];
+                if (!owner) {
+                    wait_ev(st, ev);
+                    continue;
+                }
+                if (!SB.njobs) continue;
+                if (sd == 0) {
+                    SB.r0 = r0;
+                    SB.rows = r1;
+                } else {
+                    SB.c0 = c0;
+                    SB.cols = c1;
+                }
+                e.prof_begin("sum_batch_kernel", st);
+                ck(launch_sum_batch(SB, st), sd == 0 ? "sum_batch (A)" : "sum_batch (B)");
+                e.prof_end(st);
                 ++launches;
-            }
-            launches += run_fused_window(e, s, P, F, dests, cq, C, alpha, c0, c1,
-                                         [&] { wait_c(w); });
-            if (win) {
-                ck(cudaEventRecord(win->done[w], s), "window done");
-                win->issue_out(w);
+                if (nw > 1) ck(cudaEventRecord(ev, st), "sum event");
             }
         }
-    } catch (...) {
-        delete side_sums[0];
-        delete side_sums[1];
-        throw;
+        launches += run_fused_window(e, st, P, F, dests, cq, C, alpha, r0, r1, c0, c1,
+                                     [&] { wait_c(st, w); });
+        finish(st, w);
     }
-    delete side_sums[0];
-    delete side_sums[1];
+    join();
     return launches;
 }
 }  // namespace

@@ -64,8 +64,14 @@ struct Engine {
     bool pipelining = true;  // strassen_ctx_set_pipelining
     cudaStream_t d2h_stream = nullptr;
     cudaEvent_t ev_d2h = nullptr;
-    static constexpr int kMaxWindows = 8;
-    cudaEvent_t ev_win_b[kMaxWindows] = {}, ev_win_c[kMaxWindows] = {}, ev_win_done[kMaxWindows] = {};
+    static constexpr int kMaxStrips = 8, kMaxWindows = kMaxStrips * kMaxStrips;
+    cudaEvent_t ev_win_a[kMaxStrips] = {}, ev_win_b[kMaxStrips] = {};
+    cudaEvent_t ev_win_c[kMaxWindows] = {}, ev_win_done[kMaxWindows] = {};
+    // windows alternate between the call stream and aux_stream so that one
+    // window's tail wave overlaps the next window's first
+    cudaStream_t aux_stream = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_sum_a[kMaxStrips] = {}, ev_sum_b[kMaxStrips] = {};
     double* ensure(DeviceBuffer& b, size_t bytes);
     size_t workspace_bytes() const;
 };
@@ -84,33 +90,45 @@ inline void wait_ready(cudaStream_t s, const DView& v) {
     if (v.ready) cudaStreamWaitEvent(s, v.ready, 0);
 }
 
-// Host-call pipeline: B and C arrive (and C leaves) in column windows of the
-// quadrant partition -- window w is quadrant columns [w*qcols, (w+1)*qcols) of
-// every quadrant column block -- so the transfers of one window overlap the
-// kernels of the others.  Per element the arithmetic is exactly that of the
-// unwindowed call (same partition, same launch modes, same k order).
-struct ColumnWindows {
-    int count = 0;
-    long qcols = 0;                       // multiple of the 128-column tile
-    std::function<void(int)> issue_in;   // enqueue window w's B and C copies, record b/c_ready[w]
-    std::function<void(int)> issue_out;  // enqueue window w's result copy after done[w]
+// Host-call pipeline: the output is cut into R x Cn windows of the quadrant
+// partition -- window w = r*Cn + c is quadrant rows [r*qrows, (r+1)*qrows) and
+// quadrant columns [c*qcols, (c+1)*qcols) of every quadrant.  A arrives in R
+// row strips, B in Cn column strips, C in windows; each window's result leaves
+// as soon as it is final.  Windows run in growing shells (max(r, c) = 0, 1,
+// ...), so each shell needs one new A strip and one new B strip while its
+// compute grows: transfers of later windows overlap the kernels of earlier
+// ones.  Per element the
+// arithmetic is exactly that of the unwindowed call (same partition, same
+// launch modes, same k order).
+struct Windows {
+    int rows = 0, cols = 0;              // R x Cn windows (0: none)
+    long qrows = 0, qcols = 0;           // multiples of the 128 x 128 tile
+    std::function<void(int)> issue_a;    // enqueue A row strip r, record a_ready[r]
+    std::function<void(int)> issue_b;    // enqueue B column strip c, record b_ready[c]
+    std::function<void(int)> issue_c;    // enqueue C window w, record c_ready[w]
+    std::function<void(int)> issue_out;  // enqueue window w's copy-back after done[w]
+    cudaEvent_t* a_ready = nullptr;
     cudaEvent_t* b_ready = nullptr;
     cudaEvent_t* c_ready = nullptr;
     cudaEvent_t* done = nullptr;         // recorded on s after window w's last kernel
+    int count() const { return rows * cols; }
 };
 
-// Number of column windows worth pipelining a host call into (0: none) and
-// their width in quadrant columns.
-int plan_windows(const Engine& e, strassen_variant variant, int level, long m, long n, long k,
-                 long& qcols);
+// Processing order of an R x Cn window grid (window ids r*Cn + c): shells of
+// max(r, c) = s, each as (0..s-1, s) then (s, 0..s).
+std::vector<int> window_order(int rows, int cols);
+
+// Window grid worth pipelining a host call into (rows = cols = 0: none).
+// row_windows: A can arrive in row strips (host, column-major).
+void plan_windows(const Engine& e, strassen_variant variant, int level, long m, long n, long k,
+                  bool row_windows, Windows& w);
 
 // C := alpha A B + C on device views, enqueued on `s` (no synchronisation).
 // variant/level already validated.  Returns the number of kernel launches.
-// With `win`, B's and C's windows are copied in by win->issue_in (their views
-// carry no ready event) and every window is handed to win->issue_out.
+// With `win`, the operands arrive through win->issue_* (their views carry no
+// ready event) and every window is handed to win->issue_out.
 long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, double alpha,
-                const DView& A, const DView& B, const DView& C,
-                const ColumnWindows* win = nullptr);
+                const DView& A, const DView& B, const DView& C, const Windows* win = nullptr);
 
 // C := beta C on a device view.
 long scale_device(Engine& e, cudaStream_t s, const DView& C, double beta);

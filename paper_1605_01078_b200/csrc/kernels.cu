@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     const int first_m = grp * P.group_m;
     const int gsz = min(P.tiles_m - first_m, P.group_m);
     const int rr = bid - grp * per_group;
-    const int tm = first_m + rr % gsz;
+    const int tm = first_m + rr % gsz + P.tm0;
     const int tn = rr / gsz + P.tn0;
 
     if (threadIdx.x == 0) {
@@ -464,7 +464,7 @@ __global__ void sum_batch_kernel(const __grid_constant__ SumBatchParams P) {
     // one thread = rows (2r, 2r+1) of two columns: 16-byte loads/stores
     // (sources are TMA-ready quadrants: 16-byte aligned, even leading dims)
     const int z = blockIdx.z;
-    const long long i = 2 * (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x);
+    const long long i = P.r0 + 2 * (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x);
     if (i >= P.rows) return;
     const int n = P.nterms[z];
     double* dst = P.dst[z];
@@ -514,8 +514,8 @@ __global__ void sum_batch_kernel(const __grid_constant__ SumBatchParams P) {
 // (alpha * gamma) * M_p(i, j)  (variants.cpp:99-109, applied entry by entry).
 __global__ void stream_update_kernel(const StreamParams P) {
     const int quad = blockIdx.z;
-    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= P.crows[quad]) return;
+    const long long i = P.r0 + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= P.crows[quad] || i >= P.r1) return;
     double* C = P.cptr[quad];
     const int ns = P.nsrc[quad];
     const long long jend = P.ccols[quad] < P.c1 ? P.ccols[quad] : P.c1;
@@ -550,7 +550,7 @@ struct SumGatherParams {
     int8_t tcoeff[kMaxSumJobs][kMaxTerms];
     int njobs;
     long long rows, cols, ld;
-    long long c0;
+    long long r0, c0;
 };
 constexpr int kGatherThreads = 128;
 
@@ -558,7 +558,7 @@ __global__ void __launch_bounds__(kGatherThreads)
 sum_gather_kernel(const __grid_constant__ SumGatherParams P) {
     __shared__ double2 xs[kMaxQuad][kGatherThreads];  // 32 KB
     const int tid = threadIdx.x;
-    const long long i = 2 * (static_cast<long long>(blockIdx.x) * kGatherThreads + tid);
+    const long long i = P.r0 + 2 * (static_cast<long long>(blockIdx.x) * kGatherThreads + tid);
     if (i >= P.rows) return;
     const bool pair = i + 1 < P.rows;
     for (long long j = P.c0 + blockIdx.y; j < P.cols; j += gridDim.y) {
@@ -610,7 +610,7 @@ struct StreamGatherParams {
     int8_t dcoeff[kMaxProducts][kMaxQuad];
     double alpha;
     int qm, qn;
-    int c0, c1;
+    int r0, r1, c0, c1;
 };
 constexpr int kStreamThreads = 256;
 constexpr int kStreamBatch = 8;  // M loads in flight per thread
@@ -619,8 +619,8 @@ __global__ void __launch_bounds__(kStreamThreads)
 stream_gather_kernel(const __grid_constant__ StreamGatherParams P) {
     __shared__ double cs[kMaxQuad][kStreamThreads];  // 32 KB
     const int tid = threadIdx.x;
-    const long long i = static_cast<long long>(blockIdx.x) * kStreamThreads + tid;
-    if (i >= P.qm) return;
+    const long long i = P.r0 + static_cast<long long>(blockIdx.x) * kStreamThreads + tid;
+    if (i >= P.r1) return;
     for (long long j = P.c0 + blockIdx.y; j < P.c1; j += gridDim.y) {
 #pragma unroll
         for (int q = 0; q < kMaxQuad; ++q)
@@ -736,6 +736,7 @@ static bool to_gather(const SumBatchParams& p, SumGatherParams& g) {
     g.rows = p.rows;
     g.cols = p.cols;
     g.ld = p.ld;
+    g.r0 = p.r0;
     g.c0 = p.c0;
     return true;
 }
@@ -744,14 +745,14 @@ cudaError_t launch_sum_batch(const SumBatchParams& p, cudaStream_t s) {
     if (p.njobs == 0) return cudaSuccess;
     static thread_local SumGatherParams g;  // host staging; copied at launch
     if (to_gather(p, g)) {
-        const long long pairs = (p.rows + 1) / 2;
+        const long long pairs = (p.rows - p.r0 + 1) / 2;
         const long long w = p.cols - p.c0;
         dim3 grid(static_cast<unsigned>((pairs + kGatherThreads - 1) / kGatherThreads),
                   static_cast<unsigned>(w < 2048 ? w : 2048));
         sum_gather_kernel<<<grid, kGatherThreads, 0, s>>>(g);
         return cudaGetLastError();
     }
-    const long long pairs = (p.rows + 1) / 2, cpairs = (p.cols - p.c0 + 1) / 2;
+    const long long pairs = (p.rows - p.r0 + 1) / 2, cpairs = (p.cols - p.c0 + 1) / 2;
     dim3 grid(static_cast<unsigned>((pairs + 127) / 128),
               static_cast<unsigned>(cpairs < 1024 ? cpairs : 1024), p.njobs);
     sum_batch_kernel<<<grid, 128, 0, s>>>(p);
@@ -788,6 +789,8 @@ static bool to_gather(const StreamParams& p, StreamGatherParams& g) {
     g.alpha = p.alpha;
     g.qm = p.qm;
     g.qn = p.qn;
+    g.r0 = p.r0;
+    g.r1 = p.r1;
     g.c0 = p.c0;
     g.c1 = p.c1;
     return true;
@@ -797,12 +800,12 @@ cudaError_t launch_stream_update(const StreamParams& p, cudaStream_t s) {
     static thread_local StreamGatherParams g;
     if (to_gather(p, g)) {
         const int w = p.c1 - p.c0;
-        dim3 grid(static_cast<unsigned>((p.qm + kStreamThreads - 1) / kStreamThreads),
+        dim3 grid(static_cast<unsigned>((p.r1 - p.r0 + kStreamThreads - 1) / kStreamThreads),
                   static_cast<unsigned>(w < 4096 ? w : 4096));
         stream_gather_kernel<<<grid, kStreamThreads, 0, s>>>(g);
         return cudaGetLastError();
     }
-    dim3 grid(static_cast<unsigned>((p.qm + 255) / 256), col_grid(p.c1 - p.c0), p.nquad);
+    dim3 grid(static_cast<unsigned>((p.r1 - p.r0 + 255) / 256), col_grid(p.c1 - p.c0), p.nquad);
     stream_update_kernel<<<grid, 256, 0, s>>>(p);
     return cudaGetLastError();
 }

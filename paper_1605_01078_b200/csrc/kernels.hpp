@@ -61,7 +61,7 @@ struct alignas(64) MMParams {
     int tiles_m, tiles_n, ktiles;
     int mode;
     int group_m;                // tile rasterisation group height
-    int tn0;                    // first tile column (column windows of the host pipeline)
+    int tm0, tn0;               // first tile row / column (windows of the host pipeline)
     int c_vec;                  // C column-major, even ldc, 16-byte aligned quadrants
     // split mode (few output tiles): blockIdx -> (tile, product, k-chunk); each
     // CTA stores its partial product to M_{p*ksplit+s} (kEpiStore)
@@ -94,7 +94,7 @@ struct SumBatchParams {
     int nterms[kMaxSumJobs];
     int njobs;
     long long rows, cols, ld;
-    long long c0;  // first column computed (cols = one past the last)
+    long long r0, c0;  // first row / column computed (rows, cols = one past the last)
 };
 cudaError_t launch_sum_batch(const SumBatchParams& p, cudaStream_t s);
 
@@ -113,7 +113,7 @@ struct StreamParams {
     int nquad;
     int qm, qn;
     int ksplit;  // M_p = sum_{s < ksplit} mbase[(p*ksplit + s) * mstride], s ascending
-    int c0, c1;  // quadrant-column window [c0, c1)
+    int r0, r1, c0, c1;  // quadrant window: rows [r0, r1), columns [c0, c1)
 };
 cudaError_t launch_stream_update(const StreamParams& p, cudaStream_t s);
 

@@ -276,13 +276,20 @@ def test_profiling_reports_each_launch(ctx):
     a, b, c0 = inputs(m, n, k, (71, 72, 73))
     c = S.Ctx()
     c.enable_profiling(True)
+    c.set_pipelining(False)  # one window: A sums, B sums, products, stream pass
     out = np.array(c0, order="F")
     c.gemm("naive", 2, 1.0, a, b, out)
     prof = c.last_profile()
     names = [p["kernel"] for p in prof]
-    assert names.count("mm_kernel") == 1 and "stream_update_kernel" in names
+    assert names == ["sum_batch_kernel", "sum_batch_kernel", "mm_kernel", "stream_update_kernel"]
     assert all(p["ms"] > 0 for p in prof)
     assert c.last_launches() == len(prof)
+    c.set_pipelining(True)  # windows: every launch still profiled and counted
+    c.gemm("naive", 2, 1.0, a, b, out)
+    prof = c.last_profile()
+    assert c.last_launches() == len(prof) and all(p["ms"] > 0 for p in prof)
+    names = [p["kernel"] for p in prof]
+    assert names.count("mm_kernel") == names.count("stream_update_kernel") >= 1
 
 
 def test_host_staging_overlap_each_variant_and_operand_kind(ctx):
@@ -302,19 +309,22 @@ def test_host_staging_overlap_each_variant_and_operand_kind(ctx):
             check(v, L, got, ref, c0, a, b)
 
 
-@pytest.mark.parametrize("v,L,m,n,k", [
-    ("naive", 2, 4096, 4096, 1024),   # 4 windows
-    ("c", 2, 4096, 4000, 768),        # last window partial, clipped quadrant columns
-    ("ab", 2, 4096, 4352, 512),
-    ("naive", 1, 4096, 6144, 640),
-    ("abc", 1, 10240, 10240, 256),    # RMW epilogue per window
-    ("dgemm", 0, 10240, 10240, 256),
-    ("naive", 2, 4097, 4099, 1030),   # ragged: peeled, windows fall back to whole-operand order
+@pytest.mark.parametrize("v,L,m,n,k,grid", [
+    ("naive", 2, 4096, 4096, 1024, None),   # planner's choice
+    ("naive", 2, 4096, 4000, 768, "3x4"),   # partial last windows, clipped quadrant columns
+    ("c", 2, 4096, 4352, 512, "2x3"),
+    ("ab", 2, 3968, 4096, 512, "4x1"),
+    ("naive", 1, 4096, 6144, 640, "1x4"),
+    ("abc", 1, 10240, 10240, 256, "2x3"),   # RMW epilogue per window
+    ("dgemm", 0, 10240, 10240, 256, None),
+    ("naive", 2, 4097, 4099, 1030, "2x2"),  # ragged: peeled, windows fall back to whole operands
 ])
-def test_host_pipeline_bitwise_equal_to_unpipelined(v, L, m, n, k):
-    """Host calls in column windows (strassen_ctx_set_pipelining) compute exactly the
-    unwindowed result; ldc > m exercises strided window spans."""
+def test_host_pipeline_bitwise_equal_to_unpipelined(monkeypatch, v, L, m, n, k, grid):
+    """Host calls in windows (strassen_ctx_set_pipelining) compute exactly the unwindowed
+    result; ldc > m exercises strided 2-D window copies."""
     import torch
+    if grid:
+        monkeypatch.setenv("STRASSEN_B200_WINDOWS", grid)
     g = torch.Generator().manual_seed(m + n + k)
     a = np.asfortranarray((torch.rand(m, k, dtype=torch.float64, generator=g) * 2 - 1).numpy())
     b = np.asfortranarray((torch.rand(k, n, dtype=torch.float64, generator=g) * 2 - 1).numpy())
