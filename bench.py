@@ -411,6 +411,16 @@ def main():
                        "d2h_bytes_per_step": 8 * m * n, "ms_per_step": dt * 1e3,
                        "api": "strassen_gemm (C ABI, pinned host pointers)"}
         line["gpu_launches"] += ctx.last_launches() * e2e_steps
+        # the link the e2e number rides on: pinned H2D / D2H of one operand (2 GiB at 16384)
+        dev = torch.empty_like(A)
+        for kind, (dst, src) in (("h2d_gbs", (dev, Ah)), ("d2h_gbs", (Ch, dev))):
+            dst.copy_(src, non_blocking=True)
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            dst.copy_(src, non_blocking=True)
+            torch.cuda.synchronize()
+            line["e2e"][kind] = 8 * A.numel() / (time.perf_counter() - t1) / 1e9
+        del dev
 
     if rank == 0 and world == 1 and not args.no_cpu:
         r = reference_cpu(args.cpu_sample, args.variant, args.level)

@@ -351,6 +351,7 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
     S.nquad = static_cast<int>(cq.size());
     S.qm = P.qm;
     S.qn = P.qn;
+    S.c_vec = P.c_vec;
     S.r0 = static_cast<int>(r0);
     S.r1 = static_cast<int>(r1);
     S.c0 = static_cast<int>(c0);

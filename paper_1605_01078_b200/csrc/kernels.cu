@@ -554,28 +554,37 @@ struct SumGatherParams {
 };
 constexpr int kGatherThreads = 128;
 
+__device__ __forceinline__ void gather_sources(const SumGatherParams& P, long long i, long long j,
+                                               double2 (&x)[kMaxQuad]) {
+#pragma unroll
+    for (int q = 0; q < kMaxQuad; ++q) {
+        x[q] = make_double2(0.0, 0.0);
+        if (q < P.nsrc && j < P.scols[q]) {
+            const double* px = P.src[q] + i + j * P.sld[q];
+            if (i + 1 < P.srows[q])
+                x[q] = *reinterpret_cast<const double2*>(px);
+            else if (i < P.srows[q])
+                x[q].x = *px;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kGatherThreads)
 sum_gather_kernel(const __grid_constant__ SumGatherParams P) {
     __shared__ double2 xs[kMaxQuad][kGatherThreads];  // 32 KB
     const int tid = threadIdx.x;
     const long long i = P.r0 + 2 * (static_cast<long long>(blockIdx.x) * kGatherThreads + tid);
-    if (i >= P.rows) return;
+    long long j = P.c0 + blockIdx.y;
+    if (i >= P.rows || j >= P.cols) return;
     const bool pair = i + 1 < P.rows;
-    for (long long j = P.c0 + blockIdx.y; j < P.cols; j += gridDim.y) {
+    // the next column's sources are loaded while this column's sums are formed
+    double2 nx[kMaxQuad];
+    gather_sources(P, i, j, nx);
+    for (; j < P.cols; j += gridDim.y) {
 #pragma unroll
-        for (int q = 0; q < kMaxQuad; ++q) {
-            if (q < P.nsrc) {
-                double2 x = make_double2(0.0, 0.0);
-                if (j < P.scols[q]) {
-                    const double* px = P.src[q] + i + j * P.sld[q];
-                    if (i + 1 < P.srows[q])
-                        x = *reinterpret_cast<const double2*>(px);
-                    else if (i < P.srows[q])
-                        x.x = *px;
-                }
-                xs[q][tid] = x;
-            }
-        }
+        for (int q = 0; q < kMaxQuad; ++q)
+            if (q < P.nsrc) xs[q][tid] = nx[q];
+        if (j + gridDim.y < P.cols) gather_sources(P, i, j + gridDim.y, nx);
         for (int z = 0; z < P.njobs; ++z) {
             const int n = P.nterms[z];
             const double c0 = P.tcoeff[z][0];
@@ -611,6 +620,7 @@ struct StreamGatherParams {
     double alpha;
     int qm, qn;
     int r0, r1, c0, c1;
+    int c_vec;
 };
 constexpr int kStreamThreads = 256;
 constexpr int kStreamBatch = 8;  // M loads in flight per thread
@@ -653,6 +663,71 @@ stream_gather_kernel(const __grid_constant__ StreamGatherParams P) {
         for (int q = 0; q < kMaxQuad; ++q)
             if (q < P.nquad && i < P.crows[q] && j < P.ccols[q])
                 P.cptr[q][i * P.rs_c + j * P.cs_c] = cs[q][tid];
+    }
+}
+
+// Row-pair form (C column-major with 16-byte aligned quadrants, even ldm):
+// 16-byte loads and stores, otherwise identical per element.
+constexpr int kStream2Threads = 128;
+
+__global__ void __launch_bounds__(kStream2Threads)
+stream_gather2_kernel(const __grid_constant__ StreamGatherParams P) {
+    __shared__ double2 cs[kMaxQuad][kStream2Threads];  // 32 KB
+    const int tid = threadIdx.x;
+    const long long i = P.r0 + 2 * (static_cast<long long>(blockIdx.x) * kStream2Threads + tid);
+    if (i >= P.r1) return;
+    for (long long j = P.c0 + blockIdx.y; j < P.c1; j += gridDim.y) {
+#pragma unroll
+        for (int q = 0; q < kMaxQuad; ++q)
+            if (q < P.nquad) {
+                double2 c = make_double2(0.0, 0.0);
+                if (j < P.ccols[q]) {
+                    const double* pc = P.cptr[q] + i + j * P.cs_c;
+                    if (i + 1 < P.crows[q])
+                        c = *reinterpret_cast<const double2*>(pc);
+                    else if (i < P.crows[q])
+                        c.x = *pc;
+                }
+                cs[q][tid] = c;
+            }
+        const double* Mij = P.mbase + i + j * P.ldm;
+        for (int p0 = 0; p0 < P.nprod; p0 += kStreamBatch) {
+            double2 v[kStreamBatch];
+#pragma unroll
+            for (int t = 0; t < kStreamBatch; ++t) {
+                if (p0 + t < P.nprod) {
+                    const double* M = Mij + static_cast<long long>(p0 + t) * P.ksplit * P.mstride;
+                    v[t] = *reinterpret_cast<const double2*>(M);
+                    for (int sp = 1; sp < P.ksplit; ++sp) {
+                        const double2 x = *reinterpret_cast<const double2*>(M + sp * P.mstride);
+                        v[t].x += x.x;
+                        v[t].y += x.y;
+                    }
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < kStreamBatch; ++t) {
+                if (p0 + t >= P.nprod) break;
+                const int nd = P.ndest[p0 + t];
+                for (int d = 0; d < nd; ++d) {
+                    const int q = P.dq[p0 + t][d];
+                    const double g = P.alpha * static_cast<double>(P.dcoeff[p0 + t][d]);
+                    double2 c = cs[q][tid];
+                    c.x = fma(g, v[t].x, c.x);
+                    c.y = fma(g, v[t].y, c.y);
+                    cs[q][tid] = c;
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kMaxQuad; ++q)
+            if (q < P.nquad && j < P.ccols[q]) {
+                double* pc = P.cptr[q] + i + j * P.cs_c;
+                if (i + 1 < P.crows[q])
+                    *reinterpret_cast<double2*>(pc) = cs[q][tid];
+                else if (i < P.crows[q])
+                    *pc = cs[q][tid].x;
+            }
     }
 }
 
@@ -793,6 +868,7 @@ static bool to_gather(const StreamParams& p, StreamGatherParams& g) {
     g.r1 = p.r1;
     g.c0 = p.c0;
     g.c1 = p.c1;
+    g.c_vec = p.c_vec;
     return true;
 }
 
@@ -800,6 +876,13 @@ cudaError_t launch_stream_update(const StreamParams& p, cudaStream_t s) {
     static thread_local StreamGatherParams g;
     if (to_gather(p, g)) {
         const int w = p.c1 - p.c0;
+        if (p.c_vec && p.ldm % 2 == 0 && p.mstride % 2 == 0) {  // 16-byte rows pairs
+            dim3 grid(static_cast<unsigned>(((p.r1 - p.r0 + 1) / 2 + kStream2Threads - 1) /
+                                            kStream2Threads),
+                      static_cast<unsigned>(w < 4096 ? w : 4096));
+            stream_gather2_kernel<<<grid, kStream2Threads, 0, s>>>(g);
+            return cudaGetLastError();
+        }
         dim3 grid(static_cast<unsigned>((p.r1 - p.r0 + kStreamThreads - 1) / kStreamThreads),
                   static_cast<unsigned>(w < 4096 ? w : 4096));
         stream_gather_kernel<<<grid, kStreamThreads, 0, s>>>(g);

@@ -114,6 +114,7 @@ struct StreamParams {
     int qm, qn;
     int ksplit;  // M_p = sum_{s < ksplit} mbase[(p*ksplit + s) * mstride], s ascending
     int r0, r1, c0, c1;  // quadrant window: rows [r0, r1), columns [c0, c1)
+    int c_vec;           // C column-major, even ldc, 16-byte aligned quadrants
 };
 cudaError_t launch_stream_update(const StreamParams& p, cudaStream_t s);
 
