@@ -548,6 +548,8 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
     P.tiles_n = static_cast<int>(ceil_div(qn, kBN));
     P.ktiles = static_cast<int>(ceil_div(qk, kBK));
     P.group_m = 8;
+    if (const char* g = std::getenv("STRASSEN_B200_GROUP_M"))  // rasterisation experiments
+        P.group_m = std::max(1, std::atoi(g));
 
     // Live products in table order (variants.cpp:130-133 skip rule).
     struct Live {
@@ -668,6 +670,16 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
             }
         }
     }
+
+    // First A and B terms at +1 (kernels.cu product_kloop): a side whose first
+    // coefficient is -1 is negated as a whole, and so are the destination
+    // coefficients.  Exact: (-S) x T = -(S x T) bit for bit under round-to-nearest.
+    for (Live& l : live)
+        for (Terms* t : {&l.a, &l.b})
+            if (t->front().second < 0) {
+                for (auto& x : *t) x.second = -x.second;
+                for (auto& x : l.c) x.second = -x.second;
+            }
 
     P.nprod = static_cast<int>(live.size());
     std::vector<Terms> dests;

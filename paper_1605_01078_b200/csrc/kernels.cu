@@ -160,6 +160,65 @@ __device__ __forceinline__ void dmma_substep(const Frags& f, int ss, double (&ac
             dmma(acc[mf][nf][0], acc[mf][nf][1], f.a[ss][mf], f.b[ss][nf]);
 }
 
+// One product's k-loop with compile-time term counts (NA, NB): no branches
+// inside a k-step, so ptxas can overlap the operand loads and sums of the next
+// substep pair with the DMMAs of the current one.  The host normalises every
+// product so its first A and B terms have coefficient +1 (negating the other
+// terms and the destination coefficients instead: exact, round-to-nearest is
+// sign-symmetric), so the first term is a plain load.
+template <int NA, int NB>
+__device__ __forceinline__ void product_kloop(const uint8_t* raw, uint64_t* raw_full,
+                                              uint64_t* raw_empty, uint32_t& slot,
+                                              uint32_t& phase, int kt_lo, int kt_hi,
+                                              const ProductDesc& pd, int wm, int wn, int g,
+                                              int j, int lane, double (&acc)[8][4][2]) {
+    double ca[NA], cb[NB];
+#pragma unroll
+    for (int u = 0; u < NA; ++u) ca[u] = static_cast<double>(pd.as[u]);
+#pragma unroll
+    for (int u = 0; u < NB; ++u) cb[u] = static_cast<double>(pd.bs[u]);
+    for (int kt = kt_lo; kt < kt_hi; ++kt) {
+        const uint8_t* sA[NA];
+        const uint8_t* sB[NB];
+        const uint32_t slot0 = slot;
+#pragma unroll
+        for (int u = 0; u < NA + NB; ++u) {
+            uint32_t su = slot0 + u;
+            const uint32_t pu = (su >= kRawSlots) ? phase ^ 1 : phase;
+            su = (su >= kRawSlots) ? su - kRawSlots : su;
+            if (u < NA) sA[u] = raw + su * kSlotBytes;
+            else sB[u - NA] = raw + su * kSlotBytes;
+            mbar_wait(&raw_full[su], pu);
+        }
+        slot += NA + NB;
+        if (slot >= kRawSlots) {
+            slot -= kRawSlots;
+            phase ^= 1;
+        }
+#pragma unroll
+        for (int sp = 0; sp < 2; ++sp) {
+            Frags f;
+            frag_a_term<true>(sA[0], sp, wm, g, j, 1.0, f);
+            frag_b_term<true>(sB[0], sp, wn, g, j, 1.0, f);
+#pragma unroll
+            for (int u = 1; u < NA; ++u) frag_a_term<false>(sA[u], sp, wm, g, j, ca[u], f);
+#pragma unroll
+            for (int u = 1; u < NB; ++u) frag_b_term<false>(sB[u], sp, wn, g, j, cb[u], f);
+            dmma_substep(f, 0, acc);
+            dmma_substep(f, 1, acc);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            uint32_t s2 = slot0;
+#pragma unroll
+            for (int u = 0; u < NA + NB; ++u) {
+                mbar_arrive(&raw_empty[s2]);
+                if (++s2 == kRawSlots) s2 = 0;
+            }
+        }
+    }
+}
+
 template <int MAXT>
 __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__ MMParams P) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -264,6 +323,42 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
 #pragma unroll
             for (int nf = 0; nf < 4; ++nf) acc[mf][nf][0] = acc[mf][nf][1] = 0.0;
 
+        // compile-time term counts for the combinations the tables produce
+        // (1, 2 or 4 terms per side); anything else (clipped quadrants drop
+        // terms) takes the generic loop
+        const int combo = na * 8 + nb;
+        bool done = true;
+        if (combo == 9) {
+            product_kloop<1, 1>(raw, raw_full, raw_empty, slot, phase, kt_lo, kt_hi, pd, wm, wn,
+                                g, j, lane, acc);
+        } else if (MAXT >= 2 && combo == 10) {
+            product_kloop<1, (MAXT >= 2 ? 2 : 1)>(raw, raw_full, raw_empty, slot, phase, kt_lo,
+                                                  kt_hi, pd, wm, wn, g, j, lane, acc);
+        } else if (MAXT >= 2 && combo == 17) {
+            product_kloop<(MAXT >= 2 ? 2 : 1), 1>(raw, raw_full, raw_empty, slot, phase, kt_lo,
+                                                  kt_hi, pd, wm, wn, g, j, lane, acc);
+        } else if (MAXT >= 2 && combo == 18) {
+            product_kloop<(MAXT >= 2 ? 2 : 1), (MAXT >= 2 ? 2 : 1)>(
+                raw, raw_full, raw_empty, slot, phase, kt_lo, kt_hi, pd, wm, wn, g, j, lane, acc);
+        } else if (MAXT >= 4 && combo == 12) {
+            product_kloop<1, (MAXT >= 4 ? 4 : 1)>(raw, raw_full, raw_empty, slot, phase, kt_lo,
+                                                  kt_hi, pd, wm, wn, g, j, lane, acc);
+        } else if (MAXT >= 4 && combo == 33) {
+            product_kloop<(MAXT >= 4 ? 4 : 1), 1>(raw, raw_full, raw_empty, slot, phase, kt_lo,
+                                                  kt_hi, pd, wm, wn, g, j, lane, acc);
+        } else if (MAXT >= 4 && combo == 20) {
+            product_kloop<(MAXT >= 4 ? 2 : 1), (MAXT >= 4 ? 4 : 1)>(
+                raw, raw_full, raw_empty, slot, phase, kt_lo, kt_hi, pd, wm, wn, g, j, lane, acc);
+        } else if (MAXT >= 4 && combo == 34) {
+            product_kloop<(MAXT >= 4 ? 4 : 1), (MAXT >= 4 ? 2 : 1)>(
+                raw, raw_full, raw_empty, slot, phase, kt_lo, kt_hi, pd, wm, wn, g, j, lane, acc);
+        } else if (MAXT >= 4 && combo == 36) {
+            product_kloop<(MAXT >= 4 ? 4 : 1), (MAXT >= 4 ? 4 : 1)>(
+                raw, raw_full, raw_empty, slot, phase, kt_lo, kt_hi, pd, wm, wn, g, j, lane, acc);
+        } else {
+            done = false;
+        }
+        if (!done)
         for (int kt = kt_lo; kt < kt_hi; ++kt) {
             // term tiles of this k-step: A terms, then B terms, in ring order
             // (a k-step uses at most 2*MAXT <= 8 < kRawSlots slots: one wrap at most)
