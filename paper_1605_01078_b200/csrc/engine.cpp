@@ -45,8 +45,9 @@ EncodeFn encode_fn() {
 }
 
 // Column-major (rows x cols, leading dimension ld) fp64 tensor map.
+// swizzle_bytes: 128 (boxes of 128-byte rows), 64 (B half tiles) or 0.
 void encode_map(CUtensorMap* map, const double* base, long rows, long cols, long long ld,
-                uint32_t box0, uint32_t box1, bool swizzle128) {
+                uint32_t box0, uint32_t box1, int swizzle_bytes) {
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(cols)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 8};
     cuuint32_t box[2] = {box0, box1};
@@ -54,7 +55,9 @@ void encode_map(CUtensorMap* map, const double* base, long rows, long cols, long
     CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
                              const_cast<double*>(base), dims, strides, box, estr,
                              CU_TENSOR_MAP_INTERLEAVE_NONE,
-                             swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                             swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                             : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                   : CU_TENSOR_MAP_SWIZZLE_NONE,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw Error(STRASSEN_ERR_DEVICE, "cuTensorMapEncodeTiled failed");
@@ -156,6 +159,9 @@ void fill_desc(ProductDesc& d, const Terms& a, const Terms& b, const Terms& c) {
     d.na = static_cast<int8_t>(a.size());
     d.nb = static_cast<int8_t>(b.size());
     d.nc = static_cast<int8_t>(c.size());
+    // 4 + 4 terms: stream 8-k half tiles (kernels.cu product_kloop_half; measured
+    // slower for 4 + 2, whose 16-k steps already leave the ring 8 slots ahead)
+    d.half = (a.size() == 4 && b.size() == 4) ? 1 : 0;
     for (size_t u = 0; u < a.size(); ++u) {
         d.aq[u] = static_cast<int8_t>(a[u].first);
         d.as[u] = static_cast<int8_t>(a[u].second);
@@ -524,10 +530,16 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
             const int qi = I * side + J;
             if (a_live[qi])
                 encode_map(&P.tmA[qi], quad_origin(ta, I, J), quad_rows(ta, I), quad_cols(ta, J),
-                           ta.ld, 16, kBK, true);
+                           ta.ld, 16, kBK, 128);
             if (b_live[qi])
                 encode_map(&P.tmB[qi], quad_origin(tb, I, J), quad_rows(tb, I), quad_cols(tb, J),
-                           tb.ld, kBK, kBN, true);
+                           tb.ld, kBK, kBN, 128);
+            if (L == 2 && a_live[qi])  // half-k maps for the (4,4) products
+                encode_map(&P.tmAh[qi], quad_origin(ta, I, J), quad_rows(ta, I),
+                           quad_cols(ta, J), ta.ld, 16, kBK / 2, 128);
+            if (L == 2 && b_live[qi])
+                encode_map(&P.tmBh[qi], quad_origin(tb, I, J), quad_rows(tb, I),
+                           quad_cols(tb, J), tb.ld, kBK / 2, kBN, 64);
             P.cptr[qi] = cq[qi].p;
             P.crows[qi] = static_cast<int>(cq[qi].rows);
             P.ccols[qi] = static_cast<int>(cq[qi].cols);
@@ -663,9 +675,9 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
                 const int mi = next_map++;
                 if (mi >= kMaxMaps) throw Error(STRASSEN_ERR_PARAM, "too many operand maps");
                 if (sd == 0)
-                    encode_map(&P.tmA[mi], dst, qm, qk, lda_t, 16, kBK, true);
+                    encode_map(&P.tmA[mi], dst, qm, qk, lda_t, 16, kBK, 128);
                 else
-                    encode_map(&P.tmB[mi], dst, qk, qn, ldb_t, kBK, kBN, true);
+                    encode_map(&P.tmB[mi], dst, qk, qn, ldb_t, kBK, kBN, 128);
                 terms = {{mi, 1}};
             }
         }

@@ -46,6 +46,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Predicated arrive: no branch, so the caller's instruction stream stays one
+// basic block (ptxas can overlap the work on either side).
+__device__ __forceinline__ void mbar_arrive_if(uint64_t* bar, bool pred) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %1, 0;\n"
+        "@p mbarrier.arrive.shared::cta.b64 _, [%0];\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(static_cast<int>(pred))
+        : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n"
@@ -160,6 +173,133 @@ __device__ __forceinline__ void dmma_substep(const Frags& f, int ss, double (&ac
             dmma(acc[mf][nf][0], acc[mf][nf][1], f.a[ss][mf], f.b[ss][nf]);
 }
 
+// ---- half-k tiles (ProductDesc::half: products with 4 + 4 terms) ----------
+// A (4,4) product needs 8 term tiles per 16-k step; with 16-k tiles the ring
+// could prefetch only a fraction of the next step, exposing TMA latency.  Such
+// products stream 8-k half tiles instead, two per 16 KB slot (term u at slot
+// u/2, byte offset (u%2)*8 KB), so the ring holds 3.5 steps.
+// A half tile (128 m x 8 k): 8 boxes {16 m, 8 k}, 128-byte swizzle: (m, k) at
+// (m/16)*1024 + k*128 + (((m%16)/2 ^ k) << 4) + (m%2)*8.
+// B half tile (8 k x 128 n): one box {8 k, 128 n}, 64-byte swizzle: (k, n) at
+// n*64 + (((k/2) ^ (n/2)%4) << 4) + (k%2)*8.
+// Lane (g, j) feeds k = 2j + ss in both (the same k order as the 16-k path:
+// bitwise-identical sums), A rows as in the 16-k path, and B column g
+// (identity column map; the epilogue uses the matching accumulator columns).
+// Both are conflict-free: per quarter-warp, A chunks g ^ k are 8 distinct,
+// B lanes cover the two 64-byte halves (n parity) x 4 chunks.
+constexpr int kHalfBytes = kSlotBytes / 2;
+
+template <bool FIRST>
+__device__ __forceinline__ void frag_a_half(const uint8_t* sA, int wm, int g, int j, double c,
+                                            Frags& f) {
+#pragma unroll
+    for (int ss = 0; ss < 2; ++ss) {
+        const int k = 2 * j + ss;
+        const uint8_t* pa = sA + (wm * 4) * 1024 + k * 128 + ((g ^ k) << 4);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            const double2 v = *reinterpret_cast<const double2*>(pa + h * 1024);
+            if (FIRST) {
+                f.a[ss][2 * h] = v.x;
+                f.a[ss][2 * h + 1] = v.y;
+            } else {
+                f.a[ss][2 * h] = fma(c, v.x, f.a[ss][2 * h]);
+                f.a[ss][2 * h + 1] = fma(c, v.y, f.a[ss][2 * h + 1]);
+            }
+        }
+    }
+}
+template <bool FIRST>
+__device__ __forceinline__ void frag_b_half(const uint8_t* sB, int wn, int g, int j, double c,
+                                            Frags& f) {
+    const uint8_t* pb = sB + (wn * 32 + g) * 64 + ((j ^ ((g >> 1) & 3)) << 4);
+#pragma unroll
+    for (int nf = 0; nf < 4; ++nf) {
+        const double2 v = *reinterpret_cast<const double2*>(pb + nf * 8 * 64);
+        if (FIRST) {
+            f.b[0][nf] = v.x;
+            f.b[1][nf] = v.y;
+        } else {
+            f.b[0][nf] = fma(c, v.x, f.b[0][nf]);
+            f.b[1][nf] = fma(c, v.y, f.b[1][nf]);
+        }
+    }
+}
+
+// Half tiles of one 8-k step: term u (A terms first) in slot slot0 + u/2.
+template <int NT>
+struct HalfStep {
+    const uint8_t* t[NT];
+    uint32_t slot0;
+};
+
+template <int NT>
+__device__ __forceinline__ void half_acquire(const uint8_t* raw, uint64_t* raw_full,
+                                             uint32_t& slot, uint32_t& phase, HalfStep<NT>& hs) {
+    constexpr int kSlots = (NT + 1) / 2;
+    hs.slot0 = slot;
+#pragma unroll
+    for (int v = 0; v < kSlots; ++v) {
+        uint32_t sv = slot + v;
+        const uint32_t pv = (sv >= kRawSlots) ? phase ^ 1 : phase;
+        sv = (sv >= kRawSlots) ? sv - kRawSlots : sv;
+        hs.t[2 * v] = raw + sv * kSlotBytes;
+        if (2 * v + 1 < NT) hs.t[2 * v + 1] = raw + sv * kSlotBytes + kHalfBytes;
+        mbar_wait(&raw_full[sv], pv);
+    }
+    slot += kSlots;
+    if (slot >= kRawSlots) {
+        slot -= kRawSlots;
+        phase ^= 1;
+    }
+}
+
+template <int NT>
+__device__ __forceinline__ void half_release(uint64_t* raw_empty, const HalfStep<NT>& hs,
+                                             int lane) {
+    __syncwarp();
+    uint32_t s2 = hs.slot0;
+#pragma unroll
+    for (int v = 0; v < (NT + 1) / 2; ++v) {
+        mbar_arrive_if(&raw_empty[s2], lane == 0);  // predicated: no branch
+        s2 = (s2 + 1 == kRawSlots) ? 0 : s2 + 1;
+    }
+}
+
+// One product's k-loop over half tiles: two 8-k steps per 16-k tile (both
+// waits first, then one straight-line block that returns the first step's
+// slots as soon as it is done).  kt_lo / kt_hi count 16-k tiles.
+template <int NA, int NB>
+__device__ __forceinline__ void product_kloop_half(const uint8_t* raw, uint64_t* raw_full,
+                                                   uint64_t* raw_empty, uint32_t& slot,
+                                                   uint32_t& phase, int kt_lo, int kt_hi,
+                                                   const ProductDesc& pd, int wm, int wn, int g,
+                                                   int j, int lane, double (&acc)[8][4][2]) {
+    double ca[NA], cb[NB];
+#pragma unroll
+    for (int u = 0; u < NA; ++u) ca[u] = static_cast<double>(pd.as[u]);
+#pragma unroll
+    for (int u = 0; u < NB; ++u) cb[u] = static_cast<double>(pd.bs[u]);
+    for (int kt = kt_lo; kt < kt_hi; ++kt) {
+        HalfStep<NA + NB> h[2];
+        half_acquire(raw, raw_full, slot, phase, h[0]);
+        half_acquire(raw, raw_full, slot, phase, h[1]);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            Frags f;
+            frag_a_half<true>(h[e].t[0], wm, g, j, 1.0, f);
+            frag_b_half<true>(h[e].t[NA], wn, g, j, 1.0, f);
+#pragma unroll
+            for (int u = 1; u < NA; ++u) frag_a_half<false>(h[e].t[u], wm, g, j, ca[u], f);
+#pragma unroll
+            for (int u = 1; u < NB; ++u) frag_b_half<false>(h[e].t[NA + u], wn, g, j, cb[u], f);
+            dmma_substep(f, 0, acc);
+            dmma_substep(f, 1, acc);
+            half_release(raw_empty, h[e], lane);  // first half's slots back mid-tile
+        }
+    }
+}
+
 // One product's k-loop with compile-time term counts (NA, NB): no branches
 // inside a k-step, so ptxas can overlap the operand loads and sums of the next
 // substep pair with the DMMAs of the current one.  The host normalises every
@@ -270,6 +410,35 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         const int m0 = tm * kBM, n0 = tn * kBN;
         for (int p = p_lo; p < p_hi; ++p) {
             const ProductDesc& pd = P.prod[p];
+            if (pd.half) {
+                // 8-k half tiles, two terms per slot (A terms first, then B)
+                const int nt = pd.na + pd.nb;
+                for (int kh = 2 * kt_lo; kh < 2 * kt_hi; ++kh) {
+                    const int k0 = kh * (kBK / 2);
+                    for (int u = 0; u < nt; u += 2) {
+                        mbar_wait(&raw_empty[s], phase ^ 1);
+                        mbar_expect_tx(&raw_full[s], (u + 1 < nt ? 2 : 1) * kHalfBytes);
+                        for (int e = 0; e < 2 && u + e < nt; ++e) {
+                            uint8_t* dst = raw + s * kSlotBytes + e * kHalfBytes;
+                            const int t = u + e;
+                            if (t < pd.na) {
+                                const CUtensorMap* map = &P.tmAh[pd.aq[t]];
+#pragma unroll
+                                for (int box = 0; box < kBM / 16; ++box)
+                                    tma_load_2d(dst + box * 1024, map, m0 + 16 * box, k0,
+                                                &raw_full[s]);
+                            } else {
+                                tma_load_2d(dst, &P.tmBh[pd.bq[t - pd.na]], k0, n0, &raw_full[s]);
+                            }
+                        }
+                        if (++s == kRawSlots) {
+                            s = 0;
+                            phase ^= 1;
+                        }
+                    }
+                }
+                continue;
+            }
             for (int kt = kt_lo; kt < kt_hi; ++kt) {
                 const int k0 = kt * kBK;
                 for (int u = 0; u < pd.na + pd.nb; ++u) {
@@ -352,6 +521,9 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         } else if (MAXT >= 4 && combo == 34) {
             product_kloop<(MAXT >= 4 ? 4 : 1), (MAXT >= 4 ? 2 : 1)>(
                 raw, raw_full, raw_empty, slot, phase, kt_lo, kt_hi, pd, wm, wn, g, j, lane, acc);
+        } else if (MAXT >= 4 && combo == 36 && pd.half) {
+            product_kloop_half<(MAXT >= 4 ? 4 : 1), (MAXT >= 4 ? 4 : 1)>(
+                raw, raw_full, raw_empty, slot, phase, kt_lo, kt_hi, pd, wm, wn, g, j, lane, acc);
         } else if (MAXT >= 4 && combo == 36) {
             product_kloop<(MAXT >= 4 ? 4 : 1), (MAXT >= 4 ? 4 : 1)>(
                 raw, raw_full, raw_empty, slot, phase, kt_lo, kt_hi, pd, wm, wn, g, j, lane, acc);
@@ -422,7 +594,8 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         // warp's 64 x 32 tile.
         const int mrow0 = tm * kBM + wm * 64 + 2 * g;
         const int ncol0 = tn * kBN + wn * 32;
-        const int c0 = nperm(2 * j), c1 = nperm(2 * j + 1);
+        // (half-tile products map B columns without the permutation)
+        const int c0 = pd.half ? 2 * j : nperm(2 * j), c1 = pd.half ? 2 * j + 1 : nperm(2 * j + 1);
         if (P.mode == kEpiRMW) {
             // 16-byte path: C column-major with rows (2g, 2g+1) of the fragment
             // pair (2h, 2h+1) adjacent and 16-byte aligned (checked on the host)

@@ -19,7 +19,7 @@ constexpr int kMaxTerms = 4;        // operand terms / destinations per product 
 constexpr int kConsumerWarps = 8;   // 2 warpgroups; 2 (m) x 4 (n) warps of 64 x 32
 constexpr int kThreads = 128 + kConsumerWarps * 32;  // 384: + TMA warpgroup (1 active warp)
 constexpr int kSlotBytes = kBM * kBK * 8;            // one 128x16 fp64 operand tile (16 KB)
-constexpr int kRawSlots = 13;                        // TMA ring of operand-term tiles (208 KB)
+constexpr int kRawSlots = 14;                        // TMA ring of operand-term tiles (224 KB)
 constexpr int kProducerRegs = 24;                    // setmaxnreg split
 constexpr int kConsumerRegs = 240;
 // setmaxnreg moves registers inside the CTA's launch allocation (384 threads x
@@ -33,7 +33,8 @@ static_assert(kMMSmemBytes <= 227 * 1024, "shared memory budget");
 // One Strassen product M_p = (sum_u as_u A_{aq_u}) (sum_u bs_u B_{bq_u});
 // destinations C_{cq_u} += alpha * cs_u * M_p.
 struct ProductDesc {
-    int8_t na, nb, nc, pad;
+    int8_t na, nb, nc;
+    int8_t half;  // stream 8-k half tiles, two per ring slot (4 + 4-term products)
     int8_t aq[kMaxTerms], as[kMaxTerms];
     int8_t bq[kMaxTerms], bs[kMaxTerms];
     int8_t cq[kMaxTerms], cs[kMaxTerms];
@@ -47,6 +48,10 @@ enum EpilogueMode : int {
 struct alignas(64) MMParams {
     CUtensorMap tmA[kMaxMaps];  // A operands: dims (rows, cols), box 16 x 16, swizzle 128B
     CUtensorMap tmB[kMaxMaps];  // B operands: dims (k rows, n cols), box 16 x 128, swizzle 128B
+    // half-k maps of the 16 quadrants for ProductDesc::half products:
+    // A box 16 x 8 (128B swizzle), B box 8 x 128 (64B swizzle)
+    CUtensorMap tmAh[kMaxQuad];
+    CUtensorMap tmBh[kMaxQuad];
     ProductDesc prod[kMaxProducts];
     double* cptr[kMaxQuad];     // C quadrant views (clipped)
     int crows[kMaxQuad];
