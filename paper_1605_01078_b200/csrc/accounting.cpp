@@ -16,6 +16,7 @@
 #include <cmath>
 #include <stdexcept>
 
+#include "plan.hpp"
 #include "table.hpp"
 
 namespace sb200 {
@@ -293,9 +294,11 @@ double b200_predict_seconds(strassen_variant v, int level, long m, long n, long 
     const bool split = tiles < 2.0 * sms;
     double ctas = (per_product_grid || split) ? tiles * mul : tiles;
     double ks = 1;
-    if (split) {  // k-chunks as engine.cpp launch_fused picks them
-        const double ktiles = std::ceil(qk / 16.0);
-        while (tiles * mul * ks < 4.0 * sms && std::floor(ktiles / (ks + 1)) >= 4) ks += 1;
+    if (per_product_grid || split) {  // k-chunks as engine.cpp plan_fused picks them
+        const double terms = (v == STRASSEN_ABC || v == STRASSEN_AB) ? (L == 1 ? 1.71 : 2.94) : 1.0;
+        ks = choose_ksplit(static_cast<long>(tiles), static_cast<long>(mul),
+                           static_cast<long>(std::ceil(qk / 16.0)), sms, qm * qn,
+                           1.0 + 0.15 * (terms - 1.0), nullptr);
         ctas *= ks;
     }
     // per-CTA fixed cost (barrier init, pipeline fill, epilogue): ~4 us per wave

@@ -11,6 +11,7 @@
 #include <cstdlib>
 
 #include "kernels.hpp"
+#include "plan.hpp"
 #include "table.hpp"
 
 namespace sb200 {
@@ -304,11 +305,13 @@ FusedPlan plan_fused(Engine& e, const MMParams& P, bool force_split) {
     const int ntiles = P.tiles_m * P.tiles_n;
     const int sms = e.num_sms > 0 ? e.num_sms : 148;
     if (ntiles >= 2 * sms && !force_split) return F;
-    int ksplit = 1;
-    const long base = static_cast<long>(ntiles) * P.nprod;
-    while (base * ksplit < 4L * sms && P.ktiles / (ksplit + 1) >= 4) ++ksplit;
-    F.per = (P.ktiles + ksplit - 1) / ksplit;
-    F.ksplit = (P.ktiles + F.per - 1) / F.per;
+    double terms = 0.0;  // mean operand terms per side: fused sums lengthen a k-tile
+    for (int p = 0; p < P.nprod; ++p) terms += 0.5 * (P.prod[p].na + P.prod[p].nb);
+    terms /= P.nprod > 0 ? P.nprod : 1;
+    long per = P.ktiles;
+    F.ksplit = choose_ksplit(ntiles, P.nprod, P.ktiles, sms,
+                             static_cast<double>(P.qm) * P.qn, 1.0 + 0.15 * (terms - 1.0), &per);
+    F.per = static_cast<int>(per);
     F.split = true;
     F.ldm = (P.qm + 1) / 2 * 2;  // even: 16-B stores
     F.mstride = F.ldm * P.qn;

@@ -59,6 +59,16 @@ __device__ __forceinline__ void mbar_arrive_if(uint64_t* bar, bool pred) {
         : "memory");
 }
 
+// Consumer side of a ring slot hand-back.  The slot was read with generic-proxy
+// LDS; the producer refills it with TMA (async proxy).  Every lane fences its
+// reads against the async proxy before lane 0 arrives -- without it ptxas may
+// issue the arrive while this k-step's last LDS are still in flight (it hoists
+// the predicated arrive above the trailing DMMAs), and a refill can then race
+// the read.
+__device__ __forceinline__ void consumer_fence() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n"
@@ -257,6 +267,7 @@ __device__ __forceinline__ void half_acquire(const uint8_t* raw, uint64_t* raw_f
 template <int NT>
 __device__ __forceinline__ void half_release(uint64_t* raw_empty, const HalfStep<NT>& hs,
                                              int lane) {
+    consumer_fence();
     __syncwarp();
     uint32_t s2 = hs.slot0;
 #pragma unroll
@@ -347,6 +358,7 @@ __device__ __forceinline__ void product_kloop(const uint8_t* raw, uint64_t* raw_
             dmma_substep(f, 0, acc);
             dmma_substep(f, 1, acc);
         }
+        consumer_fence();
         __syncwarp();
         if (lane == 0) {
             uint32_t s2 = slot0;
@@ -579,6 +591,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                 dmma_substep(f, 0, acc);
                 dmma_substep(f, 1, acc);
             }
+            consumer_fence();
             __syncwarp();
             if (lane == 0) {
                 uint32_t s2 = slot0;
@@ -1032,7 +1045,7 @@ cudaError_t launch_mm(const MMParams& p, cudaStream_t s) {
         maxt = p.prod[i].na > maxt ? p.prod[i].na : maxt;
         maxt = p.prod[i].nb > maxt ? p.prod[i].nb : maxt;
     }
-    if (maxt == 1) return launch_mm_t<1>(p, s);  // single-term programs: no sum code at all
+    if (maxt == 1) return launch_mm_t<1>(p, s);  // single-term programs: no sum code at all  // single-term programs: no sum code at all
     return maxt <= 2 ? launch_mm_t<2>(p, s) : launch_mm_t<kMaxTerms>(p, s);
 }
 

@@ -346,3 +346,35 @@ def test_host_pipeline_bitwise_equal_to_unpipelined(monkeypatch, v, L, m, n, k, 
     S.Ctx().gemm(v, L, 1.0, torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), C0)
     assert np.array_equal(C0.cpu().numpy(), outs[0]), (v, L)
     assert freivalds(1.0, a, b, c0, outs[0]) < 1e-14
+
+
+@pytest.mark.parametrize("dim,configs", [
+    (5120, [("abc", 1), ("ab", 1), ("naive", 1), ("c", 1), ("dgemm", 0)]),
+    (9216, [("abc", 2), ("ab", 2), ("naive", 2), ("c", 2)]),
+])
+def test_tile_ownership_mode_every_variant_repeated(dim, configs):
+    """Sizes with >= 2 waves of output tiles run the tile-ownership (RMW) epilogue, where a
+    CTA walks every product of its tile; repeated runs catch ring-slot races (a released
+    slot refilled while its last fragment loads were in flight corrupted whole 16-row
+    fragment bands of the C variant). Checked against cuBLAS on the same inputs."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(dim)
+    A = (torch.rand(dim, dim, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    B = (torch.rand(dim, dim, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    C0 = (torch.rand(dim, dim, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    ref = C0 + A @ B
+    den = (torch.linalg.norm(A) * torch.linalg.norm(B)).item()
+    ctx = S.Ctx()
+    for v, L in configs:
+        first = None
+        for rep in range(3):
+            C = C0.clone().t().contiguous().t()
+            ctx.gemm_device(v, L, 1.0, A, B, C)
+            torch.cuda.synchronize()
+            nw = (torch.linalg.norm(C - ref) / den).item()
+            assert nw <= (5e-12 if L == 2 else 1e-12), (v, L, rep, nw)
+            if first is None:
+                first = C.clone()
+            else:
+                assert torch.equal(C, first), (v, L, rep)  # run-to-run bitwise
+    ctx.close()
