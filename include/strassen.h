@@ -213,6 +213,11 @@ strassen_status strassen_ctx_workspace_bytes(const strassen_ctx* ctx, long* out)
  * PAPER.md:894-895): the variant and level a B200 cost model, fitted to the
  * measured kernel efficiencies, predicts fastest for an m x n x k multiply,
  * and the predicted seconds (may be NULL).  No device needed. */
+/* The B200 cost model's predicted seconds for one configuration on this
+ * device (the quantity strassen_select minimises). */
+strassen_status strassen_predict_b200(strassen_variant variant, int level, long m, long n, long k,
+                                      double* seconds_out);
+
 strassen_status strassen_select(long m, long n, long k, strassen_variant* variant_out,
                                 int* level_out, double* seconds_out);
 

@@ -123,6 +123,7 @@ def _declare(lib):
         "strassen_ctx_set_pipelining": (_ST, [vp, C.c_int]),
         "strassen_ctx_last_profile": (_ST, [vp, C.c_char_p, _L]),
         "strassen_select": (_ST, [_L, _L, _L, C.POINTER(C.c_int), C.POINTER(C.c_int), _dp]),
+        "strassen_predict_b200": (_ST, [C.c_int, C.c_int, _L, _L, _L, _dp]),
         "strassen_build_info": (C.c_char_p, []),
         "strassen_last_error": (C.c_char_p, []),
     }
@@ -391,6 +392,14 @@ def predicted_counters(variant, level, m, n, k, blocking=None):
     _check(lib().strassen_count_call(_variant(variant), int(level), m, n, k, C.byref(bp),
                                      C.byref(c)), "count_call")
     return {f: getattr(c, f) for f in COUNTER_FIELDS}
+
+
+def predict_b200(variant, level, m, n, k):
+    """The B200 cost model's predicted seconds for one configuration."""
+    t = C.c_double()
+    _check(lib().strassen_predict_b200(_variant(variant), level, m, n, k, C.byref(t)),
+           "predict_b200")
+    return t.value
 
 
 def select(m, n, k):

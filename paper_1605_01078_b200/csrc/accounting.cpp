@@ -279,17 +279,20 @@ double waves_eff(double ctas, double sms) {
 }
 }  // namespace
 
-double b200_predict_seconds(strassen_variant v, int level, long m, long n, long k, int sms) {
+static double predict_core(strassen_variant v, int L, long m, long n, long k, int sms) {
     const double P = 37.05e12, BW = 5.5e12, launch = 6e-6;
-    const int L = (v == STRASSEN_DGEMM) ? 0 : level;
     const long S = 1L << L;
     const double qm = static_cast<double>(ceil_div(m, S)), qn = static_cast<double>(ceil_div(n, S)),
                  qk = static_cast<double>(ceil_div(k, S));
     static const double tc[3][4] = {{1, 0, 0, 1}, {7, 5, 5, 12}, {49, 95, 95, 144}};
-    const double mul = tc[L][0], aa = tc[L][1], ba = tc[L][2], cu = tc[L][3];
+    static const double n_sums[3] = {0, 5, 45};  // multi-term operand sums per side
+    const double mul = tc[L][0], cu = tc[L][3];
     const double tiles = std::ceil(qm / 128.0) * std::ceil(qn / 128.0);
-    double e_mm = 0.96;
-    if (v == STRASSEN_ABC || v == STRASSEN_AB) e_mm = (L == 1) ? 0.86 : 0.62;
+    // mm_kernel efficiency (executed flops / DMMA peak) measured at 16384^3:
+    // single-term 0.976; fused operand sums 0.89 (L1), 0.745 (ABC L2), 0.775 (AB L2)
+    double e_mm = 0.976;
+    if (v == STRASSEN_ABC || v == STRASSEN_AB)
+        e_mm = (L == 1) ? 0.89 : (v == STRASSEN_ABC ? 0.745 : 0.775);
     const bool per_product_grid = (v == STRASSEN_AB || v == STRASSEN_NAIVE);
     const bool split = tiles < 2.0 * sms;
     double ctas = (per_product_grid || split) ? tiles * mul : tiles;
@@ -306,19 +309,40 @@ double b200_predict_seconds(strassen_variant v, int level, long m, long n, long 
                4e-6 * std::ceil(ctas / sms);
     double bytes = 0.0;
     int launches = 1;
-    if (v == STRASSEN_NAIVE || v == STRASSEN_C) {  // materialised sums, both sides
-        bytes += 8.0 * ((aa + mul) * qm * qk + (ba + mul) * qk * qn);
+    if (v == STRASSEN_NAIVE || v == STRASSEN_C) {  // gather-form sum passes, both sides:
+        const double quads = S * S + n_sums[L];     // sources read once, sums written once
+        bytes += 8.0 * quads * (qm * qk + qk * qn);
         launches += 2;
     }
-    if (per_product_grid || split || v == STRASSEN_NAIVE) {  // M_{p,s} + stream pass
-        // write every partial M_{p,s}; each C update reads its product's partials
-        bytes += 8.0 * (ks * mul * qm * qn + ks * cu * qm * qn + 2.0 * m * n);
+    if (per_product_grid || split) {  // M_{p,s} written, read once by the stream pass
+        bytes += 8.0 * (2.0 * ks * mul * qm * qn + 2.0 * m * n);
         launches += 1;
     } else {  // fused epilogue: C read + write per C update
         bytes += 16.0 * cu * qm * qn;
     }
     t += bytes / BW + launches * launch;
     return t;
+}
+
+double b200_predict_seconds(strassen_variant v, int level, long m, long n, long k, int sms) {
+    const int L = (v == STRASSEN_DGEMM) ? 0 : level;
+    const long S = 1L << L;
+    const long me = m & ~(S - 1), ne = n & ~(S - 1), ke = k & ~(S - 1);
+    // dynamic peeling as engine.cpp run_device applies it: the even core, then
+    // three classical fringe updates
+    auto work = [&](long mm, long nn, long kk) {
+        return ceil_div(ceil_div(mm, S), 128) * ceil_div(ceil_div(nn, S), 128) *
+               ceil_div(ceil_div(kk, S), 16);
+    };
+    if (L > 0 && (me != m || ne != n || ke != k) && me >= S * 128 && ne >= S * 128 &&
+        ke >= S * 16 && work(me, ne, ke) < work(m, n, k)) {
+        double t = predict_core(v, L, me, ne, ke, sms);
+        if (ke < k) t += predict_core(STRASSEN_DGEMM, 0, me, ne, k - ke, sms);
+        if (me < m) t += predict_core(STRASSEN_DGEMM, 0, m - me, n, k, sms);
+        if (ne < n) t += predict_core(STRASSEN_DGEMM, 0, me, n - ne, k, sms);
+        return t;
+    }
+    return predict_core(v, L, m, n, k, sms);
 }
 
 void b200_select(long m, long n, long k, int sms, strassen_variant& v_out, int& l_out,

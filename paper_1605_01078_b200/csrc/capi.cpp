@@ -469,6 +469,24 @@ const char* strassen_status_str(strassen_status s) {
     return "unknown";
 }
 
+static int device_sms() {
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    else
+        cudaGetLastError();
+    return sms > 0 ? sms : 148;
+}
+
+strassen_status strassen_predict_b200(strassen_variant variant, int level, long m, long n, long k,
+                                      double* seconds_out) {
+    if (!seconds_out) return STRASSEN_ERR_NULL;
+    if (strassen_status st = check_variant_level(variant, level)) return st;
+    if (m < 1 || n < 1 || k < 1) return STRASSEN_ERR_PARAM;
+    *seconds_out = sb200::b200_predict_seconds(variant, level, m, n, k, device_sms());
+    return STRASSEN_OK;
+}
+
 strassen_status strassen_select(long m, long n, long k, strassen_variant* variant_out,
                                 int* level_out, double* seconds_out) {
     if (!variant_out || !level_out) return STRASSEN_ERR_NULL;

@@ -267,6 +267,12 @@ def test_model_guided_selection_against_measured_sweeps():
             assert t > 0
     assert not misses, misses
     assert S.select(16384, 16384, 16384)[:2] == ("naive", 2)
+    # the prediction strassen_select minimises, per configuration
+    assert S.predict_b200("naive", 2, 16384, 16384, 16384) == pytest.approx(
+        S.select(16384, 16384, 16384)[2])
+    assert S.predict_b200("dgemm", 0, 4096, 4096, 4096) > 0
+    with pytest.raises(S.StrassenError):
+        S.predict_b200("dgemm", 1, 64, 64, 64)
     assert S.select(1024, 1024, 1024)[:2] == ("dgemm", 0)
     with pytest.raises(S.StrassenError):
         S.select(0, 4, 4)
