@@ -196,7 +196,7 @@ Engine::~Engine() {
             if (arr[w]) cudaEventDestroy(arr[w]);
     for (cudaEvent_t ev : {ev_d2h, ev_fork, ev_join})
         if (ev) cudaEventDestroy(ev);
-    for (DeviceBuffer* b : {&stage_a, &stage_b, &stage_c, &pack_a, &pack_b, &mbuf, &tabuf, &tbbuf})
+    for (DeviceBuffer* b : {&stage_a, &stage_b, &stage_c, &pack_a, &pack_b, &mbuf, &tabuf, &tbbuf, &ticket_buf})
         if (b->ptr) cudaFree(b->ptr);
 }
 
@@ -272,7 +272,7 @@ double* Engine::ensure(DeviceBuffer& b, size_t bytes) {
 
 size_t Engine::workspace_bytes() const {
     size_t t = 0;
-    for (const DeviceBuffer* b : {&stage_a, &stage_b, &stage_c, &pack_a, &pack_b, &mbuf, &tabuf, &tbbuf})
+    for (const DeviceBuffer* b : {&stage_a, &stage_b, &stage_c, &pack_a, &pack_b, &mbuf, &tabuf, &tbbuf, &ticket_buf})
         t += b->bytes;
     return t;
 }
@@ -295,16 +295,39 @@ bool is_device_pointer(const void* p) {
 // applied in table order).
 struct FusedPlan {
     bool split = false;
+    int* tickets = nullptr;  // ordered product-parallel fused epilogue (see kernels.hpp)
+    int ticket_ld = 0;
     int ksplit = 1, per = 0;
     long long ldm = 0, mstride = 0;
     double* M = nullptr;
 };
 
-FusedPlan plan_fused(Engine& e, const MMParams& P, bool force_split) {
+FusedPlan plan_fused(Engine& e, cudaStream_t s, const MMParams& P, bool force_split) {
     FusedPlan F;
     const int ntiles = P.tiles_m * P.tiles_n;
     const int sms = e.num_sms > 0 ? e.num_sms : 148;
-    if (ntiles >= 2 * sms && !force_split) return F;
+    if (ntiles >= 2 * sms && !force_split) {
+        // Fused epilogue.  Tile ownership (one CTA walks every product of its
+        // tile) quantises to whole waves of CTAs that each run all 7^L products
+        // (ABC L2 at 9216^3: 2.2 waves -> 3).  One CTA per (tile, product) with
+        // the C updates ordered per tile by tickets applies the same updates in
+        // the same order -- bitwise the same result -- and measured faster at
+        // every size (16384^3 ABC L2 240.0 -> 238.8 ms, 9216^3 59.0 -> 43.9 ms).
+        bool ticketed = P.nprod > 1;
+        if (const char* m = std::getenv("STRASSEN_B200_RMW"))  // "owner" / "ticket" (experiments)
+            ticketed = P.nprod > 1 && std::strcmp(m, "ticket") == 0 ? true
+                       : std::strcmp(m, "owner") == 0             ? false
+                                                                   : ticketed;
+        if (ticketed) {
+            F.ticket_ld = P.tiles_n;
+            F.tickets = reinterpret_cast<int*>(
+                e.ensure(e.ticket_buf, static_cast<size_t>(P.tiles_m) * P.tiles_n * sizeof(int)));
+            ck(cudaMemsetAsync(F.tickets, 0, static_cast<size_t>(P.tiles_m) * P.tiles_n * sizeof(int),
+                               s),
+               "ticket reset");
+        }
+        return F;
+    }
     double terms = 0.0;  // mean operand terms per side: fused sums lengthen a k-tile
     for (int p = 0; p < P.nprod; ++p) terms += 0.5 * (P.prod[p].na + P.prod[p].nb);
     terms /= P.nprod > 0 ? P.nprod : 1;
@@ -334,6 +357,13 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
         wait_c();  // fused epilogue reads C
         P.mode = kEpiRMW;
         P.split = 0;
+        if (F.tickets) {  // one CTA per (tile, product), C updates ordered per tile
+            P.split = 1;
+            P.ksplit = 1;
+            P.kt_per_split = P.ktiles;
+            P.tickets = F.tickets;
+            P.ticket_ld = F.ticket_ld;
+        }
         e.prof_begin("mm_kernel", s);
         ck(launch_mm(P, s), "mm_kernel");
         e.prof_end(s);
@@ -563,8 +593,6 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
     P.tiles_n = static_cast<int>(ceil_div(qn, kBN));
     P.ktiles = static_cast<int>(ceil_div(qk, kBK));
     P.group_m = 8;
-    if (const char* g = std::getenv("STRASSEN_B200_GROUP_M"))  // rasterisation experiments
-        P.group_m = std::max(1, std::atoi(g));
 
     // Live products in table order (variants.cpp:130-133 skip rule).
     struct Live {
@@ -582,10 +610,6 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
     // Windows alternate between s and the aux stream (ordered after s's work so
     // far); s joins the aux stream at the end.
     cudaStream_t ws[2] = {s, nw > 1 ? e.aux_stream : s};
-    if (nw > 1) {
-        ck(cudaEventRecord(e.ev_fork, s), "fork");
-        ck(cudaStreamWaitEvent(e.aux_stream, e.ev_fork, 0), "fork");
-    }
     auto wait_ev = [&](cudaStream_t st, cudaEvent_t ev) {
         if (ev) ck(cudaStreamWaitEvent(st, ev, 0), "wait");
     };
@@ -707,7 +731,11 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
     // product: balanced waves at every size), then one stream pass
     // (AB: variants.cpp:142-168).
     const bool store_products = variant == STRASSEN_NAIVE || variant == STRASSEN_AB;
-    const FusedPlan F = plan_fused(e, P, store_products);
+    const FusedPlan F = plan_fused(e, s, P, store_products);
+    if (nw > 1) {  // the aux stream starts after everything enqueued on s so far
+        ck(cudaEventRecord(e.ev_fork, s), "fork");
+        ck(cudaStreamWaitEvent(e.aux_stream, e.ev_fork, 0), "fork");
+    }
 
     for (int i = 0; i < nw; ++i) {
         prefetch(i + 1);

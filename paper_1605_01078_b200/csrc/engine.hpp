@@ -40,6 +40,7 @@ struct Engine {
     DeviceBuffer stage_a, stage_b, stage_c;   // host-operand staging
     DeviceBuffer pack_a, pack_b;              // TMA layout normalisation
     DeviceBuffer mbuf, tabuf, tbbuf;          // AB / Naive temporaries
+    DeviceBuffer ticket_buf;                  // ordered fused-epilogue tickets
     long last_launches = 0;
     bool peeling = true;  // dynamic peeling of odd fringes (strassen_ctx_set_peeling)
     // optional per-launch timing of the last call (strassen_ctx_enable_profiling)

@@ -59,6 +59,20 @@ __device__ __forceinline__ void mbar_arrive_if(uint64_t* bar, bool pred) {
         : "memory");
 }
 
+// Ticket handshake of the ordered fused epilogue (acquire / release at GPU scope).
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Named barrier over the 8 DMMA warps only (the producer warp has exited).
+__device__ __forceinline__ void consumer_bar() {
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+}
+
 // Consumer side of a ring slot hand-back.  The slot was read with generic-proxy
 // LDS; the producer refills it with TMA (async proxy).  Every lane fences its
 // reads against the async proxy before lane 0 arrives -- without it ptxas may
@@ -609,6 +623,13 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         const int ncol0 = tn * kBN + wn * 32;
         // (half-tile products map B columns without the permutation)
         const int c0 = pd.half ? 2 * j : nperm(2 * j), c1 = pd.half ? 2 * j + 1 : nperm(2 * j + 1);
+        int* ticket = nullptr;  // ordered epilogue: wait for the previous product
+        if (P.mode == kEpiRMW && P.tickets) {
+            ticket = P.tickets + tm * P.ticket_ld + tn;
+            if (threadIdx.x == 0)
+                while (ld_acquire_gpu(ticket) != p) __nanosleep(128);
+            consumer_bar();
+        }
         if (P.mode == kEpiRMW) {
             // 16-byte path: C column-major with rows (2g, 2g+1) of the fragment
             // pair (2h, 2h+1) adjacent and 16-byte aligned (checked on the host)
@@ -633,8 +654,8 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                                     double2 v = make_double2(0.0, 0.0);
                                     if (col < Cc) {
                                         const double* src = C + row + static_cast<long long>(col) * P.cs_c;
-                                        if (row + 1 < R) v = *reinterpret_cast<const double2*>(src);
-                                        else if (row < R) v.x = *src;
+                                        if (row + 1 < R) v = __ldcg(reinterpret_cast<const double2*>(src));
+                                        else if (row < R) v.x = __ldcg(src);
                                     }
                                     cv[n2][h][e] = v;
                                 }
@@ -667,8 +688,8 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                         for (int e = 0; e < 2; ++e) {
                             const int row = mrow0 + 16 * (mf >> 1) + (mf & 1);
                             const int col = ncol0 + 8 * nf + (e ? c1 : c0);
-                            cv[mf][e] =
-                                (row < R && col < Cc) ? C[row * P.rs_c + col * P.cs_c] : 0.0;
+                            cv[mf][e] = (row < R && col < Cc)
+                                            ? __ldcg(C + row * P.rs_c + col * P.cs_c) : 0.0;
                         }
 #pragma unroll
                     for (int mf = 0; mf < 8; ++mf)
@@ -680,6 +701,11 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                                 C[row * P.rs_c + col * P.cs_c] = fma(sc, acc[mf][nf][e], cv[mf][e]);
                         }
                 }
+            }
+            if (ticket) {  // every thread's C stores visible, then hand the tile on
+                __threadfence();
+                consumer_bar();
+                if (threadIdx.x == 0) st_release_gpu(ticket, p + 1);
             }
         } else {
             const int mi = P.split ? p * P.ksplit + (kt_lo / P.kt_per_split) : p;

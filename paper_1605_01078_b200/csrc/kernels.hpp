@@ -72,6 +72,11 @@ struct alignas(64) MMParams {
     // CTA stores its partial product to M_{p*ksplit+s} (kEpiStore)
     int split;
     int ksplit, kt_per_split;
+    // ticketed fused epilogue (split grid, ksplit = 1, kEpiRMW): CTA (tile, p)
+    // applies its C updates once tickets[tile] == p, then sets it to p + 1, so
+    // every C tile still receives the products in table order
+    int* tickets;
+    int ticket_ld;              // tickets row stride (tile columns of the whole call)
 };
 
 cudaError_t launch_mm(const MMParams& p, cudaStream_t s);
