@@ -295,7 +295,8 @@ static double predict_core(strassen_variant v, int L, long m, long n, long k, in
         e_mm = (L == 1) ? 0.89 : (v == STRASSEN_ABC ? 0.745 : 0.775);
     const bool per_product_grid = (v == STRASSEN_AB || v == STRASSEN_NAIVE);
     const bool split = tiles < 2.0 * sms;
-    double ctas = (per_product_grid || split) ? tiles * mul : tiles;
+    // fused epilogue with several products: one CTA per (tile, product), ticketed
+    double ctas = (per_product_grid || split || mul > 1) ? tiles * mul : tiles;
     double ks = 1;
     if (per_product_grid || split) {  // k-chunks as engine.cpp plan_fused picks them
         const double terms = (v == STRASSEN_ABC || v == STRASSEN_AB) ? (L == 1 ? 1.71 : 2.94) : 1.0;
@@ -314,13 +315,15 @@ static double predict_core(strassen_variant v, int L, long m, long n, long k, in
         bytes += 8.0 * quads * (qm * qk + qk * qn);
         launches += 2;
     }
-    if (per_product_grid || split) {  // M_{p,s} written, read once by the stream pass
-        bytes += 8.0 * (2.0 * ks * mul * qm * qn + 2.0 * m * n);
+    double rmw_bytes = 0.0;
+    if (per_product_grid || split) {  // M_{p,s} written (mostly hidden under the DMMAs),
+        // then read once by the stream pass with C read and written once
+        bytes += 8.0 * (1.5 * ks * mul * qm * qn + 2.0 * m * n);
         launches += 1;
-    } else {  // fused epilogue: C read + write per C update
-        bytes += 16.0 * cu * qm * qn;
+    } else {  // fused epilogue: C read + write per C update, issued by the DMMA warps
+        rmw_bytes = 16.0 * cu * qm * qn;
     }
-    t += bytes / BW + launches * launch;
+    t += bytes / BW + rmw_bytes / 4.6e12 + launches * launch;
     return t;
 }
 
