@@ -378,3 +378,30 @@ def test_tile_ownership_mode_every_variant_repeated(dim, configs):
             else:
                 assert torch.equal(C, first), (v, L, rep)  # run-to-run bitwise
     ctx.close()
+
+
+@pytest.mark.parametrize("variant,level", [("naive", 2), ("abc", 2), ("c", 2), ("abc", 1)])
+def test_full_size_sampled_tiles_against_oracle(variant, level):
+    """BASELINE's headline size, 16384^3, checked against the oracle on sampled output
+    tiles (the reference DGEMM on 256 x 256 x k tiles through
+    strided views of the same buffers), including tiles that straddle quadrant
+    boundaries. Tolerance: BASELINE.json normwise bound on each tile."""
+    import torch
+    n = 16384
+    g = torch.Generator(device="cuda").manual_seed(16384 + level)
+    A = (torch.rand(n, n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    B = (torch.rand(n, n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    C0 = (torch.rand(n, n, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    C = C0.clone().t().contiguous().t()
+    ctx = S.Ctx()
+    ctx.gemm_device(variant, level, 1.0, A, B, C)
+    torch.cuda.synchronize()
+    ctx.close()
+    # quadrant boundaries sit at multiples of n / 2^level
+    for r0, c0 in [(0, 0), (n // 4 - 128, n // 2 - 128), (n - 256, 3 * n // 4 - 128)]:
+        a = np.asfortranarray(A[r0:r0 + 256, :].cpu().numpy())
+        b = np.asfortranarray(B[:, c0:c0 + 256].cpu().numpy())
+        c0h = np.asfortranarray(C0[r0:r0 + 256, c0:c0 + 256].cpu().numpy())
+        ref = oracle_result("dgemm", 0, 1.0, a, b, c0h, use_reference_gemm=False)
+        got = C[r0:r0 + 256, c0:c0 + 256].cpu().numpy()
+        check(variant, level, got, ref, c0h, a, b)
