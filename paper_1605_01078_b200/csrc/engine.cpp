@@ -593,6 +593,12 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
     P.tiles_n = static_cast<int>(ceil_div(qn, kBN));
     P.ktiles = static_cast<int>(ceil_div(qk, kBK));
     P.group_m = 8;
+    // bulk-reduction epilogue for products of <= 128 k-tiles (measured at
+    // 16384^2 x k: ABC L2 k = 1024 23.8 -> 21.2 ms, 2048 38.2 -> 35.7, 4096
+    // 67.4 -> 64.8; ABC L1 k = 4096 60.8 -> 60.1; at k = 16384 (256+ k-tiles)
+    // the register path is ~1% faster)
+    P.bulk_max_kt = 128;
+    if (const char* b = std::getenv("STRASSEN_B200_BULK_MAX_KT")) P.bulk_max_kt = std::atoi(b);
 
     // Live products in table order (variants.cpp:130-133 skip rule).
     struct Live {

@@ -68,6 +68,12 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
 __device__ __forceinline__ void st_release_gpu(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// Bulk reduction smem -> global, f64 add performed at L2 (UBLKRED.ADD.F64.RN).
+__device__ __forceinline__ void bulk_reduce_add_f64(double* gdst, const void* ssrc, uint32_t bytes) {
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;"
+                 ::"l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes) : "memory");
+}
+
 // Named barrier over the 8 DMMA warps only (the producer warp has exited).
 __device__ __forceinline__ void consumer_bar() {
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
@@ -623,6 +629,80 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         const int ncol0 = tn * kBN + wn * 32;
         // (half-tile products map B columns without the permutation)
         const int c0 = pd.half ? 2 * j : nperm(2 * j), c1 = pd.half ? 2 * j + 1 : nperm(2 * j + 1);
+        // ---- fused epilogue through bulk reductions.  The DMMA warps stage
+        // (alpha gamma) M in shared memory (the ring is idle once this CTA's
+        // only product is done) and warp 0 hands each C column to the TMA
+        // engine as an f64 add performed at L2 (cp.reduce.async.bulk): C never
+        // passes through the SM and the warps do not wait on HBM.  Per element
+        // the result is C + round(alpha gamma M) -- with |alpha| = 1 exactly the
+        // fma(alpha gamma, M, C) of the register path.  Used for whole,
+        // column-major tiles of single-product CTAs with short k loops (the
+        // CTA stays resident until its reductions complete, which costs more
+        // than the register path saves once the mainloop is long); anything
+        // else takes the register read-modify-write below.
+        bool bulk = P.mode == kEpiRMW && P.c_vec && p_hi - p_lo == 1 &&
+                    kt_hi - kt_lo <= P.bulk_max_kt;
+        for (int u = 0; u < pd.nc && bulk; ++u) {
+            const int cq = pd.cq[u];
+            bulk = tm * kBM + kBM <= P.crows[cq] && tn * kBN + kBN <= P.ccols[cq];
+        }
+        if (bulk) {
+            constexpr int kColStride = kBM * 8 + 16;  // 1040 B: skews banks across columns
+            uint8_t* stage = raw;
+            int* ticket = P.tickets ? P.tickets + tm * P.ticket_ld + tn : nullptr;
+            bool issued = false;
+            consumer_bar();  // every warp is done reading the ring before it is reused
+            for (int pass = 0; pass < 2; ++pass) {  // destinations with coefficient +1, then -1
+                int any = 0;
+                for (int u = 0; u < pd.nc; ++u) any |= (pd.cs[u] > 0) == (pass == 0);
+                if (!any) continue;
+                if (issued) {  // previous pass's reductions must have read the stage
+                    if (warp == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    consumer_bar();
+                }
+                const double sc = P.alpha * (pass == 0 ? 1.0 : -1.0);
+#pragma unroll
+                for (int nf = 0; nf < 4; ++nf)
+#pragma unroll
+                    for (int h = 0; h < 4; ++h)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int row = wm * 64 + 16 * h + 2 * g;
+                            const int col = wn * 32 + 8 * nf + (e ? c1 : c0);
+                            *reinterpret_cast<double2*>(stage + col * kColStride + row * 8) =
+                                make_double2(sc * acc[2 * h][nf][e], sc * acc[2 * h + 1][nf][e]);
+                        }
+                consumer_fence();  // generic smem writes before the async-proxy reads
+                if (!issued && ticket) {
+                    if (threadIdx.x == 0)
+                        while (ld_acquire_gpu(ticket) != p) __nanosleep(128);
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                }
+                consumer_bar();
+                if (warp == 0) {
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                    for (int u = 0; u < pd.nc; ++u) {
+                        if ((pd.cs[u] > 0) != (pass == 0)) continue;
+                        double* Cq = P.cptr[pd.cq[u]] + tm * kBM;
+                        for (int c = lane; c < kBN; c += 32)
+                            bulk_reduce_add_f64(Cq + static_cast<long long>(tn * kBN + c) * P.cs_c,
+                                                stage + c * kColStride, kBM * 8);
+                    }
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+                issued = true;
+            }
+            if (warp == 0) {  // all reductions performed, then hand the tile on
+                asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                __syncwarp();
+                if (lane == 0 && ticket) {
+                    __threadfence();
+                    st_release_gpu(ticket, p + 1);
+                }
+            }
+            continue;  // next product (none: single-product CTA)
+        }
         int* ticket = nullptr;  // ordered epilogue: wait for the previous product
         if (P.mode == kEpiRMW && P.tickets) {
             ticket = P.tickets + tm * P.ticket_ld + tn;

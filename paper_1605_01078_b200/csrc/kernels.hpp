@@ -77,6 +77,10 @@ struct alignas(64) MMParams {
     // every C tile still receives the products in table order
     int* tickets;
     int ticket_ld;              // tickets row stride (tile columns of the whole call)
+    // fused epilogue through TMA bulk f64 reductions for CTAs of at most this
+    // many k-tiles (short products, where the register read-modify-write would
+    // be a large share of the CTA); 0 = never
+    int bulk_max_kt;
 };
 
 cudaError_t launch_mm(const MMParams& p, cudaStream_t s);

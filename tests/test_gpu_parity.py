@@ -405,3 +405,31 @@ def test_full_size_sampled_tiles_against_oracle(variant, level):
         ref = oracle_result("dgemm", 0, 1.0, a, b, c0h, use_reference_gemm=False)
         got = C[r0:r0 + 256, c0:c0 + 256].cpu().numpy()
         check(variant, level, got, ref, c0h, a, b)
+
+
+@pytest.mark.parametrize("alpha", [1.0, -0.5])
+def test_bulk_reduction_epilogue_short_k(alpha):
+    """Short products (<= 128 k-tiles) in fused-epilogue launches add (alpha gamma) M into C
+    through TMA bulk f64 reductions at L2, a pass per coefficient sign; checked against
+    cuBLAS for non-unit alpha, with repeated runs bitwise equal (ticket ordering)."""
+    import torch
+    m = n = 9216
+    k = 1024
+    g = torch.Generator(device="cuda").manual_seed(1024)
+    A = (torch.rand(k, m, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    B = (torch.rand(n, k, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    C0 = (torch.rand(n, m, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    ref = C0 + alpha * (A @ B)
+    den = (torch.linalg.norm(A) * torch.linalg.norm(B)).item()
+    ctx = S.Ctx()
+    for v, L in [("abc", 2), ("c", 2), ("abc", 1), ("c", 1), ("dgemm", 0)]:
+        runs = []
+        for _ in range(2):
+            C = C0.clone().t().contiguous().t()
+            ctx.gemm_device(v, L, alpha, A, B, C)
+            torch.cuda.synchronize()
+            runs.append(C)
+        nw = (torch.linalg.norm(runs[0] - ref) / den).item()
+        assert nw <= (5e-12 if L == 2 else 1e-12), (v, L, alpha, nw)
+        assert torch.equal(runs[0], runs[1]), (v, L, alpha)
+    ctx.close()
