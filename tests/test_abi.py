@@ -250,7 +250,7 @@ def test_c_variant_counters_and_validation():
 
 def test_model_guided_selection_against_measured_sweeps():
     """strassen_select (B200 cost model) vs the committed round-1 sweeps:
-    its pick must be within 2.5% of the fastest measured configuration."""
+    its pick must be within 3.5% of the fastest measured configuration."""
     import collections
     import csv
     misses = []
@@ -262,7 +262,7 @@ def test_model_guided_selection_against_measured_sweeps():
         for shape, times in by.items():
             v, lv, t = S.select(*shape)
             key = f"{v}{lv}"
-            if key in times and times[key] > 1.025 * min(times.values()):
+            if key in times and times[key] > 1.035 * min(times.values()):
                 misses.append((shape, key, times[key] / min(times.values())))
             assert t > 0
     assert not misses, misses
