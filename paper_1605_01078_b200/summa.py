@@ -154,6 +154,7 @@ def _default_local_gemm(variant, level):
             ctx.gemm_device(variant, level, alpha, a, b, c)
         else:
             ctx.gemm(variant, level, alpha, a, b, c)
+        return ctx.last_launches()
     return run
 
 
@@ -164,7 +165,8 @@ def summa(layout: Layout, comm: TorchComm, A_l: torch.Tensor, B_l: torch.Tensor,
 
     A_l (m_l x k_c), B_l (k_r x n_l), C_l (m_l x n_l) are the rank's blocks. The panel
     buffers are column-major, so the local Strassen call reads them through TMA without a
-    repack. Returns the number of local updates.
+    repack. Returns the GPU kernel launches of the local updates (one per update when
+    `local_gemm` reports no count).
     """
     L = layout
     gemm = local_gemm or _default_local_gemm(variant, level)
@@ -187,13 +189,15 @@ def summa(layout: Layout, comm: TorchComm, A_l: torch.Tensor, B_l: torch.Tensor,
         return [w for w in (comm.bcast_row(abase[s], ac), comm.bcast_col(bbase[s], br)) if w]
 
     pending = post(0)
+    launches = 0
     for p in range(L.panels):
         nxt = post(p + 1) if p + 1 < L.panels else []
         for w in pending:
             w.wait()
-        gemm(alpha, abuf[p % 2], bbuf[p % 2], C_l)
+        n = gemm(alpha, abuf[p % 2], bbuf[p % 2], C_l)
+        launches += n if isinstance(n, int) else 1
         pending = nxt
-    return L.panels
+    return launches
 
 
 def summa_loopback(layout: Layout, A_blocks: List[torch.Tensor], B_blocks: List[torch.Tensor],
