@@ -105,10 +105,10 @@ def hbm_bytes(kernel, m, n, k, level, ordinal=0):
     s = 1 << level
     qm, qn, qk = -(-m // s), -(-n // s), -(-k // s)
     mul, aa, ba, cu = table_counts(level)
-    if kernel == "sum_batch_kernel" and level > 0:  # ordinal 0: A side, 1: B side
+    if kernel == "sum_gather_kernel" and level > 0:  # ordinal 0: A side, 1: B side
         quads = s * s + MULTI_TERM_SUMS[level]
         return 8.0 * quads * (qm * qk if ordinal == 0 else qk * qn)
-    if kernel == "stream_update_kernel":
+    if kernel == "stream_gather_kernel":
         return 8.0 * (mul * qm * qn + 2 * m * n)
     return None
 

@@ -408,7 +408,7 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
             ++S.nsrc[q];
         }
     wait_c();  // first reader of C: its copy-in overlapped the products
-    e.prof_begin("stream_update_kernel", s);
+    e.prof_begin("stream_gather_kernel", s);
     ck(launch_stream_update(S, s), "stream_update");
     e.prof_end(s);
     return 2;
@@ -770,7 +770,7 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
                     SB.c0 = c0;
                     SB.cols = c1;
                 }
-                e.prof_begin("sum_batch_kernel", st);
+                e.prof_begin("sum_gather_kernel", st);
                 ck(launch_sum_batch(SB, st), sd == 0 ? "sum_batch (A)" : "sum_batch (B)");
                 e.prof_end(st);
                 ++launches;

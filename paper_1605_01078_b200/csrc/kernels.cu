@@ -844,88 +844,16 @@ __global__ void repack_kernel(const double* __restrict__ src, long long rs, long
     }
 }
 
-// -------------------------------------------------------------- sum batch ---
-// C variant: all multi-term operand sums of a launch, one job per blockIdx.z.
-// Arithmetic of materialize_sum (variants.cpp:53-96): d0*x0, then += ds*xs in order.
-__global__ void sum_batch_kernel(const __grid_constant__ SumBatchParams P) {
-    // one thread = rows (2r, 2r+1) of two columns: 16-byte loads/stores
-    // (sources are TMA-ready quadrants: 16-byte aligned, even leading dims)
-    const int z = blockIdx.z;
-    const long long i = P.r0 + 2 * (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x);
-    if (i >= P.rows) return;
-    const int n = P.nterms[z];
-    double* dst = P.dst[z];
-    for (long long j = P.c0 + 2 * blockIdx.y; j < P.cols; j += 2 * gridDim.y) {
-        double2 v[2];
-#pragma unroll
-        for (int c = 0; c < 2; ++c) v[c] = make_double2(0.0, 0.0);
-#pragma unroll
-        for (int u = 0; u < kMaxTerms; ++u) {
-            if (u >= n) break;
-            const SumTerm& t = P.t[z][u];
-            const double cu = t.coeff;
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const long long jj = j + c;
-                double2 x = make_double2(0.0, 0.0);
-                if (jj < t.cols) {
-                    if (i + 1 < t.rows) {
-                        x = *reinterpret_cast<const double2*>(t.x + i + jj * t.ld);
-                    } else if (i < t.rows) {
-                        x.x = t.x[i + jj * t.ld];
-                    }
-                }
-                if (u == 0) {
-                    v[c].x = cu * x.x;
-                    v[c].y = cu * x.y;
-                } else {
-                    v[c].x = fma(cu, x.x, v[c].x);
-                    v[c].y = fma(cu, x.y, v[c].y);
-                }
-            }
-        }
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const long long jj = j + c;
-            if (jj >= P.cols) continue;
-            if (i + 1 < P.rows)
-                *reinterpret_cast<double2*>(dst + i + jj * P.ld) = v[c];
-            else
-                dst[i + jj * P.ld] = v[c].x;
-        }
-    }
-}
-
-// --------------------------------------------------------- stream update ---
-// C_q(i, j) += sum over (p, gamma) feeding q, in table order, of
-// (alpha * gamma) * M_p(i, j)  (variants.cpp:99-109, applied entry by entry).
-__global__ void stream_update_kernel(const StreamParams P) {
-    const int quad = blockIdx.z;
-    const long long i = P.r0 + static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= P.crows[quad] || i >= P.r1) return;
-    double* C = P.cptr[quad];
-    const int ns = P.nsrc[quad];
-    const long long jend = P.ccols[quad] < P.c1 ? P.ccols[quad] : P.c1;
-    for (long long j = P.c0 + blockIdx.y; j < jend; j += gridDim.y) {
-        double* cp = C + i * P.rs_c + j * P.cs_c;
-        double c = *cp;
-        for (int u = 0; u < ns; ++u) {
-            const double* M = P.mbase + P.src_prod[quad][u] * P.ksplit * P.mstride;
-            double v = M[i + j * P.ldm];
-            for (int sp = 1; sp < P.ksplit; ++sp) v += M[sp * P.mstride + i + j * P.ldm];
-            c = fma(P.alpha * static_cast<double>(P.src_coeff[quad][u]), v, c);
-        }
-        *cp = c;
-    }
-}
-
-// ------------------------------------------------- gather forms (one pass) ---
-// The batched passes above read each source once per use: a level-2 side has 16
-// quadrants feeding 45 sums through 185 term reads.  The gather forms read every
-// source ONCE per position, keep the values in shared memory (indexable, each
-// thread touches only its own slots, so no barrier), and emit every output:
-// HBM traffic = sources + outputs.  Per element the arithmetic and its order
-// are exactly those of sum_batch_kernel / stream_update_kernel.
+// ------------------------------------------- sum and stream passes (gather) ---
+// A level-2 side has 16 quadrants feeding 45 operand sums (185 term reads if
+// each sum read its own terms).  The gather forms read every source ONCE per
+// position, keep the values in shared memory (indexable; each thread touches
+// only its own slots, so no barrier) and emit every output: HBM traffic =
+// sources + outputs.
+// Sum pass: materialize_sum (variants.cpp:53-96) for all entries at once,
+// d0*x0 then += ds*xs in listed order per element.
+// Stream pass: C_r += (alpha gamma) M_p (variants.cpp:99-109), each quadrant's
+// updates in table order.
 struct SumGatherParams {
     const double* src[kMaxQuad];
     int srows[kMaxQuad], scols[kMaxQuad];
@@ -1214,11 +1142,7 @@ cudaError_t launch_sum_batch(const SumBatchParams& p, cudaStream_t s) {
         sum_gather_kernel<<<grid, kGatherThreads, 0, s>>>(g);
         return cudaGetLastError();
     }
-    const long long pairs = (p.rows - p.r0 + 1) / 2, cpairs = (p.cols - p.c0 + 1) / 2;
-    dim3 grid(static_cast<unsigned>((pairs + 127) / 128),
-              static_cast<unsigned>(cpairs < 1024 ? cpairs : 1024), p.njobs);
-    sum_batch_kernel<<<grid, 128, 0, s>>>(p);
-    return cudaGetLastError();
+    return cudaErrorInvalidValue;  // > kMaxQuad distinct sources: not produced at L <= 2
 }
 
 // Product-major gather form: valid when every quadrant's sources are in
@@ -1275,9 +1199,7 @@ cudaError_t launch_stream_update(const StreamParams& p, cudaStream_t s) {
         stream_gather_kernel<<<grid, kStreamThreads, 0, s>>>(g);
         return cudaGetLastError();
     }
-    dim3 grid(static_cast<unsigned>((p.r1 - p.r0 + 255) / 256), col_grid(p.c1 - p.c0), p.nquad);
-    stream_update_kernel<<<grid, 256, 0, s>>>(p);
-    return cudaGetLastError();
+    return cudaErrorInvalidValue;  // per-quadrant lists not in table order: never built
 }
 
 cudaError_t launch_scale(double* c, long rows, long cols, long long rs, long long cs, double beta,

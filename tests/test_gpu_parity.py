@@ -281,7 +281,7 @@ def test_profiling_reports_each_launch(ctx):
     c.gemm("naive", 2, 1.0, a, b, out)
     prof = c.last_profile()
     names = [p["kernel"] for p in prof]
-    assert names == ["sum_batch_kernel", "sum_batch_kernel", "mm_kernel", "stream_update_kernel"]
+    assert names == ["sum_gather_kernel", "sum_gather_kernel", "mm_kernel", "stream_gather_kernel"]
     assert all(p["ms"] > 0 for p in prof)
     assert c.last_launches() == len(prof)
     c.set_pipelining(True)  # windows: every launch still profiled and counted
@@ -289,7 +289,7 @@ def test_profiling_reports_each_launch(ctx):
     prof = c.last_profile()
     assert c.last_launches() == len(prof) and all(p["ms"] > 0 for p in prof)
     names = [p["kernel"] for p in prof]
-    assert names.count("mm_kernel") == names.count("stream_update_kernel") >= 1
+    assert names.count("mm_kernel") == names.count("stream_gather_kernel") >= 1
 
 
 def test_host_staging_overlap_each_variant_and_operand_kind(ctx):
