@@ -8,7 +8,8 @@ namespace sb200 {
 
 // Split mode (one CTA per tile x product x k-chunk, partials + one stream
 // pass): the k-chunk count minimising
-//   waves(CTAs) x (chunk k-tiles x t_k + t_cta) + partial-sum bytes / HBM rate,
+//   waves(CTAs) x (chunk k-tiles x t_k + t_cta) + stream pass (bandwidth or
+//   the latency of its per-thread chain of partial loads),
 // where a 16-k tile costs t_k = 2.1 us x term_factor of DMMA work (4096 cycles
 // at 1.965 GHz; term_factor > 1 for fused operand sums) and t_cta ~3 us covers
 // a CTA's prologue, pipeline fill and epilogue.  q_elems = qm * qn (one
@@ -25,7 +26,10 @@ inline int choose_ksplit(long ntiles, long nprod, long ktiles, long sms, double 
         if (ks2 != ks) continue;  // same chunking as a smaller ks
         const double ctas = static_cast<double>(ntiles) * nprod * ks2;
         const double waves = std::ceil(ctas / static_cast<double>(sms));
-        const double t = waves * (per * t_k + t_cta) + 8.0 * q_elems * nprod * ks2 / bw;
+        // stream pass: bandwidth, or at small sizes the chain of nprod * ks dependent
+        // partial loads per thread (~0.7 us each; 1024^3 Naive L2 measured 68 us at ks = 2)
+        const double t_stream = std::fmax(8.0 * q_elems * nprod * ks2 / bw, nprod * ks2 * 0.7e-6);
+        const double t = waves * (per * t_k + t_cta) + t_stream;
         if (t < best * 0.995) {  // prefer fewer chunks on near-ties
             best = t;
             best_ks = static_cast<int>(ks2);
