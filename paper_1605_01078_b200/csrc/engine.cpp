@@ -349,6 +349,16 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
                       const std::vector<Terms>& dests, const std::vector<QuadView>& cq,
                       const DView& C, double alpha, long r0, long r1, long c0, long c1,
                       const std::function<void()>& wait_c) {
+    // persistent launches (one CTA per SM walking the units) except where a
+    // unit would take the bulk-reduction epilogue, which reuses the ring
+    static const int persist_env = [] {
+        const char* v = std::getenv("STRASSEN_B200_PERSISTENT");  // 0 / 1 (experiments)
+        return v ? std::atoi(v) : -1;
+    }();
+    auto cap = [&](bool bulk_units) {
+        const bool on = persist_env >= 0 ? persist_env != 0 : !bulk_units;
+        return on ? (e.num_sms > 0 ? e.num_sms : 148) : 0;
+    };
     P.tm0 = static_cast<int>(r0 / kBM);
     P.tiles_m = static_cast<int>(ceil_div(r1 - r0, kBM));
     P.tn0 = static_cast<int>(c0 / kBN);
@@ -364,6 +374,7 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
             P.tickets = F.tickets;
             P.ticket_ld = F.ticket_ld;
         }
+        P.grid_cap = cap(P.c_vec && P.ktiles <= P.bulk_max_kt);
         e.prof_begin("mm_kernel", s);
         ck(launch_mm(P, s), "mm_kernel");
         e.prof_end(s);
@@ -376,6 +387,7 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
     P.mbase = F.M;
     P.ldm = F.ldm;
     P.mstride = F.mstride;
+    P.grid_cap = cap(false);
     e.prof_begin("mm_kernel", s);
     ck(launch_mm(P, s), "mm_kernel (split)");
     e.prof_end(s);

@@ -391,7 +391,47 @@ __device__ __forceinline__ void product_kloop(const uint8_t* raw, uint64_t* raw_
     }
 }
 
-template <int MAXT>
+// One work unit of an mm launch: a C tile and the products / k-range it runs.
+struct Unit {
+    int tm, tn, p_lo, p_hi, kt_lo, kt_hi;
+};
+__device__ __forceinline__ int unit_count(const MMParams& P) {
+    return P.tiles_m * P.tiles_n * (P.split ? P.nprod * P.ksplit : 1);
+}
+// unit -> (tile, product, k-chunk) in split mode, tile (all products) otherwise;
+// tiles in grouped raster order (group_m tile rows share B column panels in L2)
+__device__ __forceinline__ Unit decode_unit(const MMParams& P, int bid) {
+    Unit U;
+    U.p_lo = 0;
+    U.p_hi = P.nprod;
+    U.kt_lo = 0;
+    U.kt_hi = P.ktiles;
+    if (P.split) {
+        const int ntiles = P.tiles_m * P.tiles_n;
+        const int s_idx = (bid / ntiles) % P.ksplit;
+        U.p_lo = bid / (ntiles * P.ksplit);
+        U.p_hi = U.p_lo + 1;
+        U.kt_lo = s_idx * P.kt_per_split;
+        U.kt_hi = min(P.ktiles, U.kt_lo + P.kt_per_split);
+        bid %= ntiles;
+    }
+    const int per_group = P.group_m * P.tiles_n;
+    const int grp = bid / per_group;
+    const int first_m = grp * P.group_m;
+    const int gsz = min(P.tiles_m - first_m, P.group_m);
+    const int rr = bid - grp * per_group;
+    U.tm = first_m + rr % gsz + P.tm0;
+    U.tn = rr / gsz + P.tn0;
+    return U;
+}
+
+// Each CTA processes units blockIdx.x, + gridDim.x, ... in increasing order.
+// With one CTA per unit that is a single pass; a persistent launch (one CTA
+// per SM) keeps the producer streaming the next unit's operand tiles into the
+// ring while the DMMA warps finish the current unit's epilogue.  Ticket waits
+// only ever point at smaller units, which every CTA reaches first, so
+// persistence cannot deadlock them.
+template <int MAXT, bool PERSIST>
 __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__ MMParams P) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment (128B-swizzle atoms) by offsetting the shared array
@@ -403,26 +443,10 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
 
-    // split mode: blockIdx -> (tile, product, k-chunk)
-    int bid = blockIdx.x;
-    int p_lo = 0, p_hi = P.nprod, kt_lo = 0, kt_hi = P.ktiles;
-    if (P.split) {
-        const int ntiles = P.tiles_m * P.tiles_n;
-        const int s_idx = (bid / ntiles) % P.ksplit;
-        p_lo = bid / (ntiles * P.ksplit);
-        p_hi = p_lo + 1;
-        kt_lo = s_idx * P.kt_per_split;
-        kt_hi = min(P.ktiles, kt_lo + P.kt_per_split);
-        bid %= ntiles;
-    }
-    // grouped rasterisation: group_m tile rows share B column panels in L2
-    const int per_group = P.group_m * P.tiles_n;
-    const int grp = bid / per_group;
-    const int first_m = grp * P.group_m;
-    const int gsz = min(P.tiles_m - first_m, P.group_m);
-    const int rr = bid - grp * per_group;
-    const int tm = first_m + rr % gsz + P.tm0;
-    const int tn = rr / gsz + P.tn0;
+    // PERSIST = false: exactly one unit per CTA (keeps the 4-term instantiation,
+    // which runs at the register limit, free of the loop state)
+    const int n_units = PERSIST ? unit_count(P) : static_cast<int>(blockIdx.x) + 1;
+    const bool persistent = PERSIST && static_cast<int>(gridDim.x) < n_units;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kRawSlots; ++s) {
@@ -439,8 +463,11 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
         if (warp != kConsumerWarps || lane != 0) return;
         uint32_t s = 0, phase = 0;
-        const int m0 = tm * kBM, n0 = tn * kBN;
-        for (int p = p_lo; p < p_hi; ++p) {
+        for (int unit = blockIdx.x; unit < n_units; unit += PERSIST ? gridDim.x : 1) {
+        const Unit U = decode_unit(P, unit);
+        const int m0 = U.tm * kBM, n0 = U.tn * kBN;
+        const int kt_lo = U.kt_lo, kt_hi = U.kt_hi;
+        for (int p = U.p_lo; p < U.p_hi; ++p) {
             const ProductDesc& pd = P.prod[p];
             if (pd.half) {
                 // 8-k half tiles, two terms per slot (A terms first, then B)
@@ -492,6 +519,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                 }
             }
         }
+        }  // unit
         return;
     }
 
@@ -509,6 +537,10 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     // ring position of the next term tile: slot index and its fill parity
     uint32_t slot = 0, phase = 0;
 
+    for (int unit = blockIdx.x; unit < n_units; unit += PERSIST ? gridDim.x : 1) {
+    const Unit U = decode_unit(P, unit);
+    const int tm = U.tm, tn = U.tn, p_lo = U.p_lo, p_hi = U.p_hi;
+    const int kt_lo = U.kt_lo, kt_hi = U.kt_hi;
     for (int p = p_lo; p < p_hi; ++p) {
         const ProductDesc& pd = P.prod[p];
         const int na = pd.na, nb = pd.nb;
@@ -641,7 +673,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         // than the register path saves once the mainloop is long); anything
         // else takes the register read-modify-write below.
         bool bulk = P.mode == kEpiRMW && P.c_vec && p_hi - p_lo == 1 &&
-                    kt_hi - kt_lo <= P.bulk_max_kt;
+                    kt_hi - kt_lo <= P.bulk_max_kt && !persistent;
         for (int u = 0; u < pd.nc && bulk; ++u) {
             const int cq = pd.cq[u];
             bulk = tm * kBM + kBM <= P.crows[cq] && tn * kBN + kBN <= P.ccols[cq];
@@ -813,6 +845,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                     }
         }
     }
+    }  // unit
 }
 
 // ---------------------------------------------------------------- repack ----
@@ -1058,18 +1091,19 @@ __global__ void scale_kernel(double* c, long rows, long cols, long long rs, long
 
 }  // namespace
 
-template <int MAXT>
+template <int MAXT, bool PERSIST>
 static cudaError_t launch_mm_t(const MMParams& p, cudaStream_t s) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(mm_kernel<MAXT>,
+        cudaError_t e = cudaFuncSetAttribute(mm_kernel<MAXT, PERSIST>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              kMMSmemBytes);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    const int grid = p.tiles_m * p.tiles_n * (p.split ? p.nprod * p.ksplit : 1);
-    mm_kernel<MAXT><<<grid, kThreads, kMMSmemBytes, s>>>(p);
+    const int units = p.tiles_m * p.tiles_n * (p.split ? p.nprod * p.ksplit : 1);
+    const int grid = PERSIST && p.grid_cap > 0 && p.grid_cap < units ? p.grid_cap : units;
+    mm_kernel<MAXT, PERSIST><<<grid, kThreads, kMMSmemBytes, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -1079,8 +1113,13 @@ cudaError_t launch_mm(const MMParams& p, cudaStream_t s) {
         maxt = p.prod[i].na > maxt ? p.prod[i].na : maxt;
         maxt = p.prod[i].nb > maxt ? p.prod[i].nb : maxt;
     }
-    if (maxt == 1) return launch_mm_t<1>(p, s);  // single-term programs: no sum code at all  // single-term programs: no sum code at all
-    return maxt <= 2 ? launch_mm_t<2>(p, s) : launch_mm_t<kMaxTerms>(p, s);
+    // Persistent launches for single-term programs (DGEMM, Naive, C): at 16384^3
+    // mm_kernel 192.4 -> 188.7 ms (Naive L2), 251.4 -> 247.7 (DGEMM) on one box.
+    // Fused-sum programs keep one CTA per unit: their units' costs differ by term
+    // count and dynamic dispatch balances them better (ABC L1 233.8 vs 236.5 ms).
+    if (maxt == 1)  // single-term programs: no sum code at all
+        return p.grid_cap > 0 ? launch_mm_t<1, true>(p, s) : launch_mm_t<1, false>(p, s);
+    return maxt <= 2 ? launch_mm_t<2, false>(p, s) : launch_mm_t<kMaxTerms, false>(p, s);
 }
 
 cudaError_t launch_repack(const double* src, long long rs, long long cs, long rows, long cols,

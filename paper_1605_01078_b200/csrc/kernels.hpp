@@ -81,6 +81,9 @@ struct alignas(64) MMParams {
     // many k-tiles (short products, where the register read-modify-write would
     // be a large share of the CTA); 0 = never
     int bulk_max_kt;
+    // persistent launch: at most this many CTAs (one per SM), each walking
+    // units blockIdx.x + i * gridDim.x; 0 = one CTA per unit
+    int grid_cap;
 };
 
 cudaError_t launch_mm(const MMParams& p, cudaStream_t s);
