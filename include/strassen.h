@@ -200,7 +200,8 @@ strassen_status strassen_ctx_set_peeling(strassen_ctx* ctx, int enabled);
 strassen_status strassen_ctx_set_pipelining(strassen_ctx* ctx, int enabled);
 
 /* Per-launch CUDA-event timing of the calls on this ctx (off by default).
- * strassen_ctx_last_profile writes a JSON list [{"kernel": name, "ms": t}, ...]
+ * strassen_ctx_last_profile writes a JSON list [{"kernel": name, "ms": t,
+ * "start_ms": offset from the first launch}, ...]
  * for the last compute call into buf (NUL-terminated; STRASSEN_ERR_ALLOC if
  * it did not fit).  Synchronises with the recorded events. */
 strassen_status strassen_ctx_enable_profiling(strassen_ctx* ctx, int enabled);

@@ -243,8 +243,11 @@ std::string Engine::last_profile() {
         float ms = -1.0f;
         if (cudaEventSynchronize(timed[i].stop) == cudaSuccess)
             cudaEventElapsedTime(&ms, timed[i].start, timed[i].stop);
+        float at = 0.0f;  // start relative to the call's first timed launch
+        if (i > 0) cudaEventElapsedTime(&at, timed[0].start, timed[i].start);
         out += (i ? ", " : "") + std::string("{\"kernel\": \"") + timed[i].name +
-               "\", \"ms\": " + std::to_string(ms) + "}";
+               "\", \"ms\": " + std::to_string(ms) + ", \"start_ms\": " + std::to_string(at) +
+               "}";
     }
     return out + "]";
 }
@@ -460,12 +463,12 @@ void plan_windows(const Engine& e, strassen_variant variant, int level, long m, 
     const long qm = ceil_div(m, side), qn = ceil_div(n, side);
     const long tiles_m = ceil_div(qm, kBM), tiles_n = ceil_div(qn, kBN);
     const long sms = e.num_sms > 0 ? e.num_sms : 148;
-    long per_tile = 1;  // CTAs per output tile
-    if (variant == STRASSEN_NAIVE || variant == STRASSEN_AB) {
-        for (int l = 0; l < L; ++l) per_tile *= 7;
-    } else if (tiles_m * tiles_n < 2 * sms) {
+    // CTAs per output tile: one per product (AB / Naive store products; ABC / C
+    // run the ticketed (tile, product) grid), one for DGEMM
+    long per_tile = 1;
+    for (int l = 0; l < L; ++l) per_tile *= 7;
+    if (variant != STRASSEN_NAIVE && variant != STRASSEN_AB && tiles_m * tiles_n < 2 * sms)
         return;  // split-mode sizes: a few milliseconds, nothing to overlap
-    }
     // windows of >= 2 waves each (consecutive windows overlap on two streams);
     // grow the grid keeping it square-ish
     const long max_w = tiles_m * tiles_n * per_tile / (2 * sms);

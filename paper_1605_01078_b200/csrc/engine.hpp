@@ -52,7 +52,7 @@ struct Engine {
     std::vector<Timed> timed;
     void prof_begin(const char* name, cudaStream_t s);
     void prof_end(cudaStream_t s);
-    std::string last_profile();  // JSON list of {"kernel": name, "ms": t}
+    std::string last_profile();  // JSON list of {"kernel", "ms", "start_ms"}
 
     ~Engine();
     void init();
