@@ -158,13 +158,14 @@ strassen_status gemm_impl(strassen_ctx* ctx, bool explicit_stream, cudaStream_t 
         if (windowed) {
             const int L = (variant == STRASSEN_DGEMM) ? 0 : level;
             const long side = 1L << L, qm = (m + side - 1) / side, qn = (n + side - 1) / side;
-            // global index ranges of strip w (width q_w) inside every quadrant
-            // block of extent q, clipped to [0, total) and merged when adjacent
-            auto ranges = [&](long total, long q, long q_w, int w) {
+            // global index ranges of strip w (quadrant bounds b[w], b[w+1]) inside
+            // every quadrant block of extent q, clipped to [0, total) and merged
+            // when adjacent
+            auto ranges = [&](long total, long q, const std::vector<long>& b, int w) {
                 std::vector<std::pair<long, long>> out;
                 for (long I = 0; I < side; ++I) {
-                    const long lo = std::min(total, I * q + w * q_w);
-                    const long hi = std::min(total, I * q + std::min(q, (w + 1) * q_w));
+                    const long lo = std::min(total, I * q + b[w]);
+                    const long hi = std::min(total, I * q + b[w + 1]);
                     if (lo >= hi) continue;
                     if (!out.empty() && out.back().second == lo) out.back().second = hi;
                     else out.emplace_back(lo, hi);
@@ -185,20 +186,20 @@ strassen_status gemm_impl(strassen_ctx* ctx, bool explicit_stream, cudaStream_t 
             W.done = e.ev_win_done;
             W.issue_a = [&](int r) {
                 if (a_windowed)
-                    for (auto [i0, i1] : ranges(m, qm, W.qrows, r))
+                    for (auto [i0, i1] : ranges(m, qm, W.rb, r))
                         copy_block(A.p, a, cs_a, i0, i1, 0, k, cudaMemcpyHostToDevice,
                                    e.copy_stream);
                 // otherwise A was staged whole (or is resident): the event follows it
                 cuda_ck(cudaEventRecord(e.ev_win_a[r], e.copy_stream), "window event");
             };
             W.issue_b = [&](int cw) {
-                for (auto [j0, j1] : ranges(n, qn, W.qcols, cw))
+                for (auto [j0, j1] : ranges(n, qn, W.cb, cw))
                     copy_block(B.p, b, cs_b, 0, k, j0, j1, cudaMemcpyHostToDevice, e.copy_stream);
                 cuda_ck(cudaEventRecord(e.ev_win_b[cw], e.copy_stream), "window event");
             };
             auto c_blocks = [&](int w, cudaMemcpyKind kind, cudaStream_t st) {
-                const auto rr = ranges(m, qm, W.qrows, w / W.cols);
-                const auto cc = ranges(n, qn, W.qcols, w % W.cols);
+                const auto rr = ranges(m, qm, W.rb, w / W.cols);
+                const auto cc = ranges(n, qn, W.cb, w % W.cols);
                 for (auto [i0, i1] : rr)
                     for (auto [j0, j1] : cc)
                         if (kind == cudaMemcpyHostToDevice)

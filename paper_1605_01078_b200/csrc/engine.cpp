@@ -472,10 +472,11 @@ void plan_windows(const Engine& e, strassen_variant variant, int level, long m, 
     // windows of >= 2 waves each (consecutive windows overlap on two streams);
     // grow the grid keeping it square-ish
     const long max_w = tiles_m * tiles_n * per_tile / (2 * sms);
+    constexpr long kUniform = 8;  // uniform strips per side
     long R = 1, Cn = 1;
     for (;;) {
-        const bool grow_c = Cn < Engine::kMaxStrips && Cn < tiles_n && R * (Cn + 1) <= max_w;
-        const bool grow_r = row_windows && R < Engine::kMaxStrips && R < tiles_m &&
+        const bool grow_c = Cn < kUniform && Cn < tiles_n && R * (Cn + 1) <= max_w;
+        const bool grow_r = row_windows && R < kUniform && R < tiles_m &&
                             (R + 1) * Cn <= max_w;
         if (grow_c && (Cn <= R || !grow_r)) ++Cn;
         else if (grow_r) ++R;
@@ -489,10 +490,45 @@ void plan_windows(const Engine& e, strassen_variant variant, int level, long m, 
         }
     }
     if (R * Cn < 2) return;
-    w.qrows = ceil_div(tiles_m, R) * kBM;
-    w.qcols = ceil_div(tiles_n, Cn) * kBN;
-    w.rows = static_cast<int>(ceil_div(qm, w.qrows));
-    w.cols = static_cast<int>(ceil_div(qn, w.qcols));
+    // Strips of equal width, the first one replaced by a ramp 1, 1, 2, 4, ... tiles:
+    // the first windows need only a sliver of A and B, so compute starts after
+    // ~1/16 of the transfer time instead of ~1/4 (windows stay small at the end,
+    // where each one's copy-back is exposed).
+    // optional ramp (experiments): STRASSEN_B200_RAMP="1,1,2" splits the first
+    // strip into those tile counts
+    std::vector<long> ramp;
+    if (const char* rs = std::getenv("STRASSEN_B200_RAMP")) {
+        for (const char* c = rs; *c;) {
+            char* end = nullptr;
+            const long v = std::strtol(c, &end, 10);
+            if (end == c) break;
+            if (v > 0) ramp.push_back(v);
+            c = (*end == ',') ? end + 1 : end;
+        }
+    }
+    auto bounds = [&](long tiles, long count, long q) {
+        const long u = ceil_div(tiles, count);
+        std::vector<long> sizes;
+        long left = u;
+        for (long r : ramp) {
+            if (left <= 0) break;
+            sizes.push_back(std::min(r, left));
+            left -= sizes.back();
+        }
+        if (left > 0) sizes.push_back(left);
+        for (long t = u; t < tiles; t += u) sizes.push_back(std::min(u, tiles - t));
+        std::vector<long> b{0};
+        for (long sz : sizes) b.push_back(std::min(q, b.back() + sz * kBM));
+        b.back() = q;
+        return b;
+    };
+    w.rb = bounds(tiles_m, R, qm);
+    w.cb = bounds(tiles_n, Cn, qn);
+    if (static_cast<long>(w.rb.size()) - 1 > Engine::kMaxStrips ||
+        static_cast<long>(w.cb.size()) - 1 > Engine::kMaxStrips)
+        return;  // too many strips for the event pools: keep the unwindowed call
+    w.rows = static_cast<int>(w.rb.size()) - 1;
+    w.cols = static_cast<int>(w.cb.size()) - 1;
 }
 
 // Dynamic peeling (north star; the reference pads instead, matrix.cpp:14-22):
@@ -627,7 +663,7 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
     }
     // Windows (r, c) in row-major order; without `win` one window covers all.
     const int nr = win ? win->rows : 1, nc = win ? win->cols : 1, nw = nr * nc;
-    const long wrows = win ? win->qrows : qm, wcols = win ? win->qcols : qn;
+
     // Windows alternate between s and the aux stream (ordered after s's work so
     // far); s joins the aux stream at the end.
     cudaStream_t ws[2] = {s, nw > 1 ? e.aux_stream : s};
@@ -762,8 +798,8 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
         prefetch(i + 1);
         const int w = order[i], r = w / nc, c = w % nc;
         cudaStream_t st = ws[i % 2];
-        const long r0 = r * wrows, r1 = std::min(qm, r0 + wrows);
-        const long c0 = c * wcols, c1 = std::min(qn, c0 + wcols);
+        const long r0 = win ? win->rb[r] : 0, r1 = win ? win->rb[r + 1] : qm;
+        const long c0 = win ? win->cb[c] : 0, c1 = win ? win->cb[c + 1] : qn;
         wait_a(st, r);
         wait_b(st, c);
         if (sums) {

@@ -65,7 +65,7 @@ struct Engine {
     bool pipelining = true;  // strassen_ctx_set_pipelining
     cudaStream_t d2h_stream = nullptr;
     cudaEvent_t ev_d2h = nullptr;
-    static constexpr int kMaxStrips = 8, kMaxWindows = kMaxStrips * kMaxStrips;
+    static constexpr int kMaxStrips = 16, kMaxWindows = kMaxStrips * kMaxStrips;
     cudaEvent_t ev_win_a[kMaxStrips] = {}, ev_win_b[kMaxStrips] = {};
     cudaEvent_t ev_win_c[kMaxWindows] = {}, ev_win_done[kMaxWindows] = {};
     // windows alternate between the call stream and aux_stream so that one
@@ -103,7 +103,9 @@ inline void wait_ready(cudaStream_t s, const DView& v) {
 // launch modes, same k order).
 struct Windows {
     int rows = 0, cols = 0;              // R x Cn windows (0: none)
-    long qrows = 0, qcols = 0;           // multiples of the 128 x 128 tile
+    // strip boundaries in quadrant rows / columns (rows + 1, cols + 1 entries;
+    // tile multiples except the last)
+    std::vector<long> rb, cb;
     std::function<void(int)> issue_a;    // enqueue A row strip r, record a_ready[r]
     std::function<void(int)> issue_b;    // enqueue B column strip c, record b_ready[c]
     std::function<void(int)> issue_c;    // enqueue C window w, record c_ready[w]

@@ -1,6 +1,7 @@
 """Kernel timeline of one host-pointer strassen_gemm call (profiling on): where the
 end-to-end time goes beyond the kernels.  usage: e2e_timeline.py [dim] [variant]"""
-import os, sys, time
+import os, signal, sys, time
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_1605_01078_b200 as S
