@@ -298,6 +298,8 @@ bool is_device_pointer(const void* p) {
 // applied in table order).
 struct FusedPlan {
     bool split = false;
+    bool fixup = false;      // split mode finished in the epilogue (no stream pass)
+    int* arrive = nullptr;   // per (tile, product) chunk-arrival counters
     int* tickets = nullptr;  // ordered product-parallel fused epilogue (see kernels.hpp)
     int ticket_ld = 0;
     int ksplit = 1, per = 0;
@@ -342,6 +344,27 @@ FusedPlan plan_fused(Engine& e, cudaStream_t s, const MMParams& P, bool force_sp
     F.ldm = (P.qm + 1) / 2 * 2;  // even: 16-B stores
     F.mstride = F.ldm * P.qn;
     F.M = e.ensure(e.mbuf, static_cast<size_t>(F.mstride) * P.nprod * F.ksplit * 8);
+    // Classical (one product): the last k-chunk CTA of each tile sums the
+    // partials in chunk order and applies the C update -- the stream pass's
+    // arithmetic, in its order, without its launch (1024^3 105 -> 98 us, 2048^3
+    // 598 -> 575 us).  Not for Strassen programs: their 7^L updates per tile
+    // would serialise on the tile's ticket (1024^3 ABC L2 139 -> 696 us), where
+    // the stream pass applies them in parallel over elements.
+    static const bool fixup_on = [] {
+        const char* v = std::getenv("STRASSEN_B200_FIXUP");  // 0 / 1 (experiments)
+        return v ? std::atoi(v) != 0 : true;
+    }();
+    if (!force_split && fixup_on && P.nprod == 1) {
+        const size_t nt = static_cast<size_t>(P.tiles_m) * P.tiles_n;
+        int* buf = reinterpret_cast<int*>(
+            e.ensure(e.ticket_buf, nt * (1 + static_cast<size_t>(P.nprod)) * sizeof(int)));
+        ck(cudaMemsetAsync(buf, 0, nt * (1 + static_cast<size_t>(P.nprod)) * sizeof(int), s),
+           "ticket reset");
+        F.fixup = true;
+        F.tickets = buf;
+        F.arrive = buf + nt;
+        F.ticket_ld = P.tiles_n;
+    }
     return F;
 }
 
@@ -380,6 +403,24 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
         P.grid_cap = cap(P.c_vec && P.ktiles <= P.bulk_max_kt);
         e.prof_begin("mm_kernel", s);
         ck(launch_mm(P, s), "mm_kernel");
+        e.prof_end(s);
+        return 1;
+    }
+    if (F.fixup) {  // split mode finished by the last chunk's epilogue
+        wait_c();
+        P.mode = kEpiRMW;
+        P.split = 1;
+        P.ksplit = F.ksplit;
+        P.kt_per_split = F.per;
+        P.mbase = F.M;
+        P.ldm = F.ldm;
+        P.mstride = F.mstride;
+        P.tickets = F.tickets;
+        P.ticket_ld = F.ticket_ld;
+        P.arrive = F.arrive;
+        P.grid_cap = cap(false);
+        e.prof_begin("mm_kernel", s);
+        ck(launch_mm(P, s), "mm_kernel (split, fused epilogue)");
         e.prof_end(s);
         return 1;
     }

@@ -673,7 +673,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         // than the register path saves once the mainloop is long); anything
         // else takes the register read-modify-write below.
         bool bulk = P.mode == kEpiRMW && P.c_vec && p_hi - p_lo == 1 &&
-                    kt_hi - kt_lo <= P.bulk_max_kt && !persistent;
+                    kt_hi - kt_lo <= P.bulk_max_kt && !persistent && !(P.split && P.ksplit > 1);
         for (int u = 0; u < pd.nc && bulk; ++u) {
             const int cq = pd.cq[u];
             bulk = tm * kBM + kBM <= P.crows[cq] && tn * kBN + kBN <= P.ccols[cq];
@@ -734,6 +734,63 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                 }
             }
             continue;  // next product (none: single-product CTA)
+        }
+        if (P.mode == kEpiRMW && P.arrive && P.ksplit > 1) {
+            // ---- k-split fused epilogue: partial out, the last chunk sums ----
+            const int s_idx = kt_lo / P.kt_per_split;
+            const long long ldm = P.ldm;
+            {
+                double* Mo = P.mbase + static_cast<long long>(p * P.ksplit + s_idx) * P.mstride;
+#pragma unroll
+                for (int nf = 0; nf < 4; ++nf)
+#pragma unroll
+                    for (int h = 0; h < 4; ++h)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int row = mrow0 + 16 * h;
+                            const int col = ncol0 + 8 * nf + (e ? c1 : c0);
+                            if (col >= P.qn || row >= P.qm) continue;
+                            double* dst = Mo + row + static_cast<long long>(col) * ldm;
+                            __stcg(reinterpret_cast<double2*>(dst),
+                                   make_double2(acc[2 * h][nf][e], acc[2 * h + 1][nf][e]));
+                        }
+            }
+            __threadfence();
+            consumer_bar();
+            __shared__ int last_flag;
+            if (threadIdx.x == 0) {
+                int* cnt = P.arrive + (tm * P.ticket_ld + tn) * P.nprod + p;
+                last_flag = atomicAdd(cnt, 1) == P.ksplit - 1;
+            }
+            consumer_bar();
+            if (!last_flag) continue;  // another chunk finishes this product
+            __threadfence();
+            // M_p = P_0 + P_1 + ... in s order (the stream pass's order), read
+            // back from L2 (this CTA's own partial included)
+            const double* Mp = P.mbase + static_cast<long long>(p * P.ksplit) * P.mstride;
+            for (int sp = 0; sp < P.ksplit; ++sp) {
+#pragma unroll
+                for (int nf = 0; nf < 4; ++nf)
+#pragma unroll
+                    for (int h = 0; h < 4; ++h)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int row = mrow0 + 16 * h;
+                            const int col = ncol0 + 8 * nf + (e ? c1 : c0);
+                            double2 x = make_double2(0.0, 0.0);
+                            if (col < P.qn && row < P.qm)
+                                x = __ldcg(reinterpret_cast<const double2*>(
+                                    Mp + static_cast<long long>(sp) * P.mstride + row +
+                                    static_cast<long long>(col) * ldm));
+                            if (sp == 0) {
+                                acc[2 * h][nf][e] = x.x;
+                                acc[2 * h + 1][nf][e] = x.y;
+                            } else {
+                                acc[2 * h][nf][e] += x.x;
+                                acc[2 * h + 1][nf][e] += x.y;
+                            }
+                        }
+            }
         }
         int* ticket = nullptr;  // ordered epilogue: wait for the previous product
         if (P.mode == kEpiRMW && P.tickets) {

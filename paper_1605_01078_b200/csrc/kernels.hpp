@@ -77,6 +77,11 @@ struct alignas(64) MMParams {
     // every C tile still receives the products in table order
     int* tickets;
     int ticket_ld;              // tickets row stride (tile columns of the whole call)
+    // k-split fused epilogue (split grid, ksplit > 1, kEpiRMW): every CTA of
+    // (tile, product) stores its partial to M_{p,s}; the last to arrive
+    // (counter arrive[tile * nprod + p]) sums the partials in s order and does
+    // the ticketed read-modify-write -- no separate stream pass
+    int* arrive;
     // fused epilogue through TMA bulk f64 reductions for CTAs of at most this
     // many k-tiles (short products, where the register read-modify-write would
     // be a large share of the CTA); 0 = never
