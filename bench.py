@@ -24,7 +24,9 @@ Multi-GPU (torchrun, N > 1): SUMMA over NCCL (paper_1605_01078_b200/summa.py),
 weak scaling.  The pr x pc grid comes from grid_for(N) (1x2, 2x2, 2x4).  Rank
 (i, j) owns a 16384 x 16384 block of C, and the global problem is
 m = 16384*pr, n = 16384*pc, k = 16384.  A panels are broadcast along rows and
-B panels along columns, overlapped with the local Strassen rank-b updates.
+B panels along columns, overlapped with the local Strassen rank-b updates
+(panel width b = 8192: two 16384^2 x 8192 local updates per step; a panel
+straddling the k/pc columns a rank owns is assembled from per-owner pieces).
 Every rank therefore does one 16384^3 of work per step; time = max over ranks.
 """
 import argparse
@@ -461,6 +463,26 @@ def run_summa(args, rank, world, local, colmajor, barrier, max_over_ranks):
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     flops = 2.0 * L.m * L.n * L.k
+    # roofline of the local update's mm_kernel: one profiled panel-shaped local call
+    # (m_l x n_l x b) on this rank, timed by the library's events on the launch stream
+    peaks = json.load(open(os.path.join(ROOT, "profiles", "fp64_peaks.json")))
+    lctx = local_gemm.ctx
+    ap, bp = colmajor(L.m_l, L.b), colmajor(L.b, L.n_l)
+    lctx.enable_profiling(True)
+    lctx.gemm_device(args.variant, args.level, 1.0, ap, bp, C_l, torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    prof = lctx.last_profile()
+    lctx.enable_profiling(False)
+    del ap, bp
+    mm_ms = sum(x["ms"] for x in prof if x["kernel"] == "mm_kernel")
+    f_exec = executed_flops(L.m_l, L.n_l, L.b, args.level, args.variant)
+    achieved = max_over_ranks(-(f_exec / (mm_ms * 1e-3) / 1e12)) * -1.0  # min over ranks
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["dmma_tflops"],
+                "unit": "TFLOP/s", "frac": achieved / peaks["dmma_tflops"], "traffic": None,
+                "flops_per_launch": f_exec, "kernel_ms": mm_ms, "kernel": "mm_kernel",
+                "launches_per_step": launches // max(args.steps, 1), "step_profile_ms": prof,
+                "scope": "one local update (m_l x n_l x b) per rank; min over ranks",
+                "peak_source": "measured FP64 DMMA peak, profiles/fp64_peaks.json"}
     line = {
         "metric": "effective FP64 TFLOPS (2mnk/t)", "value": flops / (ms * 1e-3) / 1e12,
         "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -471,6 +493,7 @@ def run_summa(args, rank, world, local, colmajor, barrier, max_over_ranks):
                    "level": args.level, "m": L.m, "n": L.n, "k": L.k, "panel_b": L.b,
                    "grid": [L.pr, L.pc], "parallelism": f"summa{L.pr}x{L.pc}",
                    "l2": "inputs larger than the 126 MB L2"},
+        "roofline": roofline,
         "clocks": clk.summary(),
         "gpu_launches": launches,
     }

@@ -12,10 +12,11 @@ design followed here.
   B_ij = B[i*k_r:(i+1)*k_r, j*n_l:(j+1)*n_l]   (k_r = k/pr, n_l = n/pc)
   C_ij = C[i*m_l:(i+1)*m_l, j*n_l:(j+1)*n_l]
 * One exchange step per k-panel p of width b:
-  * the rank in process row i owning A columns [p*b, (p+1)*b) broadcasts that
-    m_l x b slice along row i;
-  * the rank in process column j owning B rows [p*b, (p+1)*b) broadcasts that
-    b x n_l slice along column j.
+  * the rank(s) in process row i owning A columns [p*b, (p+1)*b) broadcast their
+    m_l x w pieces along row i (one broadcast per owner when the panel straddles
+    the k_c = k/pc columns a rank owns);
+  * the rank(s) in process column j owning B rows [p*b, (p+1)*b) broadcast their
+    w x n_l pieces along column j.
   Then every rank runs C_ij += alpha * A_panel @ B_panel locally, with the chosen variant
   and level (strassen_gemm_device on the current CUDA stream).
 * Broadcasts for panel p+1 are issued asynchronously before the local update of panel p,
@@ -80,7 +81,7 @@ class Layout:
         return self.k // self.b
 
     def a_owner_col(self, p):
-        """Process column owning A panel p, and the local column offset."""
+        """Process column owning the first column of A panel p, and its local offset."""
         g = p * self.b
         return g // self.k_c, g % self.k_c
 
@@ -88,18 +89,42 @@ class Layout:
         g = p * self.b
         return g // self.k_r, g % self.k_r
 
+    @staticmethod
+    def _pieces(g0, width, per_owner):
+        """Split global k range [g0, g0+width) at owner boundaries (multiples of per_owner):
+        a list of (owner, local offset, piece width, offset inside the panel)."""
+        out, g = [], g0
+        while g < g0 + width:
+            owner, off = divmod(g, per_owner)
+            w = min(per_owner - off, g0 + width - g)
+            out.append((owner, off, w, g - g0))
+            g += w
+        return out
+
+    def a_pieces(self, p):
+        """A panel p by owning process column: (col, local col offset, width, panel offset)."""
+        return self._pieces(p * self.b, self.b, self.k_c)
+
+    def b_pieces(self, p):
+        """B panel p by owning process row: (row, local row offset, width, panel offset)."""
+        return self._pieces(p * self.b, self.b, self.k_r)
+
 
 def make_layout(m, n, k, p, b=None):
+    """Panels may straddle owner boundaries: a panel is then assembled from one broadcast
+    per owning piece, so the panel width (the local update's k) is not capped by the
+    k / pc columns of A a rank owns.  Default b: k halved while above 8192 (16384^2 local
+    updates: naive L2 45.0 TF/s at k = 8192 against 43.5 at 4096, profiles/r01_sweep_rankk.csv,
+    with one 1 GB panel broadcast exposed)."""
     pr, pc = grid_for(p)
     if m % pr or n % pc or k % pr or k % pc:
         raise ValueError(f"m={m}, n={n}, k={k} must divide the {pr}x{pc} grid")
-    step = math.gcd(k // pr, k // pc)  # a panel must not straddle an owner boundary
     if b is None:
-        b = step
-        while b > 4096 and b % 2 == 0:  # bound the panel buffers
+        b = k
+        while b > 8192 and b % 2 == 0:  # bound the panel buffers
             b //= 2
-    if step % b:
-        raise ValueError(f"panel width {b} must divide gcd(k/pr, k/pc) = {step}")
+    if b < 1 or k % b:
+        raise ValueError(f"panel width {b} must divide k = {k}")
     return Layout(m, n, k, pr, pc, b)
 
 
@@ -155,6 +180,7 @@ def _default_local_gemm(variant, level):
         else:
             ctx.gemm(variant, level, alpha, a, b, c)
         return ctx.last_launches()
+    run.ctx = ctx  # for profiling one local update (bench.py roofline at N > 1)
     return run
 
 
@@ -179,21 +205,42 @@ def summa(layout: Layout, comm: TorchComm, A_l: torch.Tensor, B_l: torch.Tensor,
     bbuf = [t.t() for t in bbase]
 
     def post(p):
+        """Issue panel p's broadcasts into buffer p % 2.  Returns the pending works and the
+        B pieces that arrive in contiguous staging (a B panel straddling process rows:
+        its row pieces are strided in the column-major panel) to be placed after the wait."""
         s = p % 2
-        ac, aoff = L.a_owner_col(p)
-        br, boff = L.b_owner_row(p)
-        if comm.j == ac:
-            abuf[s].copy_(A_l[:, aoff:aoff + L.b])
-        if comm.i == br:
-            bbuf[s].copy_(B_l[boff:boff + L.b, :])
-        return [w for w in (comm.bcast_row(abase[s], ac), comm.bcast_col(bbase[s], br)) if w]
+        works, fixups = [], []
+        for oc, lo, w, po in L.a_pieces(p):   # column pieces: contiguous in abase
+            if comm.j == oc:
+                abuf[s][:, po:po + w].copy_(A_l[:, lo:lo + w])
+            works.append(comm.bcast_row(abase[s][po:po + w], oc))
+        pieces = L.b_pieces(p)
+        for idx, (orow, lo, w, po) in enumerate(pieces):
+            if len(pieces) == 1:
+                dst = bbase[s]
+                if comm.i == orow:
+                    bbuf[s].copy_(B_l[lo:lo + w, :])
+            else:
+                key = (s, idx, w)
+                if key not in bstage:
+                    bstage[key] = torch.empty((L.n_l, w), dtype=torch.float64, device=dev)
+                dst = bstage[key]
+                if comm.i == orow:
+                    dst.t().copy_(B_l[lo:lo + w, :])
+                fixups.append((dst, po, w))
+            works.append(comm.bcast_col(dst, orow))
+        return [x for x in works if x], fixups
 
+    bstage = {}
     pending = post(0)
     launches = 0
     for p in range(L.panels):
-        nxt = post(p + 1) if p + 1 < L.panels else []
-        for w in pending:
+        nxt = post(p + 1) if p + 1 < L.panels else ([], [])
+        works, fixups = pending
+        for w in works:
             w.wait()
+        for src, po, w in fixups:
+            bbuf[p % 2][po:po + w, :].copy_(src.t())
         n = gemm(alpha, abuf[p % 2], bbuf[p % 2], C_l)
         launches += n if isinstance(n, int) else 1
         pending = nxt
@@ -215,11 +262,11 @@ def summa_loopback(layout: Layout, A_blocks: List[torch.Tensor], B_blocks: List[
     abuf = torch.empty((L.b, L.m_l), dtype=torch.float64, device=dev).t()
     bbuf = torch.empty((L.n_l, L.b), dtype=torch.float64, device=dev).t()
     for p in range(L.panels):
-        ac, aoff = L.a_owner_col(p)
-        br, boff = L.b_owner_row(p)
         for r in range(P):
             i, j = divmod(r, L.pc)
-            abuf.copy_(A_blocks[i * L.pc + ac][:, aoff:aoff + L.b])   # row-i broadcast
-            bbuf.copy_(B_blocks[br * L.pc + j][boff:boff + L.b, :])   # column-j broadcast
+            for oc, lo, w, po in L.a_pieces(p):        # row-i broadcasts
+                abuf[:, po:po + w].copy_(A_blocks[i * L.pc + oc][:, lo:lo + w])
+            for orow, lo, w, po in L.b_pieces(p):      # column-j broadcasts
+                bbuf[po:po + w, :].copy_(B_blocks[orow * L.pc + j][lo:lo + w, :])
             gemm(alpha, abuf, bbuf, C_blocks[r])
     return L.panels

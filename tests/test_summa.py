@@ -32,18 +32,26 @@ def test_grids_and_layout():
     assert (L.pr, L.pc, L.m_l, L.n_l, L.k_c, L.k_r, L.panels) == (2, 4, 32, 24, 12, 24, 12)
     assert L.a_owner_col(5) == (1, 8)   # k columns 20..23 live on process column 1
     assert L.b_owner_row(7) == (1, 4)   # k rows 28..31 live on process row 1
+    # panels straddling owner boundaries are assembled from per-owner pieces
+    L2 = SU.make_layout(64, 96, 48, 8, b=24)
+    assert L2.a_pieces(1) == [(2, 0, 12, 0), (3, 0, 12, 12)]
+    assert L2.b_pieces(1) == [(1, 0, 24, 0)]
+    assert SU.make_layout(64, 96, 48, 8, b=48).b_pieces(0) == [(0, 0, 24, 0), (1, 0, 24, 24)]
+    assert SU.make_layout(65536, 65536, 65536, 8).b == 8192
+    assert SU.make_layout(32768, 65536, 16384, 8).b == 8192
     with pytest.raises(ValueError):
         SU.make_layout(64, 96, 48, 8, b=5)
     with pytest.raises(ValueError):
         SU.make_layout(63, 96, 48, 8)
 
 
-@pytest.mark.parametrize("P", [1, 2, 4, 8])
-def test_loopback_schedule_matches_dense(P):
+@pytest.mark.parametrize("P,b", [(1, 4), (2, 4), (4, 4), (8, 4), (2, 64), (4, 64), (8, 32),
+                                 (8, 64)])
+def test_loopback_schedule_matches_dense(P, b):
     m, n, k = 48, 40, 64
     A, B, C = dense(m, n, k, 7)
     want = C + 0.5 * (A @ B)
-    L = SU.make_layout(m, n, k, P, b=4)
+    L = SU.make_layout(m, n, k, P, b=b)
     blocks = [SU.local_blocks(L, r, A, B, C) for r in range(P)]
     Cb = [c.clone() for _, _, c in blocks]
     SU.summa_loopback(L, [a for a, _, _ in blocks], [b for _, b, _ in blocks], Cb, alpha=0.5,
@@ -79,7 +87,7 @@ def _worker(rank, world, port, m, n, k, b, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,b", [(2, 8), (4, 4), (4, 16)])
+@pytest.mark.parametrize("world,b", [(2, 8), (4, 4), (4, 16), (2, 64), (4, 64), (4, 32)])
 def test_summa_gloo_matches_dense(world, b):
     m, n, k = 32, 48, 64
     ctx = mp.get_context("spawn")
@@ -99,12 +107,13 @@ def test_summa_gloo_matches_dense(world, b):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("P,variant,level", [(2, "abc", 1), (4, "abc", 2), (8, "c", 2)])
-def test_loopback_on_gpu_with_strassen_kernels(cuda, P, variant, level):
+@pytest.mark.parametrize("P,variant,level,b", [(2, "abc", 1, 256), (4, "abc", 2, 256),
+                                               (8, "c", 2, 256), (8, "naive", 2, 2048)])
+def test_loopback_on_gpu_with_strassen_kernels(cuda, P, variant, level, b):
     """Full SUMMA data path with the real sm_100a kernels (virtual ranks, one GPU)."""
     m, n, k = 1024, 2048, 2048
     A, B, C = (x.to(cuda) for x in dense(m, n, k, 3))
-    L = SU.make_layout(m, n, k, P, b=256)
+    L = SU.make_layout(m, n, k, P, b=b)  # b = 2048: panels straddle A and B owners
     blocks = [SU.local_blocks(L, r, A, B, C) for r in range(P)]
     Cb = [c.t().contiguous().t() for _, _, c in blocks]  # column-major C blocks
     SU.summa_loopback(L, [a for a, _, _ in blocks], [b for _, b, _ in blocks], Cb,
