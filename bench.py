@@ -71,7 +71,10 @@ def parse():
 
 
 def table_counts(level):
-    return {0: (1, 0, 0, 1), 1: (7, 5, 5, 12), 2: (49, 95, 95, 144)}[level]
+    # level 3 (naive / c only): 343 products; its C updates are those of the seven
+    # level-2 calls (7 x 144 at the inner quadrant size) -- the outer level is a
+    # stream pass, not mm_kernel work
+    return {0: (1, 0, 0, 1), 1: (7, 5, 5, 12), 2: (49, 95, 95, 144), 3: (343, 0, 0, 1008)}[level]
 
 
 def executed_flops(m, n, k, level, variant="abc"):
@@ -104,6 +107,8 @@ def hbm_bytes(kernel, m, n, k, level, ordinal=0):
     sum pass (gather form): every source quadrant read once + every sum written once;
     stream pass: every M_p read once + each C element read and written once.
     """
+    if level > 2:  # sum / stream passes at two levels of the recursion: not tabulated
+        return None
     s = 1 << level
     qm, qn, qk = -(-m // s), -(-n // s), -(-k // s)
     mul, aa, ba, cu = table_counts(level)
@@ -281,6 +286,7 @@ def main():
         return x.t()  # (r, c) with strides (1, r)
 
     ctx = S.Ctx()
+    ctx.set_max_level(3)  # admits naive3 / c3 (B200 extension) beside the reference's levels
     stream = torch.cuda.current_stream()
     if world > 1:
         return run_summa(args, rank, world, local, colmajor, barrier, max_over_ranks)
@@ -370,7 +376,7 @@ def main():
     if not args.no_variants:
         table = {}
         for v, lv in [("dgemm", 0), ("abc", 1), ("ab", 1), ("naive", 1), ("c", 1), ("abc", 2),
-                      ("ab", 2), ("naive", 2), ("c", 2)]:
+                      ("ab", 2), ("naive", 2), ("c", 2), ("naive", 3), ("c", 3)]:
             tt, _, _ = time_device(v, lv, 2, 1)
             t_ms = max_over_ranks(tt) / 2
             table[f"{v}{lv}"] = {"value": world * flops / (t_ms * 1e-3) / 1e12, "ms": t_ms}

@@ -199,6 +199,14 @@ strassen_status strassen_ctx_set_peeling(strassen_ctx* ctx, int enabled);
  * Results are bitwise identical either way. */
 strassen_status strassen_ctx_set_pipelining(strassen_ctx* ctx, int enabled);
 
+/* Highest Strassen level this ctx accepts: 2 (default, the reference's limit,
+ * capi.cpp:133-135 / table.cpp:101) or 3.  At 3, STRASSEN_NAIVE and STRASSEN_C
+ * also run level 3: one materialised outer level (the one-level table,
+ * table.cpp:18-33) over level-2 calls of the same variant, i.e. the 343
+ * products of the composed level-3 table (acceptance.cpp:86-88).  ABC / AB at
+ * level 3 stay STRASSEN_ERR_PARAM.  Other values: STRASSEN_ERR_PARAM. */
+strassen_status strassen_ctx_set_max_level(strassen_ctx* ctx, int max_level);
+
 /* Per-launch CUDA-event timing of the calls on this ctx (off by default).
  * strassen_ctx_last_profile writes a JSON list [{"kernel": name, "ms": t,
  * "start_ms": offset from the first launch}, ...]

@@ -121,6 +121,7 @@ def _declare(lib):
         "strassen_ctx_enable_profiling": (_ST, [vp, C.c_int]),
         "strassen_ctx_set_peeling": (_ST, [vp, C.c_int]),
         "strassen_ctx_set_pipelining": (_ST, [vp, C.c_int]),
+        "strassen_ctx_set_max_level": (_ST, [vp, C.c_int]),
         "strassen_ctx_last_profile": (_ST, [vp, C.c_char_p, _L]),
         "strassen_select": (_ST, [_L, _L, _L, C.POINTER(C.c_int), C.POINTER(C.c_int), _dp]),
         "strassen_predict_b200": (_ST, [C.c_int, C.c_int, _L, _L, _L, _dp]),
@@ -243,6 +244,10 @@ class Ctx:
     def set_pipelining(self, on=True):
         """Host calls: column-window pipelining of transfers and kernels (default on)."""
         _check(self._l.strassen_ctx_set_pipelining(self.ptr, int(bool(on))), "set_pipelining")
+
+    def set_max_level(self, level):
+        """2 (default) or 3: level 3 for the naive / c variants (B200 extension)."""
+        _check(self._l.strassen_ctx_set_max_level(self.ptr, int(level)), "set_max_level")
 
     def enable_profiling(self, on=True):
         _check(self._l.strassen_ctx_enable_profiling(self.ptr, int(bool(on))), "enable_profiling")

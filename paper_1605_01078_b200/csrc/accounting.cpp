@@ -136,7 +136,7 @@ void count_call(strassen_variant variant, int level, long m, long n, long k,
     const std::vector<Ext> ga = partition(m, k, level, qm, qk);
     const std::vector<Ext> gb = partition(k, n, level, qk2, qn);
     const std::vector<Ext> gc = partition(m, n, level, qm2, qn2);
-    for (const Product& e : program_for_level(level).products) {
+    for (const Product& e : (level == 3 ? program_level3() : program_for_level(level)).products) {
         const std::vector<Ext> a = pick(e.a, ga), b = pick(e.b, gb), d = pick(e.c, gc);
         if (all_empty(a) || all_empty(b) || all_empty(d)) continue;
         if (variant == STRASSEN_ABC) {

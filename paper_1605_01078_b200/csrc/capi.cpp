@@ -123,7 +123,13 @@ strassen_status gemm_impl(strassen_ctx* ctx, bool explicit_stream, cudaStream_t 
                           long rs_b, long cs_b, double* c, long rs_c, long cs_c, bool has_beta,
                           double beta) {
     if (!ctx || !a || !b || !c) return STRASSEN_ERR_NULL;
-    if (strassen_status st = check_variant_level(variant, level)) return st;
+    if (strassen_status st = check_variant_level(variant, level)) {
+        // level 3 (B200 extension) only after strassen_ctx_set_max_level(ctx, 3),
+        // and only for the materialising variants (Naive, C)
+        const bool l3 = level == 3 && ctx->engine.max_level >= 3 &&
+                        (variant == STRASSEN_NAIVE || variant == STRASSEN_C);
+        if (!l3) return st;
+    }
     return guarded([&] {
         validate_call(variant, m, n, k, ctx->blocking);
         sb200::Engine& e = ctx->engine;
@@ -353,6 +359,13 @@ strassen_status strassen_ctx_set_peeling(strassen_ctx* ctx, int enabled) {
 strassen_status strassen_ctx_set_pipelining(strassen_ctx* ctx, int enabled) {
     if (!ctx) return STRASSEN_ERR_NULL;
     ctx->engine.pipelining = enabled != 0;
+    return STRASSEN_OK;
+}
+
+strassen_status strassen_ctx_set_max_level(strassen_ctx* ctx, int max_level) {
+    if (!ctx) return STRASSEN_ERR_NULL;
+    if (max_level < 2 || max_level > 3) return STRASSEN_ERR_PARAM;
+    ctx->engine.max_level = max_level;
     return STRASSEN_OK;
 }
 

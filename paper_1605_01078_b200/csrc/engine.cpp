@@ -196,7 +196,8 @@ Engine::~Engine() {
             if (arr[w]) cudaEventDestroy(arr[w]);
     for (cudaEvent_t ev : {ev_d2h, ev_fork, ev_join})
         if (ev) cudaEventDestroy(ev);
-    for (DeviceBuffer* b : {&stage_a, &stage_b, &stage_c, &pack_a, &pack_b, &mbuf, &tabuf, &tbbuf, &ticket_buf})
+    for (DeviceBuffer* b : {&stage_a, &stage_b, &stage_c, &pack_a, &pack_b, &mbuf, &tabuf, &tbbuf, &ticket_buf,
+                               &pack_a3, &pack_b3, &l3_a, &l3_b, &l3_m})
         if (b->ptr) cudaFree(b->ptr);
 }
 
@@ -275,7 +276,8 @@ double* Engine::ensure(DeviceBuffer& b, size_t bytes) {
 
 size_t Engine::workspace_bytes() const {
     size_t t = 0;
-    for (const DeviceBuffer* b : {&stage_a, &stage_b, &stage_c, &pack_a, &pack_b, &mbuf, &tabuf, &tbbuf, &ticket_buf})
+    for (const DeviceBuffer* b : {&stage_a, &stage_b, &stage_c, &pack_a, &pack_b, &mbuf, &tabuf, &tbbuf, &ticket_buf,
+                               &pack_a3, &pack_b3, &l3_a, &l3_b, &l3_m})
         t += b->bytes;
     return t;
 }
@@ -474,6 +476,16 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
 namespace {
 long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level, double alpha,
                   const DView& A, const DView& B, const DView& C, const Windows* win);
+long run_outer(Engine& e, cudaStream_t s, strassen_variant variant, int level, double alpha,
+               const DView& A, const DView& B, const DView& C);
+
+// Levels 0-2 run as one batched program (run_strassen); level 3 (B200
+// extension) as one materialised outer level over level-2 calls (run_outer).
+long run_level(Engine& e, cudaStream_t s, strassen_variant variant, int level, double alpha,
+               const DView& A, const DView& B, const DView& C, const Windows* win) {
+    if (variant != STRASSEN_DGEMM && level == 3) return run_outer(e, s, variant, level, alpha, A, B, C);
+    return run_strassen(e, s, variant, level, alpha, A, B, C, win);
+}
 
 DView sub(const DView& v, long r0, long c0, long rows, long cols) {
     DView o = v;
@@ -500,6 +512,7 @@ void plan_windows(const Engine& e, strassen_variant variant, int level, long m, 
     (void)k;
     w.rows = w.cols = 0;
     const int L = (variant == STRASSEN_DGEMM) ? 0 : level;
+    if (L > 2) return;  // level 3: the outer level runs whole-operand (run_outer)
     const long side = 1L << L;
     const long qm = ceil_div(m, side), qn = ceil_div(n, side);
     const long tiles_m = ceil_div(qm, kBM), tiles_n = ceil_div(qn, kBN);
@@ -612,9 +625,9 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
         }
         return launches;
     }
-    if (!peel) return run_strassen(e, s, variant, level, alpha, A, B, C, win);
-    long launches = run_strassen(e, s, variant, level, alpha, sub(A, 0, 0, me, ke),
-                                 sub(B, 0, 0, ke, ne), sub(C, 0, 0, me, ne), nullptr);
+    if (!peel) return run_level(e, s, variant, level, alpha, A, B, C, win);
+    long launches = run_level(e, s, variant, level, alpha, sub(A, 0, 0, me, ke),
+                              sub(B, 0, 0, ke, ne), sub(C, 0, 0, me, ne), nullptr);
     if (ke < k)
         launches += run_strassen(e, s, STRASSEN_DGEMM, 0, alpha, sub(A, 0, ke, me, k - ke),
                                  sub(B, ke, 0, k - ke, ne), sub(C, 0, 0, me, ne), nullptr);
@@ -875,6 +888,162 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
     }
     join();
     return launches;
+}
+}  // namespace
+
+namespace {
+// Level 3 for the materialising variants (Naive, C) -- a B200 extension: the
+// reference composes level-3 tables symbolically (table.cpp:47-67,
+// acceptance.cpp:86-88) but its runtime stops at level 2 (table.cpp:101).
+// Level 3 = the one-level table (table.cpp:18-33) applied with Naive semantics
+// (variants.cpp:170-208) over level-2 calls of the same variant:
+//   1. every outer operand sum S_r = sum_u c_u X_{q_u} (quadrants of the even
+//      ceil partition, matrix.cpp:8-35; clipped terms read as zero) in one
+//      sum_gather launch per side -- a full, unclipped single +1 term is passed
+//      through as a view instead;
+//   2. M_r := S^A_r S^B_r by the level-2 program (into zeroed temporaries, with
+//      alpha = 1 as AB / Naive do, variants.cpp:161);
+//   3. one stream pass C_q += (alpha gamma) M_r in table order (variants.cpp:99-109).
+// The products are those of the composed level-3 table (entry 49 r + inner);
+// only the association of the operand-sum and update additions differs.
+long run_outer(Engine& e, cudaStream_t s, strassen_variant variant, int level, double alpha,
+               const DView& A, const DView& B, const DView& C) {
+    const long m = A.rows, k = A.cols, n = B.cols;
+    const long qm = ceil_div(m, 2), qk = ceil_div(k, 2), qn = ceil_div(n, 2);
+    long launches = 0;
+    const TmaOperand ta = prepare(e, s, A, qm, qk, 2, e.pack_a3, launches);
+    const TmaOperand tb = prepare(e, s, B, qk, qn, 2, e.pack_b3, launches);
+    std::vector<bool> a_live(4), b_live(4), c_live(4);
+    std::vector<QuadView> cq(4);
+    for (int I = 0; I < 2; ++I)
+        for (int J = 0; J < 2; ++J) {
+            a_live[I * 2 + J] = quad_rows(ta, I) > 0 && quad_cols(ta, J) > 0;
+            b_live[I * 2 + J] = quad_rows(tb, I) > 0 && quad_cols(tb, J) > 0;
+            cq[I * 2 + J] = c_quad(C, qm, qn, I, J);
+            c_live[I * 2 + J] = cq[I * 2 + J].rows > 0 && cq[I * 2 + J].cols > 0;
+        }
+    struct Live {
+        Terms a, b, c;
+    };
+    std::vector<Live> live;
+    for (const Product& pr : program_for_level(1).products) {
+        Live l{live_terms(pr.a, a_live), live_terms(pr.b, b_live), live_terms(pr.c, c_live)};
+        if (l.a.empty() || l.b.empty() || l.c.empty()) continue;  // variants.cpp:131-133
+        live.push_back(std::move(l));
+    }
+    if (live.empty()) return launches;
+
+    // outer operands: a view of the quadrant, or a materialised sum (ld multiple of 4)
+    const long long lda_t = ((qm + 3) / 4) * 4, ldb_t = ((qk + 3) / 4) * 4;
+    const long long ldm = ((qm + 3) / 4) * 4;
+    std::vector<DView> opA(live.size()), opB(live.size());
+    for (int sd = 0; sd < 2; ++sd) {
+        const TmaOperand& t = sd == 0 ? ta : tb;
+        const long rows = sd == 0 ? qm : qk, cols = sd == 0 ? qk : qn;
+        const long long ld = sd == 0 ? lda_t : ldb_t;
+        std::unique_ptr<SumBatchParams> SB(new SumBatchParams);
+        std::memset(SB.get(), 0, sizeof(SumBatchParams));
+        SB->rows = rows;
+        SB->cols = cols;
+        SB->ld = ld;
+        std::vector<int> job_of(live.size(), -1);
+        for (size_t p = 0; p < live.size(); ++p) {
+            const Terms& terms = sd == 0 ? live[p].a : live[p].b;
+            DView& op = sd == 0 ? opA[p] : opB[p];
+            op.rows = rows;
+            op.cols = cols;
+            op.rs = 1;
+            const int q0 = terms[0].first;
+            if (terms.size() == 1 && terms[0].second == 1 && quad_rows(t, q0 / 2) == rows &&
+                quad_cols(t, q0 % 2) == cols) {
+                op.p = const_cast<double*>(quad_origin(t, q0 / 2, q0 % 2));
+                op.cs = t.ld;
+                op.ready = t.ready;
+                continue;
+            }
+            const int z = SB->njobs++;
+            job_of[p] = z;
+            SB->nterms[z] = static_cast<int>(terms.size());
+            for (size_t u = 0; u < terms.size(); ++u) {
+                const int qi = terms[u].first;
+                SumTerm& st = SB->t[z][u];
+                st.x = quad_origin(t, qi / 2, qi % 2);
+                st.rows = static_cast<int>(quad_rows(t, qi / 2));
+                st.cols = static_cast<int>(quad_cols(t, qi % 2));
+                st.ld = t.ld;
+                st.coeff = terms[u].second;
+            }
+        }
+        if (SB->njobs) {
+            double* T = e.ensure(sd == 0 ? e.l3_a : e.l3_b,
+                                 static_cast<size_t>(SB->njobs) * ld * cols * 8);
+            for (size_t p = 0; p < live.size(); ++p) {
+                if (job_of[p] < 0) continue;
+                double* dst = T + static_cast<size_t>(job_of[p]) * ld * cols;
+                SB->dst[job_of[p]] = dst;
+                DView& op = sd == 0 ? opA[p] : opB[p];
+                op.p = dst;
+                op.cs = ld;
+            }
+            if (t.ready) ck(cudaStreamWaitEvent(s, t.ready, 0), "wait operand");
+            e.prof_begin("sum_gather_kernel", s);
+            ck(launch_sum_batch(*SB, s), sd == 0 ? "outer sums (A)" : "outer sums (B)");
+            e.prof_end(s);
+            ++launches;
+        }
+    }
+
+    // products M_r = S^A_r S^B_r by the level-2 program, alpha = 1, into zeroed
+    // temporaries (the inner stream pass / fused epilogue accumulates into M_r)
+    const size_t mstride = static_cast<size_t>(ldm) * qn;
+    double* M = e.ensure(e.l3_m, live.size() * mstride * 8);
+    ck(cudaMemsetAsync(M, 0, live.size() * mstride * 8, s), "zero products");
+    for (size_t p = 0; p < live.size(); ++p) {
+        DView Mp;
+        Mp.p = M + p * mstride;
+        Mp.rows = qm;
+        Mp.cols = qn;
+        Mp.rs = 1;
+        Mp.cs = ldm;
+        launches += run_device(e, s, variant, level - 1, 1.0, opA[p], opB[p], Mp, nullptr);
+    }
+
+    // C_q += alpha gamma M_r, each quadrant's updates in table order
+    std::unique_ptr<StreamParams> SP(new StreamParams);
+    std::memset(SP.get(), 0, sizeof(StreamParams));
+    for (int qi = 0; qi < 4; ++qi) {
+        SP->cptr[qi] = cq[qi].p;
+        SP->crows[qi] = static_cast<int>(cq[qi].rows);
+        SP->ccols[qi] = static_cast<int>(cq[qi].cols);
+    }
+    for (size_t p = 0; p < live.size(); ++p)
+        for (const auto& [q, coeff] : live[p].c) {
+            SP->src_prod[q][SP->nsrc[q]] = static_cast<int8_t>(p);
+            SP->src_coeff[q][SP->nsrc[q]] = static_cast<int8_t>(coeff);
+            ++SP->nsrc[q];
+        }
+    bool vec = C.rs == 1 && C.cs % 2 == 0 && (reinterpret_cast<uintptr_t>(C.p) % 16) == 0;
+    for (int qi = 0; qi < 4 && vec; ++qi) vec = (reinterpret_cast<uintptr_t>(cq[qi].p) % 16) == 0;
+    SP->c_vec = vec ? 1 : 0;
+    SP->rs_c = C.rs;
+    SP->cs_c = C.cs;
+    SP->mbase = M;
+    SP->mstride = static_cast<long long>(mstride);
+    SP->ldm = ldm;
+    SP->alpha = alpha;
+    SP->nquad = 4;
+    SP->qm = static_cast<int>(qm);
+    SP->qn = static_cast<int>(qn);
+    SP->ksplit = 1;
+    SP->r0 = 0;
+    SP->r1 = static_cast<int>(qm);
+    SP->c0 = 0;
+    SP->c1 = static_cast<int>(qn);
+    wait_ready(s, C);
+    e.prof_begin("stream_gather_kernel", s);
+    ck(launch_stream_update(*SP, s), "outer stream_update");
+    e.prof_end(s);
+    return launches + 1;
 }
 }  // namespace
 

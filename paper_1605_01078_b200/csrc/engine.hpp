@@ -41,6 +41,10 @@ struct Engine {
     DeviceBuffer pack_a, pack_b;              // TMA layout normalisation
     DeviceBuffer mbuf, tabuf, tbbuf;          // AB / Naive temporaries
     DeviceBuffer ticket_buf;                  // ordered fused-epilogue tickets
+    // level 3 (B200 extension, strassen_ctx_set_max_level): the outer level's
+    // layout normalisation, materialised operands and products (run_outer)
+    DeviceBuffer pack_a3, pack_b3, l3_a, l3_b, l3_m;
+    int max_level = 2;  // strassen_ctx_set_max_level: 3 admits Naive / C at level 3
     long last_launches = 0;
     bool peeling = true;  // dynamic peeling of odd fringes (strassen_ctx_set_peeling)
     // optional per-launch timing of the last call (strassen_ctx_enable_profiling)

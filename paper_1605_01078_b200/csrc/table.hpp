@@ -34,6 +34,10 @@ Program one_level_program();
 Program compose(const Program& outer, const Program& inner);
 // Level 1 or 2; throws std::invalid_argument otherwise (table.cpp:95-102).
 const Program& program_for_level(int level);
+// Level 3 = compose(level 1, level 2): 343 products (B200 extension; the
+// reference composes it only in acceptance.cpp:86-88).  Used for the analytic
+// counters of level-3 calls.
+const Program& program_level3();
 OpCounts count_ops(const Program& p);
 
 }  // namespace sb200
