@@ -401,8 +401,24 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
             P.kt_per_split = P.ktiles;
             P.tickets = F.tickets;
             P.ticket_ld = F.ticket_ld;
+            static const int group_env = [] {
+                const char* v = std::getenv("STRASSEN_B200_UNIT_GROUP");  // tiles (experiments)
+                return v ? std::atoi(v) : 0;
+            }();
+            P.unit_group = group_env;
         }
-        P.grid_cap = cap(P.c_vec && P.ktiles <= P.bulk_max_kt);
+        // short products take the bulk-reduction epilogue; single-term programs
+        // (C, DGEMM) then run persistent with a separate stage, collecting each
+        // unit's reductions one unit later (kernels.cu mm_kernel, RING < kRawSlots)
+        const bool bulk_units = P.c_vec && P.ktiles <= P.bulk_max_kt;
+        bool single = true;
+        for (int p = 0; p < P.nprod; ++p) single = single && P.prod[p].na == 1 && P.prod[p].nb == 1;
+        static const bool sep_on = [] {
+            const char* v = std::getenv("STRASSEN_B200_SEP");  // 0 / 1 (experiments)
+            return v ? std::atoi(v) != 0 : true;
+        }();
+        P.sep_stage = bulk_units && single && sep_on ? 1 : 0;
+        P.grid_cap = cap(bulk_units && !P.sep_stage);
         e.prof_begin("mm_kernel", s);
         ck(launch_mm(P, s), "mm_kernel");
         e.prof_end(s);

@@ -263,7 +263,7 @@ struct HalfStep {
     uint32_t slot0;
 };
 
-template <int NT>
+template <int NT, int RING>
 __device__ __forceinline__ void half_acquire(const uint8_t* raw, uint64_t* raw_full,
                                              uint32_t& slot, uint32_t& phase, HalfStep<NT>& hs) {
     constexpr int kSlots = (NT + 1) / 2;
@@ -271,20 +271,20 @@ __device__ __forceinline__ void half_acquire(const uint8_t* raw, uint64_t* raw_f
 #pragma unroll
     for (int v = 0; v < kSlots; ++v) {
         uint32_t sv = slot + v;
-        const uint32_t pv = (sv >= kRawSlots) ? phase ^ 1 : phase;
-        sv = (sv >= kRawSlots) ? sv - kRawSlots : sv;
+        const uint32_t pv = (sv >= RING) ? phase ^ 1 : phase;
+        sv = (sv >= RING) ? sv - RING : sv;
         hs.t[2 * v] = raw + sv * kSlotBytes;
         if (2 * v + 1 < NT) hs.t[2 * v + 1] = raw + sv * kSlotBytes + kHalfBytes;
         mbar_wait(&raw_full[sv], pv);
     }
     slot += kSlots;
-    if (slot >= kRawSlots) {
-        slot -= kRawSlots;
+    if (slot >= RING) {
+        slot -= RING;
         phase ^= 1;
     }
 }
 
-template <int NT>
+template <int NT, int RING>
 __device__ __forceinline__ void half_release(uint64_t* raw_empty, const HalfStep<NT>& hs,
                                              int lane) {
     consumer_fence();
@@ -293,14 +293,14 @@ __device__ __forceinline__ void half_release(uint64_t* raw_empty, const HalfStep
 #pragma unroll
     for (int v = 0; v < (NT + 1) / 2; ++v) {
         mbar_arrive_if(&raw_empty[s2], lane == 0);  // predicated: no branch
-        s2 = (s2 + 1 == kRawSlots) ? 0 : s2 + 1;
+        s2 = (s2 + 1 == RING) ? 0 : s2 + 1;
     }
 }
 
 // One product's k-loop over half tiles: two 8-k steps per 16-k tile (both
 // waits first, then one straight-line block that returns the first step's
 // slots as soon as it is done).  kt_lo / kt_hi count 16-k tiles.
-template <int NA, int NB>
+template <int NA, int NB, int RING>
 __device__ __forceinline__ void product_kloop_half(const uint8_t* raw, uint64_t* raw_full,
                                                    uint64_t* raw_empty, uint32_t& slot,
                                                    uint32_t& phase, int kt_lo, int kt_hi,
@@ -313,8 +313,8 @@ __device__ __forceinline__ void product_kloop_half(const uint8_t* raw, uint64_t*
     for (int u = 0; u < NB; ++u) cb[u] = static_cast<double>(pd.bs[u]);
     for (int kt = kt_lo; kt < kt_hi; ++kt) {
         HalfStep<NA + NB> h[2];
-        half_acquire(raw, raw_full, slot, phase, h[0]);
-        half_acquire(raw, raw_full, slot, phase, h[1]);
+        half_acquire<NA + NB, RING>(raw, raw_full, slot, phase, h[0]);
+        half_acquire<NA + NB, RING>(raw, raw_full, slot, phase, h[1]);
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
             Frags f;
@@ -326,7 +326,7 @@ __device__ __forceinline__ void product_kloop_half(const uint8_t* raw, uint64_t*
             for (int u = 1; u < NB; ++u) frag_b_half<false>(h[e].t[NA + u], wn, g, j, cb[u], f);
             dmma_substep(f, 0, acc);
             dmma_substep(f, 1, acc);
-            half_release(raw_empty, h[e], lane);  // first half's slots back mid-tile
+            half_release<NA + NB, RING>(raw_empty, h[e], lane);  // first half's slots back mid-tile
         }
     }
 }
@@ -337,7 +337,7 @@ __device__ __forceinline__ void product_kloop_half(const uint8_t* raw, uint64_t*
 // product so its first A and B terms have coefficient +1 (negating the other
 // terms and the destination coefficients instead: exact, round-to-nearest is
 // sign-symmetric), so the first term is a plain load.
-template <int NA, int NB>
+template <int NA, int NB, int RING>
 __device__ __forceinline__ void product_kloop(const uint8_t* raw, uint64_t* raw_full,
                                               uint64_t* raw_empty, uint32_t& slot,
                                               uint32_t& phase, int kt_lo, int kt_hi,
@@ -355,15 +355,15 @@ __device__ __forceinline__ void product_kloop(const uint8_t* raw, uint64_t* raw_
 #pragma unroll
         for (int u = 0; u < NA + NB; ++u) {
             uint32_t su = slot0 + u;
-            const uint32_t pu = (su >= kRawSlots) ? phase ^ 1 : phase;
-            su = (su >= kRawSlots) ? su - kRawSlots : su;
+            const uint32_t pu = (su >= RING) ? phase ^ 1 : phase;
+            su = (su >= RING) ? su - RING : su;
             if (u < NA) sA[u] = raw + su * kSlotBytes;
             else sB[u - NA] = raw + su * kSlotBytes;
             mbar_wait(&raw_full[su], pu);
         }
         slot += NA + NB;
-        if (slot >= kRawSlots) {
-            slot -= kRawSlots;
+        if (slot >= RING) {
+            slot -= RING;
             phase ^= 1;
         }
 #pragma unroll
@@ -385,7 +385,7 @@ __device__ __forceinline__ void product_kloop(const uint8_t* raw, uint64_t* raw_
 #pragma unroll
             for (int u = 0; u < NA + NB; ++u) {
                 mbar_arrive(&raw_empty[s2]);
-                if (++s2 == kRawSlots) s2 = 0;
+                if (++s2 == RING) s2 = 0;
             }
         }
     }
@@ -406,7 +406,19 @@ __device__ __forceinline__ Unit decode_unit(const MMParams& P, int bid) {
     U.p_hi = P.nprod;
     U.kt_lo = 0;
     U.kt_hi = P.ktiles;
-    if (P.split) {
+    if (P.split && P.unit_group > 0 && P.ksplit == 1) {
+        // groups of G tiles, product-major inside: unit (t, p) of group g is
+        // g*G*nprod + p*gt + t; the ticket a unit waits for, (t, p-1), always
+        // has a smaller index (every earlier group is full)
+        const int ntiles = P.tiles_m * P.tiles_n;
+        const int G = P.unit_group;
+        const int grp = bid / (G * P.nprod);
+        const int rem = bid - grp * G * P.nprod;
+        const int gt = min(G, ntiles - grp * G);
+        U.p_lo = rem / gt;
+        U.p_hi = U.p_lo + 1;
+        bid = grp * G + rem % gt;
+    } else if (P.split) {
         const int ntiles = P.tiles_m * P.tiles_n;
         const int s_idx = (bid / ntiles) % P.ksplit;
         U.p_lo = bid / (ntiles * P.ksplit);
@@ -431,14 +443,23 @@ __device__ __forceinline__ Unit decode_unit(const MMParams& P, int bid) {
 // ring while the DMMA warps finish the current unit's epilogue.  Ticket waits
 // only ever point at smaller units, which every CTA reaches first, so
 // persistence cannot deadlock them.
-template <int MAXT, bool PERSIST>
+//
+// RING < kRawSlots (persistent single-term launches with short k): a smaller
+// ring plus a separate bulk-reduction stage.  A CTA issues a unit's C
+// reductions and goes straight on to the next unit's mainloop; the reductions'
+// completion, and the ticket release that depends on it, are collected at the
+// start of its next epilogue (or after its last unit).  A CTA always releases
+// its deferred ticket before it waits on any ticket, so the ordering argument
+// above still holds.
+template <int MAXT, bool PERSIST, int RING>
 __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__ MMParams P) {
+    constexpr bool SEP = RING != kRawSlots;  // separate stage, deferred completion
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment (128B-swizzle atoms) by offsetting the shared array
     // itself, so every derived pointer stays in the shared address space (LDS/STS).
     uint8_t* raw = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint64_t* raw_full = reinterpret_cast<uint64_t*>(raw + kRawSlots * kSlotBytes);
-    uint64_t* raw_empty = raw_full + kRawSlots;
+    uint64_t* raw_full = reinterpret_cast<uint64_t*>(raw + RING * kSlotBytes);
+    uint64_t* raw_empty = raw_full + RING;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -449,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     const bool persistent = PERSIST && static_cast<int>(gridDim.x) < n_units;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kRawSlots; ++s) {
+        for (int s = 0; s < RING; ++s) {
             mbar_init(&raw_full[s], 1);
             mbar_init(&raw_empty[s], kConsumerWarps);
         }
@@ -490,7 +511,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                                 tma_load_2d(dst, &P.tmBh[pd.bq[t - pd.na]], k0, n0, &raw_full[s]);
                             }
                         }
-                        if (++s == kRawSlots) {
+                        if (++s == RING) {
                             s = 0;
                             phase ^= 1;
                         }
@@ -512,7 +533,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                     } else {
                         tma_load_2d(dst, &P.tmB[pd.bq[u - pd.na]], k0, n0, &raw_full[s]);
                     }
-                    if (++s == kRawSlots) {
+                    if (++s == RING) {
                         s = 0;
                         phase ^= 1;
                     }
@@ -536,6 +557,21 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     double acc[8][4][2];
     // ring position of the next term tile: slot index and its fill parity
     uint32_t slot = 0, phase = 0;
+    // SEP: bulk reductions of the previous unit still in flight, and the ticket
+    // (and product) to release once they complete
+    bool pend = false;
+    int* pend_ticket = nullptr;
+    int pend_p = 0;
+    auto collect = [&]() {  // every warp's reductions performed, then hand the tile on
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        consumer_bar();  // (also: the stage is free again)
+        if (threadIdx.x == 0 && pend_ticket) {
+            __threadfence();
+            st_release_gpu(pend_ticket, pend_p + 1);
+        }
+        pend = false;
+    };
 
     for (int unit = blockIdx.x; unit < n_units; unit += PERSIST ? gridDim.x : 1) {
     const Unit U = decode_unit(P, unit);
@@ -562,34 +598,34 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         const int combo = na * 8 + nb;
         bool done = true;
         if (combo == 9) {
-            product_kloop<1, 1>(raw, raw_full, raw_empty, slot, phase, kt_lo, kt_hi, pd, wm, wn,
+            product_kloop<1, 1, RING>(raw, raw_full, raw_empty, slot, phase, kt_lo, kt_hi, pd, wm, wn,
                                 g, j, lane, acc);
         } else if (MAXT >= 2 && combo == 10) {
-            product_kloop<1, (MAXT >= 2 ? 2 : 1)>(raw, raw_full, raw_empty, slot, phase, kt_lo,
+            product_kloop<1, (MAXT >= 2 ? 2 : 1), RING>(raw, raw_full, raw_empty, slot, phase, kt_lo,
                                                   kt_hi, pd, wm, wn, g, j, lane, acc);
         } else if (MAXT >= 2 && combo == 17) {
-            product_kloop<(MAXT >= 2 ? 2 : 1), 1>(raw, raw_full, raw_empty, slot, phase, kt_lo,
+            product_kloop<(MAXT >= 2 ? 2 : 1), 1, RING>(raw, raw_full, raw_empty, slot, phase, kt_lo,
                                                   kt_hi, pd, wm, wn, g, j, lane, acc);
         } else if (MAXT >= 2 && combo == 18) {
-            product_kloop<(MAXT >= 2 ? 2 : 1), (MAXT >= 2 ? 2 : 1)>(
+            product_kloop<(MAXT >= 2 ? 2 : 1), (MAXT >= 2 ? 2 : 1), RING>(
                 raw, raw_full, raw_empty, slot, phase, kt_lo, kt_hi, pd, wm, wn, g, j, lane, acc);
         } else if (MAXT >= 4 && combo == 12) {
-            product_kloop<1, (MAXT >= 4 ? 4 : 1)>(raw, raw_full, raw_empty, slot, phase, kt_lo,
+            product_kloop<1, (MAXT >= 4 ? 4 : 1), RING>(raw, raw_full, raw_empty, slot, phase, kt_lo,
                                                   kt_hi, pd, wm, wn, g, j, lane, acc);
         } else if (MAXT >= 4 && combo == 33) {
-            product_kloop<(MAXT >= 4 ? 4 : 1), 1>(raw, raw_full, raw_empty, slot, phase, kt_lo,
+            product_kloop<(MAXT >= 4 ? 4 : 1), 1, RING>(raw, raw_full, raw_empty, slot, phase, kt_lo,
                                                   kt_hi, pd, wm, wn, g, j, lane, acc);
         } else if (MAXT >= 4 && combo == 20) {
-            product_kloop<(MAXT >= 4 ? 2 : 1), (MAXT >= 4 ? 4 : 1)>(
+            product_kloop<(MAXT >= 4 ? 2 : 1), (MAXT >= 4 ? 4 : 1), RING>(
                 raw, raw_full, raw_empty, slot, phase, kt_lo, kt_hi, pd, wm, wn, g, j, lane, acc);
         } else if (MAXT >= 4 && combo == 34) {
-            product_kloop<(MAXT >= 4 ? 4 : 1), (MAXT >= 4 ? 2 : 1)>(
+            product_kloop<(MAXT >= 4 ? 4 : 1), (MAXT >= 4 ? 2 : 1), RING>(
                 raw, raw_full, raw_empty, slot, phase, kt_lo, kt_hi, pd, wm, wn, g, j, lane, acc);
         } else if (MAXT >= 4 && combo == 36 && pd.half) {
-            product_kloop_half<(MAXT >= 4 ? 4 : 1), (MAXT >= 4 ? 4 : 1)>(
+            product_kloop_half<(MAXT >= 4 ? 4 : 1), (MAXT >= 4 ? 4 : 1), RING>(
                 raw, raw_full, raw_empty, slot, phase, kt_lo, kt_hi, pd, wm, wn, g, j, lane, acc);
         } else if (MAXT >= 4 && combo == 36) {
-            product_kloop<(MAXT >= 4 ? 4 : 1), (MAXT >= 4 ? 4 : 1)>(
+            product_kloop<(MAXT >= 4 ? 4 : 1), (MAXT >= 4 ? 4 : 1), RING>(
                 raw, raw_full, raw_empty, slot, phase, kt_lo, kt_hi, pd, wm, wn, g, j, lane, acc);
         } else {
             done = false;
@@ -597,25 +633,25 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         if (!done)
         for (int kt = kt_lo; kt < kt_hi; ++kt) {
             // term tiles of this k-step: A terms, then B terms, in ring order
-            // (a k-step uses at most 2*MAXT <= 8 < kRawSlots slots: one wrap at most)
+            // (a k-step uses at most 2*MAXT <= 8 < RING slots: one wrap at most)
             const uint8_t* sA[MAXT];
             const uint8_t* sB[MAXT];
             const uint32_t slot0 = slot;
 #pragma unroll
             for (int u = 0; u < MAXT; ++u) {
                 uint32_t sa = slot0 + u, sb = slot0 + na + u;
-                const uint32_t pa = (sa >= kRawSlots) ? phase ^ 1 : phase;
-                const uint32_t pb = (sb >= kRawSlots) ? phase ^ 1 : phase;
-                sa = (sa >= kRawSlots) ? sa - kRawSlots : sa;
-                sb = (sb >= kRawSlots) ? sb - kRawSlots : sb;
+                const uint32_t pa = (sa >= RING) ? phase ^ 1 : phase;
+                const uint32_t pb = (sb >= RING) ? phase ^ 1 : phase;
+                sa = (sa >= RING) ? sa - RING : sa;
+                sb = (sb >= RING) ? sb - RING : sb;
                 sA[u] = raw + sa * kSlotBytes;
                 sB[u] = raw + sb * kSlotBytes;
                 if (u < na) mbar_wait(&raw_full[sa], pa);
                 if (u < nb) mbar_wait(&raw_full[sb], pb);
             }
             slot += na + nb;
-            if (slot >= kRawSlots) {
-                slot -= kRawSlots;
+            if (slot >= RING) {
+                slot -= RING;
                 phase ^= 1;
             }
 #pragma unroll
@@ -649,11 +685,12 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                 uint32_t s2 = slot0;
                 for (int u = 0; u < na + nb; ++u) {
                     mbar_arrive(&raw_empty[s2]);
-                    if (++s2 == kRawSlots) s2 = 0;
+                    if (++s2 == RING) s2 = 0;
                 }
             }
         }
 
+        if (SEP && pend) collect();  // previous unit's reductions: complete, release its ticket
         // ---- epilogue of product p.  Accumulator (mf, nf, e) of lane (g, j)
         // is row 16(mf/2) + 2g + mf%2 and column 8nf + nperm(2j + e) of this
         // warp's 64 x 32 tile.
@@ -673,23 +710,24 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         // than the register path saves once the mainloop is long); anything
         // else takes the register read-modify-write below.
         bool bulk = P.mode == kEpiRMW && P.c_vec && p_hi - p_lo == 1 &&
-                    kt_hi - kt_lo <= P.bulk_max_kt && !persistent && !(P.split && P.ksplit > 1);
+                    kt_hi - kt_lo <= P.bulk_max_kt && (SEP || !persistent) &&
+                    !(P.split && P.ksplit > 1);
         for (int u = 0; u < pd.nc && bulk; ++u) {
             const int cq = pd.cq[u];
             bulk = tm * kBM + kBM <= P.crows[cq] && tn * kBN + kBN <= P.ccols[cq];
         }
         if (bulk) {
             constexpr int kColStride = kBM * 8 + 16;  // 1040 B: skews banks across columns
-            uint8_t* stage = raw;
+            uint8_t* stage = SEP ? raw + RING * kSlotBytes + 256 : raw;
             int* ticket = P.tickets ? P.tickets + tm * P.ticket_ld + tn : nullptr;
             bool issued = false;
-            consumer_bar();  // every warp is done reading the ring before it is reused
+            if (!SEP) consumer_bar();  // every warp is done reading the ring before it is reused
             for (int pass = 0; pass < 2; ++pass) {  // destinations with coefficient +1, then -1
                 int any = 0;
                 for (int u = 0; u < pd.nc; ++u) any |= (pd.cs[u] > 0) == (pass == 0);
                 if (!any) continue;
                 if (issued) {  // previous pass's reductions must have read the stage
-                    if (warp == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                     consumer_bar();
                 }
                 const double sc = P.alpha * (pass == 0 ? 1.0 : -1.0);
@@ -711,27 +749,35 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                     asm volatile("fence.proxy.async.global;" ::: "memory");
                 }
                 consumer_bar();
-                if (warp == 0) {
-                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                // every DMMA warp hands 16 of the tile's columns to the TMA engine
+                // (one warp issuing all 128 x nc reductions serialised the epilogue)
+                static_assert(kConsumerWarps * 16 == kBN, "16 columns per warp");
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                if (lane < 16) {
+                    const int c = warp * 16 + lane;
                     for (int u = 0; u < pd.nc; ++u) {
                         if ((pd.cs[u] > 0) != (pass == 0)) continue;
                         double* Cq = P.cptr[pd.cq[u]] + tm * kBM;
-                        for (int c = lane; c < kBN; c += 32)
-                            bulk_reduce_add_f64(Cq + static_cast<long long>(tn * kBN + c) * P.cs_c,
-                                                stage + c * kColStride, kBM * 8);
+                        bulk_reduce_add_f64(Cq + static_cast<long long>(tn * kBN + c) * P.cs_c,
+                                            stage + c * kColStride, kBM * 8);
                     }
-                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 issued = true;
             }
-            if (warp == 0) {  // all reductions performed, then hand the tile on
-                asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-                asm volatile("fence.proxy.async.global;" ::: "memory");
-                __syncwarp();
-                if (lane == 0 && ticket) {
-                    __threadfence();
-                    st_release_gpu(ticket, p + 1);
-                }
+            if (SEP) {  // completion collected at the next epilogue (or after the loop)
+                pend = true;
+                pend_ticket = ticket;
+                pend_p = p;
+                continue;
+            }
+            // all reductions performed (every warp's), then hand the tile on
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            consumer_bar();
+            if (threadIdx.x == 0 && ticket) {
+                __threadfence();
+                st_release_gpu(ticket, p + 1);
             }
             continue;  // next product (none: single-product CTA)
         }
@@ -903,6 +949,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         }
     }
     }  // unit
+    if (SEP && pend) collect();
 }
 
 // ---------------------------------------------------------------- repack ----
@@ -1148,19 +1195,19 @@ __global__ void scale_kernel(double* c, long rows, long cols, long long rs, long
 
 }  // namespace
 
-template <int MAXT, bool PERSIST>
+template <int MAXT, bool PERSIST, int RING = kRawSlots>
 static cudaError_t launch_mm_t(const MMParams& p, cudaStream_t s) {
+    constexpr int smem = RING == kRawSlots ? kMMSmemBytes : kMMSepSmemBytes;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(mm_kernel<MAXT, PERSIST>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             kMMSmemBytes);
+        cudaError_t e = cudaFuncSetAttribute(mm_kernel<MAXT, PERSIST, RING>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     const int units = p.tiles_m * p.tiles_n * (p.split ? p.nprod * p.ksplit : 1);
     const int grid = PERSIST && p.grid_cap > 0 && p.grid_cap < units ? p.grid_cap : units;
-    mm_kernel<MAXT, PERSIST><<<grid, kThreads, kMMSmemBytes, s>>>(p);
+    mm_kernel<MAXT, PERSIST, RING><<<grid, kThreads, smem, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -1174,6 +1221,8 @@ cudaError_t launch_mm(const MMParams& p, cudaStream_t s) {
     // mm_kernel 192.4 -> 188.7 ms (Naive L2), 251.4 -> 247.7 (DGEMM) on one box.
     // Fused-sum programs keep one CTA per unit: their units' costs differ by term
     // count and dynamic dispatch balances them better (ABC L1 233.8 vs 236.5 ms).
+    if (maxt == 1 && p.grid_cap > 0 && p.sep_stage)  // persistent, deferred bulk epilogue
+        return launch_mm_t<1, true, kSepRing>(p, s);
     if (maxt == 1)  // single-term programs: no sum code at all
         return p.grid_cap > 0 ? launch_mm_t<1, true>(p, s) : launch_mm_t<1, false>(p, s);
     return maxt <= 2 ? launch_mm_t<2, false>(p, s) : launch_mm_t<kMaxTerms, false>(p, s);

@@ -29,6 +29,14 @@ static_assert(kProducerRegs * 128 + kConsumerRegs * kConsumerWarps * 32 <= kThre
               "setmaxnreg split exceeds the CTA register allocation");
 constexpr int kMMSmemBytes = kRawSlots * kSlotBytes + 1024 + 256;
 static_assert(kMMSmemBytes <= 227 * 1024, "shared memory budget");
+// persistent single-term launches with the deferred bulk epilogue: a 5-slot
+// ring (2.5 k-steps of (1, 1) products ahead) and a separate 130 KB stage of
+// one C tile (128 columns x 1040 B: the 16-byte skew spreads banks)
+constexpr int kSepRing = 5;
+constexpr int kStageBytes = kBN * (kBM * 8 + 16);
+constexpr int kMMSepSmemBytes = kSepRing * kSlotBytes + 1024 + 256 + kStageBytes;
+static_assert(kMMSepSmemBytes <= 227 * 1024, "shared memory budget (separate stage)");
+static_assert(2 * kSepRing * 8 <= 256, "ring barriers fit before the stage");
 
 // One Strassen product M_p = (sum_u as_u A_{aq_u}) (sum_u bs_u B_{bq_u});
 // destinations C_{cq_u} += alpha * cs_u * M_p.
@@ -89,6 +97,13 @@ struct alignas(64) MMParams {
     // persistent launch: at most this many CTAs (one per SM), each walking
     // units blockIdx.x + i * gridDim.x; 0 = one CTA per unit
     int grid_cap;
+    // ticketed grid (split, ksplit = 1): units in groups of this many tiles,
+    // product-major inside a group, so a group's C tiles stay L2-resident across
+    // its 7^L ordered updates; 0 = product-major over all tiles
+    int unit_group;
+    // persistent single-term launch whose bulk-reduction epilogues use a separate
+    // stage and collect their completion one unit later (kSepRing ring slots)
+    int sep_stage;
 };
 
 cudaError_t launch_mm(const MMParams& p, cudaStream_t s);

@@ -11,6 +11,8 @@ A = (torch.rand(k, m, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).
 B = (torch.rand(n, k, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
 C = (torch.rand(n, m, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
 ctx = S.Ctx()
+if L == 3:
+    ctx.set_max_level(3)
 ctx.gemm_device(v, L, 1.0, A, B, C)
 torch.cuda.synchronize()
 print("ok", ctx.last_launches())
@@ -19,4 +21,11 @@ if os.environ.get("PROFILE"):
     for _ in range(3):
         ctx.gemm_device(v, L, 1.0, A, B, C)
     torch.cuda.synchronize()
-    print(" ".join(f"{p['kernel']}={p['ms']:.3f}" for p in ctx.last_profile()))
+    prof = ctx.last_profile()
+    print(" ".join(f"{p['kernel']}={p['ms']:.3f}" for p in prof))
+    tot = {}
+    for p in prof:
+        tot[p["kernel"]] = tot.get(p["kernel"], 0.0) + p["ms"]
+    span = max(p["start_ms"] + p["ms"] for p in prof)
+    print("totals:", {k: round(v, 3) for k, v in tot.items()}, "span_ms:", round(span, 3),
+          "sum_ms:", round(sum(tot.values()), 3))
