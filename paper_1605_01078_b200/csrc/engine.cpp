@@ -706,6 +706,14 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
         for (int qi = 0; qi < side * side && vec; ++qi)
             vec = (reinterpret_cast<uintptr_t>(cq[qi].p) % 16) == 0;
         P.c_vec = vec ? 1 : 0;
+        // C quadrant tensor maps for the bulk-reduction epilogue: 16-row x
+        // 128-column boxes, 128-byte swizzle, one TMA reduce-add per box
+        if (vec && C.cs * 8 < (1LL << 40)) {
+            for (int qi = 0; qi < side * side; ++qi)
+                if (c_live[qi])
+                    encode_map(&P.tmC[qi], cq[qi].p, cq[qi].rows, cq[qi].cols, C.cs, 16, kBN, 128);
+            P.c_tma = 1;
+        }
     }
     P.qm = static_cast<int>(qm);
     P.qn = static_cast<int>(qn);

@@ -74,6 +74,17 @@ __device__ __forceinline__ void bulk_reduce_add_f64(double* gdst, const void* ss
                  ::"l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes) : "memory");
 }
 
+// Tensor reduce-add smem -> global through a tensor map (f64 add at L2,
+// UTMAREDG.2D.ADD); coordinates {row, column} of the box origin.
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, int c0, int c1,
+                                                  const void* ssrc) {
+    asm volatile(
+        "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group"
+        " [%0, {%1, %2}], [%3];" ::"l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1),
+        "r"(smem_u32(ssrc))
+        : "memory");
+}
+
 // Named barrier over the 8 DMMA warps only (the producer warp has exited).
 __device__ __forceinline__ void consumer_bar() {
     asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
@@ -709,16 +720,16 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         // CTA stays resident until its reductions complete, which costs more
         // than the register path saves once the mainloop is long); anything
         // else takes the register read-modify-write below.
-        bool bulk = P.mode == kEpiRMW && P.c_vec && p_hi - p_lo == 1 &&
-                    kt_hi - kt_lo <= P.bulk_max_kt && (SEP || !persistent) &&
-                    !(P.split && P.ksplit > 1);
-        for (int u = 0; u < pd.nc && bulk; ++u) {
-            const int cq = pd.cq[u];
-            bulk = tm * kBM + kBM <= P.crows[cq] && tn * kBN + kBN <= P.ccols[cq];
-        }
+        // C tiles are reduced through the quadrants' tensor maps (tmC), which clip
+        // partial tiles at the quadrant edge.
+        const bool bulk = P.mode == kEpiRMW && P.c_tma && p_hi - p_lo == 1 &&
+                          kt_hi - kt_lo <= P.bulk_max_kt && (SEP || !persistent) &&
+                          !(P.split && P.ksplit > 1);
         if (bulk) {
-            constexpr int kColStride = kBM * 8 + 16;  // 1040 B: skews banks across columns
-            uint8_t* stage = SEP ? raw + RING * kSlotBytes + 256 : raw;
+            // stage: 8 boxes of 16 rows x 128 columns (16 KB each, 128-byte swizzle:
+            // column c at c*128, 16-byte chunk (row%16)/2 ^ c%8) -- conflict-free for
+            // the fragment layout (chunk g ^ nperm(2j+e)%8 covers all 8 per quarter-warp)
+            uint8_t* stage = SEP ? raw + RING * kSlotBytes + 1024 : raw;
             int* ticket = P.tickets ? P.tickets + tm * P.ticket_ld + tn : nullptr;
             bool issued = false;
             if (!SEP) consumer_bar();  // every warp is done reading the ring before it is reused
@@ -737,9 +748,9 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                     for (int h = 0; h < 4; ++h)
 #pragma unroll
                         for (int e = 0; e < 2; ++e) {
-                            const int row = wm * 64 + 16 * h + 2 * g;
                             const int col = wn * 32 + 8 * nf + (e ? c1 : c0);
-                            *reinterpret_cast<double2*>(stage + col * kColStride + row * 8) =
+                            *reinterpret_cast<double2*>(stage + (wm * 4 + h) * 16384 + col * 128 +
+                                                        ((g ^ (col & 7)) << 4)) =
                                 make_double2(sc * acc[2 * h][nf][e], sc * acc[2 * h + 1][nf][e]);
                         }
                 consumer_fence();  // generic smem writes before the async-proxy reads
@@ -749,17 +760,16 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                     asm volatile("fence.proxy.async.global;" ::: "memory");
                 }
                 consumer_bar();
-                // every DMMA warp hands 16 of the tile's columns to the TMA engine
-                // (one warp issuing all 128 x nc reductions serialised the epilogue)
-                static_assert(kConsumerWarps * 16 == kBN, "16 columns per warp");
+                // DMMA warp w hands box w (rows 16w..16w+15) of every destination
+                // to the TMA engine: one tensor reduce-add each (per-column 1-D bulk
+                // reductions issued 128 x nc uniform-datapath instructions per tile)
+                static_assert(kConsumerWarps * 16 == kBM, "one 16-row box per warp");
                 asm volatile("fence.proxy.async.global;" ::: "memory");
-                if (lane < 16) {
-                    const int c = warp * 16 + lane;
+                if (lane == 0) {
                     for (int u = 0; u < pd.nc; ++u) {
                         if ((pd.cs[u] > 0) != (pass == 0)) continue;
-                        double* Cq = P.cptr[pd.cq[u]] + tm * kBM;
-                        bulk_reduce_add_f64(Cq + static_cast<long long>(tn * kBN + c) * P.cs_c,
-                                            stage + c * kColStride, kBM * 8);
+                        tma_reduce_add_2d(&P.tmC[pd.cq[u]], tm * kBM + 16 * warp, tn * kBN,
+                                          stage + warp * 16384);
                     }
                 }
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");

@@ -33,10 +33,12 @@ static_assert(kMMSmemBytes <= 227 * 1024, "shared memory budget");
 // ring (2.5 k-steps of (1, 1) products ahead) and a separate 130 KB stage of
 // one C tile (128 columns x 1040 B: the 16-byte skew spreads banks)
 constexpr int kSepRing = 5;
-constexpr int kStageBytes = kBN * (kBM * 8 + 16);
-constexpr int kMMSepSmemBytes = kSepRing * kSlotBytes + 1024 + 256 + kStageBytes;
+// (the stage holds one C tile as 8 swizzled boxes of 16 rows x 128 columns,
+// 1024-byte aligned after the ring's barriers)
+constexpr int kStageBytes = kBM * kBN * 8;
+constexpr int kMMSepSmemBytes = kSepRing * kSlotBytes + 1024 + 1024 + kStageBytes;
 static_assert(kMMSepSmemBytes <= 227 * 1024, "shared memory budget (separate stage)");
-static_assert(2 * kSepRing * 8 <= 256, "ring barriers fit before the stage");
+static_assert(2 * kSepRing * 8 <= 1024, "ring barriers fit before the stage");
 
 // One Strassen product M_p = (sum_u as_u A_{aq_u}) (sum_u bs_u B_{bq_u});
 // destinations C_{cq_u} += alpha * cs_u * M_p.
@@ -60,6 +62,9 @@ struct alignas(64) MMParams {
     // A box 16 x 8 (128B swizzle), B box 8 x 128 (64B swizzle)
     CUtensorMap tmAh[kMaxQuad];
     CUtensorMap tmBh[kMaxQuad];
+    // C quadrants (c_tma): dims (rows, cols), box 16 x 128, swizzle 128B -- the
+    // bulk-reduction epilogue's TMA reduce-add targets (clipped by the map)
+    CUtensorMap tmC[kMaxQuad];
     ProductDesc prod[kMaxProducts];
     double* cptr[kMaxQuad];     // C quadrant views (clipped)
     int crows[kMaxQuad];
@@ -104,6 +109,7 @@ struct alignas(64) MMParams {
     // persistent single-term launch whose bulk-reduction epilogues use a separate
     // stage and collect their completion one unit later (kSepRing ring slots)
     int sep_stage;
+    int c_tma;  // tmC valid: bulk epilogue through tensor reduce-adds (partial tiles too)
 };
 
 cudaError_t launch_mm(const MMParams& p, cudaStream_t s);
