@@ -407,10 +407,11 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
             }();
             P.unit_group = group_env;
         }
-        // short products take the bulk-reduction epilogue; single-term programs
-        // (C, DGEMM) then run persistent with a separate stage, collecting each
-        // unit's reductions one unit later (kernels.cu mm_kernel, RING < kRawSlots)
-        const bool bulk_units = P.c_vec && P.ktiles <= P.bulk_max_kt;
+        // bulk-reduction epilogue (C through its quadrant tensor maps); single-term
+        // programs (C, DGEMM) then run persistent with a separate stage, collecting
+        // each unit's reductions one unit later (kernels.cu mm_kernel, RING <
+        // kRawSlots); fused-sum programs stay one CTA per unit
+        const bool bulk_units = P.c_tma && P.ktiles <= P.bulk_max_kt;
         bool single = true;
         for (int p = 0; p < P.nprod; ++p) single = single && P.prod[p].na == 1 && P.prod[p].nb == 1;
         static const bool sep_on = [] {
@@ -722,11 +723,12 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
     P.tiles_n = static_cast<int>(ceil_div(qn, kBN));
     P.ktiles = static_cast<int>(ceil_div(qk, kBK));
     P.group_m = 8;
-    // bulk-reduction epilogue for products of <= 128 k-tiles (measured at
-    // 16384^2 x k: ABC L2 k = 1024 23.8 -> 21.2 ms, 2048 38.2 -> 35.7, 4096
-    // 67.4 -> 64.8; ABC L1 k = 4096 60.8 -> 60.1; at k = 16384 (256+ k-tiles)
-    // the register path is ~1% faster)
-    P.bulk_max_kt = 128;
+    // bulk-reduction epilogue (C tiles staged in smem, one TMA reduce-add per
+    // 16 x 128 box) at every k: with the tensor-map reduce-adds and the deferred
+    // completion of persistent single-term launches it beats the register
+    // read-modify-write everywhere measured (16384^3: C L2 196.5 -> 190.6 ms,
+    // DGEMM 246.9 -> 242.5, ABC L2 239.7 -> 235.9; profiles/r01_bulk_kt_probe.log)
+    P.bulk_max_kt = 1 << 30;
     if (const char* b = std::getenv("STRASSEN_B200_BULK_MAX_KT")) P.bulk_max_kt = std::atoi(b);
 
     // Live products in table order (variants.cpp:130-133 skip rule).

@@ -68,11 +68,6 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
 __device__ __forceinline__ void st_release_gpu(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-// Bulk reduction smem -> global, f64 add performed at L2 (UBLKRED.ADD.F64.RN).
-__device__ __forceinline__ void bulk_reduce_add_f64(double* gdst, const void* ssrc, uint32_t bytes) {
-    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;"
-                 ::"l"(gdst), "r"(smem_u32(ssrc)), "r"(bytes) : "memory");
-}
 
 // Tensor reduce-add smem -> global through a tensor map (f64 add at L2,
 // UTMAREDG.2D.ADD); coordinates {row, column} of the box origin.
