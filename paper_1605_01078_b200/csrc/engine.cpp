@@ -419,6 +419,11 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
             return v ? std::atoi(v) != 0 : true;
         }();
         P.sep_stage = bulk_units && single && sep_on ? 1 : 0;
+        // deferred collection: the next product of a tile is tiles-in-launch units
+        // later; defer only when that is >= 2 grid widths (small host-call windows
+        // would otherwise chain each tile's products one unit apart)
+        const long launch_tiles = static_cast<long>(P.tiles_m) * P.tiles_n;
+        P.sep_defer = (!F.tickets || launch_tiles >= 2L * (e.num_sms > 0 ? e.num_sms : 148)) ? 1 : 0;
         P.grid_cap = cap(bulk_units && !P.sep_stage);
         e.prof_begin("mm_kernel", s);
         ck(launch_mm(P, s), "mm_kernel");

@@ -770,7 +770,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 issued = true;
             }
-            if (SEP) {  // completion collected at the next epilogue (or after the loop)
+            if (SEP && P.sep_defer) {  // completion collected at the next epilogue (or after the loop)
                 pend = true;
                 pend_ticket = ticket;
                 pend_p = p;

@@ -109,6 +109,10 @@ struct alignas(64) MMParams {
     // persistent single-term launch whose bulk-reduction epilogues use a separate
     // stage and collect their completion one unit later (kSepRing ring slots)
     int sep_stage;
+    // sep_stage: collect a unit's reductions (and release its ticket) only at the
+    // CTA's next epilogue.  Safe for throughput when a tile's next product is at
+    // least two grid-widths of units away (else it would wait a whole unit)
+    int sep_defer;
     int c_tma;  // tmC valid: bulk epilogue through tensor reduce-adds (partial tiles too)
 };
 
