@@ -19,10 +19,12 @@ PEAK = 37.05
 CFG = {"dgemm": 0}
 ALL = [("dgemm", 0), ("abc", 1), ("ab", 1), ("naive", 1), ("c", 1), ("abc", 2), ("ab", 2),
        ("naive", 2), ("c", 2)]
+# level 3 (B200 extension, ctx max level 3) on the square sweep from 4096 up
+L3 = [("naive", 3), ("c", 3)]
 
 
 def table(level):
-    return {0: (1, 0, 0, 1), 1: (7, 5, 5, 12), 2: (49, 95, 95, 144)}[level]
+    return {0: (1, 0, 0, 1), 1: (7, 5, 5, 12), 2: (49, 95, 95, 144), 3: (343, 0, 0, 1008)}[level]
 
 
 def shapes(family):
@@ -47,6 +49,7 @@ def main():
     family, out = sys.argv[1], sys.argv[2]
     reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
     ctx = S.Ctx()
+    ctx.set_max_level(3)
     rows = []
     for (m, n, k) in shapes(family):
         g = torch.Generator(device="cuda").manual_seed(m * 7 + n * 3 + k)
@@ -62,7 +65,8 @@ def main():
         x = torch.rand(n, 1, dtype=torch.float64, device="cuda", generator=g)
         want = C0 @ x + A @ (B @ x)
         den = (torch.linalg.norm(A) * torch.linalg.norm(B) * torch.linalg.norm(x)).item()
-        for v, L in variants(family):
+        extra = L3 if family == "square" and min(m, n, k) >= 4096 else []
+        for v, L in variants(family) + extra:
             best = None
             for r in range(reps + 1):
                 C = C0.clone().t().contiguous().t()  # fresh column-major copy of C0
