@@ -27,14 +27,28 @@ __global__ void k(const __grid_constant__ CUtensorMap map, int r0, int c0) {
     }
 }
 
+// Finding: rows (the inner dimension) clip at 16-byte granularity -- with an odd
+// row count the element after the last row is written too -- while columns clip
+// exactly.  The Strassen epilogue therefore uses the reduce-add only where a
+// tile does not end inside a quadrant with an odd row count.
+int run(int dim_rows, int dim_cols, int r0, int c0);
 int main() {
+    int bad = run(256, 256, 32, 64);
+    bad += run(250, 256, 240, 64);   // rows 250..255 of the box outside the map: stay 1.0
+    bad += run(256, 100, 32, 64);    // columns 100..191 outside the map
+    const int odd = run(37, 256, 32, 64);  // expected to fail: row 37 is written
+    printf("odd row count clipped exactly: %s\n", odd ? "no" : "yes");
+    return bad != 0;
+}
+
+int run(int dim_rows, int dim_cols, int r0, int c0) {
     const int n = 256;
     std::vector<double> h(n * n, 1.0);
     double* d;
     cudaMalloc(&d, n * n * 8);
     cudaMemcpy(d, h.data(), n * n * 8, cudaMemcpyHostToDevice);
     CUtensorMap map;
-    cuuint64_t dims[2] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(n)};
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(dim_rows), static_cast<cuuint64_t>(dim_cols)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(n) * 8};
     cuuint32_t box[2] = {16, 128}, es[2] = {1, 1};
     void* fn = nullptr;
@@ -49,7 +63,7 @@ int main() {
                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     printf("encode: %d\n", static_cast<int>(r));
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 20000);
-    k<<<1, 128, 20000>>>(map, 32, 64);
+    k<<<1, 128, 20000>>>(map, r0, c0);
     cudaError_t e = cudaDeviceSynchronize();
     printf("kernel: %s\n", cudaGetErrorString(e));
     cudaMemcpy(h.data(), d, n * n * 8, cudaMemcpyDeviceToHost);
@@ -57,9 +71,10 @@ int main() {
     for (int c = 0; c < n; ++c)
         for (int rr = 0; rr < n; ++rr) {
             double want = 1.0;
-            if (rr >= 32 && rr < 48 && c >= 64 && c < 192) { want += 1000.0 * (c - 64) + (rr - 32); ++touched; }
+            if (rr >= r0 && rr < r0 + 16 && rr < dim_rows && c >= c0 && c < c0 + 128 && c < dim_cols) { want += 1000.0 * (c - c0) + (rr - r0); ++touched; }
             if (h[rr + c * n] != want) ++bad;
         }
-    printf("touched %ld bad %ld  sample C(33,65)=%g (want %g)\n", touched, bad, h[33 + 65 * n], 1.0 + 1000.0 + 1.0);
+    printf("dims %dx%d box at (%d,%d): touched %ld bad %ld\n", dim_rows, dim_cols, r0, c0, touched, bad);
+    cudaFree(d);
     return bad != 0;
 }

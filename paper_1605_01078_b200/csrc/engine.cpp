@@ -313,7 +313,18 @@ FusedPlan plan_fused(Engine& e, cudaStream_t s, const MMParams& P, bool force_sp
     FusedPlan F;
     const int ntiles = P.tiles_m * P.tiles_n;
     const int sms = e.num_sms > 0 ? e.num_sms : 148;
-    if (ntiles >= 2 * sms && !force_split) {
+    double terms = 0.0;  // mean operand terms per side: fused sums lengthen a k-tile
+    for (int p = 0; p < P.nprod; ++p) terms += 0.5 * (P.prod[p].na + P.prod[p].nb);
+    terms /= P.nprod > 0 ? P.nprod : 1;
+    long per = P.ktiles;
+    const int ks = choose_ksplit(ntiles, P.nprod, P.ktiles, sms, static_cast<double>(P.qm) * P.qn,
+                                 1.0 + 0.15 * (terms - 1.0), &per);
+    // Fused epilogue when the output has >= 2 waves of tiles, or -- for a
+    // multi-product program -- when the cost model would not split k anyway: the
+    // ticketed (tile, product) grid then has the same CTAs as split mode without
+    // its partials and stream pass (8192^3 C L2: 12544 CTAs on 256 tiles).
+    const bool fused = ntiles >= 2 * sms || (P.nprod > 1 && ks == 1);
+    if (fused && !force_split) {
         // Fused epilogue.  Tile ownership (one CTA walks every product of its
         // tile) quantises to whole waves of CTAs that each run all 7^L products
         // (ABC L2 at 9216^3: 2.2 waves -> 3).  One CTA per (tile, product) with
@@ -335,12 +346,7 @@ FusedPlan plan_fused(Engine& e, cudaStream_t s, const MMParams& P, bool force_sp
         }
         return F;
     }
-    double terms = 0.0;  // mean operand terms per side: fused sums lengthen a k-tile
-    for (int p = 0; p < P.nprod; ++p) terms += 0.5 * (P.prod[p].na + P.prod[p].nb);
-    terms /= P.nprod > 0 ? P.nprod : 1;
-    long per = P.ktiles;
-    F.ksplit = choose_ksplit(ntiles, P.nprod, P.ktiles, sms,
-                             static_cast<double>(P.qm) * P.qn, 1.0 + 0.15 * (terms - 1.0), &per);
+    F.ksplit = ks;
     F.per = static_cast<int>(per);
     F.split = true;
     F.ldm = (P.qm + 1) / 2 * 2;  // even: 16-B stores

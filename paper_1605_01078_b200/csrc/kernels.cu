@@ -717,9 +717,15 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         // else takes the register read-modify-write below.
         // C tiles are reduced through the quadrants' tensor maps (tmC), which clip
         // partial tiles at the quadrant edge.
-        const bool bulk = P.mode == kEpiRMW && P.c_tma && p_hi - p_lo == 1 &&
-                          kt_hi - kt_lo <= P.bulk_max_kt && (SEP || !persistent) &&
-                          !(P.split && P.ksplit > 1);
+        bool bulk = P.mode == kEpiRMW && P.c_tma && p_hi - p_lo == 1 &&
+                    kt_hi - kt_lo <= P.bulk_max_kt && (SEP || !persistent) &&
+                    !(P.split && P.ksplit > 1);
+        // the reduce-add clips rows at 16-byte granularity (microbench/tma_reduce_f64.cu):
+        // a tile ending inside a quadrant with an odd row count takes the register path
+        for (int u = 0; u < pd.nc && bulk; ++u) {
+            const int R = P.crows[pd.cq[u]];
+            bulk = (R & 1) == 0 || tm * kBM + kBM <= R;
+        }
         if (bulk) {
             // stage: 8 boxes of 16 rows x 128 columns (16 KB each, 128-byte swizzle:
             // column c at c*128, 16-byte chunk (row%16)/2 ^ c%8) -- conflict-free for
