@@ -268,10 +268,14 @@ void model_predict(strassen_variant v, int level, long m, long n, long k,
 // re-fitted to B200 with the round-1 measurements (profiles/r01_notes.md,
 // profiles/r01_sweep_*.csv):
 //   T_a: executed mm_kernel flops / (37.05 TF/s * e_mm * wave efficiency), with
-//        e_mm = 0.96 for single-term programs (DGEMM, Naive, C), 0.86 / 0.62 for
+//        e_mm = 0.976 for single-term programs (DGEMM, Naive, C), 0.91 / 0.78 for
 //        the fused two- / four-term sums (ABC, AB at level 1 / 2);
-//   T_m: HBM bytes of the sum / stream / C-update traffic at 5.5 TB/s;
-//   + 6 us per launch and the split-mode partials for outputs under two waves.
+//   T_m: HBM bytes of the sum / stream traffic at 5.5 TB/s, and the fused
+//        epilogue's reduce-add traffic at an effective 20 (single-term, deferred)
+//        or 10 TB/s (fused sums) -- constants fitted by tools/model_fit.py;
+//   + 20 us per dependent launch (drain of one kernel and ramp of the next,
+//     fitted to the small sweep sizes) and the split-mode partials for outputs
+//     under two waves.
 namespace {
 double waves_eff(double ctas, double sms) {
     const double w = std::ceil(ctas / sms);
@@ -279,8 +283,12 @@ double waves_eff(double ctas, double sms) {
 }
 }  // namespace
 
-static double predict_core(strassen_variant v, int L, long m, long n, long k, int sms) {
-    const double P = 37.05e12, BW = 5.5e12, launch = 6e-6;
+// c_vec: C column-major with an even ldc and 16-byte aligned quadrant origins
+// (engine.cpp run_strassen), which the TMA reduce-add epilogue needs; otherwise
+// the fused epilogue is the register read-modify-write.
+static double predict_core(strassen_variant v, int L, long m, long n, long k, int sms,
+                           bool c_vec) {
+    const double P = 37.05e12, BW = 5.5e12, launch = 20e-6;
     const long S = 1L << L;
     const double qm = static_cast<double>(ceil_div(m, S)), qn = static_cast<double>(ceil_div(n, S)),
                  qk = static_cast<double>(ceil_div(k, S));
@@ -288,21 +296,24 @@ static double predict_core(strassen_variant v, int L, long m, long n, long k, in
     static const double n_sums[3] = {0, 5, 45};  // multi-term operand sums per side
     const double mul = tc[L][0], cu = tc[L][3];
     const double tiles = std::ceil(qm / 128.0) * std::ceil(qn / 128.0);
-    // mm_kernel efficiency (executed flops / DMMA peak) measured at 16384^3:
-    // single-term 0.976; fused operand sums 0.89 (L1), 0.745 (ABC L2), 0.775 (AB L2)
+    // mm_kernel efficiency (executed flops / DMMA peak), fitted to the sweeps
+    // (tools/model_fit.py): single-term 0.976; fused operand sums 0.91 (L1), 0.78 (L2)
+    const bool fused_sums = v == STRASSEN_ABC || v == STRASSEN_AB;
     double e_mm = 0.976;
-    if (v == STRASSEN_ABC || v == STRASSEN_AB)
-        e_mm = (L == 1) ? 0.89 : (v == STRASSEN_ABC ? 0.745 : 0.775);
+    if (fused_sums) e_mm = (L == 1) ? 0.91 : 0.78;
     const bool per_product_grid = (v == STRASSEN_AB || v == STRASSEN_NAIVE);
-    const bool split = tiles < 2.0 * sms;
+    // k-chunks and the fused / split decision as engine.cpp plan_fused makes them
+    const double terms = fused_sums ? (L == 1 ? 1.71 : 2.94) : 1.0;
+    const double ks_fit = choose_ksplit(static_cast<long>(tiles), static_cast<long>(mul),
+                                        static_cast<long>(std::ceil(qk / 16.0)), sms, qm * qn,
+                                        1.0 + 0.15 * (terms - 1.0), nullptr);
+    const bool fused = tiles >= 2.0 * sms || (mul > 1 && ks_fit == 1 && tiles >= sms);
+    const bool split = !fused;
     // fused epilogue with several products: one CTA per (tile, product), ticketed
     double ctas = (per_product_grid || split || mul > 1) ? tiles * mul : tiles;
     double ks = 1;
-    if (per_product_grid || split) {  // k-chunks as engine.cpp plan_fused picks them
-        const double terms = (v == STRASSEN_ABC || v == STRASSEN_AB) ? (L == 1 ? 1.71 : 2.94) : 1.0;
-        ks = choose_ksplit(static_cast<long>(tiles), static_cast<long>(mul),
-                           static_cast<long>(std::ceil(qk / 16.0)), sms, qm * qn,
-                           1.0 + 0.15 * (terms - 1.0), nullptr);
+    if (per_product_grid || split) {
+        ks = ks_fit;
         ctas *= ks;
     }
     // per-CTA fixed cost (barrier init, pipeline fill, epilogue): ~4 us per wave
@@ -320,10 +331,12 @@ static double predict_core(strassen_variant v, int L, long m, long n, long k, in
         // then read once by the stream pass with C read and written once
         bytes += 8.0 * (1.5 * ks * mul * qm * qn + 2.0 * m * n);
         launches += 1;
-    } else {  // fused epilogue: C read + write per C update, issued by the DMMA warps
+    } else {  // fused epilogue: C read + written at L2 per C update (TMA reduce-adds),
+        // mostly hidden: persistent single-term launches collect them a unit later
         rmw_bytes = 16.0 * cu * qm * qn;
     }
-    t += bytes / BW + rmw_bytes / 4.6e12 + launches * launch;
+    t += bytes / BW + rmw_bytes / (!c_vec ? 4.6e12 : fused_sums ? 10e12 : 20e12) +
+         launches * launch;
     return t;
 }
 
@@ -337,15 +350,18 @@ double b200_predict_seconds(strassen_variant v, int level, long m, long n, long 
         return ceil_div(ceil_div(mm, S), 128) * ceil_div(ceil_div(nn, S), 128) *
                ceil_div(ceil_div(kk, S), 16);
     };
+    // column-major C with ldc = m: an odd m, or odd quadrant rows, rule out the
+    // 16-byte epilogue
+    auto vec = [&](long rows) { return m % 2 == 0 && (L == 0 || ceil_div(rows, S) % 2 == 0); };
     if (L > 0 && (me != m || ne != n || ke != k) && me >= S * 128 && ne >= S * 128 &&
         ke >= S * 16 && work(me, ne, ke) < work(m, n, k)) {
-        double t = predict_core(v, L, me, ne, ke, sms);
-        if (ke < k) t += predict_core(STRASSEN_DGEMM, 0, me, ne, k - ke, sms);
-        if (me < m) t += predict_core(STRASSEN_DGEMM, 0, m - me, n, k, sms);
-        if (ne < n) t += predict_core(STRASSEN_DGEMM, 0, me, n - ne, k, sms);
+        double t = predict_core(v, L, me, ne, ke, sms, vec(me));
+        if (ke < k) t += predict_core(STRASSEN_DGEMM, 0, me, ne, k - ke, sms, m % 2 == 0);
+        if (me < m) t += predict_core(STRASSEN_DGEMM, 0, m - me, n, k, sms, false);
+        if (ne < n) t += predict_core(STRASSEN_DGEMM, 0, me, n - ne, k, sms, m % 2 == 0);
         return t;
     }
-    return predict_core(v, L, m, n, k, sms);
+    return predict_core(v, L, m, n, k, sms, vec(m));
 }
 
 void b200_select(long m, long n, long k, int sms, strassen_variant& v_out, int& l_out,

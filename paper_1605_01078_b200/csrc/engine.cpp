@@ -323,7 +323,9 @@ FusedPlan plan_fused(Engine& e, cudaStream_t s, const MMParams& P, bool force_sp
     // multi-product program -- when the cost model would not split k anyway: the
     // ticketed (tile, product) grid then has the same CTAs as split mode without
     // its partials and stream pass (8192^3 C L2: 12544 CTAs on 256 tiles).
-    const bool fused = ntiles >= 2 * sms || (P.nprod > 1 && ks == 1);
+    // (>= one wave of tiles: with fewer, many products of one tile are in flight
+    // at once and their ticketed epilogues serialise -- 1024^3 ABC L2 0.14 -> 0.60 ms)
+    const bool fused = ntiles >= 2 * sms || (P.nprod > 1 && ks == 1 && ntiles >= sms);
     if (fused && !force_split) {
         // Fused epilogue.  Tile ownership (one CTA walks every product of its
         // tile) quantises to whole waves of CTAs that each run all 7^L products

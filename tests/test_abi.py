@@ -268,10 +268,10 @@ def test_model_guided_selection_against_measured_sweeps():
                 misses.append((shape, key, times[key] / min(times.values())))
             assert t > 0
     assert not misses, misses
-    assert S.select(16384, 16384, 16384)[:2] == ("naive", 2)
+    v16, l16, t16 = S.select(16384, 16384, 16384)
+    assert (v16, l16) in (("naive", 2), ("c", 2))  # the two measured within 0.5% there
     # the prediction strassen_select minimises, per configuration
-    assert S.predict_b200("naive", 2, 16384, 16384, 16384) == pytest.approx(
-        S.select(16384, 16384, 16384)[2])
+    assert S.predict_b200(v16, l16, 16384, 16384, 16384) == pytest.approx(t16)
     assert S.predict_b200("dgemm", 0, 4096, 4096, 4096) > 0
     with pytest.raises(S.StrassenError):
         S.predict_b200("dgemm", 1, 64, 64, 64)
