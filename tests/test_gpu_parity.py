@@ -433,3 +433,62 @@ def test_bulk_reduction_epilogue_short_k(alpha):
         assert nw <= (5e-12 if L == 2 else 1e-12), (v, L, alpha, nw)
         assert torch.equal(runs[0], runs[1]), (v, L, alpha)
     ctx.close()
+
+
+@pytest.mark.parametrize("m,n,k,peel", [
+    (4117, 4100, 1030, False),  # padded L2: quadrant rows 1030 x 3 + 1027 (odd, last) --
+                                # tiles ending there take the register path, the others
+                                # the TMA reduce-add boxes (16-byte row clipping)
+    (4115, 2056, 2048, False),  # padded L1: quadrant rows 2058 + 2057 (odd)
+    (6000, 6000, 3000, True),   # L1: 24 x 24 tiles, fused grid with deferred collection
+    (2304, 4608, 2048, True),   # L1: 9 x 18 = 162 tiles (one wave, < two): fused, no deferral
+])
+def test_tma_reduce_epilogue_shapes_and_deferral(m, n, k, peel):
+    """The fused epilogue's TMA reduce-adds (C-quadrant tensor maps, clipped partial
+    tiles, odd-row quadrants on the register path) and the persistent single-term
+    launches that collect a unit's reductions one unit later: against cuBLAS for
+    every fused variant, with C embedded in a larger buffer (nothing outside it may
+    change) and repeated runs bitwise equal."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(m + n + k)
+    A = (torch.rand(k, m, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    B = (torch.rand(n, k, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    C0 = (torch.rand(n, m, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    ref = C0 - 0.75 * (A @ B)
+    den = (torch.linalg.norm(A) * torch.linalg.norm(B)).item()
+    ctx = S.Ctx()
+    ctx.set_peeling(peel)
+    for v, L in [("c", 1), ("c", 2), ("abc", 1), ("abc", 2), ("dgemm", 0)]:
+        runs = []
+        for _ in range(2):
+            big = torch.full((n + 3, m + 6), -777.25, dtype=torch.float64, device="cuda").t()
+            C = big[2:2 + m, 1:1 + n]  # ldc = m + 6 (even), origin offset 2 + ldc
+            C.copy_(C0)
+            ctx.gemm_device(v, L, -0.75, A, B, C)
+            torch.cuda.synchronize()
+            outside = big.clone()
+            outside[2:2 + m, 1:1 + n] = -777.25
+            assert bool((outside == -777.25).all()), (v, L, "write outside C")
+            runs.append(C.clone())
+        nw = (torch.linalg.norm(runs[0] - ref) / den).item()
+        assert nw <= (5e-12 if L == 2 else 1e-12), (v, L, nw)
+        assert torch.equal(runs[0], runs[1]), (v, L)
+    ctx.close()
+
+
+def test_c_variant_host_windows_match_device():
+    """Host-pointer calls pipeline in small windows (no deferral there); they must match
+    the device entry bitwise for the C variant at a size with a few windows."""
+    import torch
+    d = 6144
+    a, b, c0 = inputs(d, d, d, (91, 92, 93))
+    ctx = S.Ctx()
+    host = np.array(c0, order="F")
+    ctx.gemm("c", 2, 1.0, a, b, host)
+    ta, tb = (torch.from_numpy(np.ascontiguousarray(x.T)).cuda().t() for x in (a, b))
+    tc = torch.from_numpy(np.ascontiguousarray(c0.T)).cuda().t()
+    ctx.gemm_device("c", 2, 1.0, ta, tb, tc)
+    torch.cuda.synchronize()
+    assert np.array_equal(tc.cpu().numpy(), host)
+    assert freivalds(1.0, a, b, c0, host) < 1e-14
+    ctx.close()
