@@ -61,6 +61,9 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-classical", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=CPU_SAMPLE)
+    # run the N > 1 SUMMA code path even at N = 1 (a 1 x 1 grid, no collectives):
+    # a one-GPU check of the multi-GPU bench mechanics
+    p.add_argument("--summa", action="store_true")
     a = p.parse_args()
     if a.variant == "dgemm":
         a.level = 0
@@ -263,7 +266,11 @@ def main():
 
     import paper_1605_01078_b200 as S
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.summa:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
@@ -288,7 +295,7 @@ def main():
     ctx = S.Ctx()
     ctx.set_max_level(3)  # admits naive3 / c3 (B200 extension) beside the reference's levels
     stream = torch.cuda.current_stream()
-    if world > 1:
+    if world > 1 or args.summa:
         return run_summa(args, rank, world, local, colmajor, barrier, max_over_ranks)
     A, B, C = colmajor(m, k), colmajor(k, n), colmajor(m, n)
 
