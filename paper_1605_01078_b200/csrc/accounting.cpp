@@ -319,6 +319,15 @@ static double predict_core(strassen_variant v, int L, long m, long n, long k, in
     // per-CTA fixed cost (barrier init, pipeline fill, epilogue): ~4 us per wave
     double t = mul * 2.0 * qm * qn * qk / (P * e_mm * waves_eff(ctas, sms)) +
                4e-6 * std::ceil(ctas / sms);
+    if (mul == 1 && split) {  // stream-K pieces when they beat the k-chunk waves (engine.cpp)
+        const double kt = std::ceil(qk / 16.0), total = tiles * kt;
+        const double len = std::ceil(total / std::max(1.0, std::min<double>(sms, std::floor(total / 8))));
+        const double per = std::ceil(kt / ks), t_k = 2.1e-6, t_cta = 3e-6;
+        const double t_uni = std::ceil(tiles * ks / sms) * (per * t_k + t_cta) +
+                             (ks > 1 ? 15e-6 : 0.0);
+        const double t_sk = len * t_k + t_cta + 15e-6;
+        if (t_sk < 0.97 * t_uni) t = t_sk;
+    }
     double bytes = 0.0;
     int launches = 1;
     if (v == STRASSEN_NAIVE || v == STRASSEN_C) {  // gather-form sum passes, both sides:

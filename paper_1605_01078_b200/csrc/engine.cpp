@@ -300,6 +300,8 @@ bool is_device_pointer(const void* p) {
 // applied in table order).
 struct FusedPlan {
     bool split = false;
+    bool streamk = false;    // single product, split mode: stream-K pieces (kernels.cu)
+    int sk_len = 0, sk_maxp = 0, sk_grid = 0;
     bool fixup = false;      // split mode finished in the epilogue (no stream pass)
     int* arrive = nullptr;   // per (tile, product) chunk-arrival counters
     int* tickets = nullptr;  // ordered product-parallel fused epilogue (see kernels.hpp)
@@ -364,6 +366,39 @@ FusedPlan plan_fused(Engine& e, cudaStream_t s, const MMParams& P, bool force_sp
         const char* v = std::getenv("STRASSEN_B200_FIXUP");  // 0 / 1 (experiments)
         return v ? std::atoi(v) != 0 : true;
     }();
+    static const bool streamk_on = [] {
+        const char* v = std::getenv("STRASSEN_B200_STREAMK");  // 0 / 1 (experiments)
+        return v ? std::atoi(v) != 0 : true;
+    }();
+    if (!force_split && fixup_on && P.nprod == 1 && streamk_on) {
+        // Stream-K: the flattened (tile, k-step) space cut into equal ranges, one
+        // per persistent CTA, so every SM gets the same work (uniform k-chunks
+        // quantise to whole waves: 2048^3 has 256 tiles on 148 SMs).  Pieces of a
+        // tile are summed in k order by the last to arrive: deterministic.
+        const long total = static_cast<long>(ntiles) * P.ktiles;
+        const long min_piece = 8;  // k-steps: prologue and partial traffic stay small
+        const long want = std::max(1L, std::min<long>(sms, total / min_piece));
+        const long len = ceil_div(total, want);
+        // worth it only where whole-wave quantisation of the k-chunk plan costs more
+        // than the pieces' partial round trip (~15 us): 2048^3 570 -> 518 us, while
+        // 1536^3 (144 tiles, one full wave) got slower (219 -> 232 us)
+        const double t_k = 2.1e-6, t_cta = 3e-6;
+        const double t_uni = std::ceil(static_cast<double>(ntiles) * ks / sms) *
+                                 (static_cast<double>(per) * t_k + t_cta) +
+                             (ks > 1 ? 15e-6 : 0.0);  // k-chunks take the same partial fixup
+        const double t_sk = static_cast<double>(len) * t_k + t_cta + 15e-6;
+        if (t_sk < 0.97 * t_uni) F.streamk = true;
+    }
+    if (F.streamk) {
+        const long total = static_cast<long>(ntiles) * P.ktiles;
+        const long len = ceil_div(total, std::max(1L, std::min<long>(sms, total / 8)));
+        F.sk_len = static_cast<int>(len);
+        F.sk_grid = static_cast<int>(ceil_div(total, len));
+        F.sk_maxp = static_cast<int>(ceil_div(len, P.ktiles) + 1);
+        F.ksplit = static_cast<int>(ceil_div(P.ktiles, len) + 1);  // partial slots per tile
+        F.per = P.ktiles;
+        F.M = e.ensure(e.mbuf, static_cast<size_t>(F.mstride) * F.ksplit * 8);
+    }
     if (!force_split && fixup_on && P.nprod == 1) {
         const size_t nt = static_cast<size_t>(P.tiles_m) * P.tiles_n;
         int* buf = reinterpret_cast<int*>(
@@ -451,6 +486,12 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
         P.ticket_ld = F.ticket_ld;
         P.arrive = F.arrive;
         P.grid_cap = cap(false);
+        if (F.streamk) {
+            P.streamk = 1;
+            P.sk_len = F.sk_len;
+            P.sk_maxp = F.sk_maxp;
+            P.grid_cap = F.sk_grid;  // the decode assumes exactly this many CTAs
+        }
         e.prof_begin("mm_kernel", s);
         ck(launch_mm(P, s), "mm_kernel (split, fused epilogue)");
         e.prof_end(s);

@@ -398,10 +398,14 @@ __device__ __forceinline__ void product_kloop(const uint8_t* raw, uint64_t* raw_
 }
 
 // One work unit of an mm launch: a C tile and the products / k-range it runs.
+// piece / npieces: this unit's k-range is piece `piece` of the `npieces` that
+// make up its (tile, product) -- k-chunks in split mode, stream-K pieces.
 struct Unit {
     int tm, tn, p_lo, p_hi, kt_lo, kt_hi;
+    int piece, npieces;
 };
 __device__ __forceinline__ int unit_count(const MMParams& P) {
+    if (P.streamk) return P.grid_cap * P.sk_maxp;
     return P.tiles_m * P.tiles_n * (P.split ? P.nprod * P.ksplit : 1);
 }
 // unit -> (tile, product, k-chunk) in split mode, tile (all products) otherwise;
@@ -412,7 +416,28 @@ __device__ __forceinline__ Unit decode_unit(const MMParams& P, int bid) {
     U.p_hi = P.nprod;
     U.kt_lo = 0;
     U.kt_hi = P.ktiles;
-    if (P.split && P.unit_group > 0 && P.ksplit == 1) {
+    U.piece = 0;
+    U.npieces = 1;
+    if (P.streamk) {
+        // stream-K (one product): CTA c covers k-steps [c*len, (c+1)*len) of the
+        // flattened (tile, k-step) space; its j-th unit is its piece of tile t0 + j
+        // (an empty unit when the range ends earlier).  Tile t's pieces, in k
+        // order, come from CTAs t*K/len .. ((t+1)*K-1)/len.
+        const int grid = static_cast<int>(gridDim.x);
+        const int c = bid % grid, jx = bid / grid;
+        const long long K = P.ktiles, len = P.sk_len;
+        const long long total = static_cast<long long>(P.tiles_m) * P.tiles_n * K;
+        const long long lo = c * len, hi = min(lo + len, total);
+        const long long t = lo / K + jx;
+        const long long t_lo = t * K;
+        U.p_lo = 0;
+        U.p_hi = (lo < hi && t_lo < hi) ? 1 : 0;  // empty unit: no product
+        U.kt_lo = static_cast<int>(max(lo, t_lo) - t_lo);
+        U.kt_hi = static_cast<int>(min(hi, t_lo + K) - t_lo);
+        U.piece = c - static_cast<int>(t_lo / len);
+        U.npieces = static_cast<int>((t_lo + K - 1) / len - t_lo / len + 1);
+        bid = U.p_hi ? static_cast<int>(t) : 0;
+    } else if (P.split && P.unit_group > 0 && P.ksplit == 1) {
         // groups of G tiles, product-major inside: unit (t, p) of group g is
         // g*G*nprod + p*gt + t; the ticket a unit waits for, (t, p-1), always
         // has a smaller index (every earlier group is full)
@@ -431,6 +456,8 @@ __device__ __forceinline__ Unit decode_unit(const MMParams& P, int bid) {
         U.p_hi = U.p_lo + 1;
         U.kt_lo = s_idx * P.kt_per_split;
         U.kt_hi = min(P.ktiles, U.kt_lo + P.kt_per_split);
+        U.piece = s_idx;
+        U.npieces = P.ksplit;
         bid %= ntiles;
     }
     const int per_group = P.group_m * P.tiles_n;
@@ -719,7 +746,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         // partial tiles at the quadrant edge.
         bool bulk = P.mode == kEpiRMW && P.c_tma && p_hi - p_lo == 1 &&
                     kt_hi - kt_lo <= P.bulk_max_kt && (SEP || !persistent) &&
-                    !(P.split && P.ksplit > 1);
+                    U.npieces == 1;
         // the reduce-add clips rows at 16-byte granularity (microbench/tma_reduce_f64.cu):
         // a tile ending inside a quadrant with an odd row count takes the register path
         for (int u = 0; u < pd.nc && bulk; ++u) {
@@ -792,9 +819,10 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             }
             continue;  // next product (none: single-product CTA)
         }
-        if (P.mode == kEpiRMW && P.arrive && P.ksplit > 1) {
+        if (P.mode == kEpiRMW && P.arrive && U.npieces > 1) {
             // ---- k-split fused epilogue: partial out, the last chunk sums ----
-            const int s_idx = kt_lo / P.kt_per_split;
+            // (partials in slots p * ksplit + piece; ksplit = slots per product)
+            const int s_idx = U.piece;
             const long long ldm = P.ldm;
             {
                 double* Mo = P.mbase + static_cast<long long>(p * P.ksplit + s_idx) * P.mstride;
@@ -817,7 +845,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             __shared__ int last_flag;
             if (threadIdx.x == 0) {
                 int* cnt = P.arrive + (tm * P.ticket_ld + tn) * P.nprod + p;
-                last_flag = atomicAdd(cnt, 1) == P.ksplit - 1;
+                last_flag = atomicAdd(cnt, 1) == U.npieces - 1;
             }
             consumer_bar();
             if (!last_flag) continue;  // another chunk finishes this product
@@ -825,7 +853,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             // M_p = P_0 + P_1 + ... in s order (the stream pass's order), read
             // back from L2 (this CTA's own partial included)
             const double* Mp = P.mbase + static_cast<long long>(p * P.ksplit) * P.mstride;
-            for (int sp = 0; sp < P.ksplit; ++sp) {
+            for (int sp = 0; sp < U.npieces; ++sp) {
 #pragma unroll
                 for (int nf = 0; nf < 4; ++nf)
 #pragma unroll
@@ -934,7 +962,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                 if (threadIdx.x == 0) st_release_gpu(ticket, p + 1);
             }
         } else {
-            const int mi = P.split ? p * P.ksplit + (kt_lo / P.kt_per_split) : p;
+            const int mi = P.split ? p * P.ksplit + U.piece : p;
             // product temporaries: rows 2g, 2g+1 of fragment pair (2h, 2h+1)
             // are adjacent (ldm even) -> one 16-byte streaming store
             // (st.global.cs: evict-first, keeps operand panels in L2)

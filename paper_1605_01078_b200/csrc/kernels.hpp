@@ -114,6 +114,11 @@ struct alignas(64) MMParams {
     // least two grid-widths of units away (else it would wait a whole unit)
     int sep_defer;
     int c_tma;  // tmC valid: bulk epilogue through tensor reduce-adds (partial tiles too)
+    // stream-K (single-product programs with under two waves of tiles): persistent
+    // CTA c covers k-steps [c * sk_len, (c + 1) * sk_len) of the flattened (tile,
+    // k-step) space, at most sk_maxp pieces; partial pieces go through the k-split
+    // fixup (ksplit = partial slots per tile, arrive counters per tile)
+    int streamk, sk_len, sk_maxp;
 };
 
 cudaError_t launch_mm(const MMParams& p, cudaStream_t s);
