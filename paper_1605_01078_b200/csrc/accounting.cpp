@@ -336,8 +336,11 @@ static double predict_core(strassen_variant v, int L, long m, long n, long k, in
         launches += 2;
     }
     double rmw_bytes = 0.0;
-    if (per_product_grid || split) {  // M_{p,s} written (mostly hidden under the DMMAs),
-        // then read once by the stream pass with C read and written once
+    if (mul == 1 && split) {  // classical: partials summed by the last piece's CTA, no
+        // stream pass (engine.cpp plan_fused fixup / stream-K)
+        bytes += 8.0 * (1.5 * ks * qm * qn + 2.0 * m * n);
+    } else if (per_product_grid || split) {  // M_{p,s} written (mostly hidden under the
+        // DMMAs), then read once by the stream pass with C read and written once
         bytes += 8.0 * (1.5 * ks * mul * qm * qn + 2.0 * m * n);
         launches += 1;
     } else {  // fused epilogue: C read + written at L2 per C update (TMA reduce-adds),

@@ -68,7 +68,12 @@ def main():
         extra = L3 if family == "square" and min(m, n, k) >= 4096 else []
         for v, L in variants(family) + extra:
             best = None
-            for r in range(reps + 1):
+            # small problems are a few hundred microseconds: take the best of more
+            # repetitions (at least `reps`, up to ~50 ms of calls) so clock ramps and
+            # host jitter do not dominate
+            n_rep = reps if m * n * k >= 4096 ** 3 else max(reps, min(40, int(5e-2 / max(
+                2.0 * m * n * k / 30e12, 1e-5))))
+            for r in range(n_rep + 1):
                 C = C0.clone().t().contiguous().t()  # fresh column-major copy of C0
                 torch.cuda.synchronize()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -85,7 +90,7 @@ def main():
             qm, qn, qk = -(-m // s), -(-n // s), -(-k // s)
             mul, aa, ba, cu = table(L)
             fexec = mul * 2.0 * qm * qn * qk if L else 2.0 * m * n * k
-            rows.append(dict(m=m, n=n, k=k, variant=v, level=L, threads=1, reps=reps, time_s=best,
+            rows.append(dict(m=m, n=n, k=k, variant=v, level=L, threads=1, reps=n_rep, time_s=best,
                              egf_measured=egf, egf_modeled="", rel_err=err,
                              exec_frac_of_dmma_peak=fexec / best / 1e12 / PEAK))
             print(f"{m}x{n}x{k} {v}{L}: {egf / 1e3:.2f} TF/s err {err:.1e}", flush=True)
