@@ -256,6 +256,8 @@ def summa_loopback(layout: Layout, A_blocks: List[torch.Tensor], B_blocks: List[
 
     Each "broadcast" is a copy from the owner's block, and ranks run one after another on
     one device. Nothing waits on another launch, so a single GPU can run it safely.
+    Returns the GPU kernel launches of the local updates (one per update when
+    `local_gemm` reports no count).
     """
     L = layout
     gemm = local_gemm or _default_local_gemm(variant, level)
@@ -263,6 +265,7 @@ def summa_loopback(layout: Layout, A_blocks: List[torch.Tensor], B_blocks: List[
     dev = C_blocks[0].device
     abuf = torch.empty((L.b, L.m_l), dtype=torch.float64, device=dev).t()
     bbuf = torch.empty((L.n_l, L.b), dtype=torch.float64, device=dev).t()
+    launches = 0
     for p in range(L.panels):
         for r in range(P):
             i, j = divmod(r, L.pc)
@@ -270,5 +273,6 @@ def summa_loopback(layout: Layout, A_blocks: List[torch.Tensor], B_blocks: List[
                 abuf[:, po:po + w].copy_(A_blocks[i * L.pc + oc][:, lo:lo + w])
             for orow, lo, w, po in L.b_pieces(p):      # column-j broadcasts
                 bbuf[po:po + w, :].copy_(B_blocks[orow * L.pc + j][lo:lo + w, :])
-            gemm(alpha, abuf, bbuf, C_blocks[r])
-    return L.panels
+            n = gemm(alpha, abuf, bbuf, C_blocks[r])
+            launches += n if isinstance(n, int) else 1
+    return launches

@@ -61,3 +61,46 @@ def freivalds(alpha, a, b, c0, c, seed=0):
     num = np.linalg.norm((lhs - rhs).astype(np.float64))
     den = np.linalg.norm(a) * np.linalg.norm(b) * np.linalg.norm(x.astype(np.float64))
     return float(num / den)
+
+
+# ---- counter-based RNG (distributed sizes regenerate any tile) --------
+# value(id, i, j) = 2 * h / 2^32 - 1 with h a 32-bit mix of (seed, matrix id, global row,
+# global column); the same integer arithmetic in numpy (oracle side) and torch (GPU
+# side), so shards and oracle tiles of a 65536^3 problem never need the full matrices.
+M32 = 0xFFFFFFFF
+
+
+def _mix32(x, xp_and):
+    x = xp_and(x ^ (x >> 16), M32)
+    x = xp_and(x * 0x7FEB352D, M32)
+    x = xp_and(x ^ (x >> 15), M32)
+    x = xp_and(x * 0x846CA68B, M32)
+    return xp_and(x ^ (x >> 16), M32)
+
+
+def counter_uniform_np(mid, r0, rows, c0, cols, seed=0):
+    """Column-major (Fortran) rows x cols tile of matrix `mid` at (r0, c0), uniform[-1,1)."""
+    import numpy as np
+    i = np.arange(r0, r0 + rows, dtype=np.int64)[:, None]
+    j = np.arange(c0, c0 + cols, dtype=np.int64)[None, :]
+    with np.errstate(over="ignore"):
+        x = (i * 0x9E3779B1 + j * 0x85EBCA77 + mid * 0xC2B2AE3D + seed) & M32
+        h = _mix32(x, np.bitwise_and)
+    return np.asfortranarray(h.astype(np.float64) * (2.0 / 4294967296.0) - 1.0)
+
+
+def counter_uniform_torch(mid, r0, rows, c0, cols, seed=0, device="cuda", out=None):
+    """Same values as counter_uniform_np, generated on the GPU in column chunks into a
+    column-major (rows x cols) view `out` (allocated if None)."""
+    import torch
+    if out is None:
+        out = torch.empty((cols, rows), dtype=torch.float64, device=device).t()
+    i = torch.arange(r0, r0 + rows, dtype=torch.int64, device=device)[:, None]
+    step = max(1, (1 << 27) // max(rows, 1))
+    for cs in range(0, cols, step):
+        ce = min(cols, cs + step)
+        j = torch.arange(c0 + cs, c0 + ce, dtype=torch.int64, device=device)[None, :]
+        x = (i * 0x9E3779B1 + j * 0x85EBCA77 + mid * 0xC2B2AE3D + seed) & M32
+        h = _mix32(x, torch.bitwise_and)
+        out[:, cs:ce] = h.to(torch.float64) * (2.0 / 4294967296.0) - 1.0
+    return out

@@ -125,3 +125,18 @@ def test_loopback_on_gpu_with_strassen_kernels(cuda, P, variant, level, b):
         _, _, wc = SU.local_blocks(L, r, A, B, want)
         nw = (torch.linalg.norm(Cb[r] - wc) / (an * bn)).item()
         assert nw <= (1e-12 if level == 1 else 5e-12), (r, nw)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,P,variant,level", [(16384, 8, "abc", 2), (16384, 4, "naive", 2)])
+def test_config5_loopback_counter_rng_sampled_tiles(cuda, N, P, variant, level):
+    """BASELINE config 5's protocol at a reduced size (tools/cfg5_loopback.py runs the full
+    65536^3, profiles/r01_cfg5_loopback.log): operands from the counter-based RNG, SUMMA
+    over P virtual ranks with local Strassen updates, sampled 256 x 256 tiles against the
+    oracle regenerated from the same counters, and a whole-matrix Freivalds check."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                    "tools"))
+    import cfg5_loopback
+    res = cfg5_loopback.run(N, P, variant, level)
+    assert res["pass"], res
