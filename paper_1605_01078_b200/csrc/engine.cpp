@@ -355,6 +355,8 @@ FusedPlan plan_fused(Engine& e, cudaStream_t s, const MMParams& P, bool force_sp
     F.split = true;
     F.ldm = (P.qm + 1) / 2 * 2;  // even: 16-B stores
     F.mstride = F.ldm * P.qn;
+    if (const char* v = std::getenv("STRASSEN_B200_MPAD"))  // doubles (experiments)
+        F.mstride += std::atol(v);
     F.M = e.ensure(e.mbuf, static_cast<size_t>(F.mstride) * P.nprod * F.ksplit * 8);
     // Classical (one product): the last k-chunk CTA of each tile sums the
     // partials in chunk order and applies the C update -- the stream pass's

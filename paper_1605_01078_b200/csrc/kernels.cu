@@ -18,6 +18,7 @@
 // Why DMMA, and why sums are formed once per CTA: DESIGN.md section 3
 // (profiles/r01_fp64_peak.log: DMMA 37.1 TF/s vs DFMA 34.2; DADD shares the
 // FP64 pipe with DMMA).
+#include <cstdlib>
 #include <cstring>
 
 #include <cuda.h>
@@ -1222,6 +1223,158 @@ stream_gather2_kernel(const __grid_constant__ StreamGatherParams P) {
     }
 }
 
+// Register form of the row-pair stream pass for the full level-1 / level-2 tables:
+// the destination quadrants of every product are compile-time constants (the
+// one-level table, table.cpp:18-33, composed as table.cpp:47-67 does -- in
+// constexpr code here, so nothing is hand-entered twice), so the 4^L C
+// accumulators live in registers instead of shared memory (the shared-memory
+// form spends ~2 LDS/STS per update and was bound by them).  Per element the
+// updates are the same fma's in the same order: bitwise identical results.
+// The host uses it only when the call's (product -> destination quadrant) lists
+// equal the table's.
+struct StreamTab {
+    int np;
+    int nd[kMaxProducts];
+    int dq[kMaxProducts][kMaxQuad];
+};
+constexpr StreamTab stream_tab_l1() {
+    StreamTab t{};
+    // C updates of M0..M6 (quadrant 2 * row + col), table.cpp:18-33
+    const int d[7][2] = {{0, 3}, {2, 3}, {1, 3}, {0, 2}, {1, 0}, {3, -1}, {0, -1}};
+    t.np = 7;
+    for (int p = 0; p < 7; ++p) {
+        t.nd[p] = d[p][1] < 0 ? 1 : 2;
+        for (int u = 0; u < t.nd[p]; ++u) t.dq[p][u] = d[p][u];
+    }
+    return t;
+}
+constexpr StreamTab stream_tab_compose(const StreamTab& o, const StreamTab& in) {
+    StreamTab t{};
+    t.np = o.np * in.np;
+    for (int a = 0; a < o.np; ++a)
+        for (int b = 0; b < in.np; ++b) {
+            const int p = a * in.np + b;
+            t.nd[p] = 0;
+            for (int u = 0; u < o.nd[a]; ++u)
+                for (int v = 0; v < in.nd[b]; ++v) {
+                    const int oq = o.dq[a][u], iq = in.dq[b][v];
+                    const int row = 2 * (oq / 2) + iq / 2, col = 2 * (oq % 2) + iq % 2;
+                    t.dq[p][t.nd[p]++] = row * 4 + col;
+                }
+        }
+    return t;
+}
+// each product's destinations in ascending quadrant order, as the gather form lists
+// them (to_gather below); per C element the update order is unchanged (ascending p)
+constexpr StreamTab stream_tab_sorted(StreamTab t) {
+    for (int p = 0; p < t.np; ++p)
+        for (int a = 1; a < t.nd[p]; ++a)
+            for (int b = a; b > 0 && t.dq[p][b - 1] > t.dq[p][b]; --b) {
+                const int x = t.dq[p][b];
+                t.dq[p][b] = t.dq[p][b - 1];
+                t.dq[p][b - 1] = x;
+            }
+    return t;
+}
+constexpr StreamTab kStreamTab1 = stream_tab_sorted(stream_tab_l1());
+constexpr StreamTab kStreamTab2 = stream_tab_sorted(stream_tab_compose(stream_tab_l1(), stream_tab_l1()));
+template <int L>
+__host__ __device__ constexpr const StreamTab& stream_tab() { return L == 1 ? kStreamTab1 : kStreamTab2; }
+
+template <int L, int PR, int D>
+__device__ __forceinline__ void stream_upd(double2 (&acc)[L == 1 ? 4 : 16], const double2& v,
+                                           const StreamGatherParams& P) {
+    if constexpr (D < stream_tab<L>().nd[PR]) {
+        constexpr int q = stream_tab<L>().dq[PR][D];
+        const double g = P.alpha * static_cast<double>(P.dcoeff[PR][D]);
+        acc[q].x = fma(g, v.x, acc[q].x);
+        acc[q].y = fma(g, v.y, acc[q].y);
+        stream_upd<L, PR, D + 1>(acc, v, P);
+    }
+}
+
+template <int L, int P0, int T = 0>
+__device__ __forceinline__ void stream_apply(double2 (&acc)[L == 1 ? 4 : 16],
+                                             const double2 (&v)[kStreamBatch],
+                                             const StreamGatherParams& P) {
+    if constexpr (T < kStreamBatch && P0 + T < stream_tab<L>().np) {
+        stream_upd<L, P0 + T, 0>(acc, v[T], P);
+        stream_apply<L, P0, T + 1>(acc, v, P);
+    }
+}
+
+// products B*8 .. B*8+7: their M values loaded together, then applied in order
+template <int L, int B>
+__device__ __forceinline__ void stream_batch(double2 (&acc)[L == 1 ? 4 : 16], const double* Mij,
+                                             const StreamGatherParams& P) {
+    constexpr int NP = stream_tab<L>().np;
+    if constexpr (B * kStreamBatch < NP) {
+        double2 v[kStreamBatch];
+#pragma unroll
+        for (int t = 0; t < kStreamBatch; ++t) {
+            if (B * kStreamBatch + t < NP) {
+                const double* M = Mij + static_cast<long long>(B * kStreamBatch + t) * P.ksplit *
+                                            P.mstride;
+                v[t] = *reinterpret_cast<const double2*>(M);
+                for (int sp = 1; sp < P.ksplit; ++sp) {
+                    const double2 x = *reinterpret_cast<const double2*>(M + sp * P.mstride);
+                    v[t].x += x.x;
+                    v[t].y += x.y;
+                }
+            }
+        }
+        stream_apply<L, B * kStreamBatch>(acc, v, P);
+        stream_batch<L, B + 1>(acc, Mij, P);
+    }
+}
+
+template <int L>
+__global__ void __launch_bounds__(kStream2Threads)
+stream_fixed_kernel(const __grid_constant__ StreamGatherParams P) {
+    constexpr int NQ = L == 1 ? 4 : 16;
+    const int tid = threadIdx.x;
+    const long long i = P.r0 + 2 * (static_cast<long long>(blockIdx.x) * kStream2Threads + tid);
+    if (i >= P.r1) return;
+    for (long long j = P.c0 + blockIdx.y; j < P.c1; j += gridDim.y) {
+        double2 acc[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            acc[q] = make_double2(0.0, 0.0);
+            if (j < P.ccols[q]) {
+                const double* pc = P.cptr[q] + i + j * P.cs_c;
+                if (i + 1 < P.crows[q])
+                    acc[q] = *reinterpret_cast<const double2*>(pc);
+                else if (i < P.crows[q])
+                    acc[q].x = *pc;
+            }
+        }
+        stream_batch<L, 0>(acc, P.mbase + i + j * P.ldm, P);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+            if (j < P.ccols[q]) {
+                double* pc = P.cptr[q] + i + j * P.cs_c;
+                if (i + 1 < P.crows[q])
+                    *reinterpret_cast<double2*>(pc) = acc[q];
+                else if (i < P.crows[q])
+                    *pc = acc[q].x;
+            }
+    }
+}
+
+// Does the gather form's (product -> destination quadrants) structure equal the
+// level-L table?  (Coefficients stay runtime parameters.)
+template <int L>
+bool matches_stream_tab(const StreamGatherParams& g) {
+    const StreamTab& t = stream_tab<L>();
+    if (g.nquad != (L == 1 ? 4 : 16) || g.nprod != t.np) return false;
+    for (int p = 0; p < t.np; ++p) {
+        if (g.ndest[p] != t.nd[p]) return false;
+        for (int d = 0; d < t.nd[p]; ++d)
+            if (g.dq[p][d] != t.dq[p][d]) return false;
+    }
+    return true;
+}
+
 __global__ void scale_kernel(double* c, long rows, long cols, long long rs, long long cs,
                              double beta) {
     const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1369,17 +1522,30 @@ static bool to_gather(const StreamParams& p, StreamGatherParams& g) {
 
 cudaError_t launch_stream_update(const StreamParams& p, cudaStream_t s) {
     static thread_local StreamGatherParams g;
+    static const int ycap = [] {
+        const char* v = std::getenv("STRASSEN_B200_STREAM_Y");  // grid.y cap (experiments)
+        return v ? std::atoi(v) : 4096;
+    }();
     if (to_gather(p, g)) {
-        const int w = p.c1 - p.c0;
+        const int w = p.c1 - p.c0 < ycap ? p.c1 - p.c0 : ycap;
         if (p.c_vec && p.ldm % 2 == 0 && p.mstride % 2 == 0) {  // 16-byte rows pairs
             dim3 grid(static_cast<unsigned>(((p.r1 - p.r0 + 1) / 2 + kStream2Threads - 1) /
                                             kStream2Threads),
-                      static_cast<unsigned>(w < 4096 ? w : 4096));
-            stream_gather2_kernel<<<grid, kStream2Threads, 0, s>>>(g);
+                      static_cast<unsigned>(w));
+            static const bool fixed_on = [] {
+                const char* v = std::getenv("STRASSEN_B200_STREAM_FIXED");  // 0 / 1 (experiments)
+                return v ? std::atoi(v) != 0 : true;
+            }();
+            if (fixed_on && matches_stream_tab<2>(g))
+                stream_fixed_kernel<2><<<grid, kStream2Threads, 0, s>>>(g);
+            else if (fixed_on && matches_stream_tab<1>(g))
+                stream_fixed_kernel<1><<<grid, kStream2Threads, 0, s>>>(g);
+            else
+                stream_gather2_kernel<<<grid, kStream2Threads, 0, s>>>(g);
             return cudaGetLastError();
         }
         dim3 grid(static_cast<unsigned>((p.r1 - p.r0 + kStreamThreads - 1) / kStreamThreads),
-                  static_cast<unsigned>(w < 4096 ? w : 4096));
+                  static_cast<unsigned>(w));
         stream_gather_kernel<<<grid, kStreamThreads, 0, s>>>(g);
         return cudaGetLastError();
     }

@@ -1,3 +1,5 @@
+"""Clipped-destination probe: C embedded in a larger host buffer; reports writes outside
+the view and the max error inside, per variant (tools/canary_probe.py)."""
 import sys, os
 sys.path.insert(0, '.'); sys.path.insert(0, 'tests')
 import numpy as np
