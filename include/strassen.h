@@ -230,6 +230,13 @@ strassen_status strassen_predict_b200(strassen_variant variant, int level, long 
 strassen_status strassen_select(long m, long n, long k, strassen_variant* variant_out,
                                 int* level_out, double* seconds_out);
 
+/* strassen_select over the levels this ctx admits (strassen_ctx_set_max_level):
+ * with max level 3 the Naive / C level-3 configurations are candidates too.
+ * strassen_predict_b200 also accepts level 3 for Naive and C. */
+strassen_status strassen_ctx_select(const strassen_ctx* ctx, long m, long n, long k,
+                                    strassen_variant* variant_out, int* level_out,
+                                    double* seconds_out);
+
 /* Counter values one strassen_gemm(variant, level, m, n, k) call adds under
  * blocking *bp (the analytic instrumentation; no device needed).  Same
  * validation as strassen_gemm for variant / level / dimensions / blocking. */

@@ -124,6 +124,8 @@ def _declare(lib):
         "strassen_ctx_set_max_level": (_ST, [vp, C.c_int]),
         "strassen_ctx_last_profile": (_ST, [vp, C.c_char_p, _L]),
         "strassen_select": (_ST, [_L, _L, _L, C.POINTER(C.c_int), C.POINTER(C.c_int), _dp]),
+        "strassen_ctx_select": (_ST, [vp, _L, _L, _L, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                      _dp]),
         "strassen_predict_b200": (_ST, [C.c_int, C.c_int, _L, _L, _L, _dp]),
         "strassen_build_info": (C.c_char_p, []),
         "strassen_last_error": (C.c_char_p, []),
@@ -248,6 +250,14 @@ class Ctx:
     def set_max_level(self, level):
         """2 (default) or 3: level 3 for the naive / c variants (B200 extension)."""
         _check(self._l.strassen_ctx_set_max_level(self.ptr, int(level)), "set_max_level")
+
+    def select(self, m, n, k):
+        """(variant, level, predicted seconds) over the levels this ctx admits."""
+        v, lv, t = C.c_int(), C.c_int(), C.c_double()
+        _check(self._l.strassen_ctx_select(self.ptr, m, n, k, C.byref(v), C.byref(lv),
+                                           C.byref(t)), "ctx_select")
+        name = {val: key for key, val in VARIANT_NAMES.items()}[v.value]
+        return name, lv.value, t.value
 
     def enable_profiling(self, on=True):
         _check(self._l.strassen_ctx_enable_profiling(self.ptr, int(bool(on))), "enable_profiling")

@@ -352,7 +352,32 @@ static double predict_core(strassen_variant v, int L, long m, long n, long k, in
     return t;
 }
 
+// Level 3 (Naive / C, engine.cpp run_outer): the outer operand sums (four source
+// quadrants read, five sums written per side), the products zeroed, seven level-2
+// calls on the outer quadrants, and the outer stream pass (seven M_r read, C read
+// and written), at the HBM rate of the level-2 passes.
+static double predict_level3(strassen_variant v, long m, long n, long k, int sms) {
+    const double BW = 5.5e12, launch = 20e-6;
+    const long qm = ceil_div(m, 2), qn = ceil_div(n, 2), qk = ceil_div(k, 2);
+    const double bytes = 8.0 * 9.0 * (static_cast<double>(qm) * qk + static_cast<double>(qk) * qn) +
+                         8.0 * 7.0 * qm * qn +
+                         8.0 * (7.0 * qm * qn + 2.0 * static_cast<double>(m) * n);
+    return 7.0 * b200_predict_seconds(v, 2, qm, qn, qk, sms) + bytes / BW + 4 * launch;
+}
+
 double b200_predict_seconds(strassen_variant v, int level, long m, long n, long k, int sms) {
+    if (level == 3 && (v == STRASSEN_NAIVE || v == STRASSEN_C)) {
+        // peeling on the 8-aligned core, as run_device does at level 3
+        const long me = m & ~7L, ne = n & ~7L, ke = k & ~7L;
+        if ((me != m || ne != n || ke != k) && me >= 8 * 128 && ne >= 8 * 128 && ke >= 8 * 16) {
+            double t = predict_level3(v, me, ne, ke, sms);
+            if (ke < k) t += b200_predict_seconds(STRASSEN_DGEMM, 0, me, ne, k - ke, sms);
+            if (me < m) t += b200_predict_seconds(STRASSEN_DGEMM, 0, m - me, n, k, sms);
+            if (ne < n) t += b200_predict_seconds(STRASSEN_DGEMM, 0, me, n - ne, k, sms);
+            return t;
+        }
+        return predict_level3(v, m, n, k, sms);
+    }
     const int L = (v == STRASSEN_DGEMM) ? 0 : level;
     const long S = 1L << L;
     const long me = m & ~(S - 1), ne = n & ~(S - 1), ke = k & ~(S - 1);
@@ -377,15 +402,16 @@ double b200_predict_seconds(strassen_variant v, int level, long m, long n, long 
 }
 
 void b200_select(long m, long n, long k, int sms, strassen_variant& v_out, int& l_out,
-                 double& t_out) {
+                 double& t_out, int max_level) {
     const struct {
         strassen_variant v;
         int l;
     } cand[] = {{STRASSEN_DGEMM, 0}, {STRASSEN_ABC, 1}, {STRASSEN_AB, 1}, {STRASSEN_NAIVE, 1},
                 {STRASSEN_C, 1},     {STRASSEN_ABC, 2}, {STRASSEN_AB, 2}, {STRASSEN_NAIVE, 2},
-                {STRASSEN_C, 2}};
+                {STRASSEN_C, 2},     {STRASSEN_NAIVE, 3}, {STRASSEN_C, 3}};
     t_out = 1e300;
     for (const auto& c : cand) {
+        if (c.l > max_level) continue;
         if (c.l > 0 && (m < (1L << c.l) || n < (1L << c.l) || k < (1L << c.l))) continue;
         const double t = b200_predict_seconds(c.v, c.l, m, n, k, sms);
         if (t < t_out) {

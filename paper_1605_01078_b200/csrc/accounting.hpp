@@ -24,7 +24,9 @@ void model_predict(strassen_variant v, int level, long m, long n, long k,
 // B200 cost model (strassen_select): predicted seconds of
 // one strassen_gemm call, and the fastest (variant, level) for a shape.
 double b200_predict_seconds(strassen_variant v, int level, long m, long n, long k, int sms);
+// level 3 (Naive / C) is predicted for v in {NAIVE, C}; b200_select considers it only
+// when max_level >= 3 (a ctx that admits it, strassen_ctx_select)
 void b200_select(long m, long n, long k, int sms, strassen_variant& v_out, int& l_out,
-                 double& t_out);
+                 double& t_out, int max_level = 2);
 
 }  // namespace sb200

@@ -495,9 +495,22 @@ static int device_sms() {
 strassen_status strassen_predict_b200(strassen_variant variant, int level, long m, long n, long k,
                                       double* seconds_out) {
     if (!seconds_out) return STRASSEN_ERR_NULL;
-    if (strassen_status st = check_variant_level(variant, level)) return st;
+    if (strassen_status st = check_variant_level(variant, level))
+        if (!(level == 3 && (variant == STRASSEN_NAIVE || variant == STRASSEN_C))) return st;
     if (m < 1 || n < 1 || k < 1) return STRASSEN_ERR_PARAM;
     *seconds_out = sb200::b200_predict_seconds(variant, level, m, n, k, device_sms());
+    return STRASSEN_OK;
+}
+
+strassen_status strassen_ctx_select(const strassen_ctx* ctx, long m, long n, long k,
+                                    strassen_variant* variant_out, int* level_out,
+                                    double* seconds_out) {
+    if (!ctx || !variant_out || !level_out) return STRASSEN_ERR_NULL;
+    if (m < 1 || n < 1 || k < 1) return STRASSEN_ERR_PARAM;
+    double t = 0.0;
+    sb200::b200_select(m, n, k, device_sms(), *variant_out, *level_out, t,
+                       ctx->engine.max_level);
+    if (seconds_out) *seconds_out = t;
     return STRASSEN_OK;
 }
 

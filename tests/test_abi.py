@@ -276,5 +276,19 @@ def test_model_guided_selection_against_measured_sweeps():
     with pytest.raises(S.StrassenError):
         S.predict_b200("dgemm", 1, 64, 64, 64)
     assert S.select(1024, 1024, 1024)[:2] == ("dgemm", 0)
+    # a ctx admitting level 3 also weighs the Naive / C level-3 configurations: within
+    # 3.5% of the best measured square-sweep configuration, level 3 included
+    c3 = S.Ctx()
+    c3.set_max_level(3)
+    assert c3.select(16384, 16384, 16384)[1] == 3
+    assert S.Ctx().select(16384, 16384, 16384)[1] <= 2
+    sq = collections.defaultdict(dict)
+    for r in csv.DictReader(open(os.path.join(ROOT, "profiles", "r01_sweep_square.csv"))):
+        sq[(int(r["m"]), int(r["n"]), int(r["k"]))][r["variant"] + r["level"]] = float(r["time_s"])
+    for shape, times in sq.items():
+        v, lv, _ = c3.select(*shape)
+        assert times[f"{v}{lv}"] <= 1.035 * min(times.values()), (shape, v, lv)
+    assert S.predict_b200("naive", 3, 16384, 16384, 16384) < \
+        S.predict_b200("naive", 2, 16384, 16384, 16384)
     with pytest.raises(S.StrassenError):
         S.select(0, 4, 4)
