@@ -268,7 +268,16 @@ double* Engine::ensure(DeviceBuffer& b, size_t bytes) {
             b.ptr = nullptr;
             b.bytes = 0;
         }
-        ck(cudaMalloc(&b.ptr, bytes), "cudaMalloc workspace");
+        const cudaError_t err = cudaMalloc(&b.ptr, bytes);
+        if (err != cudaSuccess) {
+            b.ptr = nullptr;
+            cudaGetLastError();
+            size_t fr = 0, tot = 0;
+            cudaMemGetInfo(&fr, &tot);
+            throw Error(err == cudaErrorMemoryAllocation ? STRASSEN_ERR_ALLOC : STRASSEN_ERR_DEVICE,
+                        "cudaMalloc workspace: " + std::to_string(bytes >> 20) + " MiB requested, " +
+                            std::to_string(fr >> 20) + " MiB free");
+        }
         b.bytes = bytes;
     }
     return static_cast<double*>(b.ptr);
@@ -311,15 +320,21 @@ struct FusedPlan {
     double* M = nullptr;
 };
 
-FusedPlan plan_fused(Engine& e, cudaStream_t s, const MMParams& P, bool force_split) {
+// nprod_plan / terms_plan: plan as for this many products with this mean term
+// count (a product group of a larger program plans like the whole program, so
+// its k-chunks -- and results -- are the same); 0 = P's own.
+FusedPlan plan_fused(Engine& e, cudaStream_t s, const MMParams& P, bool force_split,
+                     int nprod_plan = 0, double terms_plan = 0.0) {
     FusedPlan F;
     const int ntiles = P.tiles_m * P.tiles_n;
     const int sms = e.num_sms > 0 ? e.num_sms : 148;
     double terms = 0.0;  // mean operand terms per side: fused sums lengthen a k-tile
     for (int p = 0; p < P.nprod; ++p) terms += 0.5 * (P.prod[p].na + P.prod[p].nb);
     terms /= P.nprod > 0 ? P.nprod : 1;
+    if (terms_plan > 0.0) terms = terms_plan;
+    const int np = nprod_plan > 0 ? nprod_plan : P.nprod;
     long per = P.ktiles;
-    const int ks = choose_ksplit(ntiles, P.nprod, P.ktiles, sms, static_cast<double>(P.qm) * P.qn,
+    const int ks = choose_ksplit(ntiles, np, P.ktiles, sms, static_cast<double>(P.qm) * P.qn,
                                  1.0 + 0.15 * (terms - 1.0), &per);
     // Fused epilogue when the output has >= 2 waves of tiles, or -- for a
     // multi-product program -- when the cost model would not split k anyway: the
@@ -327,7 +342,7 @@ FusedPlan plan_fused(Engine& e, cudaStream_t s, const MMParams& P, bool force_sp
     // its partials and stream pass (8192^3 C L2: 12544 CTAs on 256 tiles).
     // (>= one wave of tiles: with fewer, many products of one tile are in flight
     // at once and their ticketed epilogues serialise -- 1024^3 ABC L2 0.14 -> 0.60 ms)
-    const bool fused = ntiles >= 2 * sms || (P.nprod > 1 && ks == 1 && ntiles >= sms);
+    const bool fused = ntiles >= 2 * sms || (np > 1 && ks == 1 && ntiles >= sms);
     if (fused && !force_split) {
         // Fused epilogue.  Tile ownership (one CTA walks every product of its
         // tile) quantises to whole waves of CTAs that each run all 7^L products
@@ -372,7 +387,7 @@ FusedPlan plan_fused(Engine& e, cudaStream_t s, const MMParams& P, bool force_sp
         const char* v = std::getenv("STRASSEN_B200_STREAMK");  // 0 / 1 (experiments)
         return v ? std::atoi(v) != 0 : true;
     }();
-    if (!force_split && fixup_on && P.nprod == 1 && streamk_on) {
+    if (!force_split && fixup_on && np == 1 && streamk_on) {
         // Stream-K: the flattened (tile, k-step) space cut into equal ranges, one
         // per persistent CTA, so every SM gets the same work (uniform k-chunks
         // quantise to whole waves: 2048^3 has 256 tiles on 148 SMs).  Pieces of a
@@ -401,7 +416,7 @@ FusedPlan plan_fused(Engine& e, cudaStream_t s, const MMParams& P, bool force_sp
         F.per = P.ktiles;
         F.M = e.ensure(e.mbuf, static_cast<size_t>(F.mstride) * F.ksplit * 8);
     }
-    if (!force_split && fixup_on && P.nprod == 1) {
+    if (!force_split && fixup_on && np == 1) {
         const size_t nt = static_cast<size_t>(P.tiles_m) * P.tiles_n;
         int* buf = reinterpret_cast<int*>(
             e.ensure(e.ticket_buf, nt * (1 + static_cast<size_t>(P.nprod)) * sizeof(int)));
@@ -560,6 +575,20 @@ long run_level(Engine& e, cudaStream_t s, strassen_variant variant, int level, d
     return run_strassen(e, s, variant, level, alpha, A, B, C, win);
 }
 
+// Device memory new temporaries may take: free memory less a margin of 4% of the
+// device (allocation granularity, ticket buffers, other libraries' small
+// allocations).  STRASSEN_B200_MEM_CAP overrides it (tests / experiments).
+double device_bytes_free(void) {
+    if (const char* cap = std::getenv("STRASSEN_B200_MEM_CAP")) return std::atof(cap);
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+        cudaGetLastError();
+        return 1e300;
+    }
+    return static_cast<double>(free_b) -
+           std::max(0.04 * static_cast<double>(total_b), static_cast<double>(2ULL << 30));
+}
+
 DView sub(const DView& v, long r0, long c0, long rows, long cols) {
     DView o = v;
     o.p = v.p + r0 * v.rs + c0 * v.cs;
@@ -596,6 +625,15 @@ void plan_windows(const Engine& e, strassen_variant variant, int level, long m, 
     for (int l = 0; l < L; ++l) per_tile *= 7;
     if (variant != STRASSEN_NAIVE && variant != STRASSEN_AB && tiles_m * tiles_n < 2 * sms)
         return;  // split-mode sizes: a few milliseconds, nothing to overlap
+    {   // temporaries that need product groups (run_strassen) rule out windows
+        const long qk = ceil_div(k, side);
+        const double sums = (variant == STRASSEN_NAIVE || variant == STRASSEN_C)
+                                ? (L == 1 ? 5.0 : 45.0) * 8.0 * (qm * qk + qk * qn) : 0.0;
+        const double prods = (variant == STRASSEN_NAIVE || variant == STRASSEN_AB)
+                                 ? per_tile * 8.0 * qm * qn : 0.0;
+        const double held = static_cast<double>(e.tabuf.bytes + e.tbbuf.bytes + e.mbuf.bytes);
+        if (sums + prods > device_bytes_free() + held) return;
+    }
     // windows of >= 2 waves each (consecutive windows overlap on two streams);
     // grow the grid keeping it square-ish
     const long max_w = tiles_m * tiles_n * per_tile / (2 * sms);
@@ -797,178 +835,231 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
         if (l.a.empty() || l.b.empty() || l.c.empty()) continue;
         live.push_back(std::move(l));
     }
-    // Windows (r, c) in row-major order; without `win` one window covers all.
-    const int nr = win ? win->rows : 1, nc = win ? win->cols : 1, nw = nr * nc;
+    // The whole program, or -- when the materialised operand sums and product
+    // temporaries of all live products would not fit in device memory (Naive / C /
+    // AB at very large sizes) -- consecutive groups of products in table order, each
+    // with its own sum pass, products and C updates.  Every C element still receives
+    // its updates in table order.
+    // the whole program's size and mean term count plan every group's launches
+    const int nprod_all = static_cast<int>(live.size());
+    double terms_all = 0.0;
+    for (const Live& l : live)
+        terms_all += (variant == STRASSEN_C || variant == STRASSEN_NAIVE)
+                         ? 1.0 : 0.5 * static_cast<double>(l.a.size() + l.b.size());
+    terms_all /= std::max(1, nprod_all);
+    auto run_program = [&](std::vector<Live> live, MMParams P) -> long {
+        // Windows (r, c) in row-major order; without `win` one window covers all.
+        const int nr = win ? win->rows : 1, nc = win ? win->cols : 1, nw = nr * nc;
 
-    // Windows alternate between s and the aux stream (ordered after s's work so
-    // far); s joins the aux stream at the end.
-    cudaStream_t ws[2] = {s, nw > 1 ? e.aux_stream : s};
-    auto wait_ev = [&](cudaStream_t st, cudaEvent_t ev) {
-        if (ev) ck(cudaStreamWaitEvent(st, ev, 0), "wait");
-    };
-    auto wait_a = [&](cudaStream_t st, int r) { wait_ev(st, win ? win->a_ready[r] : ta.ready); };
-    auto wait_b = [&](cudaStream_t st, int c) { wait_ev(st, win ? win->b_ready[c] : tb.ready); };
-    auto wait_c = [&](cudaStream_t st, int w) {
-        if (win) wait_ev(st, win->c_ready[w]);
-        else wait_ready(st, C);
-    };
-    auto finish = [&](cudaStream_t st, int w) {
-        if (!win) return;
-        ck(cudaEventRecord(win->done[w], st), "window done");
-        win->issue_out(w);
-    };
-    // processing order; the first window of each row strip computes its A
-    // sums (and triggers its copy), likewise for column strips and B
-    const std::vector<int> order = win ? window_order(nr, nc) : std::vector<int>{0};
-    std::vector<int> first_r(nr, -1), first_c(nc, -1);
-    for (int i = 0; i < nw; ++i) {
-        if (first_r[order[i] / nc] < 0) first_r[order[i] / nc] = order[i];
-        if (first_c[order[i] % nc] < 0) first_c[order[i] % nc] = order[i];
-    }
-    auto prefetch = [&](int i) {  // copies of the i-th window, issued one window ahead
-        if (!win || i >= nw) return;
-        const int w = order[i], r = w / nc, c = w % nc;
-        if (first_r[r] == w) win->issue_a(r);
-        if (first_c[c] == w) win->issue_b(c);
-        win->issue_c(w);
-    };
-    auto join = [&] {
-        if (nw > 1) {
-            ck(cudaEventRecord(e.ev_join, e.aux_stream), "join");
-            ck(cudaStreamWaitEvent(s, e.ev_join, 0), "join");
+        // Windows alternate between s and the aux stream (ordered after s's work so
+        // far); s joins the aux stream at the end.
+        cudaStream_t ws[2] = {s, nw > 1 ? e.aux_stream : s};
+        auto wait_ev = [&](cudaStream_t st, cudaEvent_t ev) {
+            if (ev) ck(cudaStreamWaitEvent(st, ev, 0), "wait");
+        };
+        auto wait_a = [&](cudaStream_t st, int r) { wait_ev(st, win ? win->a_ready[r] : ta.ready); };
+        auto wait_b = [&](cudaStream_t st, int c) { wait_ev(st, win ? win->b_ready[c] : tb.ready); };
+        auto wait_c = [&](cudaStream_t st, int w) {
+            if (win) wait_ev(st, win->c_ready[w]);
+            else wait_ready(st, C);
+        };
+        auto finish = [&](cudaStream_t st, int w) {
+            if (!win) return;
+            ck(cudaEventRecord(win->done[w], st), "window done");
+            win->issue_out(w);
+        };
+        // processing order; the first window of each row strip computes its A
+        // sums (and triggers its copy), likewise for column strips and B
+        const std::vector<int> order = win ? window_order(nr, nc) : std::vector<int>{0};
+        std::vector<int> first_r(nr, -1), first_c(nc, -1);
+        for (int i = 0; i < nw; ++i) {
+            if (first_r[order[i] / nc] < 0) first_r[order[i] / nc] = order[i];
+            if (first_c[order[i] % nc] < 0) first_c[order[i] % nc] = order[i];
         }
-    };
+        auto prefetch = [&](int i) {  // copies of the i-th window, issued one window ahead
+            if (!win || i >= nw) return;
+            const int w = order[i], r = w / nc, c = w % nc;
+            if (first_r[r] == w) win->issue_a(r);
+            if (first_c[c] == w) win->issue_b(c);
+            win->issue_c(w);
+        };
+        auto join = [&] {
+            if (nw > 1) {
+                ck(cudaEventRecord(e.ev_join, e.aux_stream), "join");
+                ck(cudaStreamWaitEvent(s, e.ev_join, 0), "join");
+            }
+        };
 
-    prefetch(0);
-    if (live.empty()) {
+        prefetch(0);
+        if (live.empty()) {
+            for (int i = 0; i < nw; ++i) {
+                prefetch(i + 1);
+                wait_c(s, order[i]);
+                finish(s, order[i]);
+            }
+            join();
+            return launches;
+        }
+
+        const bool sums = variant == STRASSEN_C || variant == STRASSEN_NAIVE;
+        std::unique_ptr<SumBatchParams> side_sums[2];
+        if (sums) {
+            // Every multi-term operand sum materialised by one HBM pass per side
+            // (materialize_sum, variants.cpp:53-96, for all entries at once); the
+            // mm launch then runs all 7^L products with single-term operands.
+            //   C variant (B200 addition): fused multi-destination epilogue.
+            //   Naive: products to temporaries M_p, then one stream pass applying
+            //          C_r += alpha*gamma*M_p in table order (variants.cpp:99-109).
+            const long long lda_t = ((qm + 3) / 4) * 4, ldb_t = ((qk + 3) / 4) * 4;
+            int na_sums = 0, nb_sums = 0;
+            for (const Live& l : live) {
+                na_sums += l.a.size() > 1;
+                nb_sums += l.b.size() > 1;
+            }
+            double* TA = e.ensure(e.tabuf, static_cast<size_t>(std::max(na_sums, 1)) * lda_t * qk * 8);
+            double* TB = e.ensure(e.tbbuf, static_cast<size_t>(std::max(nb_sums, 1)) * ldb_t * qn * 8);
+            for (int sd = 0; sd < 2; ++sd) {
+                side_sums[sd].reset(new SumBatchParams);  // ~10 KB: keep off the stack
+                SumBatchParams* SB = side_sums[sd].get();
+                std::memset(SB, 0, sizeof(*SB));
+                int next_map = kMaxQuad;  // tmA / tmB: 16 quadrant maps, then the sums
+                const TmaOperand& t = sd == 0 ? ta : tb;
+                SB->rows = sd == 0 ? qm : qk;
+                SB->cols = sd == 0 ? qk : qn;
+                SB->ld = sd == 0 ? lda_t : ldb_t;
+                for (size_t p = 0; p < live.size(); ++p) {
+                    Terms& terms = sd == 0 ? live[p].a : live[p].b;
+                    if (terms.size() <= 1) continue;  // single term: the quadrant map, sign in-kernel
+                    const int z = SB->njobs++;
+                    double* dst = (sd == 0 ? TA : TB) + static_cast<size_t>(z) * SB->ld * SB->cols;
+                    SB->dst[z] = dst;
+                    SB->nterms[z] = static_cast<int>(terms.size());
+                    for (size_t u = 0; u < terms.size(); ++u) {
+                        const int qi = terms[u].first;
+                        SumTerm& st = SB->t[z][u];
+                        st.x = quad_origin(t, qi / side, qi % side);
+                        st.rows = static_cast<int>(quad_rows(t, qi / side));
+                        st.cols = static_cast<int>(quad_cols(t, qi % side));
+                        st.ld = t.ld;
+                        st.coeff = terms[u].second;
+                    }
+                    const int mi = next_map++;
+                    if (mi >= kMaxMaps) throw Error(STRASSEN_ERR_PARAM, "too many operand maps");
+                    if (sd == 0)
+                        encode_map(&P.tmA[mi], dst, qm, qk, lda_t, 16, kBK, 128);
+                    else
+                        encode_map(&P.tmB[mi], dst, qk, qn, ldb_t, kBK, kBN, 128);
+                    terms = {{mi, 1}};
+                }
+            }
+        }
+
+        // First A and B terms at +1 (kernels.cu product_kloop): a side whose first
+        // coefficient is -1 is negated as a whole, and so are the destination
+        // coefficients.  Exact: (-S) x T = -(S x T) bit for bit under round-to-nearest.
+        for (Live& l : live)
+            for (Terms* t : {&l.a, &l.b})
+                if (t->front().second < 0) {
+                    for (auto& x : *t) x.second = -x.second;
+                    for (auto& x : l.c) x.second = -x.second;
+                }
+
+        P.nprod = static_cast<int>(live.size());
+        std::vector<Terms> dests;
+        for (size_t p = 0; p < live.size(); ++p) {
+            fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);
+            dests.push_back(live[p].c);
+        }
+        // C / ABC / DGEMM: fused epilogue (split only when few tiles).  AB, Naive:
+        // products to temporaries on a product-parallel grid (one CTA per tile x
+        // product: balanced waves at every size), then one stream pass
+        // (AB: variants.cpp:142-168).
+        const bool store_products = variant == STRASSEN_NAIVE || variant == STRASSEN_AB;
+        const FusedPlan F = plan_fused(e, s, P, store_products, nprod_all, terms_all);
+        if (nw > 1) {  // the aux stream starts after everything enqueued on s so far
+            ck(cudaEventRecord(e.ev_fork, s), "fork");
+            ck(cudaStreamWaitEvent(e.aux_stream, e.ev_fork, 0), "fork");
+        }
+
         for (int i = 0; i < nw; ++i) {
             prefetch(i + 1);
-            wait_c(s, order[i]);
-            finish(s, order[i]);
+            const int w = order[i], r = w / nc, c = w % nc;
+            cudaStream_t st = ws[i % 2];
+            const long r0 = win ? win->rb[r] : 0, r1 = win ? win->rb[r + 1] : qm;
+            const long c0 = win ? win->cb[c] : 0, c1 = win ? win->cb[c + 1] : qn;
+            wait_a(st, r);
+            wait_b(st, c);
+            if (sums) {
+                // A sums of row strip r in its first window, B sums of column strip c
+                // in row 0; later windows wait on them
+                for (int sd = 0; sd < 2; ++sd) {
+                    SumBatchParams& SB = *side_sums[sd];
+                    const bool owner = sd == 0 ? first_r[r] == w : first_c[c] == w;
+                    cudaEvent_t ev = sd == 0 ? e.ev_sum_a[r] : e.ev_sum_b[c];
+                    if (!owner) {
+                        wait_ev(st, ev);
+                        continue;
+                    }
+                    if (!SB.njobs) continue;
+                    if (sd == 0) {
+                        SB.r0 = r0;
+                        SB.rows = r1;
+                    } else {
+                        SB.c0 = c0;
+                        SB.cols = c1;
+                    }
+                    e.prof_begin("sum_gather_kernel", st);
+                    ck(launch_sum_batch(SB, st), sd == 0 ? "sum_batch (A)" : "sum_batch (B)");
+                    e.prof_end(st);
+                    ++launches;
+                    if (nw > 1) ck(cudaEventRecord(ev, st), "sum event");
+                }
+            }
+            launches += run_fused_window(e, st, P, F, dests, cq, C, alpha, r0, r1, c0, c1,
+                                         [&] { wait_c(st, w); });
+            finish(st, w);
         }
         join();
         return launches;
+    };
+    const bool sums_v = variant == STRASSEN_C || variant == STRASSEN_NAIVE;
+    const bool store_v = variant == STRASSEN_NAIVE || variant == STRASSEN_AB;
+    const double a_sum = 8.0 * (((qm + 3) / 4) * 4) * qk, b_sum = 8.0 * (((qk + 3) / 4) * 4) * qn;
+    const double m_tmp = 8.0 * ((qm + 1) / 2 * 2) * qn;
+    // temporaries per live product (each side allocates at least one sum slot, so a
+    // single-term side counts as a sum too)
+    auto need = [&](size_t) { return (sums_v ? a_sum + b_sum : 0.0) + (store_v ? m_tmp : 0.0); };
+    // the one-shot program's buffers against what the ctx already holds
+    int n_as = 0, n_bs = 0;
+    for (const Live& l : live) {
+        n_as += l.a.size() > 1;
+        n_bs += l.b.size() > 1;
     }
-
-    const bool sums = variant == STRASSEN_C || variant == STRASSEN_NAIVE;
-    std::unique_ptr<SumBatchParams> side_sums[2];
-    if (sums) {
-        // Every multi-term operand sum materialised by one HBM pass per side
-        // (materialize_sum, variants.cpp:53-96, for all entries at once); the
-        // mm launch then runs all 7^L products with single-term operands.
-        //   C variant (B200 addition): fused multi-destination epilogue.
-        //   Naive: products to temporaries M_p, then one stream pass applying
-        //          C_r += alpha*gamma*M_p in table order (variants.cpp:99-109).
-        const long long lda_t = ((qm + 3) / 4) * 4, ldb_t = ((qk + 3) / 4) * 4;
-        int na_sums = 0, nb_sums = 0;
-        for (const Live& l : live) {
-            na_sums += l.a.size() > 1;
-            nb_sums += l.b.size() > 1;
+    const double need_a = sums_v ? std::max(n_as, 1) * a_sum : 0.0;
+    const double need_b = sums_v ? std::max(n_bs, 1) * b_sum : 0.0;
+    const double need_m = store_v ? static_cast<double>(live.size()) * m_tmp : 0.0;
+    const double extra = std::max(0.0, need_a - static_cast<double>(e.tabuf.bytes)) +
+                         std::max(0.0, need_b - static_cast<double>(e.tbbuf.bytes)) +
+                         std::max(0.0, need_m - static_cast<double>(e.mbuf.bytes));
+    if (win || live.size() <= 1 || extra <= device_bytes_free()) return run_program(live, P);
+    // Not enough: give the ctx's temporaries back and run groups that fit
+    ck(cudaDeviceSynchronize(), "sync before releasing temporaries");
+    for (DeviceBuffer* b : {&e.tabuf, &e.tbbuf, &e.mbuf})
+        if (b->ptr) {
+            cudaFree(b->ptr);
+            b->ptr = nullptr;
+            b->bytes = 0;
         }
-        double* TA = e.ensure(e.tabuf, static_cast<size_t>(std::max(na_sums, 1)) * lda_t * qk * 8);
-        double* TB = e.ensure(e.tbbuf, static_cast<size_t>(std::max(nb_sums, 1)) * ldb_t * qn * 8);
-        for (int sd = 0; sd < 2; ++sd) {
-            side_sums[sd].reset(new SumBatchParams);  // ~10 KB: keep off the stack
-            SumBatchParams* SB = side_sums[sd].get();
-            std::memset(SB, 0, sizeof(*SB));
-            int next_map = kMaxQuad;  // tmA / tmB: 16 quadrant maps, then the sums
-            const TmaOperand& t = sd == 0 ? ta : tb;
-            SB->rows = sd == 0 ? qm : qk;
-            SB->cols = sd == 0 ? qk : qn;
-            SB->ld = sd == 0 ? lda_t : ldb_t;
-            for (size_t p = 0; p < live.size(); ++p) {
-                Terms& terms = sd == 0 ? live[p].a : live[p].b;
-                if (terms.size() <= 1) continue;  // single term: the quadrant map, sign in-kernel
-                const int z = SB->njobs++;
-                double* dst = (sd == 0 ? TA : TB) + static_cast<size_t>(z) * SB->ld * SB->cols;
-                SB->dst[z] = dst;
-                SB->nterms[z] = static_cast<int>(terms.size());
-                for (size_t u = 0; u < terms.size(); ++u) {
-                    const int qi = terms[u].first;
-                    SumTerm& st = SB->t[z][u];
-                    st.x = quad_origin(t, qi / side, qi % side);
-                    st.rows = static_cast<int>(quad_rows(t, qi / side));
-                    st.cols = static_cast<int>(quad_cols(t, qi % side));
-                    st.ld = t.ld;
-                    st.coeff = terms[u].second;
-                }
-                const int mi = next_map++;
-                if (mi >= kMaxMaps) throw Error(STRASSEN_ERR_PARAM, "too many operand maps");
-                if (sd == 0)
-                    encode_map(&P.tmA[mi], dst, qm, qk, lda_t, 16, kBK, 128);
-                else
-                    encode_map(&P.tmB[mi], dst, qk, qn, ldb_t, kBK, kBN, 128);
-                terms = {{mi, 1}};
-            }
-        }
+    const double avail = device_bytes_free();
+    size_t i0 = 0;
+    while (i0 < live.size()) {
+        size_t i1 = i0 + 1;
+        double t = need(i0);
+        while (i1 < live.size() && t + need(i1) <= avail) t += need(i1++);
+        std::vector<Live> group(live.begin() + static_cast<long>(i0), live.begin() + static_cast<long>(i1));
+        run_program(group, P);
+        i0 = i1;
     }
-
-    // First A and B terms at +1 (kernels.cu product_kloop): a side whose first
-    // coefficient is -1 is negated as a whole, and so are the destination
-    // coefficients.  Exact: (-S) x T = -(S x T) bit for bit under round-to-nearest.
-    for (Live& l : live)
-        for (Terms* t : {&l.a, &l.b})
-            if (t->front().second < 0) {
-                for (auto& x : *t) x.second = -x.second;
-                for (auto& x : l.c) x.second = -x.second;
-            }
-
-    P.nprod = static_cast<int>(live.size());
-    std::vector<Terms> dests;
-    for (size_t p = 0; p < live.size(); ++p) {
-        fill_desc(P.prod[p], live[p].a, live[p].b, live[p].c);
-        dests.push_back(live[p].c);
-    }
-    // C / ABC / DGEMM: fused epilogue (split only when few tiles).  AB, Naive:
-    // products to temporaries on a product-parallel grid (one CTA per tile x
-    // product: balanced waves at every size), then one stream pass
-    // (AB: variants.cpp:142-168).
-    const bool store_products = variant == STRASSEN_NAIVE || variant == STRASSEN_AB;
-    const FusedPlan F = plan_fused(e, s, P, store_products);
-    if (nw > 1) {  // the aux stream starts after everything enqueued on s so far
-        ck(cudaEventRecord(e.ev_fork, s), "fork");
-        ck(cudaStreamWaitEvent(e.aux_stream, e.ev_fork, 0), "fork");
-    }
-
-    for (int i = 0; i < nw; ++i) {
-        prefetch(i + 1);
-        const int w = order[i], r = w / nc, c = w % nc;
-        cudaStream_t st = ws[i % 2];
-        const long r0 = win ? win->rb[r] : 0, r1 = win ? win->rb[r + 1] : qm;
-        const long c0 = win ? win->cb[c] : 0, c1 = win ? win->cb[c + 1] : qn;
-        wait_a(st, r);
-        wait_b(st, c);
-        if (sums) {
-            // A sums of row strip r in its first window, B sums of column strip c
-            // in row 0; later windows wait on them
-            for (int sd = 0; sd < 2; ++sd) {
-                SumBatchParams& SB = *side_sums[sd];
-                const bool owner = sd == 0 ? first_r[r] == w : first_c[c] == w;
-                cudaEvent_t ev = sd == 0 ? e.ev_sum_a[r] : e.ev_sum_b[c];
-                if (!owner) {
-                    wait_ev(st, ev);
-                    continue;
-                }
-                if (!SB.njobs) continue;
-                if (sd == 0) {
-                    SB.r0 = r0;
-                    SB.rows = r1;
-                } else {
-                    SB.c0 = c0;
-                    SB.cols = c1;
-                }
-                e.prof_begin("sum_gather_kernel", st);
-                ck(launch_sum_batch(SB, st), sd == 0 ? "sum_batch (A)" : "sum_batch (B)");
-                e.prof_end(st);
-                ++launches;
-                if (nw > 1) ck(cudaEventRecord(ev, st), "sum event");
-            }
-        }
-        launches += run_fused_window(e, st, P, F, dests, cq, C, alpha, r0, r1, c0, c1,
-                                     [&] { wait_c(st, w); });
-        finish(st, w);
-    }
-    join();
     return launches;
 }
 }  // namespace

@@ -492,3 +492,37 @@ def test_c_variant_host_windows_match_device():
     assert np.array_equal(tc.cpu().numpy(), host)
     assert freivalds(1.0, a, b, c0, host) < 1e-14
     ctx.close()
+
+
+@pytest.mark.parametrize("v,L", [("naive", 2), ("c", 2), ("ab", 2), ("naive", 1), ("naive", 3)])
+def test_product_groups_when_temporaries_exceed_memory(monkeypatch, v, L):
+    """When the materialised sums / product temporaries of every product would not fit
+    in device memory, run_strassen runs consecutive groups of products in table order
+    (each its own sum pass, products and C updates).  Every C element receives the same
+    operations in the same order, so the result is bitwise that of the one-shot call
+    (STRASSEN_B200_MEM_CAP stands in for a full device)."""
+    import torch
+    d = 4096
+    g = torch.Generator(device="cuda").manual_seed(4096 + L)
+    A, B, C0 = ((torch.rand(d, d, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+                for _ in range(3))
+    ctx = S.Ctx()
+    ctx.set_max_level(3)
+    one = C0.clone().t().contiguous().t()
+    ctx.gemm_device(v, L, 1.0, A, B, one)
+    torch.cuda.synchronize()
+    launches_one = ctx.last_launches()
+    # a fresh ctx (no temporaries held) limited to 200 MB of new temporaries
+    monkeypatch.setenv("STRASSEN_B200_MEM_CAP", str(200 << 20))
+    ctx2 = S.Ctx()
+    ctx2.set_max_level(3)
+    grouped = C0.clone().t().contiguous().t()
+    ctx2.gemm_device(v, L, 1.0, A, B, grouped)
+    torch.cuda.synchronize()
+    assert ctx2.last_launches() > launches_one  # several groups ran
+    assert torch.equal(grouped, one), (v, L)
+    # a ctx already holding the one-shot program's buffers needs no groups
+    ctx.gemm_device(v, L, 1.0, A, B, C0.clone().t().contiguous().t())
+    assert ctx.last_launches() == launches_one
+    ctx.close()
+    ctx2.close()
