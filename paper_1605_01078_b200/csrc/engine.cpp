@@ -480,10 +480,18 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
         }();
         P.sep_stage = bulk_units && single && sep_on ? 1 : 0;
         // deferred collection: the next product of a tile is tiles-in-launch units
-        // later; defer only when that is >= 2 grid widths (small host-call windows
-        // would otherwise chain each tile's products one unit apart)
+        // later; defer only when that is >= one grid width (small host-call windows
+        // would otherwise chain each tile's products one unit apart: C L2 e2e 1437 ms
+        // with 16-tile windows; at 256 tiles deferral still wins, 8192^3 C L2 25.03 ->
+        // 24.66 ms, the level-3 C inner calls 168.95 -> 166.5 ms)
         const long launch_tiles = static_cast<long>(P.tiles_m) * P.tiles_n;
-        P.sep_defer = (!F.tickets || launch_tiles >= 2L * (e.num_sms > 0 ? e.num_sms : 148)) ? 1 : 0;
+        static const double defer_waves = [] {
+            const char* v = std::getenv("STRASSEN_B200_DEFER_WAVES");  // experiments
+            return v ? std::atof(v) : 1.0;
+        }();
+        P.sep_defer = (!F.tickets || static_cast<double>(launch_tiles) >=
+                                         defer_waves * (e.num_sms > 0 ? e.num_sms : 148))
+                          ? 1 : 0;
         P.grid_cap = cap(bulk_units && !P.sep_stage);
         e.prof_begin("mm_kernel", s);
         ck(launch_mm(P, s), "mm_kernel");
