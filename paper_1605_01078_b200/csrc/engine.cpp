@@ -1114,117 +1114,159 @@ long run_outer(Engine& e, cudaStream_t s, strassen_variant variant, int level, d
     }
     if (live.empty()) return launches;
 
-    // outer operands: a view of the quadrant, or a materialised sum (ld multiple of 4)
-    const long long lda_t = ((qm + 3) / 4) * 4, ldb_t = ((qk + 3) / 4) * 4;
-    const long long ldm = ((qm + 3) / 4) * 4;
-    std::vector<DView> opA(live.size()), opB(live.size());
-    for (int sd = 0; sd < 2; ++sd) {
-        const TmaOperand& t = sd == 0 ? ta : tb;
-        const long rows = sd == 0 ? qm : qk, cols = sd == 0 ? qk : qn;
-        const long long ld = sd == 0 ? lda_t : ldb_t;
-        std::unique_ptr<SumBatchParams> SB(new SumBatchParams);
-        std::memset(SB.get(), 0, sizeof(SumBatchParams));
-        SB->rows = rows;
-        SB->cols = cols;
-        SB->ld = ld;
-        std::vector<int> job_of(live.size(), -1);
-        for (size_t p = 0; p < live.size(); ++p) {
-            const Terms& terms = sd == 0 ? live[p].a : live[p].b;
-            DView& op = sd == 0 ? opA[p] : opB[p];
-            op.rows = rows;
-            op.cols = cols;
-            op.rs = 1;
-            const int q0 = terms[0].first;
-            if (terms.size() == 1 && terms[0].second == 1 && quad_rows(t, q0 / 2) == rows &&
-                quad_cols(t, q0 % 2) == cols) {
-                op.p = const_cast<double*>(quad_origin(t, q0 / 2, q0 % 2));
-                op.cs = t.ld;
-                op.ready = t.ready;
-                continue;
-            }
-            const int z = SB->njobs++;
-            job_of[p] = z;
-            SB->nterms[z] = static_cast<int>(terms.size());
-            for (size_t u = 0; u < terms.size(); ++u) {
-                const int qi = terms[u].first;
-                SumTerm& st = SB->t[z][u];
-                st.x = quad_origin(t, qi / 2, qi % 2);
-                st.rows = static_cast<int>(quad_rows(t, qi / 2));
-                st.cols = static_cast<int>(quad_cols(t, qi % 2));
-                st.ld = t.ld;
-                st.coeff = terms[u].second;
-            }
-        }
-        if (SB->njobs) {
-            double* T = e.ensure(sd == 0 ? e.l3_a : e.l3_b,
-                                 static_cast<size_t>(SB->njobs) * ld * cols * 8);
+    // The outer program over a list of live products: their operand sums, products
+    // and stream pass.  When the outer temporaries of all seven products would take
+    // more than half the free device memory (the inner level-2 calls need the rest),
+    // the products run in consecutive groups in table order -- the same operations
+    // on every C element in the same order, so the same result.
+    auto run_group = [&](const std::vector<Live>& live) {
+        // outer operands: a view of the quadrant, or a materialised sum (ld multiple of 4)
+        const long long lda_t = ((qm + 3) / 4) * 4, ldb_t = ((qk + 3) / 4) * 4;
+        const long long ldm = ((qm + 3) / 4) * 4;
+        std::vector<DView> opA(live.size()), opB(live.size());
+        for (int sd = 0; sd < 2; ++sd) {
+            const TmaOperand& t = sd == 0 ? ta : tb;
+            const long rows = sd == 0 ? qm : qk, cols = sd == 0 ? qk : qn;
+            const long long ld = sd == 0 ? lda_t : ldb_t;
+            std::unique_ptr<SumBatchParams> SB(new SumBatchParams);
+            std::memset(SB.get(), 0, sizeof(SumBatchParams));
+            SB->rows = rows;
+            SB->cols = cols;
+            SB->ld = ld;
+            std::vector<int> job_of(live.size(), -1);
             for (size_t p = 0; p < live.size(); ++p) {
-                if (job_of[p] < 0) continue;
-                double* dst = T + static_cast<size_t>(job_of[p]) * ld * cols;
-                SB->dst[job_of[p]] = dst;
+                const Terms& terms = sd == 0 ? live[p].a : live[p].b;
                 DView& op = sd == 0 ? opA[p] : opB[p];
-                op.p = dst;
-                op.cs = ld;
+                op.rows = rows;
+                op.cols = cols;
+                op.rs = 1;
+                const int q0 = terms[0].first;
+                if (terms.size() == 1 && terms[0].second == 1 && quad_rows(t, q0 / 2) == rows &&
+                    quad_cols(t, q0 % 2) == cols) {
+                    op.p = const_cast<double*>(quad_origin(t, q0 / 2, q0 % 2));
+                    op.cs = t.ld;
+                    op.ready = t.ready;
+                    continue;
+                }
+                const int z = SB->njobs++;
+                job_of[p] = z;
+                SB->nterms[z] = static_cast<int>(terms.size());
+                for (size_t u = 0; u < terms.size(); ++u) {
+                    const int qi = terms[u].first;
+                    SumTerm& st = SB->t[z][u];
+                    st.x = quad_origin(t, qi / 2, qi % 2);
+                    st.rows = static_cast<int>(quad_rows(t, qi / 2));
+                    st.cols = static_cast<int>(quad_cols(t, qi % 2));
+                    st.ld = t.ld;
+                    st.coeff = terms[u].second;
+                }
             }
-            if (t.ready) ck(cudaStreamWaitEvent(s, t.ready, 0), "wait operand");
-            e.prof_begin("sum_gather_kernel", s);
-            ck(launch_sum_batch(*SB, s), sd == 0 ? "outer sums (A)" : "outer sums (B)");
-            e.prof_end(s);
-            ++launches;
+            if (SB->njobs) {
+                double* T = e.ensure(sd == 0 ? e.l3_a : e.l3_b,
+                                     static_cast<size_t>(SB->njobs) * ld * cols * 8);
+                for (size_t p = 0; p < live.size(); ++p) {
+                    if (job_of[p] < 0) continue;
+                    double* dst = T + static_cast<size_t>(job_of[p]) * ld * cols;
+                    SB->dst[job_of[p]] = dst;
+                    DView& op = sd == 0 ? opA[p] : opB[p];
+                    op.p = dst;
+                    op.cs = ld;
+                }
+                if (t.ready) ck(cudaStreamWaitEvent(s, t.ready, 0), "wait operand");
+                e.prof_begin("sum_gather_kernel", s);
+                ck(launch_sum_batch(*SB, s), sd == 0 ? "outer sums (A)" : "outer sums (B)");
+                e.prof_end(s);
+                ++launches;
+            }
         }
-    }
 
-    // products M_r = S^A_r S^B_r by the level-2 program, alpha = 1, into zeroed
-    // temporaries (the inner stream pass / fused epilogue accumulates into M_r)
-    const size_t mstride = static_cast<size_t>(ldm) * qn;
-    double* M = e.ensure(e.l3_m, live.size() * mstride * 8);
-    ck(cudaMemsetAsync(M, 0, live.size() * mstride * 8, s), "zero products");
-    for (size_t p = 0; p < live.size(); ++p) {
-        DView Mp;
-        Mp.p = M + p * mstride;
-        Mp.rows = qm;
-        Mp.cols = qn;
-        Mp.rs = 1;
-        Mp.cs = ldm;
-        launches += run_device(e, s, variant, level - 1, 1.0, opA[p], opB[p], Mp, nullptr);
-    }
-
-    // C_q += alpha gamma M_r, each quadrant's updates in table order
-    std::unique_ptr<StreamParams> SP(new StreamParams);
-    std::memset(SP.get(), 0, sizeof(StreamParams));
-    for (int qi = 0; qi < 4; ++qi) {
-        SP->cptr[qi] = cq[qi].p;
-        SP->crows[qi] = static_cast<int>(cq[qi].rows);
-        SP->ccols[qi] = static_cast<int>(cq[qi].cols);
-    }
-    for (size_t p = 0; p < live.size(); ++p)
-        for (const auto& [q, coeff] : live[p].c) {
-            SP->src_prod[q][SP->nsrc[q]] = static_cast<int8_t>(p);
-            SP->src_coeff[q][SP->nsrc[q]] = static_cast<int8_t>(coeff);
-            ++SP->nsrc[q];
+        // products M_r = S^A_r S^B_r by the level-2 program, alpha = 1, into zeroed
+        // temporaries (the inner stream pass / fused epilogue accumulates into M_r)
+        const size_t mstride = static_cast<size_t>(ldm) * qn;
+        double* M = e.ensure(e.l3_m, live.size() * mstride * 8);
+        ck(cudaMemsetAsync(M, 0, live.size() * mstride * 8, s), "zero products");
+        for (size_t p = 0; p < live.size(); ++p) {
+            DView Mp;
+            Mp.p = M + p * mstride;
+            Mp.rows = qm;
+            Mp.cols = qn;
+            Mp.rs = 1;
+            Mp.cs = ldm;
+            launches += run_device(e, s, variant, level - 1, 1.0, opA[p], opB[p], Mp, nullptr);
         }
-    bool vec = C.rs == 1 && C.cs % 2 == 0 && (reinterpret_cast<uintptr_t>(C.p) % 16) == 0;
-    for (int qi = 0; qi < 4 && vec; ++qi) vec = (reinterpret_cast<uintptr_t>(cq[qi].p) % 16) == 0;
-    SP->c_vec = vec ? 1 : 0;
-    SP->rs_c = C.rs;
-    SP->cs_c = C.cs;
-    SP->mbase = M;
-    SP->mstride = static_cast<long long>(mstride);
-    SP->ldm = ldm;
-    SP->alpha = alpha;
-    SP->nquad = 4;
-    SP->qm = static_cast<int>(qm);
-    SP->qn = static_cast<int>(qn);
-    SP->ksplit = 1;
-    SP->r0 = 0;
-    SP->r1 = static_cast<int>(qm);
-    SP->c0 = 0;
-    SP->c1 = static_cast<int>(qn);
-    wait_ready(s, C);
-    e.prof_begin("stream_gather_kernel", s);
-    ck(launch_stream_update(*SP, s), "outer stream_update");
-    e.prof_end(s);
-    return launches + 1;
+
+        // C_q += alpha gamma M_r, each quadrant's updates in table order
+        std::unique_ptr<StreamParams> SP(new StreamParams);
+        std::memset(SP.get(), 0, sizeof(StreamParams));
+        for (int qi = 0; qi < 4; ++qi) {
+            SP->cptr[qi] = cq[qi].p;
+            SP->crows[qi] = static_cast<int>(cq[qi].rows);
+            SP->ccols[qi] = static_cast<int>(cq[qi].cols);
+        }
+        for (size_t p = 0; p < live.size(); ++p)
+            for (const auto& [q, coeff] : live[p].c) {
+                SP->src_prod[q][SP->nsrc[q]] = static_cast<int8_t>(p);
+                SP->src_coeff[q][SP->nsrc[q]] = static_cast<int8_t>(coeff);
+                ++SP->nsrc[q];
+            }
+        bool vec = C.rs == 1 && C.cs % 2 == 0 && (reinterpret_cast<uintptr_t>(C.p) % 16) == 0;
+        for (int qi = 0; qi < 4 && vec; ++qi) vec = (reinterpret_cast<uintptr_t>(cq[qi].p) % 16) == 0;
+        SP->c_vec = vec ? 1 : 0;
+        SP->rs_c = C.rs;
+        SP->cs_c = C.cs;
+        SP->mbase = M;
+        SP->mstride = static_cast<long long>(mstride);
+        SP->ldm = ldm;
+        SP->alpha = alpha;
+        SP->nquad = 4;
+        SP->qm = static_cast<int>(qm);
+        SP->qn = static_cast<int>(qn);
+        SP->ksplit = 1;
+        SP->r0 = 0;
+        SP->r1 = static_cast<int>(qm);
+        SP->c0 = 0;
+        SP->c1 = static_cast<int>(qn);
+        wait_ready(s, C);
+        e.prof_begin("stream_gather_kernel", s);
+        ck(launch_stream_update(*SP, s), "outer stream_update");
+        e.prof_end(s);
+        ++launches;
+    };
+    const double per_prod = 8.0 * (static_cast<double>(((qm + 3) / 4) * 4) * qk +
+                                   static_cast<double>(((qk + 3) / 4) * 4) * qn +
+                                   static_cast<double>(((qm + 3) / 4) * 4) * qn);
+    // one shot when the new allocations it needs (beyond the outer buffers the ctx
+    // already holds) take at most half the free memory
+    double ja = 0.0, jb = 0.0;  // materialised outer sums (multi-term sides)
+    for (const Live& l : live) {
+        ja += l.a.size() > 1;
+        jb += l.b.size() > 1;
+    }
+    const double np = static_cast<double>(live.size());
+    const double side_a = 8.0 * static_cast<double>(((qm + 3) / 4) * 4) * qk;
+    const double side_b = 8.0 * static_cast<double>(((qk + 3) / 4) * 4) * qn;
+    const double side_m = 8.0 * static_cast<double>(((qm + 3) / 4) * 4) * qn;
+    const double extra = std::max(0.0, ja * side_a - static_cast<double>(e.l3_a.bytes)) +
+                         std::max(0.0, jb * side_b - static_cast<double>(e.l3_b.bytes)) +
+                         std::max(0.0, np * side_m - static_cast<double>(e.l3_m.bytes));
+    if (extra <= 0.5 * device_bytes_free()) {
+        run_group(live);
+        return launches;
+    }
+    ck(cudaDeviceSynchronize(), "sync before releasing temporaries");
+    for (DeviceBuffer* b : {&e.l3_a, &e.l3_b, &e.l3_m})
+        if (b->ptr) {
+            cudaFree(b->ptr);
+            b->ptr = nullptr;
+            b->bytes = 0;
+        }
+    const size_t g = std::max<size_t>(1, static_cast<size_t>(0.5 * device_bytes_free() / per_prod));
+    for (size_t i0 = 0; i0 < live.size(); i0 += g) {
+        const size_t i1 = std::min(live.size(), i0 + g);
+        run_group(std::vector<Live>(live.begin() + static_cast<long>(i0),
+                                    live.begin() + static_cast<long>(i1)));
+    }
+    return launches;
 }
 }  // namespace
 

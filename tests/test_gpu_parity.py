@@ -494,7 +494,7 @@ def test_c_variant_host_windows_match_device():
     ctx.close()
 
 
-@pytest.mark.parametrize("v,L", [("naive", 2), ("c", 2), ("ab", 2), ("naive", 1), ("naive", 3)])
+@pytest.mark.parametrize("v,L", [("naive", 2), ("c", 2), ("ab", 2), ("naive", 1), ("naive", 3), ("c", 3)])
 def test_product_groups_when_temporaries_exceed_memory(monkeypatch, v, L):
     """When the materialised sums / product temporaries of every product would not fit
     in device memory, run_strassen runs consecutive groups of products in table order
