@@ -640,7 +640,7 @@ void plan_windows(const Engine& e, strassen_variant variant, int level, long m, 
         const double prods = (variant == STRASSEN_NAIVE || variant == STRASSEN_AB)
                                  ? per_tile * 8.0 * qm * qn : 0.0;
         const double held = static_cast<double>(e.tabuf.bytes + e.tbbuf.bytes + e.mbuf.bytes);
-        if (sums + prods > device_bytes_free() + held) return;
+        if (sums + prods > held && sums + prods > device_bytes_free() + held) return;
     }
     // windows of >= 2 waves each (consecutive windows overlap on two streams);
     // grow the grid keeping it square-ish
@@ -1049,7 +1049,10 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
     const double extra = std::max(0.0, need_a - static_cast<double>(e.tabuf.bytes)) +
                          std::max(0.0, need_b - static_cast<double>(e.tbbuf.bytes)) +
                          std::max(0.0, need_m - static_cast<double>(e.mbuf.bytes));
-    if (win || live.size() <= 1 || extra <= device_bytes_free()) return run_program(live, P);
+    // (cudaMemGetInfo only when the buffers must grow: on the hot path it stalled
+    // calls by up to ~80 ms now and then -- profiles/r01_notes.md)
+    if (win || live.size() <= 1 || extra <= 0.0 || extra <= device_bytes_free())
+        return run_program(live, P);
     // Not enough: give the ctx's temporaries back and run groups that fit
     ck(cudaDeviceSynchronize(), "sync before releasing temporaries");
     for (DeviceBuffer* b : {&e.tabuf, &e.tbbuf, &e.mbuf})
@@ -1249,7 +1252,7 @@ long run_outer(Engine& e, cudaStream_t s, strassen_variant variant, int level, d
     const double extra = std::max(0.0, ja * side_a - static_cast<double>(e.l3_a.bytes)) +
                          std::max(0.0, jb * side_b - static_cast<double>(e.l3_b.bytes)) +
                          std::max(0.0, np * side_m - static_cast<double>(e.l3_m.bytes));
-    if (extra <= 0.5 * device_bytes_free()) {
+    if (extra <= 0.0 || extra <= 0.5 * device_bytes_free()) {
         run_group(live);
         return launches;
     }
