@@ -513,11 +513,22 @@ def run_summa(args, rank, world, local, colmajor, barrier, max_over_ranks):
     if not args.no_e2e:
         # end to end: pinned host blocks in, C block out, around one SUMMA step
         Ah, Bh, Ch = (x.t().cpu().pin_memory().t() for x in (A_l, B_l, C_l))
+        copy_stream = torch.cuda.Stream()
         barrier()
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
-        A_l.copy_(Ah, non_blocking=True)
-        B_l.copy_(Bh, non_blocking=True)
-        C_l.copy_(Ch, non_blocking=True)
+        # A and B blocks first; C's copy overlaps the first local update's operand sums
+        # and products (its kernels wait on ev_c right before they read C)
+        with torch.cuda.stream(copy_stream):
+            A_l.copy_(Ah, non_blocking=True)
+            B_l.copy_(Bh, non_blocking=True)
+            ev_ab = torch.cuda.Event()
+            ev_ab.record(copy_stream)
+            C_l.copy_(Ch, non_blocking=True)
+            ev_c = torch.cuda.Event()
+            ev_c.record(copy_stream)
+        torch.cuda.current_stream().wait_event(ev_ab)
+        local_gemm.c_ready = ev_c
         step()
         Ch.copy_(C_l)
         torch.cuda.synchronize()

@@ -184,6 +184,14 @@ strassen_status strassen_dgemm(strassen_ctx* ctx, strassen_variant variant, int 
  * default (and NULL) = the CUDA legacy default stream. */
 strassen_status strassen_ctx_set_stream(strassen_ctx* ctx, void* stream);
 
+/* Events (cudaEvent_t passed as void*, NULL = none) that the NEXT compute call on
+ * this ctx waits on right before its first kernel reading device operand A, B or C:
+ * an operand still being produced (a copy or a collective on another stream) then
+ * overlaps the work that does not need it -- e.g. C arriving while the operand
+ * sums and products run.  Applies to that one call, then cleared. */
+strassen_status strassen_ctx_set_operand_events(strassen_ctx* ctx, void* a_ready, void* b_ready,
+                                               void* c_ready);
+
 /* Number of CUDA kernels the last compute call on this ctx launched. */
 strassen_status strassen_ctx_last_launches(const strassen_ctx* ctx, long* out);
 

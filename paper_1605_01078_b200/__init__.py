@@ -122,6 +122,7 @@ def _declare(lib):
         "strassen_ctx_set_peeling": (_ST, [vp, C.c_int]),
         "strassen_ctx_set_pipelining": (_ST, [vp, C.c_int]),
         "strassen_ctx_set_max_level": (_ST, [vp, C.c_int]),
+        "strassen_ctx_set_operand_events": (_ST, [vp, vp, vp, vp]),
         "strassen_ctx_last_profile": (_ST, [vp, C.c_char_p, _L]),
         "strassen_select": (_ST, [_L, _L, _L, C.POINTER(C.c_int), C.POINTER(C.c_int), _dp]),
         "strassen_ctx_select": (_ST, [vp, _L, _L, _L, C.POINTER(C.c_int), C.POINTER(C.c_int),
@@ -246,6 +247,12 @@ class Ctx:
     def set_pipelining(self, on=True):
         """Host calls: column-window pipelining of transfers and kernels (default on)."""
         _check(self._l.strassen_ctx_set_pipelining(self.ptr, int(bool(on))), "set_pipelining")
+
+    def set_operand_events(self, a=None, b=None, c=None):
+        """torch.cuda.Event (or None) per operand: the next call's kernels wait on it
+        right before first reading that device operand."""
+        h = [C.c_void_p(e.cuda_event if e is not None else None) for e in (a, b, c)]
+        _check(self._l.strassen_ctx_set_operand_events(self.ptr, *h), "set_operand_events")
 
     def set_max_level(self, level):
         """2 (default) or 3: level 3 for the naive / c variants (B200 extension)."""

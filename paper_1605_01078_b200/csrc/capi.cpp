@@ -123,6 +123,10 @@ strassen_status gemm_impl(strassen_ctx* ctx, bool explicit_stream, cudaStream_t 
                           long rs_b, long cs_b, double* c, long rs_c, long cs_c, bool has_beta,
                           double beta) {
     if (!ctx || !a || !b || !c) return STRASSEN_ERR_NULL;
+    // operand events apply to this call only, whatever its outcome
+    const cudaEvent_t ready[3] = {ctx->engine.next_ready[0], ctx->engine.next_ready[1],
+                                  ctx->engine.next_ready[2]};
+    ctx->engine.next_ready[0] = ctx->engine.next_ready[1] = ctx->engine.next_ready[2] = nullptr;
     if (strassen_status st = check_variant_level(variant, level)) {
         // level 3 (B200 extension) only after strassen_ctx_set_max_level(ctx, 3),
         // and only for the materialising variants (Naive, C)
@@ -151,9 +155,14 @@ strassen_status gemm_impl(strassen_ctx* ctx, bool explicit_stream, cudaStream_t 
             sb200::plan_windows(e, variant, level, m, n, k, a_strips, W);
         const bool windowed = W.count() > 0;
         const bool a_windowed = windowed && W.rows > 1;
-        const sb200::DView A = stage_in(e, s, a, m, k, rs_a, cs_a, e.stage_a, !a_windowed, sa, e.ev_ready[0]);
-        const sb200::DView B = stage_in(e, s, b, k, n, rs_b, cs_b, e.stage_b, !windowed, sb, e.ev_ready[1]);
-        const sb200::DView C = stage_in(e, s, c, m, n, rs_c, cs_c, e.stage_c, !windowed, sc, e.ev_ready[2]);
+        sb200::DView A = stage_in(e, s, a, m, k, rs_a, cs_a, e.stage_a, !a_windowed, sa, e.ev_ready[0]);
+        sb200::DView B = stage_in(e, s, b, k, n, rs_b, cs_b, e.stage_b, !windowed, sb, e.ev_ready[1]);
+        sb200::DView C = stage_in(e, s, c, m, n, rs_c, cs_c, e.stage_c, !windowed, sc, e.ev_ready[2]);
+        // device operands still being produced elsewhere (strassen_ctx_set_operand_events):
+        // kernels wait on their event right before first reading them
+        if (!sa && ready[0]) A.ready = ready[0];
+        if (!sb && ready[1]) B.ready = ready[1];
+        if (!sc && ready[2]) C.ready = ready[2];
         if (device_only && (sa || sb || sc))
             throw std::invalid_argument("strassen_gemm_device: operands must be device memory");
         for (auto& t : e.timed) {
@@ -335,6 +344,15 @@ strassen_status strassen_dgemm(strassen_ctx* ctx, strassen_variant variant, int 
     const long rs_b = tb ? ldb : 1, cs_b = tb ? 1 : ldb;
     return gemm_impl(ctx, false, nullptr, false, variant, level, m, n, k, alpha, a, rs_a, cs_a, b,
                      rs_b, cs_b, c, 1, ldc, true, beta);
+}
+
+strassen_status strassen_ctx_set_operand_events(strassen_ctx* ctx, void* a_ready, void* b_ready,
+                                               void* c_ready) {
+    if (!ctx) return STRASSEN_ERR_NULL;
+    ctx->engine.next_ready[0] = static_cast<cudaEvent_t>(a_ready);
+    ctx->engine.next_ready[1] = static_cast<cudaEvent_t>(b_ready);
+    ctx->engine.next_ready[2] = static_cast<cudaEvent_t>(c_ready);
+    return STRASSEN_OK;
 }
 
 strassen_status strassen_ctx_set_stream(strassen_ctx* ctx, void* stream) {

@@ -45,6 +45,9 @@ struct Engine {
     // layout normalisation, materialised operands and products (run_outer)
     DeviceBuffer pack_a3, pack_b3, l3_a, l3_b, l3_m;
     int max_level = 2;  // strassen_ctx_set_max_level: 3 admits Naive / C at level 3
+    // strassen_ctx_set_operand_events: events the next call's kernels wait on right
+    // before first reading A / B / C (device operands), then cleared
+    cudaEvent_t next_ready[3] = {nullptr, nullptr, nullptr};
     long last_launches = 0;
     bool peeling = true;  // dynamic peeling of odd fringes (strassen_ctx_set_peeling)
     // optional per-launch timing of the last call (strassen_ctx_enable_profiling)

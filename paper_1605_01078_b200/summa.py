@@ -177,12 +177,16 @@ def _default_local_gemm(variant, level):
         ctx.set_max_level(3)
 
     def run(alpha, a, b, c):
+        if run.c_ready is not None:  # C still arriving: kernels wait right before reading it
+            ctx.set_operand_events(c=run.c_ready)
+            run.c_ready = None
         if c.is_cuda:
             ctx.gemm_device(variant, level, alpha, a, b, c)
         else:
             ctx.gemm(variant, level, alpha, a, b, c)
         return ctx.last_launches()
     run.ctx = ctx  # for profiling one local update (bench.py roofline at N > 1)
+    run.c_ready = None  # torch.cuda.Event the next local update's C reads wait on
     return run
 
 

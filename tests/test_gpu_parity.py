@@ -526,3 +526,31 @@ def test_product_groups_when_temporaries_exceed_memory(monkeypatch, v, L):
     assert ctx.last_launches() == launches_one
     ctx.close()
     ctx2.close()
+
+
+@pytest.mark.parametrize("v,L", [("naive", 2), ("c", 2), ("abc", 1), ("dgemm", 0)])
+def test_operand_events_order_late_c(v, L):
+    """strassen_ctx_set_operand_events: C arrives on another stream behind a ~30 ms
+    delay; the call's kernels must wait for it right before first reading C (the result
+    would use stale C otherwise), while the work that does not read C goes ahead."""
+    import torch
+    d = 3072
+    g = torch.Generator(device="cuda").manual_seed(77)
+    A, B, C0 = ((torch.rand(d, d, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+                for _ in range(3))
+    ref = C0 + A @ B
+    ctx = S.Ctx()
+    side = torch.cuda.Stream()
+    C = torch.zeros((d, d), dtype=torch.float64, device="cuda").t()  # stale contents
+    torch.cuda.synchronize()
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(60_000_000)  # ~30 ms at 1.9 GHz before C lands
+        C.copy_(C0)
+        ev = torch.cuda.Event()
+        ev.record(side)
+    ctx.set_operand_events(c=ev)
+    ctx.gemm_device(v, L, 1.0, A, B, C)
+    torch.cuda.synchronize()
+    nw = (torch.linalg.norm(C - ref) / (torch.linalg.norm(A) * torch.linalg.norm(B))).item()
+    assert nw <= 5e-12, (v, L, nw)
+    ctx.close()
