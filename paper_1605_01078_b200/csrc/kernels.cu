@@ -1,23 +1,26 @@
 // sm_100a kernels of the B200 Strassen DGEMM.
 //
 // mm_kernel is the fused ABC Strassen tile kernel (it also runs the classical
-// DGEMM as a one-product program and the AB/Naive product stage).  It replaces
-// the reference's whole L1+L0 engine:
+// DGEMM as a one-product program and the AB / Naive / C product stages).  It
+// replaces the reference's whole L1+L0 engine:
 //   pack_a_sum / pack_b_sum      (blocking.cpp:12-66)  -> TMA operand-term loads
-//                                   into a shared-memory ring + an in-place,
-//                                   once-per-CTA operand-sum stage
+//                                   into a shared-memory ring; each DMMA warp sums
+//                                   the terms of exactly the fragments it
+//                                   multiplies, in registers
 //   microkernel / accumulate     (kernel.cpp:8-47)     -> DMMA (mma.sync m8n8k4 f64)
 //                                   mainloop over 64x32 warp tiles
-//   multi-destination update     (kernel.cpp:49-76)    -> register epilogue that
-//                                   adds alpha*gamma*M into each C quadrant tile
-//   five-loop driver + OpenMP ic (blocking.cpp:82-131) -> the CTA grid; each CTA
-//                                   owns one tile position in every C quadrant and
-//                                   walks all 7^L products in table order, so the
-//                                   multi-destination updates are race-free and
-//                                   bitwise deterministic run to run.
-// Why DMMA, and why sums are formed once per CTA: DESIGN.md section 3
-// (profiles/r01_fp64_peak.log: DMMA 37.1 TF/s vs DFMA 34.2; DADD shares the
-// FP64 pipe with DMMA).
+//   multi-destination update     (kernel.cpp:49-76)    -> epilogue adding
+//                                   alpha*gamma*M into each C quadrant tile: TMA
+//                                   tensor reduce-adds from a staged tile, or a
+//                                   register read-modify-write
+//   five-loop driver + OpenMP ic (blocking.cpp:82-131) -> the CTA grid: one CTA per
+//                                   (tile, product[, k-chunk]) or persistent CTAs
+//                                   walking those units; per-tile tickets apply
+//                                   every C tile's updates in table order, so the
+//                                   results are bitwise deterministic run to run.
+// Why DMMA, and why the sums sit in the DMMA warps' own instruction stream:
+// DESIGN.md section 3 (profiles/r01_fp64_peak.log: DMMA 37.1 TF/s vs DFMA 34.2;
+// DADDs issued by other warps starve while DMMA saturates the FP64 pipe).
 #include <cstdlib>
 #include <cstring>
 
