@@ -551,7 +551,8 @@ strassen_status strassen_select(long m, long n, long k, strassen_variant* varian
 strassen_status strassen_count_call(strassen_variant variant, int level, long m, long n, long k,
                                     const strassen_blocking* bp, strassen_counter_values* out) {
     if (!bp || !out) return STRASSEN_ERR_NULL;
-    if (strassen_status st = check_variant_level(variant, level)) return st;
+    if (strassen_status st = check_variant_level(variant, level))  // level 3: Naive / C
+        if (!(level == 3 && (variant == STRASSEN_NAIVE || variant == STRASSEN_C))) return st;
     return guarded([&] {
         validate_call(variant, m, n, k, *bp);
         strassen_counter_values d{};

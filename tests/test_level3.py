@@ -44,6 +44,20 @@ def test_level3_gate_without_device():
     assert ctx.gemm_raw(S.NAIVE, 3, 8, 8, 8, 1.0, pa, 8, 1, pa, 8, 1, pa, 8, 1) == S.ERR_PARAM
 
 
+def test_level3_predicted_counters_and_model():
+    """Analytic counters of a level-3 call (the composed 343-product table) and the B200
+    model's level-3 prediction, without a device."""
+    c = S.predicted_counters("naive", 3, 64, 64, 64)
+    assert c["kernel_fma_flops"] == 343 * 2 * 8 ** 3
+    l2 = S.predicted_counters("naive", 2, 64, 64, 64)
+    assert c["kernel_fma_flops"] < l2["kernel_fma_flops"]  # 343 * 8^3 < 49 * 16^3
+    with pytest.raises(S.StrassenError):
+        S.predicted_counters("abc", 3, 64, 64, 64)
+    t3 = S.predict_b200("c", 3, 16384, 16384, 16384)
+    t2 = S.predict_b200("c", 2, 16384, 16384, 16384)
+    assert 0 < t3 < t2
+
+
 @pytest.fixture(scope="module")
 def ctx3(cuda):
     c = S.Ctx()
