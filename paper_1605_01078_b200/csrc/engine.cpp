@@ -831,6 +831,13 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
     // read-modify-write everywhere measured (16384^3: C L2 196.5 -> 190.6 ms,
     // DGEMM 246.9 -> 242.5, ABC L2 239.7 -> 235.9; profiles/r01_bulk_kt_probe.log)
     P.bulk_max_kt = 1 << 30;
+    {
+        static const bool lay1 = [] {
+            const char* v = std::getenv("STRASSEN_B200_LAYOUT1");  // 0 / 1 (experiments)
+            return v ? std::atoi(v) != 0 : true;
+        }();
+        P.a_heavy_layout = lay1 ? 1 : 0;
+    }
     if (const char* b = std::getenv("STRASSEN_B200_BULK_MAX_KT")) P.bulk_max_kt = std::atoi(b);
 
     // Live products in table order (variants.cpp:130-133 skip rule).

@@ -213,6 +213,61 @@ __device__ __forceinline__ void dmma_substep(const Frags& f, int ss, double (&ac
             dmma(acc[mf][nf][0], acc[mf][nf][1], f.a[ss][mf], f.b[ss][nf]);
 }
 
+// ---- A-heavy layout: 4 (m) x 2 (n) warps of 32 x 64 -----------------------
+// For products with more A terms than B terms each A element is summed by two
+// warps instead of four (the 2 x 4 layout's A-heavy products cost 6.5-8% more than
+// their B-heavy mirrors, profiles/r01_abc2_combo_costs.log).  Accumulator (mf, nf)
+// of this layout (mf < 4, nf < 8) lives in acc[(8 mf + nf) / 4][(8 mf + nf) % 4],
+// and relayout_to_2x4 moves the tile back to the 2 x 4 layout the epilogues expect.
+struct Frags1 {
+    double a[2][4];  // [substep in pair][m fragment]
+    double b[2][8];  // [substep in pair][n fragment]
+};
+template <bool FIRST>
+__device__ __forceinline__ void frag_a_term1(const uint8_t* sA, int sp, int wm1, int g, int j,
+                                             double c, Frags1& f) {
+#pragma unroll
+    for (int ss = 0; ss < 2; ++ss) {
+        const int k = 2 * j + ss + 8 * sp;
+        const uint8_t* pa = sA + (wm1 * 2) * 2048 + k * 128 + ((g ^ (k & 7)) << 4);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const double2 v = *reinterpret_cast<const double2*>(pa + h * 2048);
+            if (FIRST) {
+                f.a[ss][2 * h] = v.x;
+                f.a[ss][2 * h + 1] = v.y;
+            } else {
+                f.a[ss][2 * h] = fma(c, v.x, f.a[ss][2 * h]);
+                f.a[ss][2 * h + 1] = fma(c, v.y, f.a[ss][2 * h + 1]);
+            }
+        }
+    }
+}
+template <bool FIRST>
+__device__ __forceinline__ void frag_b_term1(const uint8_t* sB, int sp, int wn1, int g, int j,
+                                             double c, Frags1& f) {
+    const uint8_t* pb = sB + (wn1 * 64 + nperm(g)) * 128 + (((j + 4 * sp) ^ nperm(g)) << 4);
+#pragma unroll
+    for (int nf = 0; nf < 8; ++nf) {
+        const double2 v = *reinterpret_cast<const double2*>(pb + nf * 8 * 128);
+        if (FIRST) {
+            f.b[0][nf] = v.x;
+            f.b[1][nf] = v.y;
+        } else {
+            f.b[0][nf] = fma(c, v.x, f.b[0][nf]);
+            f.b[1][nf] = fma(c, v.y, f.b[1][nf]);
+        }
+    }
+}
+__device__ __forceinline__ void dmma_substep1(const Frags1& f, int ss, double (&acc)[8][4][2]) {
+#pragma unroll
+    for (int mf = 0; mf < 4; ++mf)
+#pragma unroll
+        for (int nf = 0; nf < 8; ++nf)
+            dmma(acc[(8 * mf + nf) >> 2][(8 * mf + nf) & 3][0],
+                 acc[(8 * mf + nf) >> 2][(8 * mf + nf) & 3][1], f.a[ss][mf], f.b[ss][nf]);
+}
+
 // ---- half-k tiles (ProductDesc::half: products with 4 + 4 terms) ----------
 // A (4,4) product needs 8 term tiles per 16-k step; with 16-k tiles the ring
 // could prefetch only a fraction of the next step, exposing TMA latency.  Such
@@ -399,6 +454,99 @@ __device__ __forceinline__ void product_kloop(const uint8_t* raw, uint64_t* raw_
             }
         }
     }
+}
+
+// product_kloop in the 4 x 2 warp layout (A-heavy products, one CTA per unit).
+template <int NA, int NB, int RING>
+__device__ __forceinline__ void product_kloop1(const uint8_t* raw, uint64_t* raw_full,
+                                               uint64_t* raw_empty, uint32_t& slot,
+                                               uint32_t& phase, int kt_lo, int kt_hi,
+                                               const ProductDesc& pd, int wm1, int wn1, int g,
+                                               int j, int lane, double (&acc)[8][4][2]) {
+    double ca[NA], cb[NB];
+#pragma unroll
+    for (int u = 0; u < NA; ++u) ca[u] = static_cast<double>(pd.as[u]);
+#pragma unroll
+    for (int u = 0; u < NB; ++u) cb[u] = static_cast<double>(pd.bs[u]);
+    for (int kt = kt_lo; kt < kt_hi; ++kt) {
+        const uint8_t* sA[NA];
+        const uint8_t* sB[NB];
+        const uint32_t slot0 = slot;
+#pragma unroll
+        for (int u = 0; u < NA + NB; ++u) {
+            uint32_t su = slot0 + u;
+            const uint32_t pu = (su >= RING) ? phase ^ 1 : phase;
+            su = (su >= RING) ? su - RING : su;
+            if (u < NA) sA[u] = raw + su * kSlotBytes;
+            else sB[u - NA] = raw + su * kSlotBytes;
+            mbar_wait(&raw_full[su], pu);
+        }
+        slot += NA + NB;
+        if (slot >= RING) {
+            slot -= RING;
+            phase ^= 1;
+        }
+#pragma unroll
+        for (int sp = 0; sp < 2; ++sp) {
+            Frags1 f;
+            frag_a_term1<true>(sA[0], sp, wm1, g, j, 1.0, f);
+            frag_b_term1<true>(sB[0], sp, wn1, g, j, 1.0, f);
+#pragma unroll
+            for (int u = 1; u < NA; ++u) frag_a_term1<false>(sA[u], sp, wm1, g, j, ca[u], f);
+#pragma unroll
+            for (int u = 1; u < NB; ++u) frag_b_term1<false>(sB[u], sp, wn1, g, j, cb[u], f);
+            dmma_substep1(f, 0, acc);
+            dmma_substep1(f, 1, acc);
+        }
+        consumer_fence();
+        __syncwarp();
+        if (lane == 0) {
+            uint32_t s2 = slot0;
+#pragma unroll
+            for (int u = 0; u < NA + NB; ++u) {
+                mbar_arrive(&raw_empty[s2]);
+                if (++s2 == RING) s2 = 0;
+            }
+        }
+    }
+}
+
+// The C tile from the 4 x 2 warp layout to the 2 x 4 one, through the (idle) ring:
+// a 128 x 129-double row-major scratch (the pad spreads the banks).
+__device__ __forceinline__ void relayout_to_2x4(uint8_t* raw, double (&acc)[8][4][2], int warp,
+                                                int g, int j) {
+    double* T = reinterpret_cast<double*>(raw);
+    constexpr int LD = kBN + 1;
+    const int c0 = nperm(2 * j), c1 = nperm(2 * j + 1);
+    consumer_bar();  // every warp is done reading the ring
+    {
+        const int wm1 = warp & 3, wn1 = warp >> 2;
+#pragma unroll
+        for (int mf = 0; mf < 4; ++mf)
+#pragma unroll
+            for (int nf = 0; nf < 8; ++nf)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int row = wm1 * 32 + 16 * (mf >> 1) + 2 * g + (mf & 1);
+                    const int col = wn1 * 64 + 8 * nf + (e ? c1 : c0);
+                    T[row * LD + col] = acc[(8 * mf + nf) >> 2][(8 * mf + nf) & 3][e];
+                }
+    }
+    consumer_bar();
+    {
+        const int wm = warp & 1, wn = warp >> 1;
+#pragma unroll
+        for (int mf = 0; mf < 8; ++mf)
+#pragma unroll
+            for (int nf = 0; nf < 4; ++nf)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int row = wm * 64 + 16 * (mf >> 1) + 2 * g + (mf & 1);
+                    const int col = wn * 32 + 8 * nf + (e ? c1 : c0);
+                    acc[mf][nf][e] = T[row * LD + col];
+                }
+    }
+    consumer_bar();  // the ring is free for the epilogue's stage again
 }
 
 // One work unit of an mm launch: a C tile and the products / k-range it runs.
@@ -640,6 +788,11 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         } else if (MAXT >= 2 && combo == 10) {
             product_kloop<1, (MAXT >= 2 ? 2 : 1), RING>(raw, raw_full, raw_empty, slot, phase, kt_lo,
                                                   kt_hi, pd, wm, wn, g, j, lane, acc);
+        } else if (!PERSIST && MAXT >= 2 && combo == 17 && P.a_heavy_layout) {
+            product_kloop1<(MAXT >= 2 ? 2 : 1), 1, RING>(raw, raw_full, raw_empty, slot, phase,
+                                                   kt_lo, kt_hi, pd, warp & 3, warp >> 2, g, j,
+                                                   lane, acc);
+            relayout_to_2x4(raw, acc, warp, g, j);
         } else if (MAXT >= 2 && combo == 17) {
             product_kloop<(MAXT >= 2 ? 2 : 1), 1, RING>(raw, raw_full, raw_empty, slot, phase, kt_lo,
                                                   kt_hi, pd, wm, wn, g, j, lane, acc);
@@ -649,12 +802,22 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         } else if (MAXT >= 4 && combo == 12) {
             product_kloop<1, (MAXT >= 4 ? 4 : 1), RING>(raw, raw_full, raw_empty, slot, phase, kt_lo,
                                                   kt_hi, pd, wm, wn, g, j, lane, acc);
+        } else if (!PERSIST && MAXT >= 4 && combo == 33 && P.a_heavy_layout) {
+            product_kloop1<(MAXT >= 4 ? 4 : 1), 1, RING>(raw, raw_full, raw_empty, slot, phase,
+                                                   kt_lo, kt_hi, pd, warp & 3, warp >> 2, g, j,
+                                                   lane, acc);
+            relayout_to_2x4(raw, acc, warp, g, j);
         } else if (MAXT >= 4 && combo == 33) {
             product_kloop<(MAXT >= 4 ? 4 : 1), 1, RING>(raw, raw_full, raw_empty, slot, phase, kt_lo,
                                                   kt_hi, pd, wm, wn, g, j, lane, acc);
         } else if (MAXT >= 4 && combo == 20) {
             product_kloop<(MAXT >= 4 ? 2 : 1), (MAXT >= 4 ? 4 : 1), RING>(
                 raw, raw_full, raw_empty, slot, phase, kt_lo, kt_hi, pd, wm, wn, g, j, lane, acc);
+        } else if (!PERSIST && MAXT >= 4 && combo == 34 && P.a_heavy_layout) {
+            product_kloop1<(MAXT >= 4 ? 4 : 1), (MAXT >= 4 ? 2 : 1), RING>(
+                raw, raw_full, raw_empty, slot, phase, kt_lo, kt_hi, pd, warp & 3, warp >> 2, g, j,
+                lane, acc);
+            relayout_to_2x4(raw, acc, warp, g, j);
         } else if (MAXT >= 4 && combo == 34) {
             product_kloop<(MAXT >= 4 ? 4 : 1), (MAXT >= 4 ? 2 : 1), RING>(
                 raw, raw_full, raw_empty, slot, phase, kt_lo, kt_hi, pd, wm, wn, g, j, lane, acc);

@@ -119,6 +119,9 @@ struct alignas(64) MMParams {
     // k-step) space, at most sk_maxp pieces; partial pieces go through the k-split
     // fixup (ksplit = partial slots per tile, arrive counters per tile)
     int streamk, sk_len, sk_maxp;
+    // A-heavy products (more A than B terms) in one-CTA-per-unit launches run the
+    // 4 x 2 warp layout (kernels.cu product_kloop1)
+    int a_heavy_layout;
 };
 
 cudaError_t launch_mm(const MMParams& p, cudaStream_t s);
