@@ -64,6 +64,9 @@ def parse():
     # run the N > 1 SUMMA code path even at N = 1 (a 1 x 1 grid, no collectives):
     # a one-GPU check of the multi-GPU bench mechanics
     p.add_argument("--summa", action="store_true")
+    p.add_argument("--p2p", action="store_true",
+                   help="N > 1: peer-memory SUMMA (operands read from the owners' blocks "
+                        "over CUDA IPC, no NCCL broadcasts; summa.summa_p2p)")
     a = p.parse_args()
     if a.variant == "dgemm":
         a.level = 0
@@ -459,8 +462,15 @@ def run_summa(args, rank, world, local, colmajor, barrier, max_over_ranks):
     comm = SU.TorchComm(L)
     A_l, B_l, C_l = colmajor(L.m_l, L.k_c), colmajor(L.k_r, L.n_l), colmajor(L.m_l, L.n_l)
     local_gemm = SU._default_local_gemm(args.variant, args.level)
-    step = lambda: SU.summa(L, comm, A_l, B_l, C_l, 1.0, args.variant, args.level,  # noqa: E731
-                            local_gemm=local_gemm)
+    if args.p2p:
+        torch.cuda.synchronize()
+        Ap, Bp = SU.open_peer_blocks(A_l, B_l)
+        barrier()
+        step = lambda: SU.summa_p2p(L, rank, Ap, Bp, C_l, 1.0, args.variant,  # noqa: E731
+                                    args.level, local_gemm=local_gemm)
+    else:
+        step = lambda: SU.summa(L, comm, A_l, B_l, C_l, 1.0, args.variant,  # noqa: E731
+                                args.level, local_gemm=local_gemm)
     for _ in range(args.warmup):
         step()
     barrier()
@@ -505,6 +515,8 @@ def run_summa(args, rank, world, local, colmajor, barrier, max_over_ranks):
                                f"(16384^2 C block per rank)", "variant": args.variant,
                    "level": args.level, "m": L.m, "n": L.n, "k": L.k, "panel_b": L.b,
                    "grid": [L.pr, L.pc], "parallelism": f"summa{L.pr}x{L.pc}",
+                   "exchange": "peer memory (CUDA IPC), no broadcasts" if args.p2p
+                   else "NCCL row/column panel broadcasts",
                    "l2": "inputs larger than the 126 MB L2"},
         "roofline": roofline,
         "clocks": clk.summary(),
@@ -529,6 +541,9 @@ def run_summa(args, rank, world, local, colmajor, barrier, max_over_ranks):
             ev_c.record(copy_stream)
         torch.cuda.current_stream().wait_event(ev_ab)
         local_gemm.c_ready = ev_c
+        if args.p2p:  # peers read this rank's A and B: every copy lands before any step
+            torch.cuda.synchronize()
+            barrier()
         step()
         Ch.copy_(C_l)
         torch.cuda.synchronize()
@@ -536,7 +551,8 @@ def run_summa(args, rank, world, local, colmajor, barrier, max_over_ranks):
         line["e2e"] = {"value": flops / dt / 1e12, "unit": "TFLOP/s",
                        "h2d_bytes_per_step": world * 8 * (L.m_l * L.k_c + L.k_r * L.n_l + L.m_l * L.n_l),
                        "d2h_bytes_per_step": world * 8 * L.m_l * L.n_l, "ms_per_step": dt * 1e3,
-                       "api": "summa() over strassen_gemm_device, pinned host blocks"}
+                       "api": ("summa_p2p()" if args.p2p else "summa()")
+                       + " over strassen_gemm_device, pinned host blocks"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     import torch.distributed as dist

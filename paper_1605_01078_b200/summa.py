@@ -27,6 +27,12 @@ Communicators:
 * :class:`TorchComm` uses torch.distributed with one process per GPU. Row and column
   groups come from ``new_group``. NCCL runs over NVLink/NVSwitch; gloo runs on CPU for the
   tests.
+* :func:`summa_p2p` is the same product with no broadcasts: every rank maps the other
+  ranks' A and B blocks (:func:`open_peer_blocks`, CUDA IPC) and its local Strassen call
+  reads the owners' memory directly.  For Naive and C the operand-sum pass is the only
+  reader of A and B, so the gather over NVLink is fused into that pass; ABC, AB and the
+  classical kernel re-read operand tiles, so their pieces are pulled by a side stream
+  into a local double buffer first.
 * :func:`summa_loopback` runs P virtual ranks in ONE process. Each "broadcast" is a device
   copy and the ranks execute one after another. It exercises the full data path and the
   real kernels on a single GPU; nothing waits on another launch.
@@ -108,6 +114,20 @@ class Layout:
     def b_pieces(self, p):
         """B panel p by owning process row: (row, local row offset, width, panel offset)."""
         return self._pieces(p * self.b, self.b, self.k_r)
+
+    def k_pieces(self):
+        """The k range cut at A-owner (k_c), B-owner (k_r) and panel (b) boundaries, for the
+        peer-memory schedule: (g0, w, a_col, a_off, b_row, b_off) means A columns
+        [a_off, a_off + w) of process column a_col times B rows [b_off, b_off + w) of
+        process row b_row."""
+        out, g = [], 0
+        while g < self.k:
+            ac, ao = divmod(g, self.k_c)
+            br, bo = divmod(g, self.k_r)
+            end = min((ac + 1) * self.k_c, (br + 1) * self.k_r, (g // self.b + 1) * self.b)
+            out.append((g, end - g, ac, ao, br, bo))
+            g = end
+        return out
 
 
 def make_layout(m, n, k, p, b=None):
@@ -279,4 +299,127 @@ def summa_loopback(layout: Layout, A_blocks: List[torch.Tensor], B_blocks: List[
                 bbuf[po:po + w, :].copy_(B_blocks[orow * L.pc + j][lo:lo + w, :])
             n = gemm(alpha, abuf, bbuf, C_blocks[r])
             launches += n if isinstance(n, int) else 1
+    return launches
+
+
+# ------------------------------------------------- peer-memory SUMMA (no broadcasts)
+# Variants whose local update starts with a materialising operand-sum pass: that pass is
+# the only reader of A and B, so it can read the owner's block in place (over NVLink on a
+# real node) and the all-gather is fused into the sum pass.
+DIRECT_VARIANTS = ("naive", "c")
+
+
+def open_peer_blocks(A_l: torch.Tensor, B_l: torch.Tensor, group=None):
+    """Map every rank's A and B blocks into this process (CUDA IPC).
+
+    Each rank exports its blocks' IPC handles (torch.multiprocessing's CUDA tensor
+    reduction: cudaIpcGetMemHandle on the allocation, plus the offset inside it); the
+    handles are exchanged with all_gather_object over `group` (metadata only, a few hundred
+    bytes) and opened with cudaIpcOpenMemHandle, which enables peer access on a multi-GPU
+    node.  Entry r of the returned lists is rank r's block; this rank's own entry is its
+    tensor.  The owners must keep A_l / B_l alive while peers use the mappings.
+    """
+    import torch.distributed as dist
+    from torch.multiprocessing.reductions import reduce_tensor
+    if not (A_l.is_cuda and B_l.is_cuda):
+        raise ValueError("open_peer_blocks needs CUDA blocks")
+    me = dist.get_rank(group)
+    if dist.get_world_size(group) == 1:      # nothing to export (and no consumer to release it)
+        return [A_l], [B_l]
+    mine = (reduce_tensor(A_l), reduce_tensor(B_l))
+    allh = [None] * dist.get_world_size(group)
+    dist.all_gather_object(allh, mine, group=group)
+    A_peers, B_peers = [], []
+    for r, (ha, hb) in enumerate(allh):
+        if r == me:
+            A_peers.append(A_l)
+            B_peers.append(B_l)
+        else:
+            A_peers.append(ha[0](*ha[1]))
+            B_peers.append(hb[0](*hb[1]))
+    return A_peers, B_peers
+
+
+def summa_p2p(layout: Layout, rank: int, A_peers: List[torch.Tensor], B_peers: List[torch.Tensor],
+              C_l: torch.Tensor, alpha: float = 1.0, variant="naive", level=2,
+              local_gemm: Optional[Callable] = None, direct: Optional[bool] = None) -> int:
+    """C_l += alpha * (A @ B)_ij with the operands read from the owners' memory.
+
+    The same product as :func:`summa`, with no broadcast: rank (i, j) walks
+    ``layout.k_pieces()`` and each rank-w update takes A columns from the block of rank
+    (i, a_col) and B rows from the block of rank (b_row, j), both as strided views of the
+    owners' memory (:func:`open_peer_blocks`, or local tensors for a loopback).
+
+    * direct (default for Naive and C): the local Strassen call reads the peer views
+      itself.  Its first kernels are the operand-sum passes, which read every A and B
+      element once and write the sums to local HBM, so the gather over NVLink is fused
+      into the pass Strassen makes anyway and no SM time goes to a collective.
+    * staged (ABC, AB, classical, whose mainloop re-reads operand tiles): piece t + 1 is
+      pulled into a local double buffer on a side stream while piece t's update runs.
+
+    The caller provides the ordering across ranks: every owner's blocks must be final
+    before any rank starts (device synchronize + barrier), and must not change until
+    every rank has finished.  Returns the GPU launches of the local updates (one per
+    update when `local_gemm` reports no count).
+    """
+    L = layout
+    i, j = divmod(rank, L.pc)
+    gemm = local_gemm or _default_local_gemm(variant, level)
+    if direct is None:
+        direct = variant in DIRECT_VARIANTS
+    pieces = L.k_pieces()
+
+    def views(pc):
+        g0, w, ac, ao, br, bo = pc
+        return A_peers[i * L.pc + ac][:, ao:ao + w], B_peers[br * L.pc + j][bo:bo + w, :]
+
+    launches = 0
+    if direct:
+        for pc in pieces:
+            a, b = views(pc)
+            n = gemm(alpha, a, b, C_l)
+            launches += n if isinstance(n, int) else 1
+        return launches
+
+    dev = C_l.device
+    wmax = max(pc[1] for pc in pieces)
+    abuf = [torch.empty((wmax, L.m_l), dtype=torch.float64, device=dev).t() for _ in range(2)]
+    bbuf = [torch.empty((L.n_l, wmax), dtype=torch.float64, device=dev).t() for _ in range(2)]
+    cuda = C_l.is_cuda
+    side = torch.cuda.Stream(device=dev) if cuda else None
+    main = torch.cuda.current_stream(dev) if cuda else None
+    ready, free = [None, None], [None, None]
+
+    def pull(t):
+        s, w = t % 2, pieces[t][1]
+        a, b = views(pieces[t])
+        if not cuda:
+            abuf[s][:, :w].copy_(a)
+            bbuf[s][:w, :].copy_(b)
+            return
+        with torch.cuda.stream(side):
+            if free[s] is not None:          # the update that last read buffer s is done
+                side.wait_event(free[s])
+            abuf[s][:, :w].copy_(a, non_blocking=True)
+            bbuf[s][:w, :].copy_(b, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(side)
+            ready[s] = ev
+
+    pull(0)
+    for t, pc in enumerate(pieces):
+        if t + 1 < len(pieces):
+            pull(t + 1)
+        s, w = t % 2, pc[1]
+        if cuda:
+            main.wait_event(ready[s])
+        n = gemm(alpha, abuf[s][:, :w], bbuf[s][:w, :], C_l)
+        launches += n if isinstance(n, int) else 1
+        if cuda:
+            ev = torch.cuda.Event()
+            ev.record(main)
+            free[s] = ev
+    if cuda:
+        for x in abuf + bbuf:                # buffers freed on the main stream's order
+            x.record_stream(side)
     return launches

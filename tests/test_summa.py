@@ -140,3 +140,108 @@ def test_config5_loopback_counter_rng_sampled_tiles(cuda, N, P, variant, level):
     import cfg5_loopback
     res = cfg5_loopback.run(N, P, variant, level)
     assert res["pass"], res
+
+
+# ------------------------------------------------------------ peer-memory SUMMA
+def test_k_pieces_cover_k_at_owner_and_panel_boundaries():
+    L = SU.make_layout(64, 96, 48, 8, b=16)          # 2 x 4 grid: k_c = 12, k_r = 24
+    pcs = L.k_pieces()
+    assert [p[0] for p in pcs] == [0, 12, 16, 24, 32, 36]
+    assert sum(p[1] for p in pcs) == 48
+    assert pcs[1] == (12, 4, 1, 0, 0, 12)            # A column 1 from 0, B row 0 from 12
+    assert pcs[3] == (24, 8, 2, 0, 1, 0)
+    for g, w, ac, ao, br, bo in pcs:
+        assert ac * L.k_c + ao == g and br * L.k_r + bo == g
+        assert ao + w <= L.k_c and bo + w <= L.k_r and g // L.b == (g + w - 1) // L.b
+    assert SU.make_layout(32, 32, 32, 1, b=32).k_pieces() == [(0, 32, 0, 0, 0, 0)]
+
+
+@pytest.mark.parametrize("P,b", [(1, 8), (2, 8), (4, 16), (8, 4), (8, 64)])
+@pytest.mark.parametrize("direct", [True, False])
+def test_p2p_schedule_matches_dense(P, b, direct):
+    m, n, k = 48, 40, 64
+    A, B, C = dense(m, n, k, 5)
+    want = C - 0.25 * (A @ B)
+    L = SU.make_layout(m, n, k, P, b=b)
+    blocks = [SU.local_blocks(L, r, A, B, C) for r in range(P)]
+    Ap, Bp = [a for a, _, _ in blocks], [bb for _, bb, _ in blocks]
+    for r in range(P):
+        c = blocks[r][2].clone()
+        n_up = SU.summa_p2p(L, r, Ap, Bp, c, alpha=-0.25, local_gemm=matmul_update,
+                            direct=direct)
+        assert n_up == len(L.k_pieces())
+        _, _, wc = SU.local_blocks(L, r, A, B, want)
+        assert torch.allclose(c, wc, rtol=0, atol=1e-12)
+
+
+def _colmajor_cuda(x):
+    return x.t().contiguous().t().cuda()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P,variant,level,b", [(2, "naive", 2, 2048), (4, "c", 2, 512),
+                                               (8, "abc", 1, 256), (4, "ab", 2, 1024),
+                                               (2, "dgemm", 0, 2048)])
+def test_p2p_loopback_on_gpu_with_strassen_kernels(cuda, P, variant, level, b):
+    """Peer-memory schedule with the real kernels reading strided views of the owners'
+    blocks (direct for Naive/C, staged for the others)."""
+    m, n, k = 1024, 2048, 2048
+    A, B, C = (x.to(cuda) for x in dense(m, n, k, 9))
+    L = SU.make_layout(m, n, k, P, b=b)
+    blocks = [[_colmajor_cuda(x.cpu()) for x in SU.local_blocks(L, r, A, B, C)] for r in range(P)]
+    Ap, Bp = [x[0] for x in blocks], [x[1] for x in blocks]
+    want = C + A @ B
+    an, bn = torch.linalg.norm(A).item(), torch.linalg.norm(B).item()
+    for r in range(P):
+        SU.summa_p2p(L, r, Ap, Bp, blocks[r][2], variant=variant, level=level)
+        torch.cuda.synchronize()
+        _, _, wc = SU.local_blocks(L, r, A, B, want)
+        nw = (torch.linalg.norm(blocks[r][2] - wc) / (an * bn)).item()
+        assert nw <= (1e-12 if level <= 1 else 5e-12), (r, nw)
+
+
+def _ipc_worker(rank, world, port, variant, level, b, q):
+    """One process of a world-2 job on ONE GPU: the peer block is a CUDA IPC mapping of
+    the other process's memory, read by this process's kernels (no kernel waits on
+    another process's kernel; the barriers order whole steps)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        m, n, k = 512, 1024, 1536
+        A, B, C = dense(m, n, k, 21)
+        L = SU.make_layout(m, n, k, world, b=b)
+        a, bb, c = (_colmajor_cuda(x) for x in SU.local_blocks(L, rank, A, B, C))
+        torch.cuda.synchronize()
+        Ap, Bp = SU.open_peer_blocks(a, bb)
+        dist.barrier()
+        SU.summa_p2p(L, rank, Ap, Bp, c, variant=variant, level=level)
+        torch.cuda.synchronize()
+        dist.barrier()                      # peers are done reading this rank's blocks
+        want = C + A @ B
+        _, _, wc = SU.local_blocks(L, rank, A, B, want)
+        nw = float(torch.linalg.norm(c.cpu() - wc) / (torch.linalg.norm(A) * torch.linalg.norm(B)))
+        q.put((rank, nw, Ap[1 - rank].data_ptr() != a.data_ptr()))
+        del Ap, Bp
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant,level,b", [("naive", 2, 1536), ("abc", 1, 512)])
+def test_p2p_ipc_two_processes_one_gpu(cuda, variant, level, b):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, variant, level, b, q))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    res = sorted(q.get(timeout=10) for _ in range(2))
+    for r, nw, mapped in res:
+        assert mapped
+        assert nw <= (1e-12 if level == 1 else 5e-12), (r, nw)
