@@ -541,8 +541,8 @@ def run_summa(args, rank, world, local, colmajor, barrier, max_over_ranks):
             ev_c.record(copy_stream)
         torch.cuda.current_stream().wait_event(ev_ab)
         local_gemm.c_ready = ev_c
-        if args.p2p:  # peers read this rank's A and B: every copy lands before any step
-            torch.cuda.synchronize()
+        if args.p2p:  # peers read this rank's A and B: they land before any rank steps
+            ev_ab.synchronize()
             barrier()
         step()
         Ch.copy_(C_l)
