@@ -1469,12 +1469,40 @@ __device__ __forceinline__ void stream_apply(double2 (&acc)[L == 1 ? 4 : 16],
     }
 }
 
-// products B*8 .. B*8+7: their M values loaded together, then applied in order
-template <int L, int B>
+// products B*8 .. B*8+7: their M values loaded together, then applied in order.
+// KS > 0: the k-split count is a compile-time constant, so all KS x 8 partial loads of
+// a batch are issued before the first add (one memory round trip per batch instead of
+// a chain of KS per product); the adds keep the split order, so the sums are bitwise
+// the same as the runtime-KS form (KS = 0).
+template <int L, int B, int KS>
 __device__ __forceinline__ void stream_batch(double2 (&acc)[L == 1 ? 4 : 16], const double* Mij,
                                              const StreamGatherParams& P) {
     constexpr int NP = stream_tab<L>().np;
-    if constexpr (B * kStreamBatch < NP) {
+    if constexpr (B * kStreamBatch < NP && KS > 0) {
+        double2 x[kStreamBatch][KS];
+#pragma unroll
+        for (int t = 0; t < kStreamBatch; ++t)
+            if (B * kStreamBatch + t < NP) {
+                const double* M = Mij + static_cast<long long>(B * kStreamBatch + t) * KS *
+                                            P.mstride;
+#pragma unroll
+                for (int sp = 0; sp < KS; ++sp)
+                    x[t][sp] = *reinterpret_cast<const double2*>(M + sp * P.mstride);
+            }
+        double2 v[kStreamBatch];
+#pragma unroll
+        for (int t = 0; t < kStreamBatch; ++t)
+            if (B * kStreamBatch + t < NP) {
+                v[t] = x[t][0];
+#pragma unroll
+                for (int sp = 1; sp < KS; ++sp) {
+                    v[t].x += x[t][sp].x;
+                    v[t].y += x[t][sp].y;
+                }
+            }
+        stream_apply<L, B * kStreamBatch>(acc, v, P);
+        stream_batch<L, B + 1, KS>(acc, Mij, P);
+    } else if constexpr (B * kStreamBatch < NP) {
         double2 v[kStreamBatch];
 #pragma unroll
         for (int t = 0; t < kStreamBatch; ++t) {
@@ -1490,11 +1518,11 @@ __device__ __forceinline__ void stream_batch(double2 (&acc)[L == 1 ? 4 : 16], co
             }
         }
         stream_apply<L, B * kStreamBatch>(acc, v, P);
-        stream_batch<L, B + 1>(acc, Mij, P);
+        stream_batch<L, B + 1, KS>(acc, Mij, P);
     }
 }
 
-template <int L>
+template <int L, int KS>
 __global__ void __launch_bounds__(kStream2Threads)
 stream_fixed_kernel(const __grid_constant__ StreamGatherParams P) {
     constexpr int NQ = L == 1 ? 4 : 16;
@@ -1514,7 +1542,7 @@ stream_fixed_kernel(const __grid_constant__ StreamGatherParams P) {
                     acc[q].x = *pc;
             }
         }
-        stream_batch<L, 0>(acc, P.mbase + i + j * P.ldm, P);
+        stream_batch<L, 0, KS>(acc, P.mbase + i + j * P.ldm, P);
 #pragma unroll
         for (int q = 0; q < NQ; ++q)
             if (j < P.ccols[q]) {
@@ -1686,6 +1714,27 @@ static bool to_gather(const StreamParams& p, StreamGatherParams& g) {
     return true;
 }
 
+// register stream pass with the k-split count as a template constant where it is small
+template <int L>
+void launch_stream_fixed(dim3 grid, const StreamGatherParams& g, cudaStream_t s) {
+    static const bool ks_on = [] {
+        const char* v = std::getenv("STRASSEN_B200_STREAM_KS");  // 0 / 1 (experiments)
+        return v ? std::atoi(v) != 0 : true;
+    }();
+    // level 1 only: at level 2 the 49 x KS loads in flight per thread measured slower
+    // (2048^3 Naive L2 stream pass 56 -> 76 us, profiles/r01_stream_ks_probe.log); KS = 1
+    // is the runtime form's schedule already
+    if constexpr (L == 1) {
+        switch (ks_on ? g.ksplit : 0) {
+            case 2: stream_fixed_kernel<L, 2><<<grid, kStream2Threads, 0, s>>>(g); return;
+            case 3: stream_fixed_kernel<L, 3><<<grid, kStream2Threads, 0, s>>>(g); return;
+            case 4: stream_fixed_kernel<L, 4><<<grid, kStream2Threads, 0, s>>>(g); return;
+            default: break;
+        }
+    }
+    stream_fixed_kernel<L, 0><<<grid, kStream2Threads, 0, s>>>(g);
+}
+
 cudaError_t launch_stream_update(const StreamParams& p, cudaStream_t s) {
     static thread_local StreamGatherParams g;
     static const int ycap = [] {
@@ -1703,9 +1752,9 @@ cudaError_t launch_stream_update(const StreamParams& p, cudaStream_t s) {
                 return v ? std::atoi(v) != 0 : true;
             }();
             if (fixed_on && matches_stream_tab<2>(g))
-                stream_fixed_kernel<2><<<grid, kStream2Threads, 0, s>>>(g);
+                launch_stream_fixed<2>(grid, g, s);
             else if (fixed_on && matches_stream_tab<1>(g))
-                stream_fixed_kernel<1><<<grid, kStream2Threads, 0, s>>>(g);
+                launch_stream_fixed<1>(grid, g, s);
             else
                 stream_gather2_kernel<<<grid, kStream2Threads, 0, s>>>(g);
             return cudaGetLastError();
