@@ -1327,6 +1327,12 @@ stream_gather_kernel(const __grid_constant__ StreamGatherParams P) {
 // Row-pair form (C column-major with 16-byte aligned quadrants, even ldm):
 // 16-byte loads and stores, otherwise identical per element.
 constexpr int kStream2Threads = 128;
+#ifndef STREAM_FIXED_MINB2
+#define STREAM_FIXED_MINB2 4
+#endif
+// level-2 register pass: resident CTAs per SM requested from ptxas (the pass is
+// latency-bound below ~4096^3; 1 = unconstrained, 168 registers, 3 CTAs per SM)
+constexpr int kStreamFixedMinBlocks2 = STREAM_FIXED_MINB2;
 
 __global__ void __launch_bounds__(kStream2Threads)
 stream_gather2_kernel(const __grid_constant__ StreamGatherParams P) {
@@ -1523,7 +1529,7 @@ __device__ __forceinline__ void stream_batch(double2 (&acc)[L == 1 ? 4 : 16], co
 }
 
 template <int L, int KS>
-__global__ void __launch_bounds__(kStream2Threads)
+__global__ void __launch_bounds__(kStream2Threads, L == 1 ? 1 : kStreamFixedMinBlocks2)
 stream_fixed_kernel(const __grid_constant__ StreamGatherParams P) {
     constexpr int NQ = L == 1 ? 4 : 16;
     const int tid = threadIdx.x;
