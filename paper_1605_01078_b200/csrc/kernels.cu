@@ -1328,10 +1328,11 @@ stream_gather_kernel(const __grid_constant__ StreamGatherParams P) {
 // 16-byte loads and stores, otherwise identical per element.
 constexpr int kStream2Threads = 128;
 #ifndef STREAM_FIXED_MINB2
-#define STREAM_FIXED_MINB2 4
+#define STREAM_FIXED_MINB2 1
 #endif
-// level-2 register pass: resident CTAs per SM requested from ptxas (the pass is
-// latency-bound below ~4096^3; 1 = unconstrained, 168 registers, 3 CTAs per SM)
+// level-2 register pass: resident CTAs per SM requested from ptxas.  1 = unconstrained
+// (168 registers, 3 CTAs per SM); 4 (128 registers, spills) measured slower inside the
+// bench step at 16384^3 (1.97 -> 2.12 ms, profiles/r01_notes.md)
 constexpr int kStreamFixedMinBlocks2 = STREAM_FIXED_MINB2;
 
 __global__ void __launch_bounds__(kStream2Threads)
