@@ -1327,13 +1327,6 @@ stream_gather_kernel(const __grid_constant__ StreamGatherParams P) {
 // Row-pair form (C column-major with 16-byte aligned quadrants, even ldm):
 // 16-byte loads and stores, otherwise identical per element.
 constexpr int kStream2Threads = 128;
-#ifndef STREAM_FIXED_MINB2
-#define STREAM_FIXED_MINB2 1
-#endif
-// level-2 register pass: resident CTAs per SM requested from ptxas.  1 = unconstrained
-// (168 registers, 3 CTAs per SM); 4 (128 registers, spills) measured slower inside the
-// bench step at 16384^3 (1.97 -> 2.12 ms, profiles/r01_notes.md)
-constexpr int kStreamFixedMinBlocks2 = STREAM_FIXED_MINB2;
 
 __global__ void __launch_bounds__(kStream2Threads)
 stream_gather2_kernel(const __grid_constant__ StreamGatherParams P) {
@@ -1530,7 +1523,7 @@ __device__ __forceinline__ void stream_batch(double2 (&acc)[L == 1 ? 4 : 16], co
 }
 
 template <int L, int KS>
-__global__ void __launch_bounds__(kStream2Threads, L == 1 ? 1 : kStreamFixedMinBlocks2)
+__global__ void __launch_bounds__(kStream2Threads)
 stream_fixed_kernel(const __grid_constant__ StreamGatherParams P) {
     constexpr int NQ = L == 1 ? 4 : 16;
     const int tid = threadIdx.x;
