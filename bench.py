@@ -20,14 +20,21 @@ Prints ONE JSON line on rank 0.
             reference sources with its own flags) on a bounded sample
   --impl reference  times that reference CPU path alone (rank 0).
 
-Multi-GPU (torchrun, N > 1): SUMMA over NCCL (paper_1605_01078_b200/summa.py),
-weak scaling.  The pr x pc grid comes from grid_for(N) (1x2, 2x2, 2x4).  Rank
-(i, j) owns a 16384 x 16384 block of C, and the global problem is
-m = 16384*pr, n = 16384*pc, k = 16384.  A panels are broadcast along rows and
-B panels along columns, overlapped with the local Strassen rank-b updates
-(panel width b = 8192: two 16384^2 x 8192 local updates per step; a panel
-straddling the k/pc columns a rank owns is assembled from per-owner pieces).
-Every rank therefore does one 16384^3 of work per step; time = max over ranks.
+Multi-GPU (N > 1): BASELINE config 5, SUMMA over NCCL (paper_1605_01078_b200/
+summa.py) with local two-level ABC Strassen.  `python bench.py --gpus N` re-executes
+itself under torchrun (one rank per GPU, 127.0.0.1 rendezvous) when it is not already
+running under it, and every rank checks WORLD_SIZE == N.  The pr x pc grid comes from
+grid_for(N) (1x2, 2x2, 2x4); rank (i, j) owns the (i, j) blocks of A, B and C.  A panels
+are broadcast along process rows and B panels along process columns, double-buffered
+against the local rank-b updates (panel width b = 8192; a panel straddling the columns
+a rank owns is assembled from per-owner pieces).  Two problems per run:
+  value         m = n = k = 65536 (config 5's fixed size; total work fixed: "strong")
+  weak_scaled   m = n = k = 32768 * sqrt(N) rounded to the nearest multiple of 256
+                (46336, 65536, 92672 at N = 2, 4, 8): config 5's weak-scaled variant
+Time = max over ranks of CUDA-event step times; value = total flops / that time.
+--summa runs the same path at N = 1 (a 1 x 1 grid, no collectives); --dry-run runs
+the launcher, grid, layout and timing logic on CPU ranks over gloo with a dense
+local update (tests/test_bench_launcher.py).
 """
 import argparse
 import json
@@ -50,7 +57,8 @@ def parse():
     p.add_argument("--steps", type=int, default=5)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    p.add_argument("--variant", default="naive", choices=["dgemm", "abc", "ab", "naive", "c"])
+    # default: naive level 2 at N = 1 (the headline); abc level 2 for SUMMA (config 5)
+    p.add_argument("--variant", default=None, choices=["dgemm", "abc", "ab", "naive", "c"])
     p.add_argument("--level", type=int, default=2)
     p.add_argument("--no-variants", action="store_true")
     p.add_argument("--dim", type=int, default=16384)
@@ -67,13 +75,44 @@ def parse():
     p.add_argument("--p2p", action="store_true",
                    help="N > 1: peer-memory SUMMA (operands read from the owners' blocks "
                         "over CUDA IPC, no NCCL broadcasts; summa.summa_p2p)")
+    p.add_argument("--summa-size", default="both", choices=["strong", "weak", "both"],
+                   help="SUMMA problems: config 5's fixed 65536^3 (strong), its weak-scaled "
+                        "32768*sqrt(N) variant, or both (value = strong)")
+    p.add_argument("--dry-run", action="store_true",
+                   help="CPU ranks over gloo, dense local update: launcher/layout/timing test")
     a = p.parse_args()
+    summa_path = a.gpus > 1 or a.summa or a.dry_run
+    if a.variant is None:
+        a.variant = "abc" if summa_path else "naive"
     if a.variant == "dgemm":
         a.level = 0
+    a.user_dims = bool(a.m or a.n or a.k or a.dim != 16384)
     a.m = a.m or a.dim
     a.n = a.n or a.dim
     a.k = a.k or a.dim
     return a
+
+
+def weak_dim(p, base=32768, mult=256):
+    """Config 5's weak-scaled size 32768 * sqrt(P), rounded to the nearest multiple of
+    256 (so every local dimension on the 1x2 / 2x2 / 2x4 grids stays a multiple of
+    2^L * 32): 32768, 46336, 65536, 92672 for P = 1, 2, 4, 8."""
+    import math
+    return int(round(base * math.sqrt(p) / mult)) * mult
+
+
+def relaunch_under_torchrun(args):
+    """`bench.py --gpus N` outside torchrun: re-execute this command under
+    torch.distributed.run with N local ranks (127.0.0.1 rendezvous)."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 def table_counts(level):
@@ -258,11 +297,17 @@ def run_reference(args, rank):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args)  # does not return
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dry_run:
+        return run_summa_dry(args, rank, world)
 
     import torch
     import torch.distributed as dist
@@ -274,6 +319,8 @@ def main():
         os.environ.setdefault("MASTER_PORT", "29517")
         os.environ.setdefault("RANK", str(rank))
         os.environ.setdefault("WORLD_SIZE", str(world))
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # comm-init lines (ranks, NVLS, P2P)
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     def barrier():
@@ -452,110 +499,204 @@ def main():
         dist.destroy_process_group()
 
 
+def summa_problems(args, world):
+    """(name, m, n, k) of the SUMMA problems this run measures (config 5)."""
+    if args.user_dims:  # explicit --dim / --m / --n / --k (one-GPU checks, experiments)
+        return [("strong", args.m, args.n, args.k)]
+    out = []
+    if args.summa_size in ("strong", "both"):
+        out.append(("strong", 65536, 65536, 65536))
+    if args.summa_size in ("weak", "both"):
+        d = weak_dim(world)
+        out.append(("weak", d, d, d))
+    return out
+
+
 def run_summa(args, rank, world, local, colmajor, barrier, max_over_ranks):
-    """N > 1: SUMMA weak scaling with 16384^2 C blocks per rank (see module doc)."""
+    """N > 1 (or --summa): BASELINE config 5 -- SUMMA with local Strassen updates
+    (see the module doc for the problems and the timing)."""
     import torch
 
     from paper_1605_01078_b200 import summa as SU
-    L = SU.make_layout(args.m * SU.grid_for(world)[0], args.n * SU.grid_for(world)[1], args.k,
-                       world)
-    comm = SU.TorchComm(L)
-    A_l, B_l, C_l = colmajor(L.m_l, L.k_c), colmajor(L.k_r, L.n_l), colmajor(L.m_l, L.n_l)
-    local_gemm = SU._default_local_gemm(args.variant, args.level)
-    if args.p2p:
-        torch.cuda.synchronize()
-        Ap, Bp = SU.open_peer_blocks(A_l, B_l)
-        barrier()
-        step = lambda: SU.summa_p2p(L, rank, Ap, Bp, C_l, 1.0, args.variant,  # noqa: E731
-                                    args.level, local_gemm=local_gemm)
-    else:
-        step = lambda: SU.summa(L, comm, A_l, B_l, C_l, 1.0, args.variant,  # noqa: E731
-                                args.level, local_gemm=local_gemm)
-    for _ in range(args.warmup):
-        step()
-    barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        launches = 0
-        for _ in range(args.steps):
-            launches += step()
-        e1.record()
-        torch.cuda.synchronize()
-    barrier()
-    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
-    flops = 2.0 * L.m * L.n * L.k
-    # roofline of the local update's mm_kernel: one profiled panel-shaped local call
-    # (m_l x n_l x b) on this rank, timed by the library's events on the launch stream
     peaks = json.load(open(os.path.join(ROOT, "profiles", "fp64_peaks.json")))
-    lctx = local_gemm.ctx
-    ap, bp = colmajor(L.m_l, L.b), colmajor(L.b, L.n_l)
-    lctx.enable_profiling(True)
-    lctx.gemm_device(args.variant, args.level, 1.0, ap, bp, C_l, torch.cuda.current_stream())
-    torch.cuda.synchronize()
-    prof = lctx.last_profile()
-    lctx.enable_profiling(False)
-    del ap, bp
-    mm_ms = sum(x["ms"] for x in prof if x["kernel"] == "mm_kernel")
-    f_exec = executed_flops(L.m_l, L.n_l, L.b, args.level, args.variant)
-    achieved = max_over_ranks(-(f_exec / (mm_ms * 1e-3) / 1e12)) * -1.0  # min over ranks
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["dmma_tflops"],
-                "unit": "TFLOP/s", "frac": achieved / peaks["dmma_tflops"], "traffic": None,
-                "flops_per_launch": f_exec, "kernel_ms": mm_ms, "kernel": "mm_kernel",
-                "launches_per_step": launches // max(args.steps, 1), "step_profile_ms": prof,
-                "scope": "one local update (m_l x n_l x b) per rank; min over ranks",
-                "peak_source": "measured FP64 DMMA peak, profiles/fp64_peaks.json"}
-    line = {
-        "metric": "effective FP64 TFLOPS (2mnk/t)", "value": flops / (ms * 1e-3) / 1e12,
-        "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic uniform[-1,1) (torch generator, column-major)",
-        "config": {"workload": f"SUMMA m={L.m} n={L.n} k={L.k} on {L.pr}x{L.pc} GPUs "
-                               f"(16384^2 C block per rank)", "variant": args.variant,
-                   "level": args.level, "m": L.m, "n": L.n, "k": L.k, "panel_b": L.b,
-                   "grid": [L.pr, L.pc], "parallelism": f"summa{L.pr}x{L.pc}",
-                   "exchange": "peer memory (CUDA IPC), no broadcasts" if args.p2p
-                   else "NCCL row/column panel broadcasts",
-                   "l2": "inputs larger than the 126 MB L2"},
-        "roofline": roofline,
-        "clocks": clk.summary(),
-        "gpu_launches": launches,
-    }
-    if not args.no_e2e:
-        # end to end: pinned host blocks in, C block out, around one SUMMA step
-        Ah, Bh, Ch = (x.t().cpu().pin_memory().t() for x in (A_l, B_l, C_l))
-        copy_stream = torch.cuda.Stream()
+    local_gemm = SU._default_local_gemm(args.variant, args.level)
+    results = {}
+    line = None
+    for name, gm, gn, gk in summa_problems(args, world):
+        L = SU.make_layout(gm, gn, gk, world)
+        comm = SU.TorchComm(L) if world > 1 or args.summa else None
+        A_l, B_l, C_l = colmajor(L.m_l, L.k_c), colmajor(L.k_r, L.n_l), colmajor(L.m_l, L.n_l)
+        if args.p2p:
+            torch.cuda.synchronize()
+            Ap, Bp = SU.open_peer_blocks(A_l, B_l)
+            barrier()
+            step = lambda: SU.summa_p2p(L, rank, Ap, Bp, C_l, 1.0, args.variant,  # noqa: E731
+                                        args.level, local_gemm=local_gemm)
+        else:
+            step = lambda: SU.summa(L, comm, A_l, B_l, C_l, 1.0, args.variant,  # noqa: E731
+                                    args.level, local_gemm=local_gemm)
+        for _ in range(args.warmup):
+            step()
         barrier()
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        # A and B blocks first; C's copy overlaps the first local update's operand sums
-        # and products (its kernels wait on ev_c right before they read C)
-        with torch.cuda.stream(copy_stream):
-            A_l.copy_(Ah, non_blocking=True)
-            B_l.copy_(Bh, non_blocking=True)
-            ev_ab = torch.cuda.Event()
-            ev_ab.record(copy_stream)
-            C_l.copy_(Ch, non_blocking=True)
-            ev_c = torch.cuda.Event()
-            ev_c.record(copy_stream)
-        torch.cuda.current_stream().wait_event(ev_ab)
-        local_gemm.c_ready = ev_c
-        if args.p2p:  # peers read this rank's A and B: they land before any rank steps
-            ev_ab.synchronize()
-            barrier()
-        step()
-        Ch.copy_(C_l)
-        torch.cuda.synchronize()
-        dt = max_over_ranks(time.perf_counter() - t0)
-        line["e2e"] = {"value": flops / dt / 1e12, "unit": "TFLOP/s",
-                       "h2d_bytes_per_step": world * 8 * (L.m_l * L.k_c + L.k_r * L.n_l + L.m_l * L.n_l),
-                       "d2h_bytes_per_step": world * 8 * L.m_l * L.n_l, "ms_per_step": dt * 1e3,
-                       "api": ("summa_p2p()" if args.p2p else "summa()")
-                       + " over strassen_gemm_device, pinned host blocks"}
+        with ClockSampler(local) as clk:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            launches = 0
+            for _ in range(args.steps):
+                launches += step()
+            e1.record()
+            torch.cuda.synchronize()
+        barrier()
+        ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+        flops = 2.0 * L.m * L.n * L.k
+        res = {"m": L.m, "n": L.n, "k": L.k, "grid": [L.pr, L.pc], "panel_b": L.b,
+               "local": [L.m_l, L.n_l, L.b], "value": flops / (ms * 1e-3) / 1e12,
+               "ms_per_step": ms, "gpu_launches": launches, "clocks": clk.summary()}
+        if line is None:
+            # roofline of the local update's mm_kernel: one profiled panel-shaped local
+            # call (m_l x n_l x b) on this rank, timed by the library's events on the
+            # launch stream; min over ranks
+            lctx = local_gemm.ctx
+            ap, bp = colmajor(L.m_l, L.b), colmajor(L.b, L.n_l)
+            lctx.enable_profiling(True)
+            lctx.gemm_device(args.variant, args.level, 1.0, ap, bp, C_l,
+                             torch.cuda.current_stream())
+            torch.cuda.synchronize()
+            prof = lctx.last_profile()
+            lctx.enable_profiling(False)
+            del ap, bp
+            mm_ms = sum(x["ms"] for x in prof if x["kernel"] == "mm_kernel")
+            f_exec = executed_flops(L.m_l, L.n_l, L.b, args.level, args.variant)
+            achieved = max_over_ranks(-(f_exec / (mm_ms * 1e-3) / 1e12)) * -1.0
+            roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["dmma_tflops"],
+                        "unit": "TFLOP/s", "frac": achieved / peaks["dmma_tflops"],
+                        "traffic": None, "flops_per_launch": f_exec, "kernel_ms": mm_ms,
+                        "kernel": "mm_kernel",
+                        "launches_per_step": launches // max(args.steps, 1),
+                        "step_profile_ms": prof,
+                        "scope": "one local update (m_l x n_l x b) per rank; min over ranks",
+                        "peak_source": "measured FP64 DMMA peak, profiles/fp64_peaks.json"}
+            line = {
+                "metric": "effective FP64 TFLOPS (2mnk/t)", "value": res["value"],
+                "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong" if name == "strong" else "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic uniform[-1,1) (torch generator, column-major)",
+                "config": {"workload": f"BASELINE config 5: SUMMA m=n=k={L.m} on {L.pr}x{L.pc} "
+                                       f"GPUs, local {args.variant} level {args.level}",
+                           "variant": args.variant, "level": args.level, "m": L.m, "n": L.n,
+                           "k": L.k, "panel_b": L.b, "grid": [L.pr, L.pc],
+                           "parallelism": f"summa{L.pr}x{L.pc}",
+                           "weak_rule": "weak_scaled: m=n=k = 32768*sqrt(N) rounded to the "
+                                        "nearest multiple of 256",
+                           "exchange": "peer memory (CUDA IPC), no broadcasts" if args.p2p
+                           else "NCCL row/column panel broadcasts",
+                           "l2": "inputs larger than the 126 MB L2"},
+                "roofline": roofline, "clocks": res["clocks"], "gpu_launches": launches,
+            }
+            if not args.no_e2e:
+                line["e2e"] = summa_e2e(args, L, A_l, B_l, C_l, step, local_gemm, barrier,
+                                        max_over_ranks, world, flops)
+        else:
+            results[name] = res
+        del A_l, B_l, C_l, step
+        torch.cuda.empty_cache()
+    if "weak" in results:
+        line["weak_scaled"] = results["weak"]
     if rank == 0:
         print(json.dumps(line), flush=True)
     import torch.distributed as dist
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
+def summa_e2e(args, L, A_l, B_l, C_l, step, local_gemm, barrier, max_over_ranks, world, flops):
+    """End to end: pinned host blocks in, one SUMMA step, the C block out."""
+    import torch
+
+    def pinned_like(x):  # column-major pinned host block holding x's values
+        h = torch.empty((x.shape[1], x.shape[0]), dtype=torch.float64, pin_memory=True).t()
+        h.copy_(x)
+        return h
+    Ah, Bh, Ch = (pinned_like(x) for x in (A_l, B_l, C_l))
+    copy_stream = torch.cuda.Stream()
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    # A and B blocks first; C's copy overlaps the first local update's operand sums
+    # and products (its kernels wait on ev_c right before they read C)
+    with torch.cuda.stream(copy_stream):
+        A_l.copy_(Ah, non_blocking=True)
+        B_l.copy_(Bh, non_blocking=True)
+        ev_ab = torch.cuda.Event()
+        ev_ab.record(copy_stream)
+        C_l.copy_(Ch, non_blocking=True)
+        ev_c = torch.cuda.Event()
+        ev_c.record(copy_stream)
+    torch.cuda.current_stream().wait_event(ev_ab)
+    local_gemm.c_ready = ev_c
+    if args.p2p:  # peers read this rank's A and B: they land before any rank steps
+        ev_ab.synchronize()
+        barrier()
+    step()
+    Ch.copy_(C_l)
+    torch.cuda.synchronize()
+    dt = max_over_ranks(time.perf_counter() - t0)
+    return {"value": flops / dt / 1e12, "unit": "TFLOP/s",
+            "h2d_bytes_per_step": world * 8 * (L.m_l * L.k_c + L.k_r * L.n_l + L.m_l * L.n_l),
+            "d2h_bytes_per_step": world * 8 * L.m_l * L.n_l, "ms_per_step": dt * 1e3,
+            "api": ("summa_p2p()" if args.p2p else "summa()")
+            + " over strassen_gemm_device, pinned host blocks"}
+
+
+def run_summa_dry(args, rank, world):
+    """--dry-run: the multi-GPU launcher and SUMMA schedule on CPU ranks over gloo,
+    with a dense local update -- checks the torchrun re-exec, the world-size check, the
+    grid and config-5 sizes (scaled down 64x per dimension) and the max-over-ranks
+    timing, and verifies the distributed product against a dense one."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1605_01078_b200 import summa as SU
+    dist.init_process_group("gloo")
+    out = {}
+    for name, gm, gn, gk in summa_problems(args, world):
+        m, n, k = gm // 64, gn // 64, gk // 64
+        L = SU.make_layout(m, n, k, world, b=max(1, k // 4))
+        comm = SU.TorchComm(L)
+        g = torch.Generator().manual_seed(5)
+        A = torch.rand(m, k, dtype=torch.float64, generator=g) * 2 - 1
+        B = torch.rand(k, n, dtype=torch.float64, generator=g) * 2 - 1
+        C = torch.rand(m, n, dtype=torch.float64, generator=g) * 2 - 1
+        a, b, c = (x.contiguous() for x in SU.local_blocks(L, rank, A, B, C))
+
+        def upd(alpha, x, y, z):
+            z.add_(alpha * (x @ y))
+        for _ in range(args.warmup):
+            SU.summa(L, comm, a, b, c.clone(), 1.0, local_gemm=upd)
+        dist.barrier()
+        t0 = time.perf_counter()
+        cc = c.clone()
+        for _ in range(args.steps):
+            cc.copy_(c)
+            SU.summa(L, comm, a, b, cc, 1.0, local_gemm=upd)
+        dt = time.perf_counter() - t0
+        t = torch.tensor([dt / args.steps], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        _, _, want = SU.local_blocks(L, rank, A, B, C + A @ B)
+        err = torch.tensor([float((cc - want).abs().max())], dtype=torch.float64)
+        dist.all_reduce(err, op=dist.ReduceOp.MAX)
+        out[name] = {"m": m, "n": n, "k": k, "config5_m": gm, "grid": [L.pr, L.pc],
+                     "ms_per_step": t.item() * 1e3, "max_abs_err": err.item()}
+    if rank == 0:
+        first = next(iter(out.values()))
+        print(json.dumps({"metric": "effective FP64 TFLOPS (2mnk/t)", "dry_run": True,
+                          "n_gpus": world, "world_size": dist.get_world_size(),
+                          "value": 2.0 * first["m"] * first["n"] * first["k"]
+                          / (first["ms_per_step"] * 1e-3) / 1e12,
+                          "unit": "TFLOP/s", "problems": out, "variant": args.variant,
+                          "level": args.level}), flush=True)
     dist.destroy_process_group()
 
 

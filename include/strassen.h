@@ -215,6 +215,16 @@ strassen_status strassen_ctx_set_pipelining(strassen_ctx* ctx, int enabled);
  * level 3 stay STRASSEN_ERR_PARAM.  Other values: STRASSEN_ERR_PARAM. */
 strassen_status strassen_ctx_set_max_level(strassen_ctx* ctx, int max_level);
 
+/* ABC / AB operand sums (the reference's pack_a_sum / pack_b_sum,
+ * blocking.cpp:12-66): an operand side of up to max_terms terms is summed in the
+ * mm kernel's registers while its term tiles stream in; a longer side is formed
+ * by one materialising HBM pass first (materialize_sum, variants.cpp:53-96).
+ * Both forms add the terms in listed order with identical roundings, so the
+ * result is bitwise the same for every setting; only speed differs.  1..4;
+ * default 2 (level 1 fully fused, level 2's 4-term sides materialised:
+ * profiles/r02_fuse_probe.log).  Other values: STRASSEN_ERR_PARAM. */
+strassen_status strassen_ctx_set_fused_terms(strassen_ctx* ctx, int max_terms);
+
 /* Per-launch CUDA-event timing of the calls on this ctx (off by default).
  * strassen_ctx_last_profile writes a JSON list [{"kernel": name, "ms": t,
  * "start_ms": offset from the first launch}, ...]

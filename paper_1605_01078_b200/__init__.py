@@ -122,6 +122,7 @@ def _declare(lib):
         "strassen_ctx_set_peeling": (_ST, [vp, C.c_int]),
         "strassen_ctx_set_pipelining": (_ST, [vp, C.c_int]),
         "strassen_ctx_set_max_level": (_ST, [vp, C.c_int]),
+        "strassen_ctx_set_fused_terms": (_ST, [vp, C.c_int]),
         "strassen_ctx_set_operand_events": (_ST, [vp, vp, vp, vp]),
         "strassen_ctx_last_profile": (_ST, [vp, C.c_char_p, _L]),
         "strassen_select": (_ST, [_L, _L, _L, C.POINTER(C.c_int), C.POINTER(C.c_int), _dp]),
@@ -253,6 +254,11 @@ class Ctx:
         right before first reading that device operand."""
         h = [C.c_void_p(e.cuda_event if e is not None else None) for e in (a, b, c)]
         _check(self._l.strassen_ctx_set_operand_events(self.ptr, *h), "set_operand_events")
+
+    def set_fused_terms(self, max_terms):
+        """ABC / AB: operand sides of up to max_terms terms summed in the kernel,
+        longer ones materialised first (bitwise-identical results)."""
+        _check(self._l.strassen_ctx_set_fused_terms(self.ptr, int(max_terms)), "set_fused_terms")
 
     def set_max_level(self, level):
         """2 (default) or 3: level 3 for the naive / c variants (B200 extension)."""

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <new>
 #include <string>
@@ -78,6 +80,21 @@ void span_of(long rows, long cols, long rs, long cs, long& lo, long& hi) {
     hi += std::max(0L, a) + std::max(0L, b);
 }
 
+// Makes `dev` current for a scope (dev < 0: no change) and restores the caller's device.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        int cur = -1;
+        if (dev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != dev &&
+            cudaSetDevice(dev) == cudaSuccess)
+            prev = cur;
+        cudaGetLastError();
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 void cuda_ck(cudaError_t e, const char* what) {
     if (e == cudaErrorMemoryAllocation) throw sb200::Error(STRASSEN_ERR_ALLOC, what);
     if (e != cudaSuccess)
@@ -137,8 +154,20 @@ strassen_status gemm_impl(strassen_ctx* ctx, bool explicit_stream, cudaStream_t 
     return guarded([&] {
         validate_call(variant, m, n, k, ctx->blocking);
         sb200::Engine& e = ctx->engine;
+        // a ctx stays on the device it was first used on (its streams, events and
+        // buffers live there): run the call there, restore the caller's device after
+        const DeviceGuard dev_guard(e.initialised ? e.device : -1);
         e.init();
         cudaStream_t s = explicit_stream ? user_stream : e.stream();
+        // device entry: reject host operands before any staging or allocation
+        if (device_only && (!sb200::is_device_pointer(a) || !sb200::is_device_pointer(b) ||
+                            !sb200::is_device_pointer(c)))
+            throw std::invalid_argument("strassen_gemm_device: operands must be device memory");
+        // the workspace is shared by every call on this ctx: order this call after the
+        // previous one even when it was issued on another stream
+        if (e.ev_last_recorded) cuda_ck(cudaStreamWaitEvent(s, e.ev_last, 0), "order after previous call");
+        e.unit_ctr_next = 0;
+        try {
         long launches = 0;
         bool sa = false, sb = false, sc = false;
         // the copy stream may only overwrite staging buffers once earlier work on s is done
@@ -163,8 +192,6 @@ strassen_status gemm_impl(strassen_ctx* ctx, bool explicit_stream, cudaStream_t 
         if (!sa && ready[0]) A.ready = ready[0];
         if (!sb && ready[1]) B.ready = ready[1];
         if (!sc && ready[2]) C.ready = ready[2];
-        if (device_only && (sa || sb || sc))
-            throw std::invalid_argument("strassen_gemm_device: operands must be device memory");
         for (auto& t : e.timed) {
             cudaEventDestroy(t.start);
             cudaEventDestroy(t.stop);
@@ -204,7 +231,10 @@ strassen_status gemm_impl(strassen_ctx* ctx, bool explicit_stream, cudaStream_t 
                     for (auto [i0, i1] : ranges(m, qm, W.rb, r))
                         copy_block(A.p, a, cs_a, i0, i1, 0, k, cudaMemcpyHostToDevice,
                                    e.copy_stream);
-                // otherwise A was staged whole (or is resident): the event follows it
+                // otherwise A was staged whole (or is resident): the event follows it,
+                // and a resident A still being produced (operand event) too
+                else if (A.ready)
+                    cuda_ck(cudaStreamWaitEvent(e.copy_stream, A.ready, 0), "operand event");
                 cuda_ck(cudaEventRecord(e.ev_win_a[r], e.copy_stream), "window event");
             };
             W.issue_b = [&](int cw) {
@@ -245,6 +275,8 @@ strassen_status gemm_impl(strassen_ctx* ctx, bool explicit_stream, cudaStream_t 
                         "D2H result");
             }
         }
+        cuda_ck(cudaEventRecord(e.ev_last, s), "call done event");
+        e.ev_last_recorded = true;
         if (!device_only) cuda_ck(cudaStreamSynchronize(s), "kernel execution");
         else cuda_ck(cudaGetLastError(), "kernel launch");
         e.last_launches = launches;
@@ -252,6 +284,16 @@ strassen_status gemm_impl(strassen_ctx* ctx, bool explicit_stream, cudaStream_t 
             strassen_counter_values d{};
             sb200::count_call(variant, level, m, n, k, ctx->blocking, d);
             sb200::add_counters(ctx->counters, d);
+        }
+        } catch (...) {
+            // nothing enqueued by this call may outlive it: copies from / to the
+            // caller's buffers and kernels reading the workspace (best effort)
+            for (cudaStream_t st : {s, e.copy_stream, e.d2h_stream, e.aux_stream})
+                if (st || st == s) cudaStreamSynchronize(st);
+            cudaGetLastError();
+            if (cudaEventRecord(e.ev_last, s) == cudaSuccess) e.ev_last_recorded = true;
+            cudaGetLastError();
+            throw;
         }
     });
 }
@@ -263,7 +305,10 @@ extern "C" {
 strassen_status strassen_ctx_create(strassen_ctx** out) {
     if (!out) return STRASSEN_ERR_NULL;
     *out = new (std::nothrow) strassen_ctx();
-    return *out ? STRASSEN_OK : STRASSEN_ERR_ALLOC;
+    if (!*out) return STRASSEN_ERR_ALLOC;
+    if (const char* v = std::getenv("STRASSEN_B200_FUSE_MAX"))  // 1-4 (experiments)
+        (*out)->engine.fuse_max_terms = std::max(1, std::min(4, std::atoi(v)));
+    return STRASSEN_OK;
 }
 
 void strassen_ctx_destroy(strassen_ctx* ctx) { delete ctx; }
@@ -384,6 +429,13 @@ strassen_status strassen_ctx_set_max_level(strassen_ctx* ctx, int max_level) {
     if (!ctx) return STRASSEN_ERR_NULL;
     if (max_level < 2 || max_level > 3) return STRASSEN_ERR_PARAM;
     ctx->engine.max_level = max_level;
+    return STRASSEN_OK;
+}
+
+strassen_status strassen_ctx_set_fused_terms(strassen_ctx* ctx, int max_terms) {
+    if (!ctx) return STRASSEN_ERR_NULL;
+    if (max_terms < 1 || max_terms > 4) return STRASSEN_ERR_PARAM;
+    ctx->engine.fuse_max_terms = max_terms;
     return STRASSEN_OK;
 }
 

@@ -196,8 +196,9 @@ Engine::~Engine() {
             if (arr[w]) cudaEventDestroy(arr[w]);
     for (cudaEvent_t ev : {ev_d2h, ev_fork, ev_join})
         if (ev) cudaEventDestroy(ev);
+    if (ev_last) cudaEventDestroy(ev_last);
     for (DeviceBuffer* b : {&stage_a, &stage_b, &stage_c, &pack_a, &pack_b, &mbuf, &tabuf, &tbbuf, &ticket_buf,
-                               &pack_a3, &pack_b3, &l3_a, &l3_b, &l3_m})
+                               &pack_a3, &pack_b3, &l3_a, &l3_b, &l3_m, &unit_ctr_buf})
         if (b->ptr) cudaFree(b->ptr);
 }
 
@@ -213,7 +214,7 @@ void Engine::init() {
     for (auto& ev : ev_ready) ck(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "event");
     ck(cudaStreamCreateWithFlags(&d2h_stream, cudaStreamNonBlocking), "d2h stream");
     ck(cudaStreamCreateWithFlags(&aux_stream, cudaStreamNonBlocking), "aux stream");
-    for (cudaEvent_t* ev : {&ev_d2h, &ev_fork, &ev_join})
+    for (cudaEvent_t* ev : {&ev_d2h, &ev_fork, &ev_join, &ev_last})
         ck(cudaEventCreateWithFlags(ev, cudaEventDisableTiming), "event");
     for (cudaEvent_t* arr : {ev_win_a, ev_win_b, ev_sum_a, ev_sum_b})
         for (int w = 0; w < kMaxStrips; ++w)
@@ -286,7 +287,7 @@ double* Engine::ensure(DeviceBuffer& b, size_t bytes) {
 size_t Engine::workspace_bytes() const {
     size_t t = 0;
     for (const DeviceBuffer* b : {&stage_a, &stage_b, &stage_c, &pack_a, &pack_b, &mbuf, &tabuf, &tbbuf, &ticket_buf,
-                               &pack_a3, &pack_b3, &l3_a, &l3_b, &l3_m})
+                               &pack_a3, &pack_b3, &l3_a, &l3_b, &l3_m, &unit_ctr_buf})
         t += b->bytes;
     return t;
 }
@@ -298,6 +299,22 @@ bool is_device_pointer(const void* p) {
         return false;
     }
     return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+// A zeroed unit counter for a persistent mm launch on s (MMParams::unit_counter):
+// distinct per launch within a call (windows run on two streams), reused across
+// calls, which are ordered after each other (gemm_impl's ev_last).
+int* next_unit_counter(Engine& e, cudaStream_t s) {
+    static const bool dyn_on = [] {
+        const char* v = std::getenv("STRASSEN_B200_DYN");  // 0 / 1 (experiments)
+        return v ? std::atoi(v) != 0 : true;
+    }();
+    if (!dyn_on) return nullptr;  // fixed unit stride
+    constexpr int kCounters = 1024;
+    int* base = reinterpret_cast<int*>(e.ensure(e.unit_ctr_buf, kCounters * sizeof(int)));
+    int* c = base + (e.unit_ctr_next++ % kCounters);
+    ck(cudaMemsetAsync(c, 0, sizeof(int), s), "unit counter reset");
+    return c;
 }
 
 // Launch plan of P (ABC / DGEMM / C / AB / Naive), decided on the WHOLE problem
@@ -493,6 +510,7 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
                                          defer_waves * (e.num_sms > 0 ? e.num_sms : 148))
                           ? 1 : 0;
         P.grid_cap = cap(bulk_units && !P.sep_stage);
+        if (P.grid_cap > 0) P.unit_counter = next_unit_counter(e, s);
         e.prof_begin("mm_kernel", s);
         ck(launch_mm(P, s), "mm_kernel");
         e.prof_end(s);
@@ -516,6 +534,8 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
             P.sk_len = F.sk_len;
             P.sk_maxp = F.sk_maxp;
             P.grid_cap = F.sk_grid;  // the decode assumes exactly this many CTAs
+        } else if (P.grid_cap > 0) {
+            P.unit_counter = next_unit_counter(e, s);
         }
         e.prof_begin("mm_kernel", s);
         ck(launch_mm(P, s), "mm_kernel (split, fused epilogue)");
@@ -530,6 +550,7 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
     P.ldm = F.ldm;
     P.mstride = F.mstride;
     P.grid_cap = cap(false);
+    if (P.grid_cap > 0) P.unit_counter = next_unit_counter(e, s);
     e.prof_begin("mm_kernel", s);
     ck(launch_mm(P, s), "mm_kernel (split)");
     e.prof_end(s);
@@ -635,8 +656,15 @@ void plan_windows(const Engine& e, strassen_variant variant, int level, long m, 
         return;  // split-mode sizes: a few milliseconds, nothing to overlap
     {   // temporaries that need product groups (run_strassen) rule out windows
         const long qk = ceil_div(k, side);
-        const double sums = (variant == STRASSEN_NAIVE || variant == STRASSEN_C)
-                                ? (L == 1 ? 5.0 : 45.0) * 8.0 * (qm * qk + qk * qn) : 0.0;
+        // materialised sums per side of the full tables: every multi-term side
+        // (Naive, C; ABC / AB fusing single terms only), or the sides longer than
+        // the fused limit (level 2's 25 four-term sides)
+        const bool all = variant == STRASSEN_NAIVE || variant == STRASSEN_C ||
+                         (variant != STRASSEN_DGEMM && e.fuse_max_terms < 2);
+        const double nsums = all ? (L == 1 ? 5.0 : 45.0)
+                             : (variant != STRASSEN_DGEMM && L == 2 && e.fuse_max_terms < 4) ? 25.0
+                                                                                             : 0.0;
+        const double sums = nsums * 8.0 * (qm * qk + qk * qn);
         const double prods = (variant == STRASSEN_NAIVE || variant == STRASSEN_AB)
                                  ? per_tile * 8.0 * qm * qn : 0.0;
         const double held = static_cast<double>(e.tabuf.bytes + e.tbbuf.bytes + e.mbuf.bytes);
@@ -845,9 +873,16 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
         Terms a, b, c;
     };
     std::vector<Live> live;
+    // profiling aid only (wrong results): keep the products with "na,nb" terms
+    static const int only_combo = [] {
+        const char* v = std::getenv("STRASSEN_B200_PROFILE_ONLY_COMBO");
+        int na = 0, nb = 0;
+        return v && std::sscanf(v, "%d,%d", &na, &nb) == 2 ? na * 8 + nb : 0;
+    }();
     for (const Product& pr : program(L).products) {
         Live l{live_terms(pr.a, a_live), live_terms(pr.b, b_live), live_terms(pr.c, c_live)};
         if (l.a.empty() || l.b.empty() || l.c.empty()) continue;
+        if (only_combo && static_cast<int>(l.a.size() * 8 + l.b.size()) != only_combo) continue;
         live.push_back(std::move(l));
     }
     // The whole program, or -- when the materialised operand sums and product
@@ -856,11 +891,20 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
     // with its own sum pass, products and C updates.  Every C element still receives
     // its updates in table order.
     // the whole program's size and mean term count plan every group's launches
+    // Operand sides with at least mat_min terms are materialised by the sum pass
+    // (materialize_sum, variants.cpp:53-96); shorter ones are summed in the mm
+    // kernel's registers (pack_a_sum / pack_b_sum, blocking.cpp:12-66).  Naive and
+    // C materialise every multi-term side; ABC and AB fuse sides of up to
+    // e.fuse_max_terms terms.  Both forms add the terms in listed order with the
+    // same roundings, so the choice never changes a bit of the result.
+    const int mat_min = (variant == STRASSEN_C || variant == STRASSEN_NAIVE) ? 2
+                        : (variant == STRASSEN_DGEMM)                        ? kMaxTerms + 1
+                                                                             : e.fuse_max_terms + 1;
+    auto fused_terms = [&](size_t t) { return t >= static_cast<size_t>(mat_min) ? size_t{1} : t; };
     const int nprod_all = static_cast<int>(live.size());
     double terms_all = 0.0;
     for (const Live& l : live)
-        terms_all += (variant == STRASSEN_C || variant == STRASSEN_NAIVE)
-                         ? 1.0 : 0.5 * static_cast<double>(l.a.size() + l.b.size());
+        terms_all += 0.5 * static_cast<double>(fused_terms(l.a.size()) + fused_terms(l.b.size()));
     terms_all /= std::max(1, nprod_all);
     auto run_program = [&](std::vector<Live> live, MMParams P) -> long {
         // Windows (r, c) in row-major order; without `win` one window covers all.
@@ -916,7 +960,10 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
             return launches;
         }
 
-        const bool sums = variant == STRASSEN_C || variant == STRASSEN_NAIVE;
+        bool sums = false;
+        for (const Live& l : live)
+            sums = sums || l.a.size() >= static_cast<size_t>(mat_min) ||
+                   l.b.size() >= static_cast<size_t>(mat_min);
         std::unique_ptr<SumBatchParams> side_sums[2];
         if (sums) {
             // Every multi-term operand sum materialised by one HBM pass per side
@@ -928,8 +975,8 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
             const long long lda_t = ((qm + 3) / 4) * 4, ldb_t = ((qk + 3) / 4) * 4;
             int na_sums = 0, nb_sums = 0;
             for (const Live& l : live) {
-                na_sums += l.a.size() > 1;
-                nb_sums += l.b.size() > 1;
+                na_sums += l.a.size() >= static_cast<size_t>(mat_min);
+                nb_sums += l.b.size() >= static_cast<size_t>(mat_min);
             }
             double* TA = e.ensure(e.tabuf, static_cast<size_t>(std::max(na_sums, 1)) * lda_t * qk * 8);
             double* TB = e.ensure(e.tbbuf, static_cast<size_t>(std::max(nb_sums, 1)) * ldb_t * qn * 8);
@@ -944,7 +991,8 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
                 SB->ld = sd == 0 ? lda_t : ldb_t;
                 for (size_t p = 0; p < live.size(); ++p) {
                     Terms& terms = sd == 0 ? live[p].a : live[p].b;
-                    if (terms.size() <= 1) continue;  // single term: the quadrant map, sign in-kernel
+                    // fused in the kernel: the quadrant maps, signs in-kernel
+                    if (terms.size() < static_cast<size_t>(mat_min)) continue;
                     const int z = SB->njobs++;
                     double* dst = (sd == 0 ? TA : TB) + static_cast<size_t>(z) * SB->ld * SB->cols;
                     SB->dst[z] = dst;
@@ -1037,7 +1085,12 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
         join();
         return launches;
     };
-    const bool sums_v = variant == STRASSEN_C || variant == STRASSEN_NAIVE;
+    int n_as = 0, n_bs = 0;
+    for (const Live& l : live) {
+        n_as += l.a.size() >= static_cast<size_t>(mat_min);
+        n_bs += l.b.size() >= static_cast<size_t>(mat_min);
+    }
+    const bool sums_v = n_as + n_bs > 0;
     const bool store_v = variant == STRASSEN_NAIVE || variant == STRASSEN_AB;
     const double a_sum = 8.0 * (((qm + 3) / 4) * 4) * qk, b_sum = 8.0 * (((qk + 3) / 4) * 4) * qn;
     const double m_tmp = 8.0 * ((qm + 1) / 2 * 2) * qn;
@@ -1045,11 +1098,6 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
     // single-term side counts as a sum too)
     auto need = [&](size_t) { return (sums_v ? a_sum + b_sum : 0.0) + (store_v ? m_tmp : 0.0); };
     // the one-shot program's buffers against what the ctx already holds
-    int n_as = 0, n_bs = 0;
-    for (const Live& l : live) {
-        n_as += l.a.size() > 1;
-        n_bs += l.b.size() > 1;
-    }
     const double need_a = sums_v ? std::max(n_as, 1) * a_sum : 0.0;
     const double need_b = sums_v ? std::max(n_bs, 1) * b_sum : 0.0;
     const double need_m = store_v ? static_cast<double>(live.size()) * m_tmp : 0.0;

@@ -41,9 +41,19 @@ struct Engine {
     DeviceBuffer pack_a, pack_b;              // TMA layout normalisation
     DeviceBuffer mbuf, tabuf, tbbuf;          // AB / Naive temporaries
     DeviceBuffer ticket_buf;                  // ordered fused-epilogue tickets
+    DeviceBuffer unit_ctr_buf;                // persistent launches' unit counters
+    int unit_ctr_next = 0;                    // next counter (reset per call)
+    // recorded on the call stream at the end of every call; the next call's stream
+    // waits on it first, so a call on another stream cannot overwrite workspace
+    // (sums, partials, tickets) that kernels of the previous call still read
+    cudaEvent_t ev_last = nullptr;
+    bool ev_last_recorded = false;
     // level 3 (B200 extension, strassen_ctx_set_max_level): the outer level's
     // layout normalisation, materialised operands and products (run_outer)
     DeviceBuffer pack_a3, pack_b3, l3_a, l3_b, l3_m;
+    // ABC / AB: operand sides of up to this many terms are summed in the mm kernel,
+    // longer ones materialised by the sum pass (run_strassen; 4 = fully fused)
+    int fuse_max_terms = 2;  // strassen_ctx_set_fused_terms
     int max_level = 2;  // strassen_ctx_set_max_level: 3 admits Naive / C at level 3
     // strassen_ctx_set_operand_events: events the next call's kernels wait on right
     // before first reading A / B / C (device operands), then cleared

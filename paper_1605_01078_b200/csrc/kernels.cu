@@ -21,6 +21,7 @@
 // Why DMMA, and why the sums sit in the DMMA warps' own instruction stream:
 // DESIGN.md section 3 (profiles/r01_fp64_peak.log: DMMA 37.1 TF/s vs DFMA 34.2;
 // DADDs issued by other warps starve while DMMA saturates the FP64 pipe).
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 
@@ -645,6 +646,11 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     uint8_t* raw = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* raw_full = reinterpret_cast<uint64_t*>(raw + RING * kSlotBytes);
     uint64_t* raw_empty = raw_full + RING;
+    // dynamic unit hand-out (persistent launches): the TMA lane takes the next unit
+    // from P.unit_counter and passes it to the DMMA warps through a small queue
+    uint64_t* q_full = raw_empty + RING;
+    uint64_t* q_empty = q_full + kUnitQueue;
+    int* q_unit = reinterpret_cast<int*>(q_empty + kUnitQueue);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -653,23 +659,58 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     // which runs at the register limit, free of the loop state)
     const int n_units = PERSIST ? unit_count(P) : static_cast<int>(blockIdx.x) + 1;
     const bool persistent = PERSIST && static_cast<int>(gridDim.x) < n_units;
+    const bool dyn = persistent && P.unit_counter != nullptr && !P.streamk;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < RING; ++s) {
             mbar_init(&raw_full[s], 1);
             mbar_init(&raw_empty[s], kConsumerWarps);
         }
+        for (int s = 0; s < kUnitQueue; ++s) {
+            mbar_init(&q_full[s], 1);
+            mbar_init(&q_empty[s], kConsumerWarps);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
     }
     __syncthreads();
+    // Unit sequence of this CTA: blockIdx.x first; then either a fixed stride of
+    // gridDim.x, or (dyn) units taken from the global counter, in increasing order
+    // across the grid.  The producer takes a unit when it starts streaming its tiles
+    // and queues it for the DMMA warps, which take it when they finish the previous
+    // one; an index >= n_units ends both loops.
+    uint32_t qslot = 0, qphase = 0;
+    auto producer_next = [&](int unit) -> int {
+        if (!dyn) return unit + (PERSIST ? static_cast<int>(gridDim.x) : 1);
+        const int nxt = static_cast<int>(gridDim.x) + atomicAdd(P.unit_counter, 1);
+        mbar_wait(&q_empty[qslot], qphase ^ 1);
+        *reinterpret_cast<volatile int*>(&q_unit[qslot]) = nxt;
+        mbar_arrive(&q_full[qslot]);  // release: the DMMA warps' wait acquires the write
+        if (++qslot == kUnitQueue) {
+            qslot = 0;
+            qphase ^= 1;
+        }
+        return nxt;
+    };
+    auto consumer_next = [&](int unit) -> int {
+        if (!dyn) return unit + (PERSIST ? static_cast<int>(gridDim.x) : 1);
+        mbar_wait(&q_full[qslot], qphase);
+        const int nxt = *reinterpret_cast<volatile int*>(&q_unit[qslot]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&q_empty[qslot]);
+        if (++qslot == kUnitQueue) {
+            qslot = 0;
+            qphase ^= 1;
+        }
+        return nxt;
+    };
 
     if (warp >= kConsumerWarps) {
         // ================= TMA warpgroup (warps 8-11; one lane issues) =======
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
         if (warp != kConsumerWarps || lane != 0) return;
         uint32_t s = 0, phase = 0;
-        for (int unit = blockIdx.x; unit < n_units; unit += PERSIST ? gridDim.x : 1) {
+        for (int unit = blockIdx.x; unit < n_units; unit = producer_next(unit)) {
         const Unit U = decode_unit(P, unit);
         const int m0 = U.tm * kBM, n0 = U.tn * kBN;
         const int kt_lo = U.kt_lo, kt_hi = U.kt_hi;
@@ -758,7 +799,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         pend = false;
     };
 
-    for (int unit = blockIdx.x; unit < n_units; unit += PERSIST ? gridDim.x : 1) {
+    for (int unit = blockIdx.x; unit < n_units; unit = consumer_next(unit)) {
     const Unit U = decode_unit(P, unit);
     const int tm = U.tm, tn = U.tn, p_lo = U.p_lo, p_hi = U.p_hi;
     const int kt_lo = U.kt_lo, kt_hi = U.kt_hi;
@@ -1584,12 +1625,16 @@ __global__ void scale_kernel(double* c, long rows, long cols, long long rs, long
 template <int MAXT, bool PERSIST, int RING = kRawSlots>
 static cudaError_t launch_mm_t(const MMParams& p, cudaStream_t s) {
     constexpr int smem = RING == kRawSlots ? kMMSmemBytes : kMMSepSmemBytes;
-    static bool attr_set = false;
-    if (!attr_set) {
+    // the > 48 KB dynamic shared-memory opt-in is per device context: once per device
+    static std::atomic<uint64_t> attr_set{0};
+    int dev = 0;
+    if (cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(attr_set.load(std::memory_order_acquire) & bit)) {
         cudaError_t e = cudaFuncSetAttribute(mm_kernel<MAXT, PERSIST, RING>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attr_set.fetch_or(bit, std::memory_order_release);
     }
     const int units = p.tiles_m * p.tiles_n * (p.split ? p.nprod * p.ksplit : 1);
     const int grid = PERSIST && p.grid_cap > 0 && p.grid_cap < units ? p.grid_cap : units;

@@ -27,7 +27,8 @@ constexpr int kConsumerRegs = 240;
 // warpgroup's release, or setmaxnreg.inc waits forever.
 static_assert(kProducerRegs * 128 + kConsumerRegs * kConsumerWarps * 32 <= kThreads * 168,
               "setmaxnreg split exceeds the CTA register allocation");
-constexpr int kMMSmemBytes = kRawSlots * kSlotBytes + 1024 + 256;
+// ring + alignment slack (up to 1023 bytes) + ring and unit-queue barriers
+constexpr int kMMSmemBytes = kRawSlots * kSlotBytes + 1024 + 512;
 static_assert(kMMSmemBytes <= 227 * 1024, "shared memory budget");
 // persistent single-term launches with the deferred bulk epilogue: a 5-slot
 // ring (2.5 k-steps of (1, 1) products ahead) and a separate 130 KB stage of
@@ -38,7 +39,12 @@ constexpr int kSepRing = 5;
 constexpr int kStageBytes = kBM * kBN * 8;
 constexpr int kMMSepSmemBytes = kSepRing * kSlotBytes + 1024 + 1024 + kStageBytes;
 static_assert(kMMSepSmemBytes <= 227 * 1024, "shared memory budget (separate stage)");
-static_assert(2 * kSepRing * 8 <= 1024, "ring barriers fit before the stage");
+// dynamic unit hand-out queue (MMParams::unit_counter): depth, after the ring barriers
+constexpr int kUnitQueue = 4;
+static_assert(2 * kSepRing * 8 + 2 * kUnitQueue * 8 + kUnitQueue * 4 <= 1024,
+              "ring and queue barriers fit before the stage");
+static_assert(2 * kRawSlots * 8 + 2 * kUnitQueue * 8 + kUnitQueue * 4 <= 1024,
+              "ring and queue barriers fit in the reserved kilobyte");
 
 // One Strassen product M_p = (sum_u as_u A_{aq_u}) (sum_u bs_u B_{bq_u});
 // destinations C_{cq_u} += alpha * cs_u * M_p.
@@ -122,6 +128,12 @@ struct alignas(64) MMParams {
     // A-heavy products (more A than B terms) in one-CTA-per-unit launches run the
     // 4 x 2 warp layout (kernels.cu product_kloop1)
     int a_heavy_layout;
+    // persistent launches (not stream-K): units beyond the first wave are handed out
+    // by this counter (zeroed before the launch), so a CTA that starts late -- an SM
+    // held by another kernel, e.g. a co-scheduled NCCL broadcast -- simply takes fewer
+    // units instead of delaying a fixed list; units are still taken in increasing
+    // order, so ticket waits (which point at smaller units) cannot deadlock
+    int* unit_counter;
 };
 
 cudaError_t launch_mm(const MMParams& p, cudaStream_t s);
