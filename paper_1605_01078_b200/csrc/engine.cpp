@@ -489,13 +489,23 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
         // each unit's reductions one unit later (kernels.cu mm_kernel, RING <
         // kRawSlots); fused-sum programs stay one CTA per unit
         const bool bulk_units = P.c_tma && P.ktiles <= P.bulk_max_kt;
-        bool single = true;
-        for (int p = 0; p < P.nprod; ++p) single = single && P.prod[p].na == 1 && P.prod[p].nb == 1;
+        int maxt = 1;
+        for (int p = 0; p < P.nprod; ++p) maxt = std::max({maxt, int{P.prod[p].na}, int{P.prod[p].nb}});
         static const bool sep_on = [] {
             const char* v = std::getenv("STRASSEN_B200_SEP");  // 0 / 1 (experiments)
             return v ? std::atoi(v) != 0 : true;
         }();
-        P.sep_stage = bulk_units && single && sep_on ? 1 : 0;
+        // fused sums of <= 2 terms: persistent with the separate stage beside a 6-slot
+        // ring only for short products, where the exposed per-unit epilogue outweighs
+        // the shallower ring (profiles/r02_sep2_{0,1}.log: 32768^2 x 1024 ABC L2
+        // 69.6 -> 64.4 ms, 16384^2 x 256 10.0 -> 8.9; but 16384^3 ABC L1 227 -> 261
+        // and 32768^2 x 1024 ABC L1, 32 k-tiles, 64.9 -> 69.0)
+        static const int sep2_kt = [] {
+            const char* v = std::getenv("STRASSEN_B200_SEP2_KT");  // k-tiles (experiments)
+            return v ? std::atoi(v) : 24;
+        }();
+        P.sep_stage = bulk_units && sep_on && (maxt == 1 || (maxt == 2 && P.ktiles <= sep2_kt))
+                          ? 1 : 0;
         // deferred collection: the next product of a tile is tiles-in-launch units
         // later; defer only when that is >= one grid width (small host-call windows
         // would otherwise chain each tile's products one unit apart: C L2 e2e 1437 ms

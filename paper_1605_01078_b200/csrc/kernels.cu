@@ -363,6 +363,22 @@ __device__ __forceinline__ void half_release(uint64_t* raw_empty, const HalfStep
     }
 }
 
+// Hand the N ring slots from slot0 on back to the producer (predicated arrive: no
+// branch).  Called right after the k-step's LAST fragment loads, before the DMMAs that
+// consume them, so the refill of these slots overlaps the step's second half; the
+// fence orders this warp's LDS before the async-proxy (TMA) writes that follow.
+template <int N, int RING>
+__device__ __forceinline__ void release_slots(uint64_t* raw_empty, uint32_t slot0, int lane) {
+    consumer_fence();
+    __syncwarp();
+    uint32_t s2 = slot0;
+#pragma unroll
+    for (int u = 0; u < N; ++u) {
+        mbar_arrive_if(&raw_empty[s2], lane == 0);
+        s2 = (s2 + 1 == RING) ? 0 : s2 + 1;
+    }
+}
+
 // One product's k-loop over half tiles: two 8-k steps per 16-k tile (both
 // waits first, then one straight-line block that returns the first step's
 // slots as soon as it is done).  kt_lo / kt_hi count 16-k tiles.
@@ -441,18 +457,9 @@ __device__ __forceinline__ void product_kloop(const uint8_t* raw, uint64_t* raw_
             for (int u = 1; u < NA; ++u) frag_a_term<false>(sA[u], sp, wm, g, j, ca[u], f);
 #pragma unroll
             for (int u = 1; u < NB; ++u) frag_b_term<false>(sB[u], sp, wn, g, j, cb[u], f);
+            if (sp == 1) release_slots<NA + NB, RING>(raw_empty, slot0, lane);
             dmma_substep(f, 0, acc);
             dmma_substep(f, 1, acc);
-        }
-        consumer_fence();
-        __syncwarp();
-        if (lane == 0) {
-            uint32_t s2 = slot0;
-#pragma unroll
-            for (int u = 0; u < NA + NB; ++u) {
-                mbar_arrive(&raw_empty[s2]);
-                if (++s2 == RING) s2 = 0;
-            }
         }
     }
 }
@@ -496,18 +503,9 @@ __device__ __forceinline__ void product_kloop1(const uint8_t* raw, uint64_t* raw
             for (int u = 1; u < NA; ++u) frag_a_term1<false>(sA[u], sp, wm1, g, j, ca[u], f);
 #pragma unroll
             for (int u = 1; u < NB; ++u) frag_b_term1<false>(sB[u], sp, wn1, g, j, cb[u], f);
+            if (sp == 1) release_slots<NA + NB, RING>(raw_empty, slot0, lane);
             dmma_substep1(f, 0, acc);
             dmma_substep1(f, 1, acc);
-        }
-        consumer_fence();
-        __syncwarp();
-        if (lane == 0) {
-            uint32_t s2 = slot0;
-#pragma unroll
-            for (int u = 0; u < NA + NB; ++u) {
-                mbar_arrive(&raw_empty[s2]);
-                if (++s2 == RING) s2 = 0;
-            }
         }
     }
 }
@@ -1624,7 +1622,7 @@ __global__ void scale_kernel(double* c, long rows, long cols, long long rs, long
 
 template <int MAXT, bool PERSIST, int RING = kRawSlots>
 static cudaError_t launch_mm_t(const MMParams& p, cudaStream_t s) {
-    constexpr int smem = RING == kRawSlots ? kMMSmemBytes : kMMSepSmemBytes;
+    constexpr int smem = RING == kRawSlots ? kMMSmemBytes : mm_sep_smem_bytes(RING);
     // the > 48 KB dynamic shared-memory opt-in is per device context: once per device
     static std::atomic<uint64_t> attr_set{0};
     int dev = 0;
@@ -1654,6 +1652,8 @@ cudaError_t launch_mm(const MMParams& p, cudaStream_t s) {
     // count and dynamic dispatch balances them better (ABC L1 233.8 vs 236.5 ms).
     if (maxt == 1 && p.grid_cap > 0 && p.sep_stage)  // persistent, deferred bulk epilogue
         return launch_mm_t<1, true, kSepRing>(p, s);
+    if (maxt == 2 && p.grid_cap > 0 && p.sep_stage)  // the same with 2-term fused sums
+        return launch_mm_t<2, true, kSepRing2>(p, s);
     if (maxt == 1)  // single-term programs: no sum code at all
         return p.grid_cap > 0 ? launch_mm_t<1, true>(p, s) : launch_mm_t<1, false>(p, s);
     return maxt <= 2 ? launch_mm_t<2, false>(p, s) : launch_mm_t<kMaxTerms, false>(p, s);

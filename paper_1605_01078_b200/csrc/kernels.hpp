@@ -34,11 +34,16 @@ static_assert(kMMSmemBytes <= 227 * 1024, "shared memory budget");
 // ring (2.5 k-steps of (1, 1) products ahead) and a separate 130 KB stage of
 // one C tile (128 columns x 1040 B: the 16-byte skew spreads banks)
 constexpr int kSepRing = 5;
+// the same for fused-sum programs of at most 2 + 2 terms (4 term tiles per k-step):
+// 6 slots, the most that fit beside the stage
+constexpr int kSepRing2 = 6;
+constexpr int mm_sep_smem_bytes(int ring) { return ring * kSlotBytes + 1024 + 1024 + kBM * kBN * 8; }
 // (the stage holds one C tile as 8 swizzled boxes of 16 rows x 128 columns,
 // 1024-byte aligned after the ring's barriers)
 constexpr int kStageBytes = kBM * kBN * 8;
 constexpr int kMMSepSmemBytes = kSepRing * kSlotBytes + 1024 + 1024 + kStageBytes;
 static_assert(kMMSepSmemBytes <= 227 * 1024, "shared memory budget (separate stage)");
+static_assert(mm_sep_smem_bytes(kSepRing2) <= 227 * 1024, "shared memory budget (fused, separate stage)");
 // dynamic unit hand-out queue (MMParams::unit_counter): depth, after the ring barriers
 constexpr int kUnitQueue = 4;
 static_assert(2 * kSepRing * 8 + 2 * kUnitQueue * 8 + kUnitQueue * 4 <= 1024,

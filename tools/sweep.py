@@ -1,8 +1,16 @@
 """BASELINE.json sweeps on one B200, CSV in the reference bench schema
 (tools/bench_lib.cpp:138-157: m,n,k,variant,level,threads,reps,time_s,
 egf_measured,egf_modeled,rel_err) plus the executed-flop fraction of the
-measured DMMA peak.  rel_err is a Freivalds estimate
-||C x - C0 x - A(B x)|| / (||A||_F ||B||_F ||x||) of the Strassen result.
+measured DMMA peak.  With the reference's semantics:
+  egf_modeled  2mnk / the reference's analytical model time (strassen_model_predict
+               with its default blocking and Ivy Bridge parameters, bench_lib.cpp:
+               80-96); empty for the B200-only configurations (C variant, level 3),
+               whose B200 cost-model figure is in egf_modeled_b200
+  rel_err      rel_frobenius (strassen_rel_error) against the reference's oracle
+               choice (bench_lib.cpp:208-221): strassen_reference_gemm when
+               max(m, n, k) <= 1200, else this library's STRASSEN_DGEMM on the same
+               inputs
+  freivalds    ||C x - C0 x - A(B x)|| / (||A||_F ||B||_F ||x||), size independent
 
 usage: python tools/sweep.py square|rankk|fixedk out.csv [reps]
 """
@@ -65,6 +73,16 @@ def main():
         x = torch.rand(n, 1, dtype=torch.float64, device="cuda", generator=g)
         want = C0 @ x + A @ (B @ x)
         den = (torch.linalg.norm(A) * torch.linalg.norm(B) * torch.linalg.norm(x)).item()
+        # the reference bench's oracle (bench_lib.cpp:208-221)
+        if max(m, n, k) <= 1200:
+            ref_h = C0.cpu().numpy().copy(order="F")
+            S.reference_gemm(1.0, A.cpu().numpy(), B.cpu().numpy(), ref_h)
+            C_ref = torch.from_numpy(ref_h).cuda()
+        else:
+            C_ref = C0.clone().t().contiguous().t()
+            ctx.gemm_device("dgemm", 0, 1.0, A, B, C_ref)
+            torch.cuda.synchronize()
+        ref_norm = max(torch.linalg.norm(C_ref).item(), 1.0)
         extra = L3 if family == "square" and min(m, n, k) >= 4096 else []
         for v, L in variants(family) + extra:
             best = None
@@ -84,17 +102,25 @@ def main():
                 t = e0.elapsed_time(e1) * 1e-3
                 if r > 0:
                     best = t if best is None else min(best, t)
-            err = (torch.linalg.norm(C @ x - want).item()) / den
+            fv = (torch.linalg.norm(C @ x - want).item()) / den
+            err = torch.linalg.norm(C - C_ref).item() / ref_norm  # strassen_rel_error
             egf = 2.0 * m * n * k / best * 1e-9
+            egf_model = ""
+            if v != "c" and L <= 2:
+                bd, _ = S.model_predict(v, L, m, n, k)
+                egf_model = 2.0 * m * n * k / bd["total"] * 1e-9
+            egf_b200 = 2.0 * m * n * k / S.predict_b200(v, L, m, n, k) * 1e-9
             s = 1 << L
             qm, qn, qk = -(-m // s), -(-n // s), -(-k // s)
             mul, aa, ba, cu = table(L)
             fexec = mul * 2.0 * qm * qn * qk if L else 2.0 * m * n * k
             rows.append(dict(m=m, n=n, k=k, variant=v, level=L, threads=1, reps=n_rep, time_s=best,
-                             egf_measured=egf, egf_modeled="", rel_err=err,
+                             egf_measured=egf, egf_modeled=egf_model, rel_err=err,
+                             freivalds=fv, egf_modeled_b200=egf_b200,
                              exec_frac_of_dmma_peak=fexec / best / 1e12 / PEAK))
-            print(f"{m}x{n}x{k} {v}{L}: {egf / 1e3:.2f} TF/s err {err:.1e}", flush=True)
-        del A, B, C0, C
+            print(f"{m}x{n}x{k} {v}{L}: {egf / 1e3:.2f} TF/s rel_err {err:.1e} "
+                  f"freivalds {fv:.1e}", flush=True)
+        del A, B, C0, C, C_ref
     with open(out, "w", newline="") as f:
         w = csv.DictWriter(f, fieldnames=list(rows[0].keys()))
         w.writeheader()
