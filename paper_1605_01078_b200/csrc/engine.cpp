@@ -326,7 +326,9 @@ int* next_unit_counter(Engine& e, cudaStream_t s) {
 // applied in table order).
 struct FusedPlan {
     bool split = false;
-    bool streamk = false;    // single product, split mode: stream-K pieces (kernels.cu)
+    bool streamk = false;    // split mode: stream-K pieces (kernels.cu)
+    bool sk_store = false;   // stream-K of a store-mode program: M_p fixed up in-kernel
+    long long part_off = 0;  // partial slots' offset from M (sk_store)
     int sk_len = 0, sk_maxp = 0, sk_grid = 0;
     bool fixup = false;      // split mode finished in the epilogue (no stream pass)
     int* arrive = nullptr;   // per (tile, product) chunk-arrival counters
@@ -341,7 +343,7 @@ struct FusedPlan {
 // count (a product group of a larger program plans like the whole program, so
 // its k-chunks -- and results -- are the same); 0 = P's own.
 FusedPlan plan_fused(Engine& e, cudaStream_t s, const MMParams& P, bool force_split,
-                     int nprod_plan = 0, double terms_plan = 0.0) {
+                     int nprod_plan = 0, double terms_plan = 0.0, bool windowed = false) {
     FusedPlan F;
     const int ntiles = P.tiles_m * P.tiles_n;
     const int sms = e.num_sms > 0 ? e.num_sms : 148;
@@ -372,13 +374,11 @@ FusedPlan plan_fused(Engine& e, cudaStream_t s, const MMParams& P, bool force_sp
             ticketed = P.nprod > 1 && std::strcmp(m, "ticket") == 0 ? true
                        : std::strcmp(m, "owner") == 0             ? false
                                                                    : ticketed;
-        if (ticketed) {
+        if (ticketed) {  // one ticket per C tile
+            const size_t nt = static_cast<size_t>(P.tiles_m) * P.tiles_n;
             F.ticket_ld = P.tiles_n;
-            F.tickets = reinterpret_cast<int*>(
-                e.ensure(e.ticket_buf, static_cast<size_t>(P.tiles_m) * P.tiles_n * sizeof(int)));
-            ck(cudaMemsetAsync(F.tickets, 0, static_cast<size_t>(P.tiles_m) * P.tiles_n * sizeof(int),
-                               s),
-               "ticket reset");
+            F.tickets = reinterpret_cast<int*>(e.ensure(e.ticket_buf, nt * sizeof(int)));
+            ck(cudaMemsetAsync(F.tickets, 0, nt * sizeof(int), s), "ticket reset");
         }
         return F;
     }
@@ -423,6 +423,42 @@ FusedPlan plan_fused(Engine& e, cudaStream_t s, const MMParams& P, bool force_sp
         const double t_sk = static_cast<double>(len) * t_k + t_cta + 15e-6;
         if (t_sk < 0.97 * t_uni) F.streamk = true;
     }
+    // (under 4 waves of (tile, product) units only: the host pipeline windows AB /
+    // Naive calls from 4 waves up, and a window cannot run the whole call's pieces)
+    if ((force_split || np > 1) && streamk_on && !windowed && np == P.nprod &&
+        static_cast<long>(ntiles) * np < 4L * sms) {
+        // Stream-K for store-mode programs (few tiles, products into temporaries,
+        // then the stream pass): the flattened (product, tile, k-step) space cut into
+        // equal ranges, one per persistent CTA; the last piece of a (tile, product)
+        // sums the pieces in k order and stores M_p.  Uniform k-chunks of 7^L x tiles
+        // CTAs quantise to whole waves (1024^3 ABC L1: 112 CTAs of 32 k-steps on 148
+        // SMs).  Fused sums lengthen a k-step (term_factor as choose_ksplit).
+        const long total = static_cast<long>(ntiles) * np * P.ktiles;
+        const long want = std::max(1L, std::min<long>(sms, total / 8));
+        const long len = ceil_div(total, want);
+        const double t_k = 2.1e-6 * (1.0 + 0.15 * (terms - 1.0)), t_cta = 3e-6;
+        const double t_uni = std::ceil(static_cast<double>(ntiles) * np * ks / sms) *
+                             (static_cast<double>(per) * t_k + t_cta);
+        // a CTA's range spans len / K + 1 pieces, each with its prologue and epilogue
+        const double t_sk = static_cast<double>(len) * t_k +
+                            std::ceil(static_cast<double>(len) / P.ktiles + 1.0) * t_cta +
+                            6e-6;  // + the fixup's partial round trip
+        if (t_sk < 0.97 * t_uni) {
+            F.streamk = F.sk_store = true;
+            F.sk_len = static_cast<int>(len);
+            F.sk_grid = static_cast<int>(ceil_div(total, len));
+            F.sk_maxp = static_cast<int>(ceil_div(len, P.ktiles) + 1);
+            F.ksplit = static_cast<int>(ceil_div(P.ktiles, len) + 1);  // partial slots
+            F.per = P.ktiles;
+            F.part_off = static_cast<long long>(P.nprod) * F.mstride;
+            F.M = e.ensure(e.mbuf, static_cast<size_t>(F.mstride) * P.nprod * (1 + F.ksplit) * 8);
+            const size_t na = static_cast<size_t>(P.tiles_m) * P.tiles_n * P.nprod;
+            F.arrive = reinterpret_cast<int*>(e.ensure(e.ticket_buf, na * sizeof(int)));
+            ck(cudaMemsetAsync(F.arrive, 0, na * sizeof(int), s), "arrive reset");
+            F.ticket_ld = P.tiles_n;
+            return F;
+        }
+    }
     if (F.streamk) {
         const long total = static_cast<long>(ntiles) * P.ktiles;
         const long len = ceil_div(total, std::max(1L, std::min<long>(sms, total / 8)));
@@ -434,11 +470,11 @@ FusedPlan plan_fused(Engine& e, cudaStream_t s, const MMParams& P, bool force_sp
         F.M = e.ensure(e.mbuf, static_cast<size_t>(F.mstride) * F.ksplit * 8);
     }
     if (!force_split && fixup_on && np == 1) {
+        // per-tile tickets, then per-(tile, product) arrival counters
         const size_t nt = static_cast<size_t>(P.tiles_m) * P.tiles_n;
-        int* buf = reinterpret_cast<int*>(
-            e.ensure(e.ticket_buf, nt * (1 + static_cast<size_t>(P.nprod)) * sizeof(int)));
-        ck(cudaMemsetAsync(buf, 0, nt * (1 + static_cast<size_t>(P.nprod)) * sizeof(int), s),
-           "ticket reset");
+        const size_t words = nt * (1 + static_cast<size_t>(P.nprod));
+        int* buf = reinterpret_cast<int*>(e.ensure(e.ticket_buf, words * sizeof(int)));
+        ck(cudaMemsetAsync(buf, 0, words * sizeof(int), s), "ticket reset");
         F.fixup = true;
         F.tickets = buf;
         F.arrive = buf + nt;
@@ -480,9 +516,29 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
             P.ticket_ld = F.ticket_ld;
             static const int group_env = [] {
                 const char* v = std::getenv("STRASSEN_B200_UNIT_GROUP");  // tiles (experiments)
-                return v ? std::atoi(v) : 0;
+                return v ? std::atoi(v) : 0;  // off: measured slower (r02_shortk_group.log)
             }();
-            P.unit_group = group_env;
+            static const int group_kt = [] {
+                const char* v = std::getenv("STRASSEN_B200_GROUP_KT");  // k-tiles (experiments)
+                return v ? std::atoi(v) : 64;
+            }();
+            // Experiment (STRASSEN_B200_UNIT_GROUP=-1 auto, or G tiles): units in groups
+            // of G tiles, all products of a group before the next, so a group's C
+            // quadrant tiles (G x 4^L x 128 KB, ~48 MB) stay in the 126 MB L2 across
+            // their ordered updates.  Measured far slower for short products
+            // (profiles/r02_shortk_group.log: 16384^2 x 256 ABC L2 9.1 -> 17.3 ms,
+            // 32768^2 x 1024 66.6 -> 93.1 ms): the updates of the in-flight products
+            // concentrate on a few quadrant tiles and their ordered reduce-adds
+            // serialise (also tried with per-(tile, quadrant) tickets).
+            long g = 0;
+            if (group_env >= 0) {
+                g = group_env;
+            } else if (P.ktiles <= group_kt) {
+                const long quads = static_cast<long>(cq.size());
+                g = std::max(1L, (48L << 20) / (quads * kBM * kBN * 8));
+            }
+            const long launch_tiles = static_cast<long>(P.tiles_m) * P.tiles_n;
+            P.unit_group = g > 0 && g < launch_tiles ? static_cast<int>(g) : 0;
         }
         // bulk-reduction epilogue (C through its quadrant tensor maps); single-term
         // programs (C, DGEMM) then run persistent with a separate stage, collecting
@@ -516,8 +572,11 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
             const char* v = std::getenv("STRASSEN_B200_DEFER_WAVES");  // experiments
             return v ? std::atof(v) : 1.0;
         }();
-        P.sep_defer = (!F.tickets || static_cast<double>(launch_tiles) >=
-                                         defer_waves * (e.num_sms > 0 ? e.num_sms : 148))
+        // (grouped units: a quadrant's next update is a few products x G units later,
+        // usually already running -- collect at once)
+        P.sep_defer = (!F.tickets || (P.unit_group == 0 &&
+                                      static_cast<double>(launch_tiles) >=
+                                          defer_waves * (e.num_sms > 0 ? e.num_sms : 148)))
                           ? 1 : 0;
         P.grid_cap = cap(bulk_units && !P.sep_stage);
         if (P.grid_cap > 0) P.unit_counter = next_unit_counter(e, s);
@@ -560,7 +619,18 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
     P.ldm = F.ldm;
     P.mstride = F.mstride;
     P.grid_cap = cap(false);
-    if (P.grid_cap > 0) P.unit_counter = next_unit_counter(e, s);
+    if (F.sk_store) {  // stream-K pieces; M_p fixed up by the last piece
+        P.streamk = 1;
+        P.sk_store = 1;
+        P.sk_len = F.sk_len;
+        P.sk_maxp = F.sk_maxp;
+        P.grid_cap = F.sk_grid;  // the decode assumes exactly this many CTAs
+        P.part_off = F.part_off;
+        P.arrive = F.arrive;
+        P.ticket_ld = F.ticket_ld;
+    } else if (P.grid_cap > 0) {
+        P.unit_counter = next_unit_counter(e, s);
+    }
     e.prof_begin("mm_kernel", s);
     ck(launch_mm(P, s), "mm_kernel (split)");
     e.prof_end(s);
@@ -571,7 +641,7 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
     S.alpha = alpha;
     S.ldm = F.ldm;
     S.mstride = F.mstride;
-    S.ksplit = F.ksplit;
+    S.ksplit = F.sk_store ? 1 : F.ksplit;
     S.nquad = static_cast<int>(cq.size());
     S.qm = P.qm;
     S.qn = P.qn;
@@ -910,11 +980,14 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
     const int mat_min = (variant == STRASSEN_C || variant == STRASSEN_NAIVE) ? 2
                         : (variant == STRASSEN_DGEMM)                        ? kMaxTerms + 1
                                                                              : e.fuse_max_terms + 1;
-    auto fused_terms = [&](size_t t) { return t >= static_cast<size_t>(mat_min) ? size_t{1} : t; };
+    // The launch plan (k-chunks, stream-K pieces) must not depend on where the sums
+    // are formed, or the fused-term setting would change roundings: it is made for the
+    // variant's own term counts (ABC / AB as fully fused, Naive / C single-term).
+    const bool fusing = variant == STRASSEN_ABC || variant == STRASSEN_AB;
     const int nprod_all = static_cast<int>(live.size());
     double terms_all = 0.0;
     for (const Live& l : live)
-        terms_all += 0.5 * static_cast<double>(fused_terms(l.a.size()) + fused_terms(l.b.size()));
+        terms_all += fusing ? 0.5 * static_cast<double>(l.a.size() + l.b.size()) : 1.0;
     terms_all /= std::max(1, nprod_all);
     auto run_program = [&](std::vector<Live> live, MMParams P) -> long {
         // Windows (r, c) in row-major order; without `win` one window covers all.
@@ -1048,7 +1121,7 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
         // product: balanced waves at every size), then one stream pass
         // (AB: variants.cpp:142-168).
         const bool store_products = variant == STRASSEN_NAIVE || variant == STRASSEN_AB;
-        const FusedPlan F = plan_fused(e, s, P, store_products, nprod_all, terms_all);
+        const FusedPlan F = plan_fused(e, s, P, store_products, nprod_all, terms_all, nw > 1);
         if (nw > 1) {  // the aux stream starts after everything enqueued on s so far
             ck(cudaEventRecord(e.ev_fork, s), "fork");
             ck(cudaStreamWaitEvent(e.aux_stream, e.ev_fork, 0), "fork");

@@ -74,6 +74,28 @@ __device__ __forceinline__ void st_release_gpu(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Tickets of the ordered epilogue (MMParams::tickets): one per C tile, holding the
+// number of products whose updates that tile has received.
+__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int* tile_ticket(const MMParams& P, int tm, int tn) {
+    return P.tickets + tm * P.ticket_ld + tn;
+}
+// Wait until tile (tm, tn) has received the updates of products 0 .. p-1 (one thread):
+// relaxed polling, then one acquire fence.
+__device__ __forceinline__ void wait_ticket(const MMParams& P, int p, int tm, int tn) {
+    const int* t = tile_ticket(P, tm, tn);
+    while (ld_relaxed_gpu(t) != p) __nanosleep(64);
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+// Hand the tile on to product p + 1 (one thread, after p's updates are visible).
+__device__ __forceinline__ void release_ticket(const MMParams& P, int p, int tm, int tn) {
+    st_release_gpu(tile_ticket(P, tm, tn), p + 1);
+}
+
 // Tensor reduce-add smem -> global through a tensor map (f64 add at L2,
 // UTMAREDG.2D.ADD); coordinates {row, column} of the box origin.
 __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, int c0, int c1,
@@ -570,24 +592,27 @@ __device__ __forceinline__ Unit decode_unit(const MMParams& P, int bid) {
     U.piece = 0;
     U.npieces = 1;
     if (P.streamk) {
-        // stream-K (one product): CTA c covers k-steps [c*len, (c+1)*len) of the
-        // flattened (tile, k-step) space; its j-th unit is its piece of tile t0 + j
-        // (an empty unit when the range ends earlier).  Tile t's pieces, in k
-        // order, come from CTAs t*K/len .. ((t+1)*K-1)/len.
+        // stream-K: CTA c covers k-steps [c*len, (c+1)*len) of the flattened
+        // (product, tile, k-step) space (product-major); its j-th unit is its piece
+        // of (tile, product) index tp0 + j (an empty unit when the range ends
+        // earlier).  The pieces of index tp, in k order, come from CTAs
+        // tp*K/len .. ((tp+1)*K-1)/len.
         const int grid = static_cast<int>(gridDim.x);
         const int c = bid % grid, jx = bid / grid;
         const long long K = P.ktiles, len = P.sk_len;
-        const long long total = static_cast<long long>(P.tiles_m) * P.tiles_n * K;
+        const long long ntiles = static_cast<long long>(P.tiles_m) * P.tiles_n;
+        const long long total = ntiles * P.nprod * K;
         const long long lo = c * len, hi = min(lo + len, total);
-        const long long t = lo / K + jx;
-        const long long t_lo = t * K;
-        U.p_lo = 0;
-        U.p_hi = (lo < hi && t_lo < hi) ? 1 : 0;  // empty unit: no product
+        const long long tp = lo / K + jx;
+        const long long t_lo = tp * K;
+        const bool live = lo < hi && t_lo < hi;
+        U.p_lo = live ? static_cast<int>(tp / ntiles) : 0;
+        U.p_hi = live ? U.p_lo + 1 : 0;  // empty unit: no product
         U.kt_lo = static_cast<int>(max(lo, t_lo) - t_lo);
         U.kt_hi = static_cast<int>(min(hi, t_lo + K) - t_lo);
         U.piece = c - static_cast<int>(t_lo / len);
         U.npieces = static_cast<int>((t_lo + K - 1) / len - t_lo / len + 1);
-        bid = U.p_hi ? static_cast<int>(t) : 0;
+        bid = live ? static_cast<int>(tp % ntiles) : 0;
     } else if (P.split && P.unit_group > 0 && P.ksplit == 1) {
         // groups of G tiles, product-major inside: unit (t, p) of group g is
         // g*G*nprod + p*gt + t; the ticket a unit waits for, (t, p-1), always
@@ -784,15 +809,14 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     // SEP: bulk reductions of the previous unit still in flight, and the ticket
     // (and product) to release once they complete
     bool pend = false;
-    int* pend_ticket = nullptr;
-    int pend_p = 0;
-    auto collect = [&]() {  // every warp's reductions performed, then hand the tile on
+    int pend_p = -1, pend_tm = 0, pend_tn = 0;  // pend_p >= 0: tickets to release
+    auto collect = [&]() {  // every warp's reductions performed, then hand the tiles on
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         asm volatile("fence.proxy.async.global;" ::: "memory");
         consumer_bar();  // (also: the stage is free again)
-        if (threadIdx.x == 0 && pend_ticket) {
+        if (threadIdx.x == 0 && pend_p >= 0) {
             __threadfence();
-            st_release_gpu(pend_ticket, pend_p + 1);
+            release_ticket(P, pend_p, pend_tm, pend_tn);
         }
         pend = false;
     };
@@ -964,7 +988,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             // column c at c*128, 16-byte chunk (row%16)/2 ^ c%8) -- conflict-free for
             // the fragment layout (chunk g ^ nperm(2j+e)%8 covers all 8 per quarter-warp)
             uint8_t* stage = SEP ? raw + RING * kSlotBytes + 1024 : raw;
-            int* ticket = P.tickets ? P.tickets + tm * P.ticket_ld + tn : nullptr;
+            const bool ticketed = P.tickets != nullptr;
             bool issued = false;
             if (!SEP) consumer_bar();  // every warp is done reading the ring before it is reused
             for (int pass = 0; pass < 2; ++pass) {  // destinations with coefficient +1, then -1
@@ -988,9 +1012,8 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                                 make_double2(sc * acc[2 * h][nf][e], sc * acc[2 * h + 1][nf][e]);
                         }
                 consumer_fence();  // generic smem writes before the async-proxy reads
-                if (!issued && ticket) {
-                    if (threadIdx.x == 0)
-                        while (ld_acquire_gpu(ticket) != p) __nanosleep(128);
+                if (!issued && ticketed) {
+                    if (threadIdx.x == 0) wait_ticket(P, p, tm, tn);
                     asm volatile("fence.proxy.async.global;" ::: "memory");
                 }
                 consumer_bar();
@@ -1011,27 +1034,30 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             }
             if (SEP && P.sep_defer) {  // completion collected at the next epilogue (or after the loop)
                 pend = true;
-                pend_ticket = ticket;
-                pend_p = p;
+                pend_p = ticketed ? p : -1;
+                pend_tm = tm;
+                pend_tn = tn;
                 continue;
             }
-            // all reductions performed (every warp's), then hand the tile on
+            // all reductions performed (every warp's), then hand the tiles on
             asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
             asm volatile("fence.proxy.async.global;" ::: "memory");
             consumer_bar();
-            if (threadIdx.x == 0 && ticket) {
+            if (threadIdx.x == 0 && ticketed) {
                 __threadfence();
-                st_release_gpu(ticket, p + 1);
+                release_ticket(P, p, tm, tn);
             }
             continue;  // next product (none: single-product CTA)
         }
-        if (P.mode == kEpiRMW && P.arrive && U.npieces > 1) {
-            // ---- k-split fused epilogue: partial out, the last chunk sums ----
-            // (partials in slots p * ksplit + piece; ksplit = slots per product)
+        if (P.arrive && U.npieces > 1) {
+            // ---- k-split / stream-K fixup: partial out, the last piece sums ----
+            // (partials in slots p * ksplit + piece; ksplit = slots per product);
+            // the RMW epilogue or (sk_store) the store of M_p follows
             const int s_idx = U.piece;
             const long long ldm = P.ldm;
             {
-                double* Mo = P.mbase + static_cast<long long>(p * P.ksplit + s_idx) * P.mstride;
+                double* Mo = P.mbase + P.part_off +
+                             static_cast<long long>(p * P.ksplit + s_idx) * P.mstride;
 #pragma unroll
                 for (int nf = 0; nf < 4; ++nf)
 #pragma unroll
@@ -1058,7 +1084,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             __threadfence();
             // M_p = P_0 + P_1 + ... in s order (the stream pass's order), read
             // back from L2 (this CTA's own partial included)
-            const double* Mp = P.mbase + static_cast<long long>(p * P.ksplit) * P.mstride;
+            const double* Mp = P.mbase + P.part_off + static_cast<long long>(p * P.ksplit) * P.mstride;
             for (int sp = 0; sp < U.npieces; ++sp) {
 #pragma unroll
                 for (int nf = 0; nf < 4; ++nf)
@@ -1083,11 +1109,9 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                         }
             }
         }
-        int* ticket = nullptr;  // ordered epilogue: wait for the previous product
-        if (P.mode == kEpiRMW && P.tickets) {
-            ticket = P.tickets + tm * P.ticket_ld + tn;
-            if (threadIdx.x == 0)
-                while (ld_acquire_gpu(ticket) != p) __nanosleep(128);
+        const bool ticketed = P.mode == kEpiRMW && P.tickets;  // ordered epilogue
+        if (ticketed) {
+            if (threadIdx.x == 0) wait_ticket(P, p, tm, tn);
             consumer_bar();
         }
         if (P.mode == kEpiRMW) {
@@ -1162,13 +1186,13 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                         }
                 }
             }
-            if (ticket) {  // every thread's C stores visible, then hand the tile on
+            if (ticketed) {  // every thread's C stores visible, then hand the tiles on
                 __threadfence();
                 consumer_bar();
-                if (threadIdx.x == 0) st_release_gpu(ticket, p + 1);
+                if (threadIdx.x == 0) release_ticket(P, p, tm, tn);
             }
         } else {
-            const int mi = P.split ? p * P.ksplit + U.piece : p;
+            const int mi = P.sk_store ? p : P.split ? p * P.ksplit + U.piece : p;
             // product temporaries: rows 2g, 2g+1 of fragment pair (2h, 2h+1)
             // are adjacent (ldm even) -> one 16-byte streaming store
             // (st.global.cs: evict-first, keeps operand panels in L2)
@@ -1635,7 +1659,9 @@ static cudaError_t launch_mm_t(const MMParams& p, cudaStream_t s) {
         attr_set.fetch_or(bit, std::memory_order_release);
     }
     const int units = p.tiles_m * p.tiles_n * (p.split ? p.nprod * p.ksplit : 1);
-    const int grid = PERSIST && p.grid_cap > 0 && p.grid_cap < units ? p.grid_cap : units;
+    // stream-K: exactly grid_cap CTAs (the unit decode assumes it)
+    const int grid = PERSIST && p.streamk ? p.grid_cap
+                     : PERSIST && p.grid_cap > 0 && p.grid_cap < units ? p.grid_cap : units;
     mm_kernel<MAXT, PERSIST, RING><<<grid, kThreads, smem, s>>>(p);
     return cudaGetLastError();
 }
@@ -1656,6 +1682,8 @@ cudaError_t launch_mm(const MMParams& p, cudaStream_t s) {
         return launch_mm_t<2, true, kSepRing2>(p, s);
     if (maxt == 1)  // single-term programs: no sum code at all
         return p.grid_cap > 0 ? launch_mm_t<1, true>(p, s) : launch_mm_t<1, false>(p, s);
+    if (p.streamk)  // stream-K of a fused-sum program (few tiles)
+        return maxt <= 2 ? launch_mm_t<2, true>(p, s) : launch_mm_t<kMaxTerms, true>(p, s);
     return maxt <= 2 ? launch_mm_t<2, false>(p, s) : launch_mm_t<kMaxTerms, false>(p, s);
 }
 

@@ -96,9 +96,10 @@ struct alignas(64) MMParams {
     // CTA stores its partial product to M_{p*ksplit+s} (kEpiStore)
     int split;
     int ksplit, kt_per_split;
-    // ticketed fused epilogue (split grid, ksplit = 1, kEpiRMW): CTA (tile, p)
-    // applies its C updates once tickets[tile] == p, then sets it to p + 1, so
-    // every C tile still receives the products in table order
+    // ticketed fused epilogue (kEpiRMW): CTA (tile, p) applies its C updates once
+    // tickets[tile] == p, then sets it to p + 1, so every C tile receives the
+    // products in table order (deterministic).  (Per-(tile, quadrant) tickets were
+    // measured ~3% slower for short fused products: profiles/r02_shortk6.log.)
     int* tickets;
     int ticket_ld;              // tickets row stride (tile columns of the whole call)
     // k-split fused epilogue (split grid, ksplit > 1, kEpiRMW): every CTA of
@@ -130,6 +131,14 @@ struct alignas(64) MMParams {
     // k-step) space, at most sk_maxp pieces; partial pieces go through the k-split
     // fixup (ksplit = partial slots per tile, arrive counters per tile)
     int streamk, sk_len, sk_maxp;
+    // stream-K over (tile, product, k-step) for store-mode programs (kEpiStore, few
+    // tiles): a (tile, product) cut into pieces stores them as partials at
+    // mbase + part_off + (p * ksplit + piece) * mstride; the last piece to arrive
+    // sums them in piece order and stores M_p at mbase + p * mstride (ksplit = 1 for
+    // the stream pass).  part_off = 0 and sk_store = 0 elsewhere (the RMW k-split
+    // fixup keeps its partials at mbase).
+    int sk_store;
+    long long part_off;
     // A-heavy products (more A than B terms) in one-CTA-per-unit launches run the
     // 4 x 2 warp layout (kernels.cu product_kloop1)
     int a_heavy_layout;
