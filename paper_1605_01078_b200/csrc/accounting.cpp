@@ -297,10 +297,13 @@ static double predict_core(strassen_variant v, int L, long m, long n, long k, in
     const double mul = tc[L][0], cu = tc[L][3];
     const double tiles = std::ceil(qm / 128.0) * std::ceil(qn / 128.0);
     // mm_kernel efficiency (executed flops / DMMA peak), fitted to the sweeps
-    // (tools/model_fit.py): single-term 0.976; fused operand sums 0.91 (L1), 0.78 (L2)
+    // (tools/model_fit.py, profiles/r02_sweep_*.csv): single-term 0.976; fused operand
+    // sums 0.91 at level 1; at level 2 the 4-term sides are materialised (the default
+    // fused-term setting, 2) and the rest fused: E_ABC2
     const bool fused_sums = v == STRASSEN_ABC || v == STRASSEN_AB;
+    constexpr double E_ABC2 = 0.93;
     double e_mm = 0.976;
-    if (fused_sums) e_mm = (L == 1) ? 0.91 : 0.78;
+    if (fused_sums) e_mm = (L == 1) ? 0.91 : E_ABC2;
     const bool per_product_grid = (v == STRASSEN_AB || v == STRASSEN_NAIVE);
     // k-chunks and the fused / split decision as engine.cpp plan_fused makes them
     const double terms = fused_sums ? (L == 1 ? 1.71 : 2.94) : 1.0;
@@ -319,6 +322,20 @@ static double predict_core(strassen_variant v, int L, long m, long n, long k, in
     // per-CTA fixed cost (barrier init, pipeline fill, epilogue): ~4 us per wave
     double t = mul * 2.0 * qm * qn * qk / (P * e_mm * waves_eff(ctas, sms)) +
                4e-6 * std::ceil(ctas / sms);
+    if (mul > 1 && split && tiles * mul < 4.0 * sms) {
+        // stream-K pieces of the (product, tile, k-step) space, as engine.cpp plan_fused
+        // decides them; the pieces run at ~0.8 of the mainloop rate at these sizes
+        // (per-piece prologue / fixup, profiles/r02_small6.log)
+        const double kt = std::ceil(qk / 16.0), total = tiles * mul * kt;
+        const double len = std::ceil(total / std::max(1.0, std::min<double>(sms, std::floor(total / 8))));
+        const double t_k = 2.1e-6 * (1.0 + 0.15 * (terms - 1.0)), t_cta = 3e-6;
+        const double per = std::ceil(kt / ks);
+        const double t_uni = std::ceil(tiles * mul * ks / sms) * (per * t_k + t_cta);
+        const double t_sk = len * t_k + std::ceil(len / kt + 1.0) * t_cta + 6e-6;
+        if (t_sk < 0.97 * t_uni)
+            t = mul * 2.0 * qm * qn * qk / (P * e_mm * 0.8 * waves_eff(std::ceil(total / len), sms)) +
+                std::ceil(len / kt + 1.0) * 4e-6;
+    }
     if (mul == 1 && split) {  // stream-K pieces when they beat the k-chunk waves (engine.cpp)
         const double kt = std::ceil(qk / 16.0), total = tiles * kt;
         const double len = std::ceil(total / std::max(1.0, std::min<double>(sms, std::floor(total / 8))));
@@ -336,6 +353,9 @@ static double predict_core(strassen_variant v, int L, long m, long n, long k, in
         const double quads = S * S + n_sums[L];     // sources read once, sums written once
         bytes += 8.0 * quads * (qm * qk + qk * qn);
         launches += 2;
+    } else if (fused_sums && L == 2) {  // the 25 four-term sides of each operand
+        bytes += 8.0 * (S * S + 25.0) * (qm * qk + qk * qn);
+        launches += 2;
     }
     double rmw_bytes = 0.0;
     if (mul == 1 && split) {  // classical: partials summed by the last piece's CTA, no
@@ -349,7 +369,10 @@ static double predict_core(strassen_variant v, int L, long m, long n, long k, in
         // mostly hidden: persistent single-term launches collect them a unit later
         rmw_bytes = 16.0 * cu * qm * qn;
     }
-    t += bytes / BW + rmw_bytes / (!c_vec ? 4.6e12 : fused_sums ? 10e12 : 20e12) +
+    // the deferred (persistent, separate-stage) epilogue: single-term programs, and
+    // fused ones whose sides are at most 2 terms with short products (engine.cpp)
+    const bool deferred = !fused_sums || (L == 2 && std::ceil(qk / 16.0) <= 24);
+    t += bytes / BW + rmw_bytes / (!c_vec ? 4.6e12 : deferred ? 20e12 : 10e12) +
          launches * launch;
     return t;
 }

@@ -268,6 +268,21 @@ def test_model_guided_selection_against_measured_sweeps():
                 misses.append((shape, key, times[key] / min(times.values())))
             assert t > 0
     assert not misses, misses
+    # round-2 sweeps (after the fused-term and stream-K changes): within 3.5% except
+    # where single calls under ~120 us are within the model's noise, at most 6%
+    for fam in ("square", "rankk", "fixedk"):
+        by = collections.defaultdict(dict)
+        for r in csv.DictReader(open(os.path.join(ROOT, "profiles", f"r02_sweep_{fam}.csv"))):
+            if int(r["level"]) <= 2:
+                by[(int(r["m"]), int(r["n"]), int(r["k"]))][r["variant"] + r["level"]] = \
+                    float(r["time_s"])
+        for shape, times in by.items():
+            v, lv, _ = S.select(*shape)
+            best = min(times.values())
+            slack = 1.06 if best < 120e-6 else 1.035
+            if f"{v}{lv}" in times:  # (the rank-k sweep does not run every configuration)
+                assert times[f"{v}{lv}"] <= slack * best, (fam, shape, v, lv,
+                                                            times[f"{v}{lv}"] / best)
     v16, l16, t16 = S.select(16384, 16384, 16384)
     assert (v16, l16) in (("naive", 2), ("c", 2))  # the two measured within 0.5% there
     # the prediction strassen_select minimises, per configuration

@@ -121,6 +121,9 @@ def main():
             print(f"{m}x{n}x{k} {v}{L}: {egf / 1e3:.2f} TF/s rel_err {err:.1e} "
                   f"freivalds {fv:.1e}", flush=True)
         del A, B, C0, C, C_ref
+        torch.cuda.empty_cache()  # freed inputs back to the device (product groups
+        # plan against cudaMemGetInfo: 30720^2 x 1024 AB / Naive L2 ran grouped in
+        # profiles/r02_sweep_fixedk.csv while the previous shape's blocks were cached)
     with open(out, "w", newline="") as f:
         w = csv.DictWriter(f, fieldnames=list(rows[0].keys()))
         w.writeheader()
