@@ -810,9 +810,16 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     // (and product) to release once they complete
     bool pend = false;
     int pend_p = -1, pend_tm = 0, pend_tn = 0;  // pend_p >= 0: tickets to release
+    // Completion of a unit's reduce-adds: a ticket successor needs them performed
+    // (wait_group 0); otherwise only the stage must be free again (wait_group.read:
+    // the writes complete before the grid does, as TMA stores do)
     auto collect = [&]() {  // every warp's reductions performed, then hand the tiles on
-        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (pend_p >= 0) {
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        } else {
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
         consumer_bar();  // (also: the stage is free again)
         if (threadIdx.x == 0 && pend_p >= 0) {
             __threadfence();
@@ -1032,20 +1039,26 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 issued = true;
             }
+            // the last product of the launch has no ticket successor
+            const bool succ = ticketed && p + 1 < P.nprod;
             if (SEP && P.sep_defer) {  // completion collected at the next epilogue (or after the loop)
                 pend = true;
-                pend_p = ticketed ? p : -1;
+                pend_p = succ ? p : -1;
                 pend_tm = tm;
                 pend_tn = tn;
                 continue;
             }
-            // all reductions performed (every warp's), then hand the tiles on
-            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-            consumer_bar();
-            if (threadIdx.x == 0 && ticketed) {
-                __threadfence();
-                release_ticket(P, p, tm, tn);
+            if (succ) {  // all reductions performed (every warp's), then hand the tile on
+                asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                consumer_bar();
+                if (threadIdx.x == 0) {
+                    __threadfence();
+                    release_ticket(P, p, tm, tn);
+                }
+            } else {  // the stage must outlive the reads (smem is freed at exit)
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                consumer_bar();
             }
             continue;  // next product (none: single-product CTA)
         }
