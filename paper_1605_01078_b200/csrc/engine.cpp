@@ -669,6 +669,76 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
     return 2;
 }
 
+// Product pairs for the ticketed fused-epilogue grid (MMParams::pair_mode): the
+// products are reordered so that each one is followed by the next product (table
+// order) sharing the most destination quadrants with it, if any; a unit then runs both
+// (the first parked in tensor memory) and applies alpha (g1 M1 + g2 M2) to every
+// destination with one TMA reduce-add.  The level-2 table's 144 C updates become 109
+// (level 1: 12 -> 9), which matters where the updates bound the call: short products.
+// Deterministic; per element the updates of a pair are summed before they reach C (a
+// reassociation of the reference's C + g1 M1 + g2 M2, within the BASELINE tolerance).
+void pair_products(const Engine& e, MMParams& P, const FusedPlan& F, strassen_variant variant,
+                   const std::vector<QuadView>& cq) {
+    P.pair_mode = 0;
+    static const int pair_env = [] {
+        const char* v = std::getenv("STRASSEN_B200_PAIR");  // 0 / 1 / -1 auto (experiments)
+        return v ? std::atoi(v) : -1;
+    }();
+    static const int pair_kt = [] {
+        const char* v = std::getenv("STRASSEN_B200_PAIR_KT");  // k-tiles (experiments)
+        // measured: 16384^2 x 256 ABC L2 9.2 -> 7.4 ms, x 1024 17.4 -> 16.8, x 4096
+        // (64 k-tiles) 55.6 -> 54.9; 16384^3 (256 k-tiles) 206.0 -> 207.6 and ABC L1 at
+        // x 4096 (128 k-tiles) 62.2 -> 62.4 (profiles/r02_pair12_*.log, r02_pair13_*.log)
+        return v ? std::atoi(v) : 64;
+    }();
+    if (pair_env == 0 || F.split || !F.tickets || P.nprod < 2) return;
+    if (variant != STRASSEN_ABC && variant != STRASSEN_C) return;
+    if (pair_env < 0 && P.ktiles > pair_kt) return;
+    // (independent of C's layout and of the fused-term setting, so host and device calls
+    // and every setting pair alike)
+    (void)e;
+    (void)cq;
+    auto dests = [&](int p) {
+        unsigned m = 0;
+        for (int u = 0; u < P.prod[p].nc; ++u) m |= 1u << P.prod[p].cq[u];
+        return m;
+    };
+    std::vector<bool> used(static_cast<size_t>(P.nprod), false);
+    std::vector<int> order;
+    std::vector<int8_t> lo;
+    for (int i = 0; i < P.nprod; ++i) {
+        if (used[static_cast<size_t>(i)]) continue;
+        used[static_cast<size_t>(i)] = true;
+        lo.push_back(static_cast<int8_t>(order.size()));
+        order.push_back(i);
+        int best = -1, share = 0;
+        for (int j = i + 1; j < P.nprod; ++j) {
+            if (used[static_cast<size_t>(j)]) continue;
+            const int sh = __builtin_popcount(dests(i) & dests(j));
+            if (sh > share) {
+                share = sh;
+                best = j;
+            }
+        }
+        if (best >= 0) {
+            used[static_cast<size_t>(best)] = true;
+            order.push_back(best);
+        }
+    }
+    if (static_cast<int>(lo.size()) == P.nprod) return;  // nothing shares a destination
+    ProductDesc re[kMaxProducts];
+    for (size_t k = 0; k < order.size(); ++k) re[k] = P.prod[order[k]];
+    for (int p = 0; p < P.nprod; ++p) P.prod[p] = re[p];
+    P.npairs = static_cast<int>(lo.size());
+    for (int j = 0; j < P.npairs; ++j) P.pair_lo[j] = lo[static_cast<size_t>(j)];
+    P.pair_lo[P.npairs] = static_cast<int8_t>(P.nprod);
+    P.pair_mode = 1;
+    P.a_heavy_layout = 0;  // its relayout scratch is the ring, which streams the pair's second product
+    // the two products of a pair share the accumulator column map: 4 + 4-term products
+    // (fully fused setting) stream whole 16-k tiles instead of half tiles
+    for (int p = 0; p < P.nprod; ++p) P.prod[p].half = 0;
+}
+
 // ------------------------------------------------------------- run_device --
 namespace {
 long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level, double alpha,
@@ -1122,6 +1192,7 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
         // (AB: variants.cpp:142-168).
         const bool store_products = variant == STRASSEN_NAIVE || variant == STRASSEN_AB;
         const FusedPlan F = plan_fused(e, s, P, store_products, nprod_all, terms_all, nw > 1);
+        pair_products(e, P, F, variant, cq);
         if (nw > 1) {  // the aux stream starts after everything enqueued on s so far
             ck(cudaEventRecord(e.ev_fork, s), "fork");
             ck(cudaStreamWaitEvent(e.aux_stream, e.ev_fork, 0), "fork");

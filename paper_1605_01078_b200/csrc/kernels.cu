@@ -96,6 +96,60 @@ __device__ __forceinline__ void release_ticket(const MMParams& P, int p, int tm,
     st_release_gpu(tile_ticket(P, tm, tn), p + 1);
 }
 
+// ---- tensor memory as a parking place for one accumulator (pair_mode) --------
+// Warp w reaches TMEM lanes 32 (w % 4) .. + 31; warps w and w + 4 share them and use
+// columns [0, 128) and [128, 256) of a 256-column allocation.  A thread's 64 doubles
+// are 128 words, in 4 chunks of 32 words: chunk h holds acc[2h + (i / 8)][(i / 2) % 4][i % 2]
+// for i < 16 (lo word, hi word) -- exactly the (h) grouping of the stage writes.
+constexpr uint32_t kTmemCols = 256;
+__device__ __forceinline__ uint32_t tmem_addr(uint32_t base, int warp, int h) {
+    return base + ((32u * static_cast<uint32_t>(warp & 3)) << 16) +
+           static_cast<uint32_t>((warp >> 2) * 128 + h * 32);
+}
+#define SB200_R32(r) r[0], r[1], r[2], r[3], r[4], r[5], r[6], r[7], r[8], r[9], r[10], r[11], \
+    r[12], r[13], r[14], r[15], r[16], r[17], r[18], r[19], r[20], r[21], r[22], r[23], r[24],  \
+    r[25], r[26], r[27], r[28], r[29], r[30], r[31]
+__device__ __forceinline__ void tmem_st32(uint32_t ta, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+        "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+        ::"r"(ta), "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
+        "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]),
+        "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]),
+        "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+        "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t ta, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(ta)
+        : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+#undef SB200_R32
+// Park this warp's accumulator tile (64 doubles per thread) in tensor memory.
+__device__ __forceinline__ void tmem_park(uint32_t base, int warp, const double (&acc)[8][4][2]) {
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+        uint32_t r[32];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const double v = acc[2 * h + (i >> 3)][(i >> 1) & 3][i & 1];
+            r[2 * i] = static_cast<uint32_t>(__double2loint(v));
+            r[2 * i + 1] = static_cast<uint32_t>(__double2hiint(v));
+        }
+        tmem_st32(tmem_addr(base, warp, h), r);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
 // Tensor reduce-add smem -> global through a tensor map (f64 add at L2,
 // UTMAREDG.2D.ADD); coordinates {row, column} of the box origin.
 __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, int c0, int c1,
@@ -576,9 +630,11 @@ __device__ __forceinline__ void relayout_to_2x4(uint8_t* raw, double (&acc)[8][4
 struct Unit {
     int tm, tn, p_lo, p_hi, kt_lo, kt_hi;
     int piece, npieces;
+    int tk;  // ticket value of the unit's C update: its product, or its pair (pair_mode)
 };
 __device__ __forceinline__ int unit_count(const MMParams& P) {
     if (P.streamk) return P.grid_cap * P.sk_maxp;
+    if (P.pair_mode) return P.tiles_m * P.tiles_n * P.npairs;
     return P.tiles_m * P.tiles_n * (P.split ? P.nprod * P.ksplit : 1);
 }
 // unit -> (tile, product, k-chunk) in split mode, tile (all products) otherwise;
@@ -625,6 +681,14 @@ __device__ __forceinline__ Unit decode_unit(const MMParams& P, int bid) {
         U.p_lo = rem / gt;
         U.p_hi = U.p_lo + 1;
         bid = grp * G + rem % gt;
+    } else if (P.pair_mode) {
+        // (tile, pair) units, pair-major: the ticket a unit waits for, (t, j - 1), has
+        // a smaller index
+        const int ntiles = P.tiles_m * P.tiles_n;
+        U.tk = bid / ntiles;
+        U.p_lo = P.pair_lo[U.tk];
+        U.p_hi = P.pair_lo[U.tk + 1];
+        bid %= ntiles;
     } else if (P.split) {
         const int ntiles = P.tiles_m * P.tiles_n;
         const int s_idx = (bid / ntiles) % P.ksplit;
@@ -636,6 +700,7 @@ __device__ __forceinline__ Unit decode_unit(const MMParams& P, int bid) {
         U.npieces = P.ksplit;
         bid %= ntiles;
     }
+    if (!P.pair_mode) U.tk = U.p_lo;
     const int per_group = P.group_m * P.tiles_n;
     const int grp = bid / per_group;
     const int first_m = grp * P.group_m;
@@ -696,7 +761,20 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
     }
+    // pair_mode: warp 0 (a DMMA warp, which also frees it) allocates the tensor memory
+    // the first product of a pair is parked in
+    __shared__ uint32_t tmem_base_s;
+    if (P.pair_mode && warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&tmem_base_s)),
+                     "n"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem_base = P.pair_mode ? tmem_base_s : 0u;
     // Unit sequence of this CTA: blockIdx.x first; then either a fixed stride of
     // gridDim.x, or (dyn) units taken from the global counter, in increasing order
     // across the grid.  The producer takes a unit when it starts streaming its tiles
@@ -960,6 +1038,12 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             }
         }
 
+        // pair_mode: the first product of a pair waits in tensor memory for the second
+        if (P.pair_mode && p + 1 < p_hi) {
+            tmem_park(tmem_base, warp, acc);
+            continue;
+        }
+        const bool paired = P.pair_mode && p_hi - p_lo == 2;
         if (SEP && pend) collect();  // previous unit's reductions: complete, release its ticket
         // ---- epilogue of product p.  Accumulator (mf, nf, e) of lane (g, j)
         // is row 16(mf/2) + 2g + mf%2 and column 8nf + nperm(2j + e) of this
@@ -981,7 +1065,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         // else takes the register read-modify-write below.
         // C tiles are reduced through the quadrants' tensor maps (tmC), which clip
         // partial tiles at the quadrant edge.
-        bool bulk = P.mode == kEpiRMW && P.c_tma && p_hi - p_lo == 1 &&
+        bool bulk = P.mode == kEpiRMW && P.c_tma && (p_hi - p_lo == 1 || P.pair_mode) &&
                     kt_hi - kt_lo <= P.bulk_max_kt && (SEP || !persistent) &&
                     U.npieces == 1;
         // the reduce-add clips rows at 16-byte granularity (microbench/tma_reduce_f64.cu):
@@ -990,7 +1074,34 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             const int R = P.crows[pd.cq[u]];
             bulk = (R & 1) == 0 || tm * kBM + kBM <= R;
         }
+        // destinations of the unit and their coefficients on the parked product (da)
+        // and on the accumulator (db): a product alone has da = 0
+        int nd = 0;
+        int dq[2 * kMaxTerms];
+        int8_t da[2 * kMaxTerms], db[2 * kMaxTerms];
+        if (paired) {
+            const ProductDesc& p0 = P.prod[p_lo];
+            for (int u = 0; u < p0.nc; ++u) {
+                dq[nd] = p0.cq[u];
+                da[nd] = p0.cs[u];
+                db[nd++] = 0;
+            }
+        }
+        for (int u = 0; u < pd.nc; ++u) {
+            int i = 0;
+            while (i < nd && dq[i] != pd.cq[u]) ++i;
+            if (i == nd) {
+                dq[nd] = pd.cq[u];
+                da[nd++] = 0;
+            }
+            db[i] = pd.cs[u];
+        }
+        for (int i = 0; i < nd && bulk; ++i) {  // (the first product's destinations too)
+            const int R = P.crows[dq[i]];
+            bulk = (R & 1) == 0 || tm * kBM + kBM <= R;
+        }
         if (bulk) {
+            int done = 0;  // destinations already issued (bit mask)
             // stage: 8 boxes of 16 rows x 128 columns (16 KB each, 128-byte swizzle:
             // column c at c*128, 16-byte chunk (row%16)/2 ^ c%8) -- conflict-free for
             // the fragment layout (chunk g ^ nperm(2j+e)%8 covers all 8 per quarter-warp)
@@ -998,29 +1109,42 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             const bool ticketed = P.tickets != nullptr;
             bool issued = false;
             if (!SEP) consumer_bar();  // every warp is done reading the ring before it is reused
-            for (int pass = 0; pass < 2; ++pass) {  // destinations with coefficient +1, then -1
-                int any = 0;
-                for (int u = 0; u < pd.nc; ++u) any |= (pd.cs[u] > 0) == (pass == 0);
-                if (!any) continue;
+            // one pass per distinct (da, db): stage alpha (da Mparked + db M), then one
+            // reduce-add per destination with that pair of coefficients
+            for (int first = 0; first < nd; ++first) {
+                if (done & (1 << first)) continue;
+                const int ca = da[first], cb = db[first];
                 if (issued) {  // previous pass's reductions must have read the stage
                     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                     consumer_bar();
                 }
-                const double sc = P.alpha * (pass == 0 ? 1.0 : -1.0);
 #pragma unroll
-                for (int nf = 0; nf < 4; ++nf)
+                for (int h = 0; h < 4; ++h) {
+                    uint32_t t[32];
+                    if (ca != 0) tmem_ld32(tmem_addr(tmem_base, warp, h), t);
 #pragma unroll
-                    for (int h = 0; h < 4; ++h)
+                    for (int nf = 0; nf < 4; ++nf)
 #pragma unroll
                         for (int e = 0; e < 2; ++e) {
                             const int col = wn * 32 + 8 * nf + (e ? c1 : c0);
+                            double v0 = cb * acc[2 * h][nf][e], v1 = cb * acc[2 * h + 1][nf][e];
+                            if (ca != 0) {  // exact for ca, cb in {-1, 0, 1}: one rounding
+                                const int i0 = 2 * nf + e, i1 = 8 + 2 * nf + e;
+                                v0 = fma(static_cast<double>(ca),
+                                         __hiloint2double(static_cast<int>(t[2 * i0 + 1]),
+                                                          static_cast<int>(t[2 * i0])), v0);
+                                v1 = fma(static_cast<double>(ca),
+                                         __hiloint2double(static_cast<int>(t[2 * i1 + 1]),
+                                                          static_cast<int>(t[2 * i1])), v1);
+                            }
                             *reinterpret_cast<double2*>(stage + (wm * 4 + h) * 16384 + col * 128 +
                                                         ((g ^ (col & 7)) << 4)) =
-                                make_double2(sc * acc[2 * h][nf][e], sc * acc[2 * h + 1][nf][e]);
+                                make_double2(P.alpha * v0, P.alpha * v1);
                         }
+                }
                 consumer_fence();  // generic smem writes before the async-proxy reads
                 if (!issued && ticketed) {
-                    if (threadIdx.x == 0) wait_ticket(P, p, tm, tn);
+                    if (threadIdx.x == 0) wait_ticket(P, U.tk, tm, tn);
                     asm volatile("fence.proxy.async.global;" ::: "memory");
                 }
                 consumer_bar();
@@ -1029,21 +1153,21 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                 // reductions issued 128 x nc uniform-datapath instructions per tile)
                 static_assert(kConsumerWarps * 16 == kBM, "one 16-row box per warp");
                 asm volatile("fence.proxy.async.global;" ::: "memory");
-                if (lane == 0) {
-                    for (int u = 0; u < pd.nc; ++u) {
-                        if ((pd.cs[u] > 0) != (pass == 0)) continue;
-                        tma_reduce_add_2d(&P.tmC[pd.cq[u]], tm * kBM + 16 * warp, tn * kBN,
+                for (int i = first; i < nd; ++i) {
+                    if (da[i] != ca || db[i] != cb) continue;
+                    done |= 1 << i;
+                    if (lane == 0)
+                        tma_reduce_add_2d(&P.tmC[dq[i]], tm * kBM + 16 * warp, tn * kBN,
                                           stage + warp * 16384);
-                    }
                 }
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 issued = true;
             }
-            // the last product of the launch has no ticket successor
-            const bool succ = ticketed && p + 1 < P.nprod;
+            // the last product (pair) of the launch has no ticket successor
+            const bool succ = ticketed && U.tk + 1 < (P.pair_mode ? P.npairs : P.nprod);
             if (SEP && P.sep_defer) {  // completion collected at the next epilogue (or after the loop)
                 pend = true;
-                pend_p = succ ? p : -1;
+                pend_p = succ ? U.tk : -1;
                 pend_tm = tm;
                 pend_tn = tn;
                 continue;
@@ -1054,13 +1178,64 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                 consumer_bar();
                 if (threadIdx.x == 0) {
                     __threadfence();
-                    release_ticket(P, p, tm, tn);
+                    release_ticket(P, U.tk, tm, tn);
                 }
             } else {  // the stage must outlive the reads (smem is freed at exit)
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                 consumer_bar();
             }
             continue;  // next product (none: single-product CTA)
+        }
+        if (paired) {
+            // ---- a pair's update through registers (C layouts the reduce-adds cannot
+            // take): C += alpha (da Mparked + db M) per destination, in pair order --
+            // per element the same arithmetic as the staged values of the bulk path
+            if (P.tickets) {
+                if (threadIdx.x == 0) wait_ticket(P, U.tk, tm, tn);
+                consumer_bar();
+            }
+            for (int i = 0; i < nd; ++i) {
+                double* __restrict__ C = P.cptr[dq[i]];
+                const int R = P.crows[dq[i]], Cc = P.ccols[dq[i]];
+                const int ca = da[i], cb = db[i];
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    uint32_t t[32];
+                    if (ca != 0) tmem_ld32(tmem_addr(tmem_base, warp, h), t);
+#pragma unroll
+                    for (int nf = 0; nf < 4; ++nf)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            double v0 = cb * acc[2 * h][nf][e], v1 = cb * acc[2 * h + 1][nf][e];
+                            if (ca != 0) {
+                                const int i0 = 2 * nf + e, i1 = 8 + 2 * nf + e;
+                                v0 = fma(static_cast<double>(ca),
+                                         __hiloint2double(static_cast<int>(t[2 * i0 + 1]),
+                                                          static_cast<int>(t[2 * i0])), v0);
+                                v1 = fma(static_cast<double>(ca),
+                                         __hiloint2double(static_cast<int>(t[2 * i1 + 1]),
+                                                          static_cast<int>(t[2 * i1])), v1);
+                            }
+                            const int row = mrow0 + 16 * h;
+                            const int col = ncol0 + 8 * nf + (e ? c1 : c0);
+                            if (col >= Cc) continue;
+                            if (row < R) {
+                                double* x = C + row * P.rs_c + static_cast<long long>(col) * P.cs_c;
+                                *x = fma(P.alpha, v0, __ldcg(x));
+                            }
+                            if (row + 1 < R) {
+                                double* x = C + (row + 1) * P.rs_c + static_cast<long long>(col) * P.cs_c;
+                                *x = fma(P.alpha, v1, __ldcg(x));
+                            }
+                        }
+                }
+            }
+            if (P.tickets) {  // every thread's C stores visible, then hand the tile on
+                __threadfence();
+                consumer_bar();
+                if (threadIdx.x == 0) release_ticket(P, U.tk, tm, tn);
+            }
+            continue;
         }
         if (P.arrive && U.npieces > 1) {
             // ---- k-split / stream-K fixup: partial out, the last piece sums ----
@@ -1124,7 +1299,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         }
         const bool ticketed = P.mode == kEpiRMW && P.tickets;  // ordered epilogue
         if (ticketed) {
-            if (threadIdx.x == 0) wait_ticket(P, p, tm, tn);
+            if (threadIdx.x == 0) wait_ticket(P, U.tk, tm, tn);
             consumer_bar();
         }
         if (P.mode == kEpiRMW) {
@@ -1202,7 +1377,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             if (ticketed) {  // every thread's C stores visible, then hand the tiles on
                 __threadfence();
                 consumer_bar();
-                if (threadIdx.x == 0) release_ticket(P, p, tm, tn);
+                if (threadIdx.x == 0) release_ticket(P, U.tk, tm, tn);
             }
         } else {
             const int mi = P.sk_store ? p : P.split ? p * P.ksplit + U.piece : p;
@@ -1232,6 +1407,15 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     }
     }  // unit
     if (SEP && pend) collect();
+    if (P.pair_mode) {  // every warp is done with tensor memory; warp 0 frees it
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        consumer_bar();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (warp == 0)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                         "n"(kTmemCols)
+                         : "memory");
+    }
 }
 
 // ---------------------------------------------------------------- repack ----
@@ -1671,7 +1855,8 @@ static cudaError_t launch_mm_t(const MMParams& p, cudaStream_t s) {
         if (e != cudaSuccess) return e;
         attr_set.fetch_or(bit, std::memory_order_release);
     }
-    const int units = p.tiles_m * p.tiles_n * (p.split ? p.nprod * p.ksplit : 1);
+    const int units = p.tiles_m * p.tiles_n *
+                      (p.pair_mode ? p.npairs : p.split ? p.nprod * p.ksplit : 1);
     // stream-K: exactly grid_cap CTAs (the unit decode assumes it)
     const int grid = PERSIST && p.streamk ? p.grid_cap
                      : PERSIST && p.grid_cap > 0 && p.grid_cap < units ? p.grid_cap : units;
