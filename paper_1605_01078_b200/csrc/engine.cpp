@@ -669,14 +669,15 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
     return 2;
 }
 
-// Product pairs for the ticketed fused-epilogue grid (MMParams::pair_mode): the
-// products are reordered so that each one is followed by the next product (table
-// order) sharing the most destination quadrants with it, if any; a unit then runs both
-// (the first parked in tensor memory) and applies alpha (g1 M1 + g2 M2) to every
-// destination with one TMA reduce-add.  The level-2 table's 144 C updates become 109
-// (level 1: 12 -> 9), which matters where the updates bound the call: short products.
-// Deterministic; per element the updates of a pair are summed before they reach C (a
-// reassociation of the reference's C + g1 M1 + g2 M2, within the BASELINE tolerance).
+// Product groups for the ticketed fused-epilogue grid (MMParams::pair_mode): the
+// products are reordered so that each one is followed by up to two later products
+// (table order) sharing the most destination quadrants with the group; a unit then
+// runs them all (the first ones parked in tensor memory) and applies alpha (g1 M1 +
+// g2 M2 + g3 M3) to every destination with one update.  The level-2 table's 144 C
+// updates become 90 (pairs: 109; level 1: 12 -> 7), which matters where the updates
+// bound the call: short products.  Deterministic; per element the updates of a group
+// are summed before they reach C (a reassociation of the reference's C + g1 M1 + g2 M2
+// + g3 M3, within the BASELINE tolerance).
 void pair_products(const Engine& e, MMParams& P, const FusedPlan& F, strassen_variant variant,
                    const std::vector<QuadView>& cq) {
     P.pair_mode = 0;
@@ -703,6 +704,10 @@ void pair_products(const Engine& e, MMParams& P, const FusedPlan& F, strassen_va
         for (int u = 0; u < P.prod[p].nc; ++u) m |= 1u << P.prod[p].cq[u];
         return m;
     };
+    static const int group_max = [] {  // products per unit: 2 or 3 (kernels.cu kParkSlots + 1)
+        const char* v = std::getenv("STRASSEN_B200_GROUP_MAX");  // experiments
+        return v ? std::max(2, std::min(3, std::atoi(v))) : 3;
+    }();
     std::vector<bool> used(static_cast<size_t>(P.nprod), false);
     std::vector<int> order;
     std::vector<int8_t> lo;
@@ -711,18 +716,23 @@ void pair_products(const Engine& e, MMParams& P, const FusedPlan& F, strassen_va
         used[static_cast<size_t>(i)] = true;
         lo.push_back(static_cast<int8_t>(order.size()));
         order.push_back(i);
-        int best = -1, share = 0;
-        for (int j = i + 1; j < P.nprod; ++j) {
-            if (used[static_cast<size_t>(j)]) continue;
-            const int sh = __builtin_popcount(dests(i) & dests(j));
-            if (sh > share) {
-                share = sh;
-                best = j;
+        // grow the group with the next products (table order) sharing the most
+        // destinations with it so far
+        unsigned uni = dests(i);
+        for (int member = 1; member < group_max; ++member) {
+            int best = -1, share = 0;
+            for (int j = i + 1; j < P.nprod; ++j) {
+                if (used[static_cast<size_t>(j)]) continue;
+                const int sh = __builtin_popcount(uni & dests(j));
+                if (sh > share) {
+                    share = sh;
+                    best = j;
+                }
             }
-        }
-        if (best >= 0) {
+            if (best < 0) break;
             used[static_cast<size_t>(best)] = true;
             order.push_back(best);
+            uni |= dests(best);
         }
     }
     if (static_cast<int>(lo.size()) == P.nprod) return;  // nothing shares a destination

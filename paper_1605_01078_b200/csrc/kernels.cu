@@ -96,15 +96,17 @@ __device__ __forceinline__ void release_ticket(const MMParams& P, int p, int tm,
     st_release_gpu(tile_ticket(P, tm, tn), p + 1);
 }
 
-// ---- tensor memory as a parking place for one accumulator (pair_mode) --------
-// Warp w reaches TMEM lanes 32 (w % 4) .. + 31; warps w and w + 4 share them and use
-// columns [0, 128) and [128, 256) of a 256-column allocation.  A thread's 64 doubles
-// are 128 words, in 4 chunks of 32 words: chunk h holds acc[2h + (i / 8)][(i / 2) % 4][i % 2]
+// ---- tensor memory as a parking place for accumulators (pair_mode) ------------
+// Warp w reaches TMEM lanes 32 (w % 4) .. + 31; warps w and w + 4 share them.  Parking
+// slot k (k < kParkSlots: the first products of a group) of warp w is columns
+// [256 k + 128 (w / 4), + 128) of a 512-column allocation.  A thread's 64 doubles are
+// 128 words, in 4 chunks of 32 words: chunk h holds acc[2h + (i / 8)][(i / 2) % 4][i % 2]
 // for i < 16 (lo word, hi word) -- exactly the (h) grouping of the stage writes.
-constexpr uint32_t kTmemCols = 256;
-__device__ __forceinline__ uint32_t tmem_addr(uint32_t base, int warp, int h) {
+constexpr int kParkSlots = 2;
+constexpr uint32_t kTmemCols = 512;
+__device__ __forceinline__ uint32_t tmem_addr(uint32_t base, int warp, int h, int slot) {
     return base + ((32u * static_cast<uint32_t>(warp & 3)) << 16) +
-           static_cast<uint32_t>((warp >> 2) * 128 + h * 32);
+           static_cast<uint32_t>(slot * 256 + (warp >> 2) * 128 + h * 32);
 }
 #define SB200_R32(r) r[0], r[1], r[2], r[3], r[4], r[5], r[6], r[7], r[8], r[9], r[10], r[11], \
     r[12], r[13], r[14], r[15], r[16], r[17], r[18], r[19], r[20], r[21], r[22], r[23], r[24],  \
@@ -135,7 +137,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t ta, uint32_t (&r)[32]) {
 }
 #undef SB200_R32
 // Park this warp's accumulator tile (64 doubles per thread) in tensor memory.
-__device__ __forceinline__ void tmem_park(uint32_t base, int warp, const double (&acc)[8][4][2]) {
+__device__ __forceinline__ void tmem_park(uint32_t base, int warp, int slot,
+                                          const double (&acc)[8][4][2]) {
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
         uint32_t r[32];
@@ -145,9 +148,29 @@ __device__ __forceinline__ void tmem_park(uint32_t base, int warp, const double 
             r[2 * i] = static_cast<uint32_t>(__double2loint(v));
             r[2 * i + 1] = static_cast<uint32_t>(__double2hiint(v));
         }
-        tmem_st32(tmem_addr(base, warp, h), r);
+        tmem_st32(tmem_addr(base, warp, h, slot), r);
     }
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+// Chunk h (16 doubles) of a group's combined update ca M_slot0 + cc M_slot1 + cb M, in
+// that order ((cb M + ca M0) + cc M1; coefficients in {-1, 0, 1}, so a destination of
+// one product is exactly +-M with no rounding): v[i] for acc[2h + i / 8][(i / 2) % 4][i % 2].
+__device__ __forceinline__ void group_values(uint32_t base, int warp, int h, int ca, int cc,
+                                             int cb, const double (&acc)[8][4][2], double (&v)[16]) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = cb * acc[2 * h + (i >> 3)][(i >> 1) & 3][i & 1];
+#pragma unroll
+    for (int k = 0; k < kParkSlots; ++k) {
+        const int c = k == 0 ? ca : cc;
+        if (c == 0) continue;
+        uint32_t t[32];
+        tmem_ld32(tmem_addr(base, warp, h, k), t);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            v[i] = fma(static_cast<double>(c),
+                       __hiloint2double(static_cast<int>(t[2 * i + 1]), static_cast<int>(t[2 * i])),
+                       v[i]);
+    }
 }
 
 // Tensor reduce-add smem -> global through a tensor map (f64 add at L2,
@@ -1038,12 +1061,12 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             }
         }
 
-        // pair_mode: the first product of a pair waits in tensor memory for the second
+        // pair_mode: the first products of a group wait in tensor memory for the last
         if (P.pair_mode && p + 1 < p_hi) {
-            tmem_park(tmem_base, warp, acc);
+            tmem_park(tmem_base, warp, p - p_lo, acc);
             continue;
         }
-        const bool paired = P.pair_mode && p_hi - p_lo == 2;
+        const bool paired = P.pair_mode && p_hi - p_lo >= 2;
         if (SEP && pend) collect();  // previous unit's reductions: complete, release its ticket
         // ---- epilogue of product p.  Accumulator (mf, nf, e) of lane (g, j)
         // is row 16(mf/2) + 2g + mf%2 and column 8nf + nperm(2j + e) of this
@@ -1074,27 +1097,25 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             const int R = P.crows[pd.cq[u]];
             bulk = (R & 1) == 0 || tm * kBM + kBM <= R;
         }
-        // destinations of the unit and their coefficients on the parked product (da)
-        // and on the accumulator (db): a product alone has da = 0
+        // destinations of the unit and their coefficients on the parked products (da:
+        // slot 0, dc: slot 1) and on the accumulator (db); a product alone has da = dc = 0
+        constexpr int kMaxDest = (kParkSlots + 1) * kMaxTerms;
         int nd = 0;
-        int dq[2 * kMaxTerms];
-        int8_t da[2 * kMaxTerms], db[2 * kMaxTerms];
-        if (paired) {
-            const ProductDesc& p0 = P.prod[p_lo];
-            for (int u = 0; u < p0.nc; ++u) {
-                dq[nd] = p0.cq[u];
-                da[nd] = p0.cs[u];
-                db[nd++] = 0;
+        int dq[kMaxDest];
+        int8_t da[kMaxDest], db[kMaxDest], dc[kMaxDest];
+        for (int pp = paired ? p_lo : p; pp <= p; ++pp) {
+            const ProductDesc& px = P.prod[pp];
+            const int k = pp == p ? 2 : pp - p_lo;  // slot 0, slot 1, accumulator
+            for (int u = 0; u < px.nc; ++u) {
+                int i = 0;
+                while (i < nd && dq[i] != px.cq[u]) ++i;
+                if (i == nd) {
+                    dq[nd] = px.cq[u];
+                    da[nd] = db[nd] = dc[nd] = 0;
+                    ++nd;
+                }
+                (k == 0 ? da : k == 1 ? dc : db)[i] = px.cs[u];
             }
-        }
-        for (int u = 0; u < pd.nc; ++u) {
-            int i = 0;
-            while (i < nd && dq[i] != pd.cq[u]) ++i;
-            if (i == nd) {
-                dq[nd] = pd.cq[u];
-                da[nd++] = 0;
-            }
-            db[i] = pd.cs[u];
         }
         for (int i = 0; i < nd && bulk; ++i) {  // (the first product's destinations too)
             const int R = P.crows[dq[i]];
@@ -1113,33 +1134,23 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             // reduce-add per destination with that pair of coefficients
             for (int first = 0; first < nd; ++first) {
                 if (done & (1 << first)) continue;
-                const int ca = da[first], cb = db[first];
+                const int ca = da[first], cb = db[first], cc = dc[first];
                 if (issued) {  // previous pass's reductions must have read the stage
                     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
                     consumer_bar();
                 }
 #pragma unroll
                 for (int h = 0; h < 4; ++h) {
-                    uint32_t t[32];
-                    if (ca != 0) tmem_ld32(tmem_addr(tmem_base, warp, h), t);
+                    double v[16];
+                    group_values(tmem_base, warp, h, ca, cc, cb, acc, v);
 #pragma unroll
                     for (int nf = 0; nf < 4; ++nf)
 #pragma unroll
                         for (int e = 0; e < 2; ++e) {
                             const int col = wn * 32 + 8 * nf + (e ? c1 : c0);
-                            double v0 = cb * acc[2 * h][nf][e], v1 = cb * acc[2 * h + 1][nf][e];
-                            if (ca != 0) {  // exact for ca, cb in {-1, 0, 1}: one rounding
-                                const int i0 = 2 * nf + e, i1 = 8 + 2 * nf + e;
-                                v0 = fma(static_cast<double>(ca),
-                                         __hiloint2double(static_cast<int>(t[2 * i0 + 1]),
-                                                          static_cast<int>(t[2 * i0])), v0);
-                                v1 = fma(static_cast<double>(ca),
-                                         __hiloint2double(static_cast<int>(t[2 * i1 + 1]),
-                                                          static_cast<int>(t[2 * i1])), v1);
-                            }
                             *reinterpret_cast<double2*>(stage + (wm * 4 + h) * 16384 + col * 128 +
                                                         ((g ^ (col & 7)) << 4)) =
-                                make_double2(P.alpha * v0, P.alpha * v1);
+                                make_double2(P.alpha * v[2 * nf + e], P.alpha * v[8 + 2 * nf + e]);
                         }
                 }
                 consumer_fence();  // generic smem writes before the async-proxy reads
@@ -1154,7 +1165,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                 static_assert(kConsumerWarps * 16 == kBM, "one 16-row box per warp");
                 asm volatile("fence.proxy.async.global;" ::: "memory");
                 for (int i = first; i < nd; ++i) {
-                    if (da[i] != ca || db[i] != cb) continue;
+                    if (da[i] != ca || db[i] != cb || dc[i] != cc) continue;
                     done |= 1 << i;
                     if (lane == 0)
                         tma_reduce_add_2d(&P.tmC[dq[i]], tm * kBM + 16 * warp, tn * kBN,
@@ -1197,25 +1208,15 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             for (int i = 0; i < nd; ++i) {
                 double* __restrict__ C = P.cptr[dq[i]];
                 const int R = P.crows[dq[i]], Cc = P.ccols[dq[i]];
-                const int ca = da[i], cb = db[i];
 #pragma unroll
                 for (int h = 0; h < 4; ++h) {
-                    uint32_t t[32];
-                    if (ca != 0) tmem_ld32(tmem_addr(tmem_base, warp, h), t);
+                    double v[16];
+                    group_values(tmem_base, warp, h, da[i], dc[i], db[i], acc, v);
 #pragma unroll
                     for (int nf = 0; nf < 4; ++nf)
 #pragma unroll
                         for (int e = 0; e < 2; ++e) {
-                            double v0 = cb * acc[2 * h][nf][e], v1 = cb * acc[2 * h + 1][nf][e];
-                            if (ca != 0) {
-                                const int i0 = 2 * nf + e, i1 = 8 + 2 * nf + e;
-                                v0 = fma(static_cast<double>(ca),
-                                         __hiloint2double(static_cast<int>(t[2 * i0 + 1]),
-                                                          static_cast<int>(t[2 * i0])), v0);
-                                v1 = fma(static_cast<double>(ca),
-                                         __hiloint2double(static_cast<int>(t[2 * i1 + 1]),
-                                                          static_cast<int>(t[2 * i1])), v1);
-                            }
+                            const double v0 = v[2 * nf + e], v1 = v[8 + 2 * nf + e];
                             const int row = mrow0 + 16 * h;
                             const int col = ncol0 + 8 * nf + (e ? c1 : c0);
                             if (col >= Cc) continue;

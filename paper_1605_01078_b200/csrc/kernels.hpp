@@ -148,13 +148,13 @@ struct alignas(64) MMParams {
     // units instead of delaying a fixed list; units are still taken in increasing
     // order, so ticket waits (which point at smaller units) cannot deadlock
     int* unit_counter;
-    // Product pairs (ticketed fused-epilogue grid): a unit is (tile, pair j) covering
-    // products [pair_lo[j], pair_lo[j + 1]) -- one or two products whose destination
-    // sets overlap (the host orders them adjacently).  The first product's accumulator
-    // is parked in tensor memory (tcgen05.st) while the second's mainloop runs; the
-    // epilogue then applies alpha (g1 M1 + g2 M2) to each destination with ONE
-    // reduce-add, so a shared destination is read and written once instead of twice.
-    // Tickets count pairs.  0 = one product per unit.
+    // Product groups (ticketed fused-epilogue grid): a unit is (tile, group j) covering
+    // products [pair_lo[j], pair_lo[j + 1]) -- one to three products whose destination
+    // sets overlap (the host orders them adjacently).  The first products' accumulators
+    // are parked in tensor memory (tcgen05.st) while the last one's mainloop runs; the
+    // epilogue then applies alpha (g1 M1 + g2 M2 + g3 M3) to each destination with ONE
+    // update, so a shared destination is read and written once instead of two or three
+    // times.  Tickets count groups.  0 = one product per unit.
     int pair_mode;
     int npairs;
     int8_t pair_lo[kMaxProducts + 1];
