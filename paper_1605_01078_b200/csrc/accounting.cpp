@@ -367,7 +367,14 @@ static double predict_core(strassen_variant v, int L, long m, long n, long k, in
         launches += 1;
     } else {  // fused epilogue: C read + written at L2 per C update (TMA reduce-adds),
         // mostly hidden: persistent single-term launches collect them a unit later
-        rmw_bytes = 16.0 * cu * qm * qn;
+        // short products of ABC / C run in groups of up to three products per unit whose
+        // shared destinations take one update (engine.cpp pair_products): the level-1/2
+        // tables' 12 / 144 updates become 7 / 90.  Credited where the updates bound the
+        // call (<= 8 k-tiles: 16384^2 x 256 ABC L2 9.1 -> 6.7 ms); at 16 k-tiles they
+        // are mostly hidden already (x 1024: 16.5 -> 16.1, profiles/r02_group14_*.log)
+        const bool grouped = (v == STRASSEN_ABC || v == STRASSEN_C) && mul > 1 &&
+                             std::ceil(qk / 16.0) <= 8;
+        rmw_bytes = 16.0 * (grouped ? (L == 1 ? 7.0 : 90.0) : cu) * qm * qn;
     }
     // the deferred (persistent, separate-stage) epilogue: single-term programs, and
     // fused ones whose sides are at most 2 terms with short products (engine.cpp)

@@ -220,6 +220,10 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+__device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -833,6 +837,20 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         // ================= TMA warpgroup (warps 8-11; one lane issues) =======
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
         if (warp != kConsumerWarps || lane != 0) return;
+        {   // warm the TMA descriptors of the first unit's first product and of the C
+            // quadrants (the first loads / reduce-adds otherwise pay the descriptor fetch)
+            const Unit U0 = decode_unit(P, blockIdx.x);
+            if (U0.p_hi > U0.p_lo) {
+                const ProductDesc& pd0 = P.prod[U0.p_lo];
+                for (int u = 0; u < pd0.na; ++u)
+                    prefetch_tensormap(pd0.half ? &P.tmAh[pd0.aq[u]] : &P.tmA[pd0.aq[u]]);
+                for (int u = 0; u < pd0.nb; ++u)
+                    prefetch_tensormap(pd0.half ? &P.tmBh[pd0.bq[u]] : &P.tmB[pd0.bq[u]]);
+            }
+            if (P.c_tma && P.mode == kEpiRMW)
+                for (int q = 0; q < kMaxQuad; ++q)
+                    if (P.crows[q] > 0 && P.ccols[q] > 0) prefetch_tensormap(&P.tmC[q]);
+        }
         uint32_t s = 0, phase = 0;
         for (int unit = blockIdx.x; unit < n_units; unit = producer_next(unit)) {
         const Unit U = decode_unit(P, unit);
