@@ -173,3 +173,29 @@ def test_device_entry_rejects_host_operands_before_staging(cuda):
     assert ei.value.status == S.ERR_PARAM
     assert ctx.workspace_bytes() == 0
     ctx.close()
+
+
+@pytest.mark.parametrize("variant,level", [("abc", 1), ("abc", 2), ("c", 1), ("c", 2)])
+@pytest.mark.parametrize("shape", [(6144, 6144, 512), (4117, 4100, 1030), (3000, 5000, 256)])
+def test_product_groups_in_tensor_memory(cuda, variant, level, shape):
+    """Short products of ABC / C run in groups of up to three per unit (the first ones
+    parked in TMEM) with one combined update per destination: against cuBLAS, bitwise
+    repeatable, and bitwise the same whether C takes the TMA reduce-add epilogue (even
+    ldc) or the register path (odd ldc) -- alpha = 1, where both round once."""
+    import torch
+    m, n, k = shape
+    A, B, C0 = _dev(m, n, k, seed=m + n + k + level)
+    ref = C0 + A @ B
+    ctx = S.Ctx()
+    outs = []
+    for ld in (m + (m & 1), m + (m & 1), m | 1):  # even ldc twice, then odd ldc
+        big = torch.zeros((n, ld), dtype=torch.float64, device="cuda").t()
+        C = big[:m, :]
+        C.copy_(C0)
+        ctx.gemm_device(variant, level, 1.0, A, B, C)
+        torch.cuda.synchronize()
+        outs.append(C.clone())
+    ctx.close()
+    assert _normwise(outs[0], ref, A, B) <= (5e-12 if level == 2 else 1e-12)
+    assert torch.equal(outs[0], outs[1])
+    assert torch.equal(outs[0], outs[2]), (variant, level, shape)
