@@ -378,7 +378,7 @@ static double predict_core(strassen_variant v, int L, long m, long n, long k, in
     }
     // the deferred (persistent, separate-stage) epilogue: single-term programs, and
     // fused ones whose sides are at most 2 terms with short products (engine.cpp)
-    const bool deferred = !fused_sums || (L == 2 && std::ceil(qk / 16.0) <= 24);
+    const bool deferred = !fused_sums || (L == 2 && std::ceil(qk / 16.0) <= 8);
     t += bytes / BW + rmw_bytes / (!c_vec ? 4.6e12 : deferred ? 20e12 : 10e12) +
          launches * launch;
     return t;

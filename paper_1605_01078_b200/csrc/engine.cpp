@@ -554,11 +554,13 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
         // fused sums of <= 2 terms: persistent with the separate stage beside a 6-slot
         // ring only for short products, where the exposed per-unit epilogue outweighs
         // the shallower ring (profiles/r02_sep2_{0,1}.log: 32768^2 x 1024 ABC L2
-        // 69.6 -> 64.4 ms, 16384^2 x 256 10.0 -> 8.9; but 16384^3 ABC L1 227 -> 261
-        // and 32768^2 x 1024 ABC L1, 32 k-tiles, 64.9 -> 69.0)
+        // 69.6 -> 64.4 ms, 16384^2 x 256 10.0 -> 8.9; but 16384^3 ABC L1 227 -> 261).
+        // With product groups (longer units) only up to 8 k-tiles pays
+        // (profiles/r02_sep2kt_*.log: 16384^2 x 256 ABC L2 7.18 -> 6.74 ms at 4 k-tiles,
+        // but 32768^2 x 1024, 16 k-tiles, 63.1 -> 64.4)
         static const int sep2_kt = [] {
             const char* v = std::getenv("STRASSEN_B200_SEP2_KT");  // k-tiles (experiments)
-            return v ? std::atoi(v) : 24;
+            return v ? std::atoi(v) : 8;
         }();
         P.sep_stage = bulk_units && sep_on && (maxt == 1 || (maxt == 2 && P.ktiles <= sep2_kt))
                           ? 1 : 0;
