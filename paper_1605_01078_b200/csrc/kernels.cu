@@ -220,10 +220,6 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
-__device__ __forceinline__ void prefetch_tensormap(const CUtensorMap* map) {
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
-}
-
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -659,13 +655,15 @@ struct Unit {
     int piece, npieces;
     int tk;  // ticket value of the unit's C update: its product, or its pair (pair_mode)
 };
+template <bool GROUPS>
 __device__ __forceinline__ int unit_count(const MMParams& P) {
     if (P.streamk) return P.grid_cap * P.sk_maxp;
-    if (P.pair_mode) return P.tiles_m * P.tiles_n * P.npairs;
+    if (GROUPS) return P.tiles_m * P.tiles_n * P.npairs;
     return P.tiles_m * P.tiles_n * (P.split ? P.nprod * P.ksplit : 1);
 }
 // unit -> (tile, product, k-chunk) in split mode, tile (all products) otherwise;
 // tiles in grouped raster order (group_m tile rows share B column panels in L2)
+template <bool GROUPS>
 __device__ __forceinline__ Unit decode_unit(const MMParams& P, int bid) {
     Unit U;
     U.p_lo = 0;
@@ -708,8 +706,8 @@ __device__ __forceinline__ Unit decode_unit(const MMParams& P, int bid) {
         U.p_lo = rem / gt;
         U.p_hi = U.p_lo + 1;
         bid = grp * G + rem % gt;
-    } else if (P.pair_mode) {
-        // (tile, pair) units, pair-major: the ticket a unit waits for, (t, j - 1), has
+    } else if (GROUPS) {
+        // (tile, group) units, group-major: the ticket a unit waits for, (t, j - 1), has
         // a smaller index
         const int ntiles = P.tiles_m * P.tiles_n;
         U.tk = bid / ntiles;
@@ -727,7 +725,7 @@ __device__ __forceinline__ Unit decode_unit(const MMParams& P, int bid) {
         U.npieces = P.ksplit;
         bid %= ntiles;
     }
-    if (!P.pair_mode) U.tk = U.p_lo;
+    if (!GROUPS) U.tk = U.p_lo;
     const int per_group = P.group_m * P.tiles_n;
     const int grp = bid / per_group;
     const int first_m = grp * P.group_m;
@@ -752,7 +750,9 @@ __device__ __forceinline__ Unit decode_unit(const MMParams& P, int bid) {
 // start of its next epilogue (or after its last unit).  A CTA always releases
 // its deferred ticket before it waits on any ticket, so the ordering argument
 // above still holds.
-template <int MAXT, bool PERSIST, int RING>
+// GROUPS: the launch runs product groups (MMParams::pair_mode); the other
+// instantiations carry none of their tensor-memory and multi-coefficient epilogue code
+template <int MAXT, bool PERSIST, int RING, bool GROUPS>
 __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__ MMParams P) {
     constexpr bool SEP = RING != kRawSlots;  // separate stage, deferred completion
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -772,7 +772,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
 
     // PERSIST = false: exactly one unit per CTA (keeps the 4-term instantiation,
     // which runs at the register limit, free of the loop state)
-    const int n_units = PERSIST ? unit_count(P) : static_cast<int>(blockIdx.x) + 1;
+    const int n_units = PERSIST ? unit_count<GROUPS>(P) : static_cast<int>(blockIdx.x) + 1;
     const bool persistent = PERSIST && static_cast<int>(gridDim.x) < n_units;
     const bool dyn = persistent && P.unit_counter != nullptr && !P.streamk;
 
@@ -788,20 +788,25 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
     }
-    // pair_mode: warp 0 (a DMMA warp, which also frees it) allocates the tensor memory
-    // the first product of a pair is parked in
-    __shared__ uint32_t tmem_base_s;
-    if (P.pair_mode && warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         smem_u32(&tmem_base_s)),
-                     "n"(kTmemCols)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    // GROUPS: warp 0 (a DMMA warp, which also frees it) allocates the tensor memory
+    // the first products of a group are parked in
+    uint32_t tmem_base = 0u;
+    if constexpr (GROUPS) {
+        __shared__ uint32_t tmem_base_s;
+        if (warp == 0) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(&tmem_base_s)),
+                         "n"(kTmemCols)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        tmem_base = tmem_base_s;
+    } else {
+        __syncthreads();
     }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem_base = P.pair_mode ? tmem_base_s : 0u;
     // Unit sequence of this CTA: blockIdx.x first; then either a fixed stride of
     // gridDim.x, or (dyn) units taken from the global counter, in increasing order
     // across the grid.  The producer takes a unit when it starts streaming its tiles
@@ -837,23 +842,9 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         // ================= TMA warpgroup (warps 8-11; one lane issues) =======
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
         if (warp != kConsumerWarps || lane != 0) return;
-        {   // warm the TMA descriptors of the first unit's first product and of the C
-            // quadrants (the first loads / reduce-adds otherwise pay the descriptor fetch)
-            const Unit U0 = decode_unit(P, blockIdx.x);
-            if (U0.p_hi > U0.p_lo) {
-                const ProductDesc& pd0 = P.prod[U0.p_lo];
-                for (int u = 0; u < pd0.na; ++u)
-                    prefetch_tensormap(pd0.half ? &P.tmAh[pd0.aq[u]] : &P.tmA[pd0.aq[u]]);
-                for (int u = 0; u < pd0.nb; ++u)
-                    prefetch_tensormap(pd0.half ? &P.tmBh[pd0.bq[u]] : &P.tmB[pd0.bq[u]]);
-            }
-            if (P.c_tma && P.mode == kEpiRMW)
-                for (int q = 0; q < kMaxQuad; ++q)
-                    if (P.crows[q] > 0 && P.ccols[q] > 0) prefetch_tensormap(&P.tmC[q]);
-        }
         uint32_t s = 0, phase = 0;
         for (int unit = blockIdx.x; unit < n_units; unit = producer_next(unit)) {
-        const Unit U = decode_unit(P, unit);
+        const Unit U = decode_unit<GROUPS>(P, unit);
         const int m0 = U.tm * kBM, n0 = U.tn * kBN;
         const int kt_lo = U.kt_lo, kt_hi = U.kt_hi;
         for (int p = U.p_lo; p < U.p_hi; ++p) {
@@ -948,7 +939,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     };
 
     for (int unit = blockIdx.x; unit < n_units; unit = consumer_next(unit)) {
-    const Unit U = decode_unit(P, unit);
+    const Unit U = decode_unit<GROUPS>(P, unit);
     const int tm = U.tm, tn = U.tn, p_lo = U.p_lo, p_hi = U.p_hi;
     const int kt_lo = U.kt_lo, kt_hi = U.kt_hi;
     for (int p = p_lo; p < p_hi; ++p) {
@@ -1079,12 +1070,14 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             }
         }
 
-        // pair_mode: the first products of a group wait in tensor memory for the last
-        if (P.pair_mode && p + 1 < p_hi) {
-            tmem_park(tmem_base, warp, p - p_lo, acc);
-            continue;
+        // product groups: the first products of a group wait in tensor memory for the last
+        if constexpr (GROUPS) {
+            if (p + 1 < p_hi) {
+                tmem_park(tmem_base, warp, p - p_lo, acc);
+                continue;
+            }
         }
-        const bool paired = P.pair_mode && p_hi - p_lo >= 2;
+        const bool paired = GROUPS && p_hi - p_lo >= 2;
         if (SEP && pend) collect();  // previous unit's reductions: complete, release its ticket
         // ---- epilogue of product p.  Accumulator (mf, nf, e) of lane (g, j)
         // is row 16(mf/2) + 2g + mf%2 and column 8nf + nperm(2j + e) of this
@@ -1106,7 +1099,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         // else takes the register read-modify-write below.
         // C tiles are reduced through the quadrants' tensor maps (tmC), which clip
         // partial tiles at the quadrant edge.
-        bool bulk = P.mode == kEpiRMW && P.c_tma && (p_hi - p_lo == 1 || P.pair_mode) &&
+        bool bulk = P.mode == kEpiRMW && P.c_tma && (p_hi - p_lo == 1 || GROUPS) &&
                     kt_hi - kt_lo <= P.bulk_max_kt && (SEP || !persistent) &&
                     U.npieces == 1;
         // the reduce-add clips rows at 16-byte granularity (microbench/tma_reduce_f64.cu):
@@ -1117,30 +1110,32 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         }
         // destinations of the unit and their coefficients on the parked products (da:
         // slot 0, dc: slot 1) and on the accumulator (db); a product alone has da = dc = 0
-        constexpr int kMaxDest = (kParkSlots + 1) * kMaxTerms;
+        // (GROUPS only: the other instantiations keep the single-product epilogue below)
+        constexpr int kMaxDest = GROUPS ? (kParkSlots + 1) * kMaxTerms : 1;
         int nd = 0;
         int dq[kMaxDest];
         int8_t da[kMaxDest], db[kMaxDest], dc[kMaxDest];
-        for (int pp = paired ? p_lo : p; pp <= p; ++pp) {
-            const ProductDesc& px = P.prod[pp];
-            const int k = pp == p ? 2 : pp - p_lo;  // slot 0, slot 1, accumulator
-            for (int u = 0; u < px.nc; ++u) {
-                int i = 0;
-                while (i < nd && dq[i] != px.cq[u]) ++i;
-                if (i == nd) {
-                    dq[nd] = px.cq[u];
-                    da[nd] = db[nd] = dc[nd] = 0;
-                    ++nd;
+        if constexpr (GROUPS) {
+            for (int pp = paired ? p_lo : p; pp <= p; ++pp) {
+                const ProductDesc& px = P.prod[pp];
+                const int k = pp == p ? 2 : pp - p_lo;  // slot 0, slot 1, accumulator
+                for (int u = 0; u < px.nc; ++u) {
+                    int i = 0;
+                    while (i < nd && dq[i] != px.cq[u]) ++i;
+                    if (i == nd) {
+                        dq[nd] = px.cq[u];
+                        da[nd] = db[nd] = dc[nd] = 0;
+                        ++nd;
+                    }
+                    (k == 0 ? da : k == 1 ? dc : db)[i] = px.cs[u];
                 }
-                (k == 0 ? da : k == 1 ? dc : db)[i] = px.cs[u];
+            }
+            for (int i = 0; i < nd && bulk; ++i) {  // (the first products' destinations too)
+                const int R = P.crows[dq[i]];
+                bulk = (R & 1) == 0 || tm * kBM + kBM <= R;
             }
         }
-        for (int i = 0; i < nd && bulk; ++i) {  // (the first product's destinations too)
-            const int R = P.crows[dq[i]];
-            bulk = (R & 1) == 0 || tm * kBM + kBM <= R;
-        }
         if (bulk) {
-            int done = 0;  // destinations already issued (bit mask)
             // stage: 8 boxes of 16 rows x 128 columns (16 KB each, 128-byte swizzle:
             // column c at c*128, 16-byte chunk (row%16)/2 ^ c%8) -- conflict-free for
             // the fragment layout (chunk g ^ nperm(2j+e)%8 covers all 8 per quarter-warp)
@@ -1148,52 +1143,93 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             const bool ticketed = P.tickets != nullptr;
             bool issued = false;
             if (!SEP) consumer_bar();  // every warp is done reading the ring before it is reused
-            // one pass per distinct (da, db): stage alpha (da Mparked + db M), then one
-            // reduce-add per destination with that pair of coefficients
-            for (int first = 0; first < nd; ++first) {
-                if (done & (1 << first)) continue;
-                const int ca = da[first], cb = db[first], cc = dc[first];
-                if (issued) {  // previous pass's reductions must have read the stage
-                    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                    consumer_bar();
-                }
+            // DMMA warp w hands box w (rows 16w..16w+15) of every destination to the TMA
+            // engine: one tensor reduce-add each (per-column 1-D bulk reductions issued
+            // 128 x nc uniform-datapath instructions per tile)
+            static_assert(kConsumerWarps * 16 == kBM, "one 16-row box per warp");
+            if constexpr (GROUPS) {
+                // one pass per distinct (da, dc, db): stage alpha (da M0 + dc M1 + db M), then
+                // one reduce-add per destination with those coefficients
+                int done = 0;  // destinations already issued (bit mask)
+                for (int first = 0; first < nd; ++first) {
+                    if (done & (1 << first)) continue;
+                    const int ca = da[first], cb = db[first], cc = dc[first];
+                    if (issued) {  // previous pass's reductions must have read the stage
+                        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                        consumer_bar();
+                    }
 #pragma unroll
-                for (int h = 0; h < 4; ++h) {
-                    double v[16];
-                    group_values(tmem_base, warp, h, ca, cc, cb, acc, v);
+                    for (int h = 0; h < 4; ++h) {
+                        double v[16];
+                        group_values(tmem_base, warp, h, ca, cc, cb, acc, v);
+#pragma unroll
+                        for (int nf = 0; nf < 4; ++nf)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                const int col = wn * 32 + 8 * nf + (e ? c1 : c0);
+                                *reinterpret_cast<double2*>(stage + (wm * 4 + h) * 16384 + col * 128 +
+                                                            ((g ^ (col & 7)) << 4)) =
+                                    make_double2(P.alpha * v[2 * nf + e], P.alpha * v[8 + 2 * nf + e]);
+                            }
+                    }
+                    consumer_fence();  // generic smem writes before the async-proxy reads
+                    if (!issued && ticketed) {
+                        if (threadIdx.x == 0) wait_ticket(P, U.tk, tm, tn);
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                    }
+                    consumer_bar();
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                    for (int i = first; i < nd; ++i) {
+                        if (da[i] != ca || db[i] != cb || dc[i] != cc) continue;
+                        done |= 1 << i;
+                        if (lane == 0)
+                            tma_reduce_add_2d(&P.tmC[dq[i]], tm * kBM + 16 * warp, tn * kBN,
+                                              stage + warp * 16384);
+                    }
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    issued = true;
+                }
+            } else {
+                for (int pass = 0; pass < 2; ++pass) {  // destinations with coefficient +1, then -1
+                    int any = 0;
+                    for (int u = 0; u < pd.nc; ++u) any |= (pd.cs[u] > 0) == (pass == 0);
+                    if (!any) continue;
+                    if (issued) {  // previous pass's reductions must have read the stage
+                        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                        consumer_bar();
+                    }
+                    const double sc = P.alpha * (pass == 0 ? 1.0 : -1.0);
 #pragma unroll
                     for (int nf = 0; nf < 4; ++nf)
 #pragma unroll
-                        for (int e = 0; e < 2; ++e) {
-                            const int col = wn * 32 + 8 * nf + (e ? c1 : c0);
-                            *reinterpret_cast<double2*>(stage + (wm * 4 + h) * 16384 + col * 128 +
-                                                        ((g ^ (col & 7)) << 4)) =
-                                make_double2(P.alpha * v[2 * nf + e], P.alpha * v[8 + 2 * nf + e]);
-                        }
-                }
-                consumer_fence();  // generic smem writes before the async-proxy reads
-                if (!issued && ticketed) {
-                    if (threadIdx.x == 0) wait_ticket(P, U.tk, tm, tn);
+                        for (int h = 0; h < 4; ++h)
+#pragma unroll
+                            for (int e = 0; e < 2; ++e) {
+                                const int col = wn * 32 + 8 * nf + (e ? c1 : c0);
+                                *reinterpret_cast<double2*>(stage + (wm * 4 + h) * 16384 + col * 128 +
+                                                            ((g ^ (col & 7)) << 4)) =
+                                    make_double2(sc * acc[2 * h][nf][e], sc * acc[2 * h + 1][nf][e]);
+                            }
+                    consumer_fence();  // generic smem writes before the async-proxy reads
+                    if (!issued && ticketed) {
+                        if (threadIdx.x == 0) wait_ticket(P, U.tk, tm, tn);
+                        asm volatile("fence.proxy.async.global;" ::: "memory");
+                    }
+                    consumer_bar();
                     asm volatile("fence.proxy.async.global;" ::: "memory");
+                    if (lane == 0) {
+                        for (int u = 0; u < pd.nc; ++u) {
+                            if ((pd.cs[u] > 0) != (pass == 0)) continue;
+                            tma_reduce_add_2d(&P.tmC[pd.cq[u]], tm * kBM + 16 * warp, tn * kBN,
+                                              stage + warp * 16384);
+                        }
+                    }
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    issued = true;
                 }
-                consumer_bar();
-                // DMMA warp w hands box w (rows 16w..16w+15) of every destination
-                // to the TMA engine: one tensor reduce-add each (per-column 1-D bulk
-                // reductions issued 128 x nc uniform-datapath instructions per tile)
-                static_assert(kConsumerWarps * 16 == kBM, "one 16-row box per warp");
-                asm volatile("fence.proxy.async.global;" ::: "memory");
-                for (int i = first; i < nd; ++i) {
-                    if (da[i] != ca || db[i] != cb || dc[i] != cc) continue;
-                    done |= 1 << i;
-                    if (lane == 0)
-                        tma_reduce_add_2d(&P.tmC[dq[i]], tm * kBM + 16 * warp, tn * kBN,
-                                          stage + warp * 16384);
-                }
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                issued = true;
             }
             // the last product (pair) of the launch has no ticket successor
-            const bool succ = ticketed && U.tk + 1 < (P.pair_mode ? P.npairs : P.nprod);
+            const bool succ = ticketed && U.tk + 1 < (GROUPS ? P.npairs : P.nprod);
             if (SEP && P.sep_defer) {  // completion collected at the next epilogue (or after the loop)
                 pend = true;
                 pend_p = succ ? U.tk : -1;
@@ -1215,8 +1251,8 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             }
             continue;  // next product (none: single-product CTA)
         }
-        if (paired) {
-            // ---- a pair's update through registers (C layouts the reduce-adds cannot
+        if (GROUPS && paired) {
+            // ---- a group's update through registers (C layouts the reduce-adds cannot
             // take): C += alpha (da Mparked + db M) per destination, in pair order --
             // per element the same arithmetic as the staged values of the bulk path
             if (P.tickets) {
@@ -1426,7 +1462,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     }
     }  // unit
     if (SEP && pend) collect();
-    if (P.pair_mode) {  // every warp is done with tensor memory; warp 0 frees it
+    if constexpr (GROUPS) {  // every warp is done with tensor memory; warp 0 frees it
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         consumer_bar();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -1860,8 +1896,15 @@ __global__ void scale_kernel(double* c, long rows, long cols, long long rs, long
 
 }  // namespace
 
+template <int MAXT, bool PERSIST, int RING, bool GROUPS>
+static cudaError_t launch_mm_g(const MMParams& p, cudaStream_t s);
 template <int MAXT, bool PERSIST, int RING = kRawSlots>
 static cudaError_t launch_mm_t(const MMParams& p, cudaStream_t s) {
+    return p.pair_mode ? launch_mm_g<MAXT, PERSIST, RING, true>(p, s)
+                       : launch_mm_g<MAXT, PERSIST, RING, false>(p, s);
+}
+template <int MAXT, bool PERSIST, int RING, bool GROUPS>
+static cudaError_t launch_mm_g(const MMParams& p, cudaStream_t s) {
     constexpr int smem = RING == kRawSlots ? kMMSmemBytes : mm_sep_smem_bytes(RING);
     // the > 48 KB dynamic shared-memory opt-in is per device context: once per device
     static std::atomic<uint64_t> attr_set{0};
@@ -1869,7 +1912,7 @@ static cudaError_t launch_mm_t(const MMParams& p, cudaStream_t s) {
     if (cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
     const uint64_t bit = 1ull << (dev & 63);
     if (!(attr_set.load(std::memory_order_acquire) & bit)) {
-        cudaError_t e = cudaFuncSetAttribute(mm_kernel<MAXT, PERSIST, RING>,
+        cudaError_t e = cudaFuncSetAttribute(mm_kernel<MAXT, PERSIST, RING, GROUPS>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr_set.fetch_or(bit, std::memory_order_release);
@@ -1879,7 +1922,7 @@ static cudaError_t launch_mm_t(const MMParams& p, cudaStream_t s) {
     // stream-K: exactly grid_cap CTAs (the unit decode assumes it)
     const int grid = PERSIST && p.streamk ? p.grid_cap
                      : PERSIST && p.grid_cap > 0 && p.grid_cap < units ? p.grid_cap : units;
-    mm_kernel<MAXT, PERSIST, RING><<<grid, kThreads, smem, s>>>(p);
+    mm_kernel<MAXT, PERSIST, RING, GROUPS><<<grid, kThreads, smem, s>>>(p);
     return cudaGetLastError();
 }
 

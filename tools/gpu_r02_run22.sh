@@ -1,0 +1,6 @@
+for rep in 1 2; do
+for lib in libstrassen_b200_cd8b6d6.so libstrassen_b200.so; do
+  echo "== $lib rep $rep"
+  STRASSEN_B200_LIB=$lib FMAX=2 REPS=3 timeout 300 python tools/fuse_probe.py naive 2 16384 16384 16384 dgemm 0 16384 16384 16384 c 2 16384 16384 16384 abc 2 16384 16384 256 2>&1 | cut -c1-120
+done; done > gpurun_out/r02_regress_ab2.log 2>&1
+timeout 1800 python -m pytest tests -m gpu -x -q > gpurun_out/r02_gputest22.log 2>&1
