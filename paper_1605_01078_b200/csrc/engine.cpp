@@ -301,6 +301,16 @@ bool is_device_pointer(const void* p) {
     return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
 }
 
+// SB200_TRACE builds: the device buffer the next mm launch records CTA events into
+// (STRASSEN_B200_TRACE_PTR, an address set by tools/cta_trace.py; read per launch)
+unsigned long long* trace_buffer() {
+#ifdef SB200_TRACE
+    if (const char* v = std::getenv("STRASSEN_B200_TRACE_PTR"))
+        return reinterpret_cast<unsigned long long*>(std::strtoull(v, nullptr, 0));
+#endif
+    return nullptr;
+}
+
 // A zeroed unit counter for a persistent mm launch on s (MMParams::unit_counter):
 // distinct per launch within a call (windows run on two streams), reused across
 // calls, which are ordered after each other (gemm_impl's ev_last).
@@ -582,6 +592,7 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
                           ? 1 : 0;
         P.grid_cap = cap(bulk_units && !P.sep_stage);
         if (P.grid_cap > 0) P.unit_counter = next_unit_counter(e, s);
+        P.trace = trace_buffer();
         e.prof_begin("mm_kernel", s);
         ck(launch_mm(P, s), "mm_kernel");
         e.prof_end(s);
@@ -608,6 +619,7 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
         } else if (P.grid_cap > 0) {
             P.unit_counter = next_unit_counter(e, s);
         }
+        P.trace = trace_buffer();
         e.prof_begin("mm_kernel", s);
         ck(launch_mm(P, s), "mm_kernel (split, fused epilogue)");
         e.prof_end(s);
@@ -633,6 +645,7 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
     } else if (P.grid_cap > 0) {
         P.unit_counter = next_unit_counter(e, s);
     }
+    P.trace = trace_buffer();
     e.prof_begin("mm_kernel", s);
     ck(launch_mm(P, s), "mm_kernel (split)");
     e.prof_end(s);

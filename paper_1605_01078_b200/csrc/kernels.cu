@@ -750,6 +750,18 @@ __device__ __forceinline__ Unit decode_unit(const MMParams& P, int bid) {
 // start of its next epilogue (or after its last unit).  A CTA always releases
 // its deferred ticket before it waits on any ticket, so the ordering argument
 // above still holds.
+#ifdef SB200_TRACE
+__device__ __forceinline__ void trace_event(const MMParams& P, int slot) {
+    if (P.trace && threadIdx.x == 0 && slot < 32) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        P.trace[blockIdx.x * 32 + slot] = t;
+    }
+}
+#else
+__device__ __forceinline__ void trace_event(const MMParams&, int) {}
+#endif
+
 // GROUPS: the launch runs product groups (MMParams::pair_mode); the other
 // instantiations carry none of their tensor-memory and multi-coefficient epilogue code
 template <int MAXT, bool PERSIST, int RING, bool GROUPS>
@@ -938,7 +950,10 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         pend = false;
     };
 
+    trace_event(P, 0);
+    int trace_i = 0;
     for (int unit = blockIdx.x; unit < n_units; unit = consumer_next(unit)) {
+    trace_event(P, 1 + 2 * trace_i);
     const Unit U = decode_unit<GROUPS>(P, unit);
     const int tm = U.tm, tn = U.tn, p_lo = U.p_lo, p_hi = U.p_hi;
     const int kt_lo = U.kt_lo, kt_hi = U.kt_hi;
@@ -1078,6 +1093,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             }
         }
         const bool paired = GROUPS && p_hi - p_lo >= 2;
+        trace_event(P, 2 + 2 * trace_i);
         if (SEP && pend) collect();  // previous unit's reductions: complete, release its ticket
         // ---- epilogue of product p.  Accumulator (mf, nf, e) of lane (g, j)
         // is row 16(mf/2) + 2g + mf%2 and column 8nf + nperm(2j + e) of this
@@ -1460,8 +1476,10 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                     }
         }
     }
+    ++trace_i;
     }  // unit
     if (SEP && pend) collect();
+    trace_event(P, 31);
     if constexpr (GROUPS) {  // every warp is done with tensor memory; warp 0 frees it
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         consumer_bar();

@@ -155,6 +155,9 @@ struct alignas(64) MMParams {
     // epilogue then applies alpha (g1 M1 + g2 M2 + g3 M3) to each destination with ONE
     // update, so a shared destination is read and written once instead of two or three
     // times.  Tickets count groups.  0 = one product per unit.
+    // SB200_TRACE builds only (libstrassen_b200_trace.so): per-CTA %globaltimer events,
+    // 32 slots per CTA -- 0 entry, 31 exit, 1 + 2i / 2 + 2i unit i's start / epilogue start
+    unsigned long long* trace;
     int pair_mode;
     int npairs;
     int8_t pair_lo[kMaxProducts + 1];
