@@ -493,6 +493,40 @@ FusedPlan plan_fused(Engine& e, cudaStream_t s, const MMParams& P, bool force_sp
     return F;
 }
 
+// The stream pass of a split / store-mode plan: C_q += alpha gamma M_p over the window,
+// each quadrant's updates in table order.
+void build_stream_params(StreamParams& S, const MMParams& P, const FusedPlan& F,
+                         const std::vector<Terms>& dests, const std::vector<QuadView>& cq,
+                         const DView& C, double alpha, long r0, long r1, long c0, long c1) {
+    std::memset(&S, 0, sizeof(S));
+    S.rs_c = C.rs;
+    S.cs_c = C.cs;
+    S.alpha = alpha;
+    S.ldm = F.ldm;
+    S.mstride = F.mstride;
+    S.ksplit = F.sk_store ? 1 : F.ksplit;
+    S.nquad = static_cast<int>(cq.size());
+    S.qm = P.qm;
+    S.qn = P.qn;
+    S.c_vec = P.c_vec;
+    S.r0 = static_cast<int>(r0);
+    S.r1 = static_cast<int>(r1);
+    S.c0 = static_cast<int>(c0);
+    S.c1 = static_cast<int>(c1);
+    S.mbase = F.M;
+    for (size_t qi = 0; qi < cq.size(); ++qi) {
+        S.cptr[qi] = cq[qi].p;
+        S.crows[qi] = static_cast<int>(cq[qi].rows);
+        S.ccols[qi] = static_cast<int>(cq[qi].cols);
+    }
+    for (size_t p = 0; p < dests.size(); ++p)
+        for (const auto& [q, g] : dests[p]) {
+            S.src_prod[q][S.nsrc[q]] = static_cast<int8_t>(p);
+            S.src_coeff[q][S.nsrc[q]] = static_cast<int8_t>(g);
+            ++S.nsrc[q];
+        }
+}
+
 // Window [r0, r1) x [c0, c1) (quadrant coordinates, r0 / c0 tile multiples) of
 // the plan: the mm launch over those tiles and, in split mode, the stream pass.
 // wait_c() is called right before the first launch that touches C.
@@ -633,7 +667,9 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
     P.ldm = F.ldm;
     P.mstride = F.mstride;
     P.grid_cap = cap(false);
-    if (F.sk_store) {  // stream-K pieces; M_p fixed up by the last piece
+    StreamParams S;
+    build_stream_params(S, P, F, dests, cq, C, alpha, r0, r1, c0, c1);
+    if (F.sk_store) {  // stream-K pieces; M_p fixed up by piece 0 (kernels.cu)
         P.streamk = 1;
         P.sk_store = 1;
         P.sk_len = F.sk_len;
@@ -649,34 +685,6 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
     e.prof_begin("mm_kernel", s);
     ck(launch_mm(P, s), "mm_kernel (split)");
     e.prof_end(s);
-    StreamParams S;
-    std::memset(&S, 0, sizeof(S));
-    S.rs_c = C.rs;
-    S.cs_c = C.cs;
-    S.alpha = alpha;
-    S.ldm = F.ldm;
-    S.mstride = F.mstride;
-    S.ksplit = F.sk_store ? 1 : F.ksplit;
-    S.nquad = static_cast<int>(cq.size());
-    S.qm = P.qm;
-    S.qn = P.qn;
-    S.c_vec = P.c_vec;
-    S.r0 = static_cast<int>(r0);
-    S.r1 = static_cast<int>(r1);
-    S.c0 = static_cast<int>(c0);
-    S.c1 = static_cast<int>(c1);
-    S.mbase = F.M;
-    for (size_t qi = 0; qi < cq.size(); ++qi) {
-        S.cptr[qi] = cq[qi].p;
-        S.crows[qi] = static_cast<int>(cq[qi].rows);
-        S.ccols[qi] = static_cast<int>(cq[qi].cols);
-    }
-    for (size_t p = 0; p < dests.size(); ++p)
-        for (const auto& [q, g] : dests[p]) {
-            S.src_prod[q][S.nsrc[q]] = static_cast<int8_t>(p);
-            S.src_coeff[q][S.nsrc[q]] = static_cast<int8_t>(g);
-            ++S.nsrc[q];
-        }
     wait_c();  // first reader of C: its copy-in overlapped the products
     e.prof_begin("stream_gather_kernel", s);
     ck(launch_stream_update(S, s), "stream_update");

@@ -750,6 +750,64 @@ __device__ __forceinline__ Unit decode_unit(const MMParams& P, int bid) {
 // start of its next epilogue (or after its last unit).  A CTA always releases
 // its deferred ticket before it waits on any ticket, so the ordering argument
 // above still holds.
+// Register form of the row-pair stream pass for the full level-1 / level-2 tables:
+// the destination quadrants of every product are compile-time constants (the
+// one-level table, table.cpp:18-33, composed as table.cpp:47-67 does -- in
+// constexpr code here, so nothing is hand-entered twice), so the 4^L C
+// accumulators live in registers instead of shared memory (the shared-memory
+// form spends ~2 LDS/STS per update and was bound by them).  Per element the
+// updates are the same fma's in the same order: bitwise identical results.
+// The host uses it only when the call's (product -> destination quadrant) lists
+// equal the table's.
+struct StreamTab {
+    int np;
+    int nd[kMaxProducts];
+    int dq[kMaxProducts][kMaxQuad];
+};
+constexpr StreamTab stream_tab_l1() {
+    StreamTab t{};
+    // C updates of M0..M6 (quadrant 2 * row + col), table.cpp:18-33
+    const int d[7][2] = {{0, 3}, {2, 3}, {1, 3}, {0, 2}, {1, 0}, {3, -1}, {0, -1}};
+    t.np = 7;
+    for (int p = 0; p < 7; ++p) {
+        t.nd[p] = d[p][1] < 0 ? 1 : 2;
+        for (int u = 0; u < t.nd[p]; ++u) t.dq[p][u] = d[p][u];
+    }
+    return t;
+}
+constexpr StreamTab stream_tab_compose(const StreamTab& o, const StreamTab& in) {
+    StreamTab t{};
+    t.np = o.np * in.np;
+    for (int a = 0; a < o.np; ++a)
+        for (int b = 0; b < in.np; ++b) {
+            const int p = a * in.np + b;
+            t.nd[p] = 0;
+            for (int u = 0; u < o.nd[a]; ++u)
+                for (int v = 0; v < in.nd[b]; ++v) {
+                    const int oq = o.dq[a][u], iq = in.dq[b][v];
+                    const int row = 2 * (oq / 2) + iq / 2, col = 2 * (oq % 2) + iq % 2;
+                    t.dq[p][t.nd[p]++] = row * 4 + col;
+                }
+        }
+    return t;
+}
+// each product's destinations in ascending quadrant order, as the gather form lists
+// them (to_gather below); per C element the update order is unchanged (ascending p)
+constexpr StreamTab stream_tab_sorted(StreamTab t) {
+    for (int p = 0; p < t.np; ++p)
+        for (int a = 1; a < t.nd[p]; ++a)
+            for (int b = a; b > 0 && t.dq[p][b - 1] > t.dq[p][b]; --b) {
+                const int x = t.dq[p][b];
+                t.dq[p][b] = t.dq[p][b - 1];
+                t.dq[p][b - 1] = x;
+            }
+    return t;
+}
+constexpr StreamTab kStreamTab1 = stream_tab_sorted(stream_tab_l1());
+constexpr StreamTab kStreamTab2 = stream_tab_sorted(stream_tab_compose(stream_tab_l1(), stream_tab_l1()));
+template <int L>
+__host__ __device__ constexpr const StreamTab& stream_tab() { return L == 1 ? kStreamTab1 : kStreamTab2; }
+
 #ifdef SB200_TRACE
 __device__ __forceinline__ void trace_event(const MMParams& P, int slot) {
     if (P.trace && threadIdx.x == 0 && slot < 32) {
@@ -1309,12 +1367,20 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             continue;
         }
         if (P.arrive && U.npieces > 1) {
-            // ---- k-split / stream-K fixup: partial out, the last piece sums ----
-            // (partials in slots p * ksplit + piece; ksplit = slots per product);
-            // the RMW epilogue or (sk_store) the store of M_p follows
+            // ---- k-split / stream-K fixup: partials out, one piece sums them ----
+            // (partials in slots p * ksplit + piece; ksplit = slots per product); the RMW
+            // epilogue or (sk_store) the store of M_p follows.  M_p = P_0 + P_1 + ... in
+            // piece (k) order, the stream pass's order.
+            // Stream-K: piece 0 finishes the unit.  Its CTA reaches it last (a unit's head
+            // lies at the end of one CTA's range, its other pieces at the start of the
+            // next CTAs'), keeps its own partial in registers and waits for the others --
+            // safe because every stream-K CTA is resident and a non-zero piece never waits.
+            // k-chunk grids (CTAs may run in waves): the last piece to arrive sums them.
             const int s_idx = U.piece;
             const long long ldm = P.ldm;
-            {
+            int* cnt = P.arrive + (tm * P.ticket_ld + tn) * P.nprod + p;
+            const bool owner0 = P.streamk && s_idx == 0;
+            if (!owner0) {
                 double* Mo = P.mbase + P.part_off +
                              static_cast<long long>(p * P.ksplit + s_idx) * P.mstride;
 #pragma unroll
@@ -1330,21 +1396,29 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                             __stcg(reinterpret_cast<double2*>(dst),
                                    make_double2(acc[2 * h][nf][e], acc[2 * h + 1][nf][e]));
                         }
+                __threadfence();
+                consumer_bar();
             }
-            __threadfence();
-            consumer_bar();
             __shared__ int last_flag;
-            if (threadIdx.x == 0) {
-                int* cnt = P.arrive + (tm * P.ticket_ld + tn) * P.nprod + p;
-                last_flag = atomicAdd(cnt, 1) == U.npieces - 1;
+            if (owner0) {  // wait for pieces 1 .. npieces - 1
+                if (threadIdx.x == 0) {
+                    while (ld_relaxed_gpu(cnt) != U.npieces - 1) __nanosleep(64);
+                    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+                }
+                consumer_bar();
+            } else {
+                if (threadIdx.x == 0) {
+                    const int before = atomicAdd(cnt, 1);
+                    last_flag = !P.streamk && before == U.npieces - 1;
+                }
+                consumer_bar();
+                if (!last_flag) continue;  // another piece finishes this product
+                __threadfence();
             }
-            consumer_bar();
-            if (!last_flag) continue;  // another chunk finishes this product
-            __threadfence();
-            // M_p = P_0 + P_1 + ... in s order (the stream pass's order), read
-            // back from L2 (this CTA's own partial included)
+            // the other pieces' partials, read back from L2 and added in piece order
+            // (piece 0's own partial is its accumulator)
             const double* Mp = P.mbase + P.part_off + static_cast<long long>(p * P.ksplit) * P.mstride;
-            for (int sp = 0; sp < U.npieces; ++sp) {
+            for (int sp = owner0 ? 1 : 0; sp < U.npieces; ++sp) {
 #pragma unroll
                 for (int nf = 0; nf < 4; ++nf)
 #pragma unroll
@@ -1721,64 +1795,6 @@ stream_gather2_kernel(const __grid_constant__ StreamGatherParams P) {
             }
     }
 }
-
-// Register form of the row-pair stream pass for the full level-1 / level-2 tables:
-// the destination quadrants of every product are compile-time constants (the
-// one-level table, table.cpp:18-33, composed as table.cpp:47-67 does -- in
-// constexpr code here, so nothing is hand-entered twice), so the 4^L C
-// accumulators live in registers instead of shared memory (the shared-memory
-// form spends ~2 LDS/STS per update and was bound by them).  Per element the
-// updates are the same fma's in the same order: bitwise identical results.
-// The host uses it only when the call's (product -> destination quadrant) lists
-// equal the table's.
-struct StreamTab {
-    int np;
-    int nd[kMaxProducts];
-    int dq[kMaxProducts][kMaxQuad];
-};
-constexpr StreamTab stream_tab_l1() {
-    StreamTab t{};
-    // C updates of M0..M6 (quadrant 2 * row + col), table.cpp:18-33
-    const int d[7][2] = {{0, 3}, {2, 3}, {1, 3}, {0, 2}, {1, 0}, {3, -1}, {0, -1}};
-    t.np = 7;
-    for (int p = 0; p < 7; ++p) {
-        t.nd[p] = d[p][1] < 0 ? 1 : 2;
-        for (int u = 0; u < t.nd[p]; ++u) t.dq[p][u] = d[p][u];
-    }
-    return t;
-}
-constexpr StreamTab stream_tab_compose(const StreamTab& o, const StreamTab& in) {
-    StreamTab t{};
-    t.np = o.np * in.np;
-    for (int a = 0; a < o.np; ++a)
-        for (int b = 0; b < in.np; ++b) {
-            const int p = a * in.np + b;
-            t.nd[p] = 0;
-            for (int u = 0; u < o.nd[a]; ++u)
-                for (int v = 0; v < in.nd[b]; ++v) {
-                    const int oq = o.dq[a][u], iq = in.dq[b][v];
-                    const int row = 2 * (oq / 2) + iq / 2, col = 2 * (oq % 2) + iq % 2;
-                    t.dq[p][t.nd[p]++] = row * 4 + col;
-                }
-        }
-    return t;
-}
-// each product's destinations in ascending quadrant order, as the gather form lists
-// them (to_gather below); per C element the update order is unchanged (ascending p)
-constexpr StreamTab stream_tab_sorted(StreamTab t) {
-    for (int p = 0; p < t.np; ++p)
-        for (int a = 1; a < t.nd[p]; ++a)
-            for (int b = a; b > 0 && t.dq[p][b - 1] > t.dq[p][b]; --b) {
-                const int x = t.dq[p][b];
-                t.dq[p][b] = t.dq[p][b - 1];
-                t.dq[p][b - 1] = x;
-            }
-    return t;
-}
-constexpr StreamTab kStreamTab1 = stream_tab_sorted(stream_tab_l1());
-constexpr StreamTab kStreamTab2 = stream_tab_sorted(stream_tab_compose(stream_tab_l1(), stream_tab_l1()));
-template <int L>
-__host__ __device__ constexpr const StreamTab& stream_tab() { return L == 1 ? kStreamTab1 : kStreamTab2; }
 
 template <int L, int PR, int D>
 __device__ __forceinline__ void stream_upd(double2 (&acc)[L == 1 ? 4 : 16], const double2& v,
