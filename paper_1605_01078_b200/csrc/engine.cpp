@@ -356,7 +356,8 @@ FusedPlan plan_fused(Engine& e, cudaStream_t s, const MMParams& P, bool force_sp
                      int nprod_plan = 0, double terms_plan = 0.0, bool windowed = false) {
     FusedPlan F;
     const int ntiles = P.tiles_m * P.tiles_n;
-    const int sms = e.num_sms > 0 ? e.num_sms : 148;
+    // (narrow tiles: two resident CTAs per SM)
+    const int sms = (e.num_sms > 0 ? e.num_sms : 148) * (P.narrow ? 2 : 1);
     double terms = 0.0;  // mean operand terms per side: fused sums lengthen a k-tile
     for (int p = 0; p < P.nprod; ++p) terms += 0.5 * (P.prod[p].na + P.prod[p].nb);
     terms /= P.nprod > 0 ? P.nprod : 1;
@@ -542,12 +543,13 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
     }();
     auto cap = [&](bool bulk_units) {
         const bool on = persist_env >= 0 ? persist_env != 0 : !bulk_units;
-        return on ? (e.num_sms > 0 ? e.num_sms : 148) : 0;
+        return on ? (e.num_sms > 0 ? e.num_sms : 148) * (P.narrow ? 2 : 1) : 0;
     };
+    const int bn = P.narrow ? kNarrowBN : kBN;
     P.tm0 = static_cast<int>(r0 / kBM);
     P.tiles_m = static_cast<int>(ceil_div(r1 - r0, kBM));
-    P.tn0 = static_cast<int>(c0 / kBN);
-    P.tiles_n = static_cast<int>(ceil_div(c1 - c0, kBN));
+    P.tn0 = static_cast<int>(c0 / bn);
+    P.tiles_n = static_cast<int>(ceil_div(c1 - c0, bn));
     if (!F.split) {
         wait_c();  // fused epilogue reads C
         P.mode = kEpiRMW;
@@ -715,7 +717,7 @@ void pair_products(const Engine& e, MMParams& P, const FusedPlan& F, strassen_va
         // x 4096 (128 k-tiles) 62.2 -> 62.4 (profiles/r02_pair12_*.log, r02_pair13_*.log)
         return v ? std::atoi(v) : 64;
     }();
-    if (pair_env == 0 || F.split || !F.tickets || P.nprod < 2) return;
+    if (pair_env == 0 || F.split || !F.tickets || P.nprod < 2 || P.narrow) return;
     if (variant != STRASSEN_ABC && variant != STRASSEN_C) return;
     if (pair_env < 0 && P.ktiles > pair_kt) return;
     // (independent of C's layout and of the fused-term setting, so host and device calls
@@ -993,6 +995,36 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
 
     MMParams P;
     std::memset(&P, 0, sizeof(P));
+    // Narrow tiles (kernels.hpp kNarrowBN: 128 x 64, two CTAs per SM) for small
+    // single-term programs: a CTA's fixed costs (pipeline fill, fixup, epilogue) then
+    // overlap the other CTA's mainloop.  Measured (profiles/r02_narrow_sweep.log,
+    // back-to-back us wide -> narrow): DGEMM 1024^3 90.5 -> 86.8, 768^3 61.4 -> 57.1;
+    // C L2 1024^3 130.9 -> 126.9, 1280^3 228.1 -> 208.8, 2048^3 570.0 -> 532.7, 2560^3
+    // 989.8 -> 943.2; C L1 1280^3 158.3 -> 154.9; neutral to slower from 1536^3
+    // (DGEMM) / 3072^3 (C L2).  Fused-sum programs (ABC, AB) lose (1024^3 ABC L1
+    // 89.9 -> 94.3: a fused k-step streams 1.5x the operand bytes per flop) and keep
+    // 128 x 128 tiles.  Naive stays under the 4 waves from which host calls run in
+    // windows (plan_windows), so host and device calls plan alike.  Decided on the
+    // problem alone (not on the fused-term setting, which must not change a bit).
+    {
+        static const int narrow_env = [] {
+            const char* v = std::getenv("STRASSEN_B200_NARROW");  // 0 / 1 / -1 auto (experiments)
+            return v ? std::atoi(v) : -1;
+        }();
+        const long sms = e.num_sms > 0 ? e.num_sms : 148;
+        const long tiles = ceil_div(qm, kBM) * ceil_div(qn, kBN);
+        const long units = tiles * (L == 0 ? 1 : L == 1 ? 7 : 49);
+        const long ktiles = ceil_div(qk, kBK);
+        const bool one_window = !win || win->rows * win->cols <= 1;
+        bool pick = false;
+        if (ktiles <= 128) {
+            if (variant == STRASSEN_DGEMM) pick = 3 * tiles < 2 * sms;
+            else if (variant == STRASSEN_C) pick = units < 10 * sms;
+            else if (variant == STRASSEN_NAIVE) pick = units < 4 * sms;
+        }
+        P.narrow = one_window && (narrow_env > 0 || (narrow_env < 0 && pick)) ? 1 : 0;
+    }
+    const int bn = P.narrow ? kNarrowBN : kBN;
     for (int I = 0; I < side; ++I)
         for (int J = 0; J < side; ++J) {
             const int qi = I * side + J;
@@ -1001,11 +1033,11 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
                            ta.ld, 16, kBK, 128);
             if (b_live[qi])
                 encode_map(&P.tmB[qi], quad_origin(tb, I, J), quad_rows(tb, I), quad_cols(tb, J),
-                           tb.ld, kBK, kBN, 128);
-            if (L == 2 && a_live[qi])  // half-k maps for the (4,4) products
+                           tb.ld, kBK, bn, 128);
+            if (L == 2 && a_live[qi] && !P.narrow)  // half-k maps for the (4,4) products
                 encode_map(&P.tmAh[qi], quad_origin(ta, I, J), quad_rows(ta, I),
                            quad_cols(ta, J), ta.ld, 16, kBK / 2, 128);
-            if (L == 2 && b_live[qi])
+            if (L == 2 && b_live[qi] && !P.narrow)
                 encode_map(&P.tmBh[qi], quad_origin(tb, I, J), quad_rows(tb, I),
                            quad_cols(tb, J), tb.ld, kBK / 2, kBN, 64);
             P.cptr[qi] = cq[qi].p;
@@ -1022,7 +1054,7 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
         P.c_vec = vec ? 1 : 0;
         // C quadrant tensor maps for the bulk-reduction epilogue: 16-row x
         // 128-column boxes, 128-byte swizzle, one TMA reduce-add per box
-        if (vec && C.cs * 8 < (1LL << 40)) {
+        if (vec && C.cs * 8 < (1LL << 40) && !P.narrow) {  // (narrow: register epilogues)
             for (int qi = 0; qi < side * side; ++qi)
                 if (c_live[qi])
                     encode_map(&P.tmC[qi], cq[qi].p, cq[qi].rows, cq[qi].cols, C.cs, 16, kBN, 128);
@@ -1033,7 +1065,7 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
     P.qn = static_cast<int>(qn);
     P.qk = static_cast<int>(qk);
     P.tiles_m = static_cast<int>(ceil_div(qm, kBM));
-    P.tiles_n = static_cast<int>(ceil_div(qn, kBN));
+    P.tiles_n = static_cast<int>(ceil_div(qn, bn));
     P.ktiles = static_cast<int>(ceil_div(qk, kBK));
     P.group_m = 8;
     // bulk-reduction epilogue (C tiles staged in smem, one TMA reduce-add per
@@ -1080,9 +1112,12 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
     // C materialise every multi-term side; ABC and AB fuse sides of up to
     // e.fuse_max_terms terms.  Both forms add the terms in listed order with the
     // same roundings, so the choice never changes a bit of the result.
-    const int mat_min = (variant == STRASSEN_C || variant == STRASSEN_NAIVE) ? 2
+    const int mat_min_f = (variant == STRASSEN_C || variant == STRASSEN_NAIVE) ? 2
                         : (variant == STRASSEN_DGEMM)                        ? kMaxTerms + 1
                                                                              : e.fuse_max_terms + 1;
+    // (narrow-tile kernels sum at most 2 terms per side: longer sides are materialised,
+    // bitwise the same as summing them in registers)
+    const int mat_min = P.narrow ? std::min(mat_min_f, 3) : mat_min_f;
     // The launch plan (k-chunks, stream-K pieces) must not depend on where the sums
     // are formed, or the fused-term setting would change roundings: it is made for the
     // variant's own term counts (ABC / AB as fully fused, Naive / C single-term).
@@ -1197,7 +1232,7 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
                     if (sd == 0)
                         encode_map(&P.tmA[mi], dst, qm, qk, lda_t, 16, kBK, 128);
                     else
-                        encode_map(&P.tmB[mi], dst, qk, qn, ldb_t, kBK, kBN, 128);
+                        encode_map(&P.tmB[mi], dst, qk, qn, ldb_t, kBK, bn, 128);
                     terms = {{mi, 1}};
                 }
             }

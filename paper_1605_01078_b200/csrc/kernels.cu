@@ -184,9 +184,11 @@ __device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, int c0
         : "memory");
 }
 
-// Named barrier over the 8 DMMA warps only (the producer warp has exited).
+// Named barrier over the DMMA warps only (the producer warp has exited): 8 warps,
+// or the narrow-tile launch's 4.
+template <int CW = kConsumerWarps>
 __device__ __forceinline__ void consumer_bar() {
-    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(CW * 32) : "memory");
 }
 
 // Consumer side of a ring slot hand-back.  The slot was read with generic-proxy
@@ -822,9 +824,13 @@ __device__ __forceinline__ void trace_event(const MMParams&, int) {}
 
 // GROUPS: the launch runs product groups (MMParams::pair_mode); the other
 // instantiations carry none of their tensor-memory and multi-coefficient epilogue code
-template <int MAXT, bool PERSIST, int RING, bool GROUPS>
-__global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__ MMParams P) {
-    constexpr bool SEP = RING != kRawSlots;  // separate stage, deferred completion
+template <int MAXT, bool PERSIST, int RING, bool GROUPS, bool NAR>
+__global__ void __launch_bounds__(NAR ? kNarrowThreads : kThreads, NAR ? 2 : 1)
+    mm_kernel(const __grid_constant__ MMParams P) {
+    constexpr bool SEP = !NAR && RING != kRawSlots;  // separate stage, deferred completion
+    // NAR: narrow tiles (kernels.hpp kNarrowBN): 4 DMMA warps, 64-column tiles
+    constexpr int CW = NAR ? kNarrowConsumerWarps : kConsumerWarps;
+    constexpr int BN = NAR ? kNarrowBN : kBN;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment (128B-swizzle atoms) by offsetting the shared array
     // itself, so every derived pointer stays in the shared address space (LDS/STS).
@@ -849,11 +855,11 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     if (threadIdx.x == 0) {
         for (int s = 0; s < RING; ++s) {
             mbar_init(&raw_full[s], 1);
-            mbar_init(&raw_empty[s], kConsumerWarps);
+            mbar_init(&raw_empty[s], CW);
         }
         for (int s = 0; s < kUnitQueue; ++s) {
             mbar_init(&q_full[s], 1);
-            mbar_init(&q_empty[s], kConsumerWarps);
+            mbar_init(&q_empty[s], CW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         fence_proxy_async();
@@ -908,18 +914,18 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         return nxt;
     };
 
-    if (warp >= kConsumerWarps) {
-        // ================= TMA warpgroup (warps 8-11; one lane issues) =======
+    if (warp >= CW) {
+        // ================= TMA warpgroup (warps 8-11 / NAR 4-7; one lane issues) =
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kProducerRegs));
-        if (warp != kConsumerWarps || lane != 0) return;
+        if (warp != CW || lane != 0) return;
         uint32_t s = 0, phase = 0;
         for (int unit = blockIdx.x; unit < n_units; unit = producer_next(unit)) {
         const Unit U = decode_unit<GROUPS>(P, unit);
-        const int m0 = U.tm * kBM, n0 = U.tn * kBN;
+        const int m0 = U.tm * kBM, n0 = U.tn * BN;
         const int kt_lo = U.kt_lo, kt_hi = U.kt_hi;
         for (int p = U.p_lo; p < U.p_hi; ++p) {
             const ProductDesc& pd = P.prod[p];
-            if (pd.half) {
+            if (!NAR && pd.half) {
                 // 8-k half tiles, two terms per slot (A terms first, then B)
                 const int nt = pd.na + pd.nb;
                 for (int kh = 2 * kt_lo; kh < 2 * kt_hi; ++kh) {
@@ -952,7 +958,8 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                 const int k0 = kt * kBK;
                 for (int u = 0; u < pd.na + pd.nb; ++u) {
                     mbar_wait(&raw_empty[s], phase ^ 1);
-                    mbar_expect_tx(&raw_full[s], kSlotBytes);
+                    // (a narrow B tile is 16 x 64: half a slot)
+                    mbar_expect_tx(&raw_full[s], NAR && u >= pd.na ? kSlotBytes / 2 : kSlotBytes);
                     uint8_t* dst = raw + s * kSlotBytes;
                     if (u < pd.na) {
                         const CUtensorMap* map = &P.tmA[pd.aq[u]];
@@ -980,7 +987,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     // other warps are starved while DMMA saturates the FP64 pipe, measured in
     // microbench/fp64_contend.cu), and no stage buffer, barrier or
     // cross-warp handoff is needed.
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kConsumerRegs));
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(NAR ? kNarrowConsumerRegs : kConsumerRegs));
     const int wm = warp & 1, wn = warp >> 1;
     const int g = lane >> 2, j = lane & 3;
     double acc[8][4][2];
@@ -1000,7 +1007,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         } else {
             asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         }
-        consumer_bar();  // (also: the stage is free again)
+        consumer_bar<CW>();  // (also: the stage is free again)
         if (threadIdx.x == 0 && pend_p >= 0) {
             __threadfence();
             release_ticket(P, pend_p, pend_tm, pend_tn);
@@ -1157,7 +1164,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         // is row 16(mf/2) + 2g + mf%2 and column 8nf + nperm(2j + e) of this
         // warp's 64 x 32 tile.
         const int mrow0 = tm * kBM + wm * 64 + 2 * g;
-        const int ncol0 = tn * kBN + wn * 32;
+        const int ncol0 = tn * BN + wn * 32;
         // (half-tile products map B columns without the permutation)
         const int c0 = pd.half ? 2 * j : nperm(2 * j), c1 = pd.half ? 2 * j + 1 : nperm(2 * j + 1);
         // ---- fused epilogue through bulk reductions.  The DMMA warps stage
@@ -1173,7 +1180,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         // else takes the register read-modify-write below.
         // C tiles are reduced through the quadrants' tensor maps (tmC), which clip
         // partial tiles at the quadrant edge.
-        bool bulk = P.mode == kEpiRMW && P.c_tma && (p_hi - p_lo == 1 || GROUPS) &&
+        bool bulk = !NAR && P.mode == kEpiRMW && P.c_tma && (p_hi - p_lo == 1 || GROUPS) &&
                     kt_hi - kt_lo <= P.bulk_max_kt && (SEP || !persistent) &&
                     U.npieces == 1;
         // the reduce-add clips rows at 16-byte granularity (microbench/tma_reduce_f64.cu):
@@ -1216,7 +1223,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             uint8_t* stage = SEP ? raw + RING * kSlotBytes + 1024 : raw;
             const bool ticketed = P.tickets != nullptr;
             bool issued = false;
-            if (!SEP) consumer_bar();  // every warp is done reading the ring before it is reused
+            if (!SEP) consumer_bar<CW>();  // every warp is done reading the ring before it is reused
             // DMMA warp w hands box w (rows 16w..16w+15) of every destination to the TMA
             // engine: one tensor reduce-add each (per-column 1-D bulk reductions issued
             // 128 x nc uniform-datapath instructions per tile)
@@ -1230,7 +1237,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                     const int ca = da[first], cb = db[first], cc = dc[first];
                     if (issued) {  // previous pass's reductions must have read the stage
                         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                        consumer_bar();
+                        consumer_bar<CW>();
                     }
 #pragma unroll
                     for (int h = 0; h < 4; ++h) {
@@ -1251,7 +1258,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                         if (threadIdx.x == 0) wait_ticket(P, U.tk, tm, tn);
                         asm volatile("fence.proxy.async.global;" ::: "memory");
                     }
-                    consumer_bar();
+                    consumer_bar<CW>();
                     asm volatile("fence.proxy.async.global;" ::: "memory");
                     for (int i = first; i < nd; ++i) {
                         if (da[i] != ca || db[i] != cb || dc[i] != cc) continue;
@@ -1270,7 +1277,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                     if (!any) continue;
                     if (issued) {  // previous pass's reductions must have read the stage
                         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                        consumer_bar();
+                        consumer_bar<CW>();
                     }
                     const double sc = P.alpha * (pass == 0 ? 1.0 : -1.0);
 #pragma unroll
@@ -1289,7 +1296,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                         if (threadIdx.x == 0) wait_ticket(P, U.tk, tm, tn);
                         asm volatile("fence.proxy.async.global;" ::: "memory");
                     }
-                    consumer_bar();
+                    consumer_bar<CW>();
                     asm volatile("fence.proxy.async.global;" ::: "memory");
                     if (lane == 0) {
                         for (int u = 0; u < pd.nc; ++u) {
@@ -1314,14 +1321,14 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             if (succ) {  // all reductions performed (every warp's), then hand the tile on
                 asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
                 asm volatile("fence.proxy.async.global;" ::: "memory");
-                consumer_bar();
+                consumer_bar<CW>();
                 if (threadIdx.x == 0) {
                     __threadfence();
                     release_ticket(P, U.tk, tm, tn);
                 }
             } else {  // the stage must outlive the reads (smem is freed at exit)
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                consumer_bar();
+                consumer_bar<CW>();
             }
             continue;  // next product (none: single-product CTA)
         }
@@ -1331,7 +1338,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             // per element the same arithmetic as the staged values of the bulk path
             if (P.tickets) {
                 if (threadIdx.x == 0) wait_ticket(P, U.tk, tm, tn);
-                consumer_bar();
+                consumer_bar<CW>();
             }
             for (int i = 0; i < nd; ++i) {
                 double* __restrict__ C = P.cptr[dq[i]];
@@ -1361,7 +1368,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             }
             if (P.tickets) {  // every thread's C stores visible, then hand the tile on
                 __threadfence();
-                consumer_bar();
+                consumer_bar<CW>();
                 if (threadIdx.x == 0) release_ticket(P, U.tk, tm, tn);
             }
             continue;
@@ -1397,7 +1404,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                                    make_double2(acc[2 * h][nf][e], acc[2 * h + 1][nf][e]));
                         }
                 __threadfence();
-                consumer_bar();
+                consumer_bar<CW>();
             }
             __shared__ int last_flag;
             if (owner0) {  // wait for pieces 1 .. npieces - 1
@@ -1405,13 +1412,13 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
                     while (ld_relaxed_gpu(cnt) != U.npieces - 1) __nanosleep(64);
                     asm volatile("fence.acq_rel.gpu;" ::: "memory");
                 }
-                consumer_bar();
+                consumer_bar<CW>();
             } else {
                 if (threadIdx.x == 0) {
                     const int before = atomicAdd(cnt, 1);
                     last_flag = !P.streamk && before == U.npieces - 1;
                 }
-                consumer_bar();
+                consumer_bar<CW>();
                 if (!last_flag) continue;  // another piece finishes this product
                 __threadfence();
             }
@@ -1445,7 +1452,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
         const bool ticketed = P.mode == kEpiRMW && P.tickets;  // ordered epilogue
         if (ticketed) {
             if (threadIdx.x == 0) wait_ticket(P, U.tk, tm, tn);
-            consumer_bar();
+            consumer_bar<CW>();
         }
         if (P.mode == kEpiRMW) {
             // 16-byte path: C column-major with rows (2g, 2g+1) of the fragment
@@ -1521,7 +1528,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
             }
             if (ticketed) {  // every thread's C stores visible, then hand the tiles on
                 __threadfence();
-                consumer_bar();
+                consumer_bar<CW>();
                 if (threadIdx.x == 0) release_ticket(P, U.tk, tm, tn);
             }
         } else {
@@ -1556,7 +1563,7 @@ __global__ void __launch_bounds__(kThreads, 1) mm_kernel(const __grid_constant__
     trace_event(P, 31);
     if constexpr (GROUPS) {  // every warp is done with tensor memory; warp 0 frees it
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-        consumer_bar();
+        consumer_bar<CW>();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if (warp == 0)
             asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
@@ -1930,23 +1937,25 @@ __global__ void scale_kernel(double* c, long rows, long cols, long long rs, long
 
 }  // namespace
 
-template <int MAXT, bool PERSIST, int RING, bool GROUPS>
+template <int MAXT, bool PERSIST, int RING, bool GROUPS, bool NAR = false>
 static cudaError_t launch_mm_g(const MMParams& p, cudaStream_t s);
 template <int MAXT, bool PERSIST, int RING = kRawSlots>
 static cudaError_t launch_mm_t(const MMParams& p, cudaStream_t s) {
     return p.pair_mode ? launch_mm_g<MAXT, PERSIST, RING, true>(p, s)
                        : launch_mm_g<MAXT, PERSIST, RING, false>(p, s);
 }
-template <int MAXT, bool PERSIST, int RING, bool GROUPS>
+template <int MAXT, bool PERSIST, int RING, bool GROUPS, bool NAR>
 static cudaError_t launch_mm_g(const MMParams& p, cudaStream_t s) {
-    constexpr int smem = RING == kRawSlots ? kMMSmemBytes : mm_sep_smem_bytes(RING);
+    constexpr int smem = NAR                ? kNarrowSmemBytes
+                         : RING == kRawSlots ? kMMSmemBytes
+                                             : mm_sep_smem_bytes(RING);
     // the > 48 KB dynamic shared-memory opt-in is per device context: once per device
     static std::atomic<uint64_t> attr_set{0};
     int dev = 0;
     if (cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
     const uint64_t bit = 1ull << (dev & 63);
     if (!(attr_set.load(std::memory_order_acquire) & bit)) {
-        cudaError_t e = cudaFuncSetAttribute(mm_kernel<MAXT, PERSIST, RING, GROUPS>,
+        cudaError_t e = cudaFuncSetAttribute(mm_kernel<MAXT, PERSIST, RING, GROUPS, NAR>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr_set.fetch_or(bit, std::memory_order_release);
@@ -1956,7 +1965,8 @@ static cudaError_t launch_mm_g(const MMParams& p, cudaStream_t s) {
     // stream-K: exactly grid_cap CTAs (the unit decode assumes it)
     const int grid = PERSIST && p.streamk ? p.grid_cap
                      : PERSIST && p.grid_cap > 0 && p.grid_cap < units ? p.grid_cap : units;
-    mm_kernel<MAXT, PERSIST, RING, GROUPS><<<grid, kThreads, smem, s>>>(p);
+    mm_kernel<MAXT, PERSIST, RING, GROUPS, NAR>
+        <<<grid, NAR ? kNarrowThreads : kThreads, smem, s>>>(p);
     return cudaGetLastError();
 }
 
@@ -1965,6 +1975,13 @@ cudaError_t launch_mm(const MMParams& p, cudaStream_t s) {
     for (int i = 0; i < p.nprod; ++i) {
         maxt = p.prod[i].na > maxt ? p.prod[i].na : maxt;
         maxt = p.prod[i].nb > maxt ? p.prod[i].nb : maxt;
+    }
+    // narrow tiles (small problems, two CTAs per SM): persistent, at most 2-term sums,
+    // register epilogues (the host plans them so)
+    if (p.narrow) {
+        if (maxt > 2 || p.pair_mode || p.c_tma || p.sep_stage) return cudaErrorInvalidValue;
+        return maxt == 1 ? launch_mm_g<1, true, kNarrowRing, false, true>(p, s)
+                         : launch_mm_g<2, true, kNarrowRing, false, true>(p, s);
     }
     // Persistent launches for single-term programs (DGEMM, Naive, C): at 16384^3
     // mm_kernel 192.4 -> 188.7 ms (Naive L2), 251.4 -> 247.7 (DGEMM) on one box.

@@ -44,6 +44,21 @@ constexpr int kStageBytes = kBM * kBN * 8;
 constexpr int kMMSepSmemBytes = kSepRing * kSlotBytes + 1024 + 1024 + kStageBytes;
 static_assert(kMMSepSmemBytes <= 227 * 1024, "shared memory budget (separate stage)");
 static_assert(mm_sep_smem_bytes(kSepRing2) <= 227 * 1024, "shared memory budget (fused, separate stage)");
+// Narrow tiles (MMParams::narrow, small problems): 128 x 64 CTA tiles, one DMMA
+// warpgroup (2 x 2 warps of 64 x 32) + the TMA warpgroup, TWO CTAs per SM, so one
+// CTA's prologue, fixup and epilogue overlap the other's mainloop.  Per CTA: half
+// the SM's registers (256 threads x 128 at launch; setmaxnreg 24 / 232) and a
+// 6-slot ring (a B term tile uses half a slot).
+constexpr int kNarrowBN = 64;
+constexpr int kNarrowConsumerWarps = 4;
+constexpr int kNarrowThreads = 128 + kNarrowConsumerWarps * 32;  // 256
+constexpr int kNarrowConsumerRegs = 232;
+static_assert(kProducerRegs * 128 + kNarrowConsumerRegs * kNarrowConsumerWarps * 32 <=
+                  kNarrowThreads * 128,
+              "narrow setmaxnreg split exceeds half the SM's registers");
+constexpr int kNarrowRing = 6;
+constexpr int kNarrowSmemBytes = kNarrowRing * kSlotBytes + 1024 + 512;
+static_assert(2 * (kNarrowSmemBytes + 1024) <= 228 * 1024, "two narrow CTAs per SM");
 // dynamic unit hand-out queue (MMParams::unit_counter): depth, after the ring barriers
 constexpr int kUnitQueue = 4;
 static_assert(2 * kSepRing * 8 + 2 * kUnitQueue * 8 + kUnitQueue * 4 <= 1024,
@@ -161,6 +176,9 @@ struct alignas(64) MMParams {
     int pair_mode;
     int npairs;
     int8_t pair_lo[kMaxProducts + 1];
+    // narrow tiles (kNarrowBN columns, two CTAs per SM): tiles_n / tn0 count 64-column
+    // tiles, tmB boxes are 16 x 64, register epilogues only (no c_tma, groups or half tiles)
+    int narrow;
 };
 
 cudaError_t launch_mm(const MMParams& p, cudaStream_t s);

@@ -1,0 +1,91 @@
+"""Narrow-tile launches (kernels.hpp kNarrowBN: 128 x 64 tiles, two CTAs per SM), which
+the planner picks for small DGEMM / C / Naive problems (engine.cpp run_strassen): against
+cuBLAS with the BASELINE normwise bounds, ragged and strided C, and -- forced on for every
+variant through STRASSEN_B200_NARROW=1 in a child process (read once per process) -- the
+fused-sum programs too, where sides longer than two terms are materialised."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+import paper_1605_01078_b200 as S
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _check(ctx, v, L, m, n, k, ld_pad, alpha, seed):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    A = (torch.rand(k, m, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    B = (torch.rand(n, k, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    big = torch.full((n, m + ld_pad), -5.5, dtype=torch.float64, device="cuda").t()
+    C = big[:m, :]
+    C.copy_((torch.rand(n, m, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t())
+    ref = C + alpha * (A @ B)
+    ctx.gemm_device(v, L, alpha, A, B, C)
+    torch.cuda.synchronize()
+    nw = (torch.linalg.norm(C - ref) / (torch.linalg.norm(A) * torch.linalg.norm(B))).item()
+    assert nw <= (5e-12 if L == 2 else 1e-12), (v, L, m, n, k, nw)
+    if ld_pad:
+        assert bool((big[m:, :] == -5.5).all())
+    return C.clone()
+
+
+@pytest.mark.parametrize("v,L,shape", [
+    ("dgemm", 0, (1024, 1024, 1024)), ("dgemm", 0, (1000, 777, 1030)), ("dgemm", 0, (64, 8000, 300)),
+    ("c", 1, (1024, 1024, 1024)), ("c", 2, (2048, 2048, 2048)), ("c", 2, (1281, 1999, 1100)),
+    ("naive", 1, (1000, 1000, 1000)), ("naive", 2, (1024, 1536, 700)),
+])
+@pytest.mark.parametrize("ld_pad", [0, 3])
+def test_narrow_planned_sizes(cuda, v, L, shape, ld_pad):
+    """Sizes the planner runs with narrow tiles: BASELINE bounds, ld padding untouched
+    (odd ldc: the scalar epilogue), and a repeated call is bitwise repeatable."""
+    import torch
+    m, n, k = shape
+    ctx = S.Ctx()
+    first = _check(ctx, v, L, m, n, k, ld_pad, 1.0 if ld_pad else -0.5, seed=m + n + k)
+    second = _check(ctx, v, L, m, n, k, ld_pad, 1.0 if ld_pad else -0.5, seed=m + n + k)
+    assert torch.equal(first, second)
+    ctx.close()
+
+
+_CHILD = r"""
+import sys, torch
+sys.path.insert(0, {root!r})
+import paper_1605_01078_b200 as S
+ctx = S.Ctx()
+worst = 0.0
+for v, L, m, n, k in [("abc", 1, 1024, 1024, 1024), ("abc", 2, 2048, 2048, 2048), ("ab", 1, 1000, 1100, 900),
+                      ("ab", 2, 1536, 1024, 1280), ("abc", 2, 777, 1030, 513), ("naive", 2, 2048, 2048, 1024),
+                      ("dgemm", 0, 3000, 2000, 1500), ("c", 1, 4096, 4096, 256)]:
+    for f in (4, 2):
+        ctx.set_fused_terms(f)
+        g = torch.Generator(device="cuda").manual_seed(m * n + k)
+        A = (torch.rand(k, m, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+        B = (torch.rand(n, k, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+        C = (torch.rand(n, m, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+        ref = C + A @ B
+        ctx.gemm_device(v, L, 1.0, A, B, C)
+        torch.cuda.synchronize()
+        nw = (torch.linalg.norm(C - ref) / (torch.linalg.norm(A) * torch.linalg.norm(B))).item()
+        assert nw <= (5e-12 if L == 2 else 1e-12), (v, L, m, n, k, f, nw)
+        if f == 4:
+            keep = C.clone()
+        else:
+            assert torch.equal(C, keep), (v, L, m, n, k)
+        worst = max(worst, nw)
+print("narrow forced ok", worst)
+"""
+
+
+def test_narrow_forced_on_every_variant(cuda):
+    """STRASSEN_B200_NARROW=1: every variant (fused-sum ones included, their 4-term sides
+    materialised) within the bounds, and the fused-term setting still bitwise neutral."""
+    env = dict(os.environ, STRASSEN_B200_NARROW="1")
+    out = subprocess.run([sys.executable, "-c", _CHILD.format(root=ROOT)], env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    assert "narrow forced ok" in out.stdout
