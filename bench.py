@@ -75,6 +75,9 @@ def parse():
     p.add_argument("--p2p", action="store_true",
                    help="N > 1: peer-memory SUMMA (operands read from the owners' blocks "
                         "over CUDA IPC, no NCCL broadcasts; summa.summa_p2p)")
+    p.add_argument("--native", action="store_true",
+                   help="SUMMA through the library's native entry point (strassen_dist_gemm, "
+                        "include/strassen_dist.h: NCCL from C++, no Python in the schedule)")
     p.add_argument("--summa-size", default="both", choices=["strong", "weak", "both"],
                    help="SUMMA problems: config 5's fixed 65536^3 (strong), its weak-scaled "
                         "32768*sqrt(N) variant, or both (value = strong)")
@@ -522,9 +525,10 @@ def run_summa(args, rank, world, local, colmajor, barrier, max_over_ranks):
     local_gemm = SU._default_local_gemm(args.variant, args.level)
     results = {}
     line = None
+    native_grid = None
     for name, gm, gn, gk in summa_problems(args, world):
         L = SU.make_layout(gm, gn, gk, world)
-        comm = SU.TorchComm(L) if world > 1 or args.summa else None
+        comm = SU.TorchComm(L) if (world > 1 or args.summa) and not args.native else None
         A_l, B_l, C_l = colmajor(L.m_l, L.k_c), colmajor(L.k_r, L.n_l), colmajor(L.m_l, L.n_l)
         if args.p2p:
             torch.cuda.synchronize()
@@ -532,6 +536,14 @@ def run_summa(args, rank, world, local, colmajor, barrier, max_over_ranks):
             barrier()
             step = lambda: SU.summa_p2p(L, rank, Ap, Bp, C_l, 1.0, args.variant,  # noqa: E731
                                         args.level, local_gemm=local_gemm)
+        elif args.native:
+            if native_grid is None:   # one NCCL job (world + row + column comms) per run
+                native_grid = (SU.NativeGrid.from_torch_distributed(local_gemm.ctx, L.pr, L.pc)
+                               if world > 1 else
+                               SU.NativeGrid.nccl(local_gemm.ctx, SU.NativeGrid.unique_id(), 0, 1,
+                                                  1, 1))
+            step = lambda: native_grid.gemm(args.variant, args.level, L.m, L.n,  # noqa: E731
+                                            L.k, 1.0, A_l, B_l, C_l, panel=L.b)
         else:
             step = lambda: SU.summa(L, comm, A_l, B_l, C_l, 1.0, args.variant,  # noqa: E731
                                     args.level, local_gemm=local_gemm)
@@ -591,6 +603,8 @@ def run_summa(args, rank, world, local, colmajor, barrier, max_over_ranks):
                            "weak_rule": "weak_scaled: m=n=k = 32768*sqrt(N) rounded to the "
                                         "nearest multiple of 256",
                            "exchange": "peer memory (CUDA IPC), no broadcasts" if args.p2p
+                           else "NCCL row/column panel broadcasts issued by the library "
+                                "(strassen_dist_gemm)" if args.native
                            else "NCCL row/column panel broadcasts",
                            "l2": "inputs larger than the 126 MB L2"},
                 "roofline": roofline, "clocks": res["clocks"], "gpu_launches": launches,
@@ -635,7 +649,10 @@ def summa_e2e(args, L, A_l, B_l, C_l, step, local_gemm, barrier, max_over_ranks,
         ev_c = torch.cuda.Event()
         ev_c.record(copy_stream)
     torch.cuda.current_stream().wait_event(ev_ab)
-    local_gemm.c_ready = ev_c
+    if args.native:   # the library's first local update waits on C right before reading it
+        local_gemm.ctx.set_operand_events(c=ev_c)
+    else:
+        local_gemm.c_ready = ev_c
     if args.p2p:  # peers read this rank's A and B: they land before any rank steps
         ev_ab.synchronize()
         barrier()
@@ -646,7 +663,7 @@ def summa_e2e(args, L, A_l, B_l, C_l, step, local_gemm, barrier, max_over_ranks,
     return {"value": flops / dt / 1e12, "unit": "TFLOP/s",
             "h2d_bytes_per_step": world * 8 * (L.m_l * L.k_c + L.k_r * L.n_l + L.m_l * L.n_l),
             "d2h_bytes_per_step": world * 8 * L.m_l * L.n_l, "ms_per_step": dt * 1e3,
-            "api": ("summa_p2p()" if args.p2p else "summa()")
+            "api": ("summa_p2p()" if args.p2p else "strassen_dist_gemm" if args.native else "summa()")
             + " over strassen_gemm_device, pinned host blocks"}
 
 

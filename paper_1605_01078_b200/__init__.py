@@ -61,6 +61,11 @@ class Counters(C.Structure):
     _fields_ = [(f, C.c_int64) for f in COUNTER_FIELDS]
 
 
+class DistPiece(C.Structure):  # strassen_dist_piece (include/strassen_dist.h)
+    _fields_ = [("owner", C.c_int), ("local_off", C.c_long), ("width", C.c_long),
+                ("panel_off", C.c_long)]
+
+
 class StrassenError(RuntimeError):
     def __init__(self, status, what=""):
         self.status = status
@@ -131,6 +136,24 @@ def _declare(lib):
         "strassen_predict_b200": (_ST, [C.c_int, C.c_int, _L, _L, _L, _dp]),
         "strassen_build_info": (C.c_char_p, []),
         "strassen_last_error": (C.c_char_p, []),
+        # include/strassen_dist.h
+        "strassen_dist_grid": (_ST, [C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+        "strassen_dist_default_panel": (_L, [_L]),
+        "strassen_dist_panel_pieces": (_ST, [_L, C.c_int, C.c_int, _L, _L, C.c_int,
+                                             C.POINTER(DistPiece), _L, C.POINTER(_L)]),
+        "strassen_dist_unique_id": (_ST, [vp]),
+        "strassen_dist_create": (_ST, [C.POINTER(vp), vp, vp, C.c_int, C.c_int, C.c_int, C.c_int]),
+        "strassen_dist_create_from_comm": (_ST, [C.POINTER(vp), vp, vp, C.c_int, C.c_int]),
+        "strassen_dist_create_custom": (_ST, [C.POINTER(vp), vp, vp, C.c_int, C.c_int, C.c_int]),
+        "strassen_dist_mailbox_create": (_ST, [C.POINTER(vp)]),
+        "strassen_dist_mailbox_destroy": (None, [vp]),
+        "strassen_dist_mailbox_set_replay": (_ST, [vp, C.c_int]),
+        "strassen_dist_create_loopback": (_ST, [C.POINTER(vp), vp, vp, C.c_int, C.c_int, C.c_int]),
+        "strassen_dist_destroy": (None, [vp]),
+        "strassen_dist_gemm": (_ST, [vp, vp, C.c_int, C.c_int, _L, _L, _L, C.c_double, vp, _L, vp,
+                                     _L, vp, _L, _L]),
+        "strassen_dist_last_counts": (_ST, [vp, C.POINTER(_L), C.POINTER(_L)]),
+        "strassen_dist_position": (_ST, [vp] + [C.POINTER(C.c_int)] * 5),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

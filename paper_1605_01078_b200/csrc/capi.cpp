@@ -27,9 +27,13 @@ struct strassen_ctx {
     sb200::Engine engine;
 };
 
-namespace {
+static thread_local std::string g_last_error;
 
-thread_local std::string g_last_error;
+namespace sb200 {
+void set_last_error(const std::string& what) { g_last_error = what; }  // dist.cpp
+}  // namespace sb200
+
+namespace {
 
 template <typename F>
 strassen_status guarded(F&& f) {

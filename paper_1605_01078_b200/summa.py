@@ -423,3 +423,175 @@ def summa_p2p(layout: Layout, rank: int, A_peers: List[torch.Tensor], B_peers: L
         for x in abuf + bbuf:                # buffers freed on the main stream's order
             x.record_stream(side)
     return launches
+
+
+# ------------------------------------------ native SUMMA (include/strassen_dist.h)
+class NativeGrid:
+    """One rank's handle on the library's native SUMMA (``strassen_dist_*``,
+    csrc/dist.cpp): the same schedule as :func:`summa`, issued by the C++ side --
+    NCCL row/column broadcasts on a communication stream, double-buffered panels,
+    ``strassen_gemm_device`` as the local update.  This is what a C / C++ caller of
+    the drop-in library uses; the Python class only forwards to it.
+    """
+
+    def __init__(self, ctx, handle, keep=()):
+        import paper_1605_01078_b200 as S
+        self._S, self._l = S, S.lib()
+        self.ctx, self.ptr, self._keep = ctx, handle, keep
+
+    # ---- schedule helpers (pure host code) ----
+    @staticmethod
+    def grid(nranks):
+        import ctypes as C
+        import paper_1605_01078_b200 as S
+        pr, pc = C.c_int(), C.c_int()
+        S._check(S.lib().strassen_dist_grid(int(nranks), C.byref(pr), C.byref(pc)), "dist_grid")
+        return pr.value, pc.value
+
+    @staticmethod
+    def default_panel(k):
+        import paper_1605_01078_b200 as S
+        return S.lib().strassen_dist_default_panel(int(k))
+
+    @staticmethod
+    def panel_pieces(k, pr, pc, b, p, side):
+        """Pieces of panel p as (owner, local offset, width, panel offset); side 'a' or 'b'."""
+        import ctypes as C
+        import paper_1605_01078_b200 as S
+        out = (S.DistPiece * 64)()
+        n = C.c_long()
+        S._check(S.lib().strassen_dist_panel_pieces(k, pr, pc, b, p, 0 if side == "a" else 1,
+                                                    out, 64, C.byref(n)), "dist_panel_pieces")
+        return [(out[t].owner, out[t].local_off, out[t].width, out[t].panel_off)
+                for t in range(n.value)]
+
+    # ---- transports ----
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes as C
+        import paper_1605_01078_b200 as S
+        buf = C.create_string_buffer(128)
+        S._check(S.lib().strassen_dist_unique_id(buf), "dist_unique_id")
+        return buf.raw
+
+    @classmethod
+    def nccl(cls, ctx, unique_id: bytes, rank, nranks, pr, pc):
+        """Collective: every rank of the job calls it with rank 0's unique id."""
+        import ctypes as C
+        import paper_1605_01078_b200 as S
+        h = C.c_void_p()
+        idbuf = C.create_string_buffer(unique_id, 128)
+        S._check(S.lib().strassen_dist_create(C.byref(h), ctx.ptr, idbuf, rank, nranks, pr, pc),
+                 "dist_create")
+        return cls(ctx, h)
+
+    @classmethod
+    def from_torch_distributed(cls, ctx, pr, pc, group=None):
+        """Joins the native NCCL job of a torch.distributed launch: rank 0 makes the
+        unique id, the existing process group carries it to the other ranks."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        box = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0, group=group)
+        return cls.nccl(ctx, box[0], rank, world, pr, pc)
+
+    @classmethod
+    def loopback(cls, ctx, mailbox, rank, pr, pc):
+        import ctypes as C
+        import paper_1605_01078_b200 as S
+        h = C.c_void_p()
+        S._check(S.lib().strassen_dist_create_loopback(C.byref(h), ctx.ptr, mailbox.ptr, rank,
+                                                       pr, pc), "dist_create_loopback")
+        return cls(ctx, h, keep=(mailbox,))
+
+    def close(self):
+        if self.ptr:
+            self._l.strassen_dist_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- the multiply ----
+    def gemm(self, variant, level, m, n, k, alpha, A_l, B_l, C_l, panel=0, stream=None):
+        """C_l += alpha (A B)_ij for the global m x n x k product (column-major blocks)."""
+        import ctypes as C
+        for t in (A_l, B_l, C_l):
+            if t.dim() != 2 or t.dtype != torch.float64 or (t.shape[0] > 1 and t.stride(0) != 1):
+                raise ValueError("blocks must be column-major float64 matrices")
+        if stream is None:
+            stream = torch.cuda.current_stream(C_l.device)
+        h = getattr(stream, "cuda_stream", stream)
+        st = self._l.strassen_dist_gemm(
+            self.ptr, C.c_void_p(h), self._S._variant(variant), int(level), m, n, k, float(alpha),
+            C.c_void_p(A_l.data_ptr()), A_l.stride(1), C.c_void_p(B_l.data_ptr()), B_l.stride(1),
+            C.c_void_p(C_l.data_ptr()), C_l.stride(1), int(panel))
+        self._S._check(st, "strassen_dist_gemm")
+        return self.last_counts()[0]
+
+    def last_counts(self):
+        import ctypes as C
+        a, b = C.c_long(), C.c_long()
+        self._S._check(self._l.strassen_dist_last_counts(self.ptr, C.byref(a), C.byref(b)),
+                       "dist_last_counts")
+        return a.value, b.value
+
+    def position(self):
+        import ctypes as C
+        v = [C.c_int() for _ in range(5)]
+        self._S._check(self._l.strassen_dist_position(self.ptr, *[C.byref(x) for x in v]),
+                       "dist_position")
+        return tuple(x.value for x in v)
+
+
+class Mailbox:
+    """Payload store of the native single-GPU loopback transport."""
+
+    def __init__(self):
+        import ctypes as C
+        import paper_1605_01078_b200 as S
+        self._l = S.lib()
+        self.ptr = C.c_void_p()
+        S._check(self._l.strassen_dist_mailbox_create(C.byref(self.ptr)), "mailbox_create")
+
+    def set_replay(self, on):
+        self._l.strassen_dist_mailbox_set_replay(self.ptr, int(bool(on)))
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                self._l.strassen_dist_mailbox_destroy(self.ptr)
+                self.ptr = None
+        except Exception:
+            pass
+
+
+def summa_native_loopback(layout: Layout, A_blocks, B_blocks, C_blocks, alpha=1.0,
+                          variant="abc", level=1) -> int:
+    """The native schedule for every rank of the grid on ONE GPU: a record pass (roots'
+    payloads kept, C restored afterwards) and a replay pass (every broadcast delivers the
+    recorded payload).  Ranks run one after another; nothing waits on another launch."""
+    import paper_1605_01078_b200 as S
+    L = layout
+    P = L.pr * L.pc
+    mb = Mailbox()
+    ctx = S.Ctx()
+    grids = [NativeGrid.loopback(ctx, mb, r, L.pr, L.pc) for r in range(P)]
+    saved = [c.clone() for c in C_blocks]
+    launches = 0
+    for replay in (False, True):
+        mb.set_replay(replay)
+        for r in range(P):
+            if replay:
+                C_blocks[r].copy_(saved[r])
+            n = grids[r].gemm(variant, level, L.m, L.n, L.k, alpha, A_blocks[r], B_blocks[r],
+                              C_blocks[r], panel=L.b)
+            if replay:
+                launches += n
+    torch.cuda.synchronize()
+    for g in grids:
+        g.close()
+    return launches
