@@ -383,11 +383,18 @@ def main():
     # roofline of the dominant kernel (mm_kernel), timed by the library's own
     # per-launch CUDA events on the launch stream (one extra profiled step)
     peaks = json.load(open(os.path.join(ROOT, "profiles", "fp64_peaks.json")))
+    # -- averaged over `steps` profiled steps issued back to back, like the timed region
     ctx.enable_profiling(True)
-    ctx.gemm_device(args.variant, args.level, 1.0, A, B, C, stream)
-    torch.cuda.synchronize()
-    prof = ctx.last_profile()
+    profs = []
+    for _ in range(max(1, args.steps)):
+        ctx.gemm_device(args.variant, args.level, 1.0, A, B, C, stream)
+        torch.cuda.synchronize()
+        profs.append(ctx.last_profile())
     ctx.enable_profiling(False)
+    prof = [dict(x) for x in profs[0]]
+    if all(len(p) == len(prof) for p in profs):
+        for i, x in enumerate(prof):
+            x["ms"] = statistics.mean(p[i]["ms"] for p in profs)
     mm_ms = [x["ms"] for x in prof if x["kernel"] == "mm_kernel"]
     kern_ms = sum(mm_ms) if mm_ms else statistics.mean(per_ms)
     f_exec = executed_flops(m, n, k, args.level, args.variant)
@@ -403,6 +410,7 @@ def main():
                 "unit": "TFLOP/s", "frac": achieved / peaks["dmma_tflops"], "traffic": traffic,
                 "flops_per_launch": f_exec, "kernel_ms": kern_ms, "kernel": "mm_kernel",
                 "launches_per_step": launches, "step_profile_ms": prof,
+                "profiled_steps": len(profs),
                 "peak_source": "measured FP64 DMMA peak, profiles/fp64_peaks.json "
                                "(MEASURED_PEAKS.json has bf16/HBM only)"}
     hbm_peak = None

@@ -634,6 +634,20 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
         e.prof_end(s);
         return 1;
     }
+    // cooperative fixup (kernels.hpp MMParams::coop_fixup): stream-K launches, and
+    // k-chunk grids with one resident CTA per unit
+    static const bool coop_on = [] {
+        const char* v = std::getenv("STRASSEN_B200_COOP");  // 0 / 1 (experiments)
+        return v ? std::atoi(v) != 0 : true;
+    }();
+    // Stream-K launches keep the single-owner fixup: sharing it measured no gain (1024^3
+    // DGEMM 88.6 -> 86.7 us) or a loss (1024^3 ABC L1 90.8 -> 93.6, 1280^3 DGEMM 147.6 ->
+    // 150.6: profiles/r02_coop_ab.log) -- every participant then also writes its own
+    // partial, which the owner keeps in registers.
+    static const bool coop_sk = [] {
+        const char* v = std::getenv("STRASSEN_B200_COOP_SK");  // 0 / 1 (experiments)
+        return v ? std::atoi(v) != 0 : false;
+    }();
     if (F.fixup) {  // split mode finished by the last chunk's epilogue
         wait_c();
         P.mode = kEpiRMW;
@@ -652,9 +666,18 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
             P.sk_len = F.sk_len;
             P.sk_maxp = F.sk_maxp;
             P.grid_cap = F.sk_grid;  // the decode assumes exactly this many CTAs
-        } else if (P.grid_cap > 0) {
-            P.unit_counter = next_unit_counter(e, s);
+            P.coop_fixup = coop_on && coop_sk ? 1 : 0;
+        } else {
+            const long units = static_cast<long>(P.tiles_m) * P.tiles_n * P.nprod * P.ksplit;
+            if (coop_on && P.ksplit > 1 && P.grid_cap > 0 && units <= P.grid_cap) {
+                P.coop_fixup = 1;  // one CTA per unit, all resident
+                P.grid_cap = 0;
+            } else if (P.grid_cap > 0) {
+                P.unit_counter = next_unit_counter(e, s);
+            }
         }
+        // (one product: each tile takes a single update, shared by the participants)
+        if (P.coop_fixup) P.tickets = nullptr;
         P.trace = trace_buffer();
         e.prof_begin("mm_kernel", s);
         ck(launch_mm(P, s), "mm_kernel (split, fused epilogue)");
@@ -680,6 +703,7 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
         P.part_off = F.part_off;
         P.arrive = F.arrive;
         P.ticket_ld = F.ticket_ld;
+        P.coop_fixup = coop_on && coop_sk ? 1 : 0;
     } else if (P.grid_cap > 0) {
         P.unit_counter = next_unit_counter(e, s);
     }

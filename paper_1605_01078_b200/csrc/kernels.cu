@@ -738,6 +738,141 @@ __device__ __forceinline__ Unit decode_unit(const MMParams& P, int bid) {
     return U;
 }
 
+// Cooperative fixup (MMParams::coop_fixup): the pieces of unit `bid`'s (tile, product)
+// that finish it together -- this piece's index among them (-1: it only hands its
+// partial over) and their number.  Stream-K: every piece that ends its CTA's range,
+// i.e. all but a tail piece whose CTA goes on to the next (tile, product); k-chunk
+// grids (one resident CTA per unit): every piece.  Computed after the mainloop (kept
+// out of Unit: two more values live across the k-loop spill inside it).
+__device__ __forceinline__ void coop_participants(const MMParams& P, int bid, int piece, int npieces,
+                                               int& part, int& nparts) {
+    part = piece;
+    nparts = npieces;
+    if (!P.streamk) return;
+    const int grid = static_cast<int>(gridDim.x);
+    const int c = bid % grid, jx = bid / grid;
+    const long long K = P.ktiles, len = P.sk_len;
+    const long long total = static_cast<long long>(P.tiles_m) * P.tiles_n * P.nprod * K;
+    const long long t_lo = (c * len / K + jx) * K;
+    const long long c_last = (t_lo + K - 1) / len;
+    const bool tail_ends = min((c_last + 1) * len, total) == t_lo + K;
+    nparts = npieces - (tail_ends ? 0 : 1);
+    part = piece < nparts ? piece : -1;
+}
+
+// Cooperative fixup, run by a participant after its unit loop (it has stored its partial
+// and arrived): wait for all the pieces of the tile, then finish the 64 x 8
+// fragment blocks b = 4 warp + nf with b % nparts == part of its tile straight from the
+// partials -- per element M = ((P_0 + P_1) + ...) + P_{n-1} in piece (k) order, the
+// single-owner fixup's arithmetic -- and applies the epilogue to them: the C update of a
+// one-product program, or the store of M_p.  mrow0 / ncol0 / c0 / c1: the lane's fragment
+// origin and column pair, as in mm_kernel's epilogue.
+template <int CW>
+__device__ __forceinline__ void coop_finish(const MMParams& P, const ProductDesc& pd, int p, int tm,
+                                            int tn, int mrow0, int ncol0, int c0, int c1, int warp,
+                                            int part, int nparts, int npieces) {
+    const long long ldm = P.ldm;
+    int* cnt = P.arrive + (tm * P.ticket_ld + tn) * P.nprod + p;
+    const double* Mq = P.mbase + P.part_off + static_cast<long long>(p * P.ksplit) * P.mstride;
+    if (threadIdx.x == 0) {
+        while (ld_relaxed_gpu(cnt) != npieces) __nanosleep(32);
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    }
+    consumer_bar<CW>();
+    // (a variant with both of a warp's blocks and their C values in flight together
+    // measured slower: 768^3 DGEMM 45.0 -> 48.2 us)
+    for (int nf = 0; nf < 4; ++nf) {
+        if ((warp * 4 + nf) % nparts != part) continue;
+        double2 v[4][2];
+        // four pieces' loads in flight together, added in piece order
+        for (int sp0 = 0; sp0 < npieces; sp0 += 4) {
+            double2 x[4][4][2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const double* Ms = Mq + static_cast<long long>(sp0 + i) * P.mstride;
+#pragma unroll
+                for (int h = 0; h < 4; ++h)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int row = mrow0 + 16 * h;
+                        const int col = ncol0 + 8 * nf + (e ? c1 : c0);
+                        x[i][h][e] = make_double2(0.0, 0.0);
+                        if (sp0 + i < npieces && col < P.qn && row < P.qm)
+                            x[i][h][e] = __ldcg(reinterpret_cast<const double2*>(
+                                Ms + row + static_cast<long long>(col) * ldm));
+                    }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                if (sp0 + i >= npieces) break;
+#pragma unroll
+                for (int h = 0; h < 4; ++h)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        if (sp0 + i == 0) {
+                            v[h][e] = x[i][h][e];
+                        } else {
+                            v[h][e].x += x[i][h][e].x;
+                            v[h][e].y += x[i][h][e].y;
+                        }
+                    }
+            }
+        }
+        // the block's epilogue: rows (2g, 2g + 1) + 16h, columns 8nf + c0 / c1
+        if (P.mode == kEpiRMW) {
+            for (int u = 0; u < pd.nc; ++u) {
+                const int cq = pd.cq[u];
+                double* __restrict__ C = P.cptr[cq];
+                const int R = P.crows[cq], Cc = P.ccols[cq];
+                const double sc = P.alpha * static_cast<double>(pd.cs[u]);
+#pragma unroll
+                for (int h = 0; h < 4; ++h)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int row = mrow0 + 16 * h;
+                        const int col = ncol0 + 8 * nf + (e ? c1 : c0);
+                        if (col >= Cc) continue;
+                        if (P.c_vec && row + 1 < R) {
+                            double2* dst = reinterpret_cast<double2*>(
+                                C + row + static_cast<long long>(col) * P.cs_c);
+                            double2 cv = __ldcg(dst);
+                            cv.x = fma(sc, v[h][e].x, cv.x);
+                            cv.y = fma(sc, v[h][e].y, cv.y);
+                            *dst = cv;
+                        } else {
+                            if (row < R) {
+                                double* x0 = C + row * P.rs_c + static_cast<long long>(col) * P.cs_c;
+                                *x0 = fma(sc, v[h][e].x, __ldcg(x0));
+                            }
+                            if (row + 1 < R) {
+                                double* x1 = C + (row + 1) * P.rs_c + static_cast<long long>(col) * P.cs_c;
+                                *x1 = fma(sc, v[h][e].y, __ldcg(x1));
+                            }
+                        }
+                    }
+            }
+        } else {
+            double* __restrict__ M = P.mbase + static_cast<long long>(p) * P.mstride;
+#pragma unroll
+            for (int h = 0; h < 4; ++h)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int row = mrow0 + 16 * h;
+                    const int col = ncol0 + 8 * nf + (e ? c1 : c0);
+                    if (col >= P.qn) continue;
+                    double* dst = M + row + static_cast<long long>(col) * ldm;
+                    if (row + 1 < P.qm) {
+                        asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(dst), "d"(v[h][e].x),
+                                     "d"(v[h][e].y)
+                                     : "memory");
+                    } else if (row < P.qm) {
+                        dst[0] = v[h][e].x;
+                    }
+                }
+        }
+    }
+}
+
 // Each CTA processes units blockIdx.x, + gridDim.x, ... in increasing order.
 // With one CTA per unit that is a single pass; a persistent launch (one CTA
 // per SM) keeps the producer streaming the next unit's operand tiles into the
@@ -845,6 +980,10 @@ __global__ void __launch_bounds__(NAR ? kNarrowThreads : kThreads, NAR ? 2 : 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    // cooperative fixup (MMParams::coop_fixup): the share of a (tile, product) this CTA
+    // finishes after its unit loop -- {pending, p, tm, tn, part, nparts, npieces, half}
+    __shared__ int coop_job[8];
+    if (threadIdx.x == 0) coop_job[0] = 0;
 
     // PERSIST = false: exactly one unit per CTA (keeps the 4-term instantiation,
     // which runs at the register limit, free of the loop state)
@@ -1386,7 +1525,14 @@ __global__ void __launch_bounds__(NAR ? kNarrowThreads : kThreads, NAR ? 2 : 1)
             const int s_idx = U.piece;
             const long long ldm = P.ldm;
             int* cnt = P.arrive + (tm * P.ticket_ld + tn) * P.nprod + p;
-            const bool owner0 = P.streamk && s_idx == 0;
+            // Cooperative fixup (MMParams::coop_fixup) when two or more pieces end
+            // their CTAs' ranges: every piece stores its partial and coop_finish (not
+            // inlined: the accumulators are dead by then, and code inlined here costs
+            // the k-loops registers) shares the sums and the epilogue among them.
+            int part_i = 0, nparts = 1;
+            if (!GROUPS && P.coop_fixup) coop_participants(P, unit, s_idx, U.npieces, part_i, nparts);
+            const bool coop = nparts >= 2;
+            const bool owner0 = !coop && P.streamk && s_idx == 0;
             if (!owner0) {
                 double* Mo = P.mbase + P.part_off +
                              static_cast<long long>(p * P.ksplit + s_idx) * P.mstride;
@@ -1405,6 +1551,24 @@ __global__ void __launch_bounds__(NAR ? kNarrowThreads : kThreads, NAR ? 2 : 1)
                         }
                 __threadfence();
                 consumer_bar<CW>();
+            }
+            if (coop) {
+                // arrive; a participant (always its CTA's last unit) finishes its share
+                // after the unit loop, where no loop state is live (coop_finish)
+                if (threadIdx.x == 0) {
+                    atomicAdd(cnt, 1);
+                    if (part_i >= 0) {
+                        coop_job[0] = 1;
+                        coop_job[1] = p;
+                        coop_job[2] = tm;
+                        coop_job[3] = tn;
+                        coop_job[4] = part_i;
+                        coop_job[5] = nparts;
+                        coop_job[6] = U.npieces;
+                        coop_job[7] = pd.half;
+                    }
+                }
+                continue;
             }
             __shared__ int last_flag;
             if (owner0) {  // wait for pieces 1 .. npieces - 1
@@ -1560,6 +1724,17 @@ __global__ void __launch_bounds__(NAR ? kNarrowThreads : kThreads, NAR ? 2 : 1)
     ++trace_i;
     }  // unit
     if (SEP && pend) collect();
+    if constexpr (!GROUPS) {  // (product groups never split k)
+    consumer_bar<CW>();  // (coop_job written by thread 0)
+    if (coop_job[0]) {
+        const int p = coop_job[1], tm = coop_job[2], tn = coop_job[3];
+        const int mrow0 = tm * kBM + wm * 64 + 2 * g;
+        const int ncol0 = tn * BN + wn * 32;
+        const int c0 = coop_job[7] ? 2 * j : nperm(2 * j), c1 = coop_job[7] ? 2 * j + 1 : nperm(2 * j + 1);
+        coop_finish<CW>(P, P.prod[p], p, tm, tn, mrow0, ncol0, c0, c1, warp, coop_job[4], coop_job[5],
+                        coop_job[6]);
+    }
+    }
     trace_event(P, 31);
     if constexpr (GROUPS) {  // every warp is done with tensor memory; warp 0 frees it
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -89,3 +89,51 @@ def test_narrow_forced_on_every_variant(cuda):
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
     assert "narrow forced ok" in out.stdout
+
+
+_COOP_CHILD = r"""
+import hashlib, sys, torch
+sys.path.insert(0, {root!r})
+import paper_1605_01078_b200 as S
+ctx = S.Ctx()
+for v, L, m, n, k, row_major in [("dgemm", 0, 768, 768, 768, 0), ("dgemm", 0, 896, 896, 896, 0),
+                                 ("dgemm", 0, 768, 640, 2048, 1), ("dgemm", 0, 777, 1031, 515, 0),
+                                 ("dgemm", 0, 777, 1031, 515, 1), ("dgemm", 0, 1024, 1024, 1024, 0),
+                                 ("abc", 1, 1024, 1024, 1024, 0), ("c", 1, 1000, 1000, 1000, 0),
+                                 ("naive", 1, 1280, 1280, 1280, 1), ("dgemm", 0, 2048, 2048, 2048, 0)]:
+    g = torch.Generator(device="cuda").manual_seed(m + 3 * n + 7 * k)
+    A = (torch.rand(k, m, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    B = (torch.rand(n, k, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    C0 = (torch.rand(n, m, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    ref = C0 + A @ B
+    out = []
+    for rep in range(2):
+        C = C0.contiguous().clone() if row_major else C0.t().clone().t()
+        ctx.gemm_device(v, L, 1.0, A, B, C)
+        torch.cuda.synchronize()
+        nw = (torch.linalg.norm(C - ref) / (torch.linalg.norm(A) * torch.linalg.norm(B))).item()
+        assert nw <= 1e-12, (v, L, m, n, k, nw)
+        out.append(hashlib.sha1(C.contiguous().cpu().numpy().tobytes()).hexdigest())
+    assert out[0] == out[1], "not repeatable"
+    print("sum", v, L, m, n, k, row_major, out[0])
+print("coop child ok")
+"""
+
+
+def test_cooperative_fixup_bitwise_equal_to_single_owner(cuda):
+    """The cooperative k-split fixup (kernels.hpp MMParams::coop_fixup: the pieces of a
+    tile share the sum of the partials and the C update) gives bit for bit the
+    single-owner fixup's result -- same piece order per element -- on k-chunk grids
+    (default) and on stream-K launches (STRASSEN_B200_COOP_SK=1), within the BASELINE
+    bound of cuBLAS and repeatably; column- and row-major C (vector / scalar updates)."""
+    sums = {}
+    for name, extra in [("off", {"STRASSEN_B200_COOP": "0"}), ("on", {"STRASSEN_B200_COOP": "1"}),
+                        ("on+sk", {"STRASSEN_B200_COOP": "1", "STRASSEN_B200_COOP_SK": "1"})]:
+        out = subprocess.run([sys.executable, "-c", _COOP_CHILD.format(root=ROOT)],
+                             env=dict(os.environ, **extra), capture_output=True, text=True,
+                             timeout=600)
+        assert out.returncode == 0, (name, out.stderr[-3000:])
+        assert "coop child ok" in out.stdout
+        sums[name] = [ln for ln in out.stdout.splitlines() if ln.startswith("sum ")]
+        assert len(sums[name]) == 10
+    assert sums["off"] == sums["on"] == sums["on+sk"]
