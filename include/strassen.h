@@ -164,7 +164,17 @@ const char* strassen_status_str(strassen_status s);  /* capi.cpp:225-235 */
 /* Device-pointer entry on a caller-provided CUDA stream (cudaStream_t passed
  * as void*, used exactly; NULL = the CUDA legacy default stream).  A, B, C must be device (or managed)
  * memory.  Asynchronous: returns after enqueueing; C is updated in stream
- * order.  Same validation and semantics as strassen_gemm. */
+ * order.  Same validation and semantics as strassen_gemm.
+ *
+ * CUDA graphs: the call may be issued on a stream that is being captured
+ * (cudaStreamBeginCapture); its kernels and counter resets become graph nodes and
+ * nothing synchronises.  Conditions: the ctx's workspace is already sized (run the
+ * same call once before capturing -- a capture that would have to grow it returns
+ * STRASSEN_ERR_ALLOC), profiling is off, and whoever replays the graph keeps the
+ * replays from overlapping other calls on the same ctx (a captured call cannot wait
+ * for, or be waited on by, calls outside its graph).  Replays are bitwise equal to
+ * the eager call.  Small problems are bound by host submission (20-60 us per
+ * call), which a graph replay removes. */
 strassen_status strassen_gemm_device(strassen_ctx* ctx, void* stream, strassen_variant variant,
                                      int level, long m, long n, long k, double alpha,
                                      const double* a, long rs_a, long cs_a, const double* b,

@@ -167,16 +167,37 @@ strassen_status gemm_impl(strassen_ctx* ctx, bool explicit_stream, cudaStream_t 
         if (device_only && (!sb200::is_device_pointer(a) || !sb200::is_device_pointer(b) ||
                             !sb200::is_device_pointer(c)))
             throw std::invalid_argument("strassen_gemm_device: operands must be device memory");
+        // CUDA graph capture (device entry on an explicit stream): the call's launches and
+        // counter resets become graph nodes.  Events recorded outside the capture cannot
+        // be waited on inside it and vice versa, so a captured call neither waits for the
+        // ctx's previous call nor leaves its own completion event; the workspace must
+        // already be sized (a warm-up call of the same shape), since growing it
+        // synchronises; and whoever replays the graph keeps it from overlapping other
+        // work on this ctx (include/strassen.h, strassen_gemm_device).
+        bool capturing = false;
+        if (s != nullptr) {
+            cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+            cuda_ck(cudaStreamIsCapturing(s, &cap), "capture status");
+            capturing = cap != cudaStreamCaptureStatusNone;
+        }
+        e.capturing = capturing;
+        if (capturing && (!device_only || e.profiling))
+            throw std::invalid_argument(
+                "stream capture: only strassen_gemm_device (device operands, no profiling)");
         // the workspace is shared by every call on this ctx: order this call after the
         // previous one even when it was issued on another stream
-        if (e.ev_last_recorded) cuda_ck(cudaStreamWaitEvent(s, e.ev_last, 0), "order after previous call");
+        if (e.ev_last_recorded && !capturing)
+            cuda_ck(cudaStreamWaitEvent(s, e.ev_last, 0), "order after previous call");
         e.unit_ctr_next = 0;
         try {
         long launches = 0;
         bool sa = false, sb = false, sc = false;
         // the copy stream may only overwrite staging buffers once earlier work on s is done
-        cuda_ck(cudaEventRecord(e.ev_call, s), "call event");
-        cuda_ck(cudaStreamWaitEvent(e.copy_stream, e.ev_call, 0), "copy stream order");
+        // (a captured call stages nothing, and an unjoined fork would fail the capture)
+        if (!capturing) {
+            cuda_ck(cudaEventRecord(e.ev_call, s), "call event");
+            cuda_ck(cudaStreamWaitEvent(e.copy_stream, e.ev_call, 0), "copy stream order");
+        }
         // Host B and C in column-major layouts: pipeline the call in windows
         // (engine.hpp Windows) when the problem is large enough; A arrives in
         // row strips when it is host column-major too.
@@ -279,8 +300,10 @@ strassen_status gemm_impl(strassen_ctx* ctx, bool explicit_stream, cudaStream_t 
                         "D2H result");
             }
         }
-        cuda_ck(cudaEventRecord(e.ev_last, s), "call done event");
-        e.ev_last_recorded = true;
+        if (!capturing) {
+            cuda_ck(cudaEventRecord(e.ev_last, s), "call done event");
+            e.ev_last_recorded = true;
+        }
         if (!device_only) cuda_ck(cudaStreamSynchronize(s), "kernel execution");
         else cuda_ck(cudaGetLastError(), "kernel launch");
         e.last_launches = launches;
@@ -292,10 +315,13 @@ strassen_status gemm_impl(strassen_ctx* ctx, bool explicit_stream, cudaStream_t 
         } catch (...) {
             // nothing enqueued by this call may outlive it: copies from / to the
             // caller's buffers and kernels reading the workspace (best effort)
-            for (cudaStream_t st : {s, e.copy_stream, e.d2h_stream, e.aux_stream})
-                if (st || st == s) cudaStreamSynchronize(st);
-            cudaGetLastError();
-            if (cudaEventRecord(e.ev_last, s) == cudaSuccess) e.ev_last_recorded = true;
+            // (a failed capture is the caller's to end: nothing has run)
+            if (!capturing) {
+                for (cudaStream_t st : {s, e.copy_stream, e.d2h_stream, e.aux_stream})
+                    if (st || st == s) cudaStreamSynchronize(st);
+                cudaGetLastError();
+                if (cudaEventRecord(e.ev_last, s) == cudaSuccess) e.ev_last_recorded = true;
+            }
             cudaGetLastError();
             throw;
         }

@@ -262,6 +262,10 @@ cudaStream_t Engine::stream() { return has_user_stream ? user_stream : nullptr; 
 double* Engine::ensure(DeviceBuffer& b, size_t bytes) {
     if (bytes == 0) bytes = 8;
     if (b.bytes < bytes) {
+        if (capturing)
+            throw Error(STRASSEN_ERR_ALLOC,
+                        "stream capture: the workspace must already be sized (run the same "
+                        "call once before capturing it)");
         if (b.ptr) {
             // earlier launches (on any stream) may still read it
             ck(cudaDeviceSynchronize(), "sync before realloc");
@@ -1355,6 +1359,9 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
     if (win || live.size() <= 1 || extra <= 0.0 || extra <= device_bytes_free())
         return run_program(live, P);
     // Not enough: give the ctx's temporaries back and run groups that fit
+    if (e.capturing)
+        throw Error(STRASSEN_ERR_ALLOC, "stream capture: the call's temporaries do not fit "
+                                        "beside the ctx's workspace (product groups release it)");
     ck(cudaDeviceSynchronize(), "sync before releasing temporaries");
     for (DeviceBuffer* b : {&e.tabuf, &e.tbbuf, &e.mbuf})
         if (b->ptr) {
@@ -1557,6 +1564,9 @@ long run_outer(Engine& e, cudaStream_t s, strassen_variant variant, int level, d
         run_group(live);
         return launches;
     }
+    if (e.capturing)
+        throw Error(STRASSEN_ERR_ALLOC, "stream capture: the call's temporaries do not fit "
+                                        "beside the ctx's workspace (product groups release it)");
     ck(cudaDeviceSynchronize(), "sync before releasing temporaries");
     for (DeviceBuffer* b : {&e.l3_a, &e.l3_b, &e.l3_m})
         if (b->ptr) {

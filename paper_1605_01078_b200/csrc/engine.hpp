@@ -62,6 +62,9 @@ struct Engine {
     bool peeling = true;  // dynamic peeling of odd fringes (strassen_ctx_set_peeling)
     // optional per-launch timing of the last call (strassen_ctx_enable_profiling)
     bool profiling = false;
+    // the current call is being captured into a CUDA graph (capi.cpp gemm_impl): the
+    // workspace may not grow (growing synchronises the device)
+    bool capturing = false;
     struct Timed {
         const char* name;
         cudaEvent_t start, stop;

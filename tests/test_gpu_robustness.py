@@ -199,3 +199,63 @@ def test_product_groups_in_tensor_memory(cuda, variant, level, shape):
     assert _normwise(outs[0], ref, A, B) <= (5e-12 if level == 2 else 1e-12)
     assert torch.equal(outs[0], outs[1])
     assert torch.equal(outs[0], outs[2]), (variant, level, shape)
+
+
+@pytest.mark.parametrize("variant,level,shape", [
+    ("dgemm", 0, (512, 512, 512)), ("dgemm", 0, (1024, 1024, 1024)), ("abc", 1, (1024, 1024, 1024)),
+    ("c", 1, (1000, 900, 1100)), ("abc", 2, (2048, 2048, 2048)), ("naive", 2, (2048, 1536, 1024)),
+    ("ab", 2, (1536, 1536, 1536)), ("c", 2, (4096, 4096, 512)),
+])
+def test_device_entry_under_cuda_graph_capture(cuda, variant, level, shape):
+    """strassen_gemm_device issued on a capturing stream (include/strassen.h): the call's
+    launches and counter resets become graph nodes; replays are bitwise equal to the eager
+    call, repeatably, and within the BASELINE bound of cuBLAS."""
+    import torch
+    m, n, k = shape
+    A, B, C0 = _dev(m, n, k, seed=m + n + k)
+    ctx = S.Ctx()
+    Ce = _clone(C0)
+    ctx.gemm_device(variant, level, 1.0, A, B, Ce)   # eager; also sizes the workspace
+    torch.cuda.synchronize()
+    ref = C0 + A @ B
+    assert _normwise(Ce, ref, A, B) <= (5e-12 if level == 2 else 1e-12)
+    Cg = _clone(C0)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        ctx.gemm_device(variant, level, 1.0, A, B, Cg, torch.cuda.current_stream())
+    for _ in range(3):
+        Cg.copy_(C0)
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(Cg, Ce)
+    # eager calls on the same ctx still work after the capture
+    Ce2 = _clone(C0)
+    ctx.gemm_device(variant, level, 1.0, A, B, Ce2)
+    torch.cuda.synchronize()
+    assert torch.equal(Ce2, Ce)
+    ctx.close()
+
+
+def test_capture_that_would_grow_the_workspace_is_refused(cuda):
+    """A captured call may not grow the ctx's workspace (growing synchronises the
+    device): STRASSEN_ERR_ALLOC before any CUDA call that would invalidate the capture,
+    and the ctx works again afterwards."""
+    import torch
+    A, B, C0 = _dev(512, 512, 512, seed=5)
+    A2, B2, C2 = _dev(2048, 2048, 2048, seed=6)
+    ctx = S.Ctx()
+    C = _clone(C0)
+    ctx.gemm_device("naive", 1, 1.0, A, B, C)        # initialises the ctx, small workspace
+    torch.cuda.synchronize()
+    Cg = _clone(C2)
+    graph = torch.cuda.CUDAGraph()
+    with pytest.raises(S.StrassenError) as ei:
+        with torch.cuda.graph(graph):
+            ctx.gemm_device("naive", 2, 1.0, A2, B2, Cg, torch.cuda.current_stream())
+    assert ei.value.status == S.ERR_ALLOC and "capture" in str(ei.value)
+    torch.cuda.synchronize()
+    Ce = _clone(C2)
+    ctx.gemm_device("naive", 2, 1.0, A2, B2, Ce)     # eager: grows the workspace, runs
+    torch.cuda.synchronize()
+    assert _normwise(Ce, C2 + A2 @ B2, A2, B2) <= 5e-12
+    ctx.close()
