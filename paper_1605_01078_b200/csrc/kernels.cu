@@ -947,7 +947,7 @@ __host__ __device__ constexpr const StreamTab& stream_tab() { return L == 1 ? kS
 
 #ifdef SB200_TRACE
 __device__ __forceinline__ void trace_event(const MMParams& P, int slot) {
-    if (P.trace && threadIdx.x == 0 && slot < 32) {
+    if (P.trace && threadIdx.x == 0 && slot < 32 && blockIdx.x < 8192) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         P.trace[blockIdx.x * 32 + slot] = t;
@@ -1394,8 +1394,10 @@ __global__ void __launch_bounds__(NAR ? kNarrowThreads : kThreads, NAR ? 2 : 1)
                     }
                     consumer_fence();  // generic smem writes before the async-proxy reads
                     if (!issued && ticketed) {
+                        trace_event(P, 20);  // (single-unit launches: first stage written)
                         if (threadIdx.x == 0) wait_ticket(P, U.tk, tm, tn);
                         asm volatile("fence.proxy.async.global;" ::: "memory");
+                        trace_event(P, 21);  // ticket held
                     }
                     consumer_bar<CW>();
                     asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -1457,10 +1459,12 @@ __global__ void __launch_bounds__(NAR ? kNarrowThreads : kThreads, NAR ? 2 : 1)
                 pend_tn = tn;
                 continue;
             }
+            trace_event(P, 22);  // every reduce-add issued
             if (succ) {  // all reductions performed (every warp's), then hand the tile on
                 asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
                 asm volatile("fence.proxy.async.global;" ::: "memory");
                 consumer_bar<CW>();
+                trace_event(P, 23);  // reductions complete
                 if (threadIdx.x == 0) {
                     __threadfence();
                     release_ticket(P, U.tk, tm, tn);
