@@ -376,7 +376,40 @@ FusedPlan plan_fused(Engine& e, cudaStream_t s, const MMParams& P, bool force_sp
     // its partials and stream pass (8192^3 C L2: 12544 CTAs on 256 tiles).
     // (>= one wave of tiles: with fewer, many products of one tile are in flight
     // at once and their ticketed epilogues serialise -- 1024^3 ABC L2 0.14 -> 0.60 ms)
-    const bool fused = ntiles >= 2 * sms || (np > 1 && ks == 1 && ntiles >= sms);
+    bool fused = ntiles >= 2 * sms || (np > 1 && ks == 1 && ntiles >= sms);
+    static const bool fixup_on = [] {
+        const char* v = std::getenv("STRASSEN_B200_FIXUP");  // 0 / 1 (experiments)
+        return v ? std::atoi(v) != 0 : true;
+    }();
+    static const bool streamk_on = [] {
+        const char* v = std::getenv("STRASSEN_B200_STREAMK");  // 0 / 1 (experiments)
+        return v ? std::atoi(v) != 0 : true;
+    }();
+    // Classical launches of two to four waves of tiles: tile ownership quantises to whole
+    // waves (2304^3 is 324 tiles on 148 SMs: three waves for 2.19 waves of work, 25.5
+    // TF/s against cuBLAS's 33.9; profiles/r02_mid_scan.log).  Stream-K over all the tiles
+    // instead, where the cost comparison says so.  Under four waves only: from there host
+    // calls run in windows (plan_windows), which cannot run the whole call's pieces, and
+    // host and device calls must plan alike.
+    bool sk_wide = false;
+    static const bool sk_wide_on = [] {
+        const char* v = std::getenv("STRASSEN_B200_STREAMK_WIDE");  // 0 / 1 (experiments)
+        return v ? std::atoi(v) != 0 : true;
+    }();
+    if (fused && !force_split && np == 1 && P.nprod == 1 && fixup_on && streamk_on && sk_wide_on &&
+        !windowed && ntiles < 4 * sms) {
+        const long total = static_cast<long>(ntiles) * P.ktiles;
+        const long len = ceil_div(total, std::max(1L, std::min<long>(sms, total / 8)));
+        const double t_k = 2.1e-6, t_cta = 3e-6;
+        const double t_uni = std::ceil(static_cast<double>(ntiles) / sms) *
+                             (static_cast<double>(P.ktiles) * t_k + t_cta);
+        const double t_sk = static_cast<double>(len) * t_k +
+                            std::ceil(static_cast<double>(len) / P.ktiles + 1.0) * t_cta + 15e-6;
+        if (t_sk < 0.97 * t_uni) {
+            fused = false;
+            sk_wide = true;
+        }
+    }
     if (fused && !force_split) {
         // Fused epilogue.  Tile ownership (one CTA walks every product of its
         // tile) quantises to whole waves of CTAs that each run all 7^L products
@@ -411,15 +444,11 @@ FusedPlan plan_fused(Engine& e, cudaStream_t s, const MMParams& P, bool force_sp
     // 598 -> 575 us).  Not for Strassen programs: their 7^L updates per tile
     // would serialise on the tile's ticket (1024^3 ABC L2 139 -> 696 us), where
     // the stream pass applies them in parallel over elements.
-    static const bool fixup_on = [] {
-        const char* v = std::getenv("STRASSEN_B200_FIXUP");  // 0 / 1 (experiments)
-        return v ? std::atoi(v) != 0 : true;
-    }();
-    static const bool streamk_on = [] {
-        const char* v = std::getenv("STRASSEN_B200_STREAMK");  // 0 / 1 (experiments)
-        return v ? std::atoi(v) != 0 : true;
-    }();
-    if (!force_split && fixup_on && np == 1 && streamk_on) {
+    if (sk_wide) {  // (decided above: one chunk per tile would be the alternative)
+        F.ksplit = 1;
+        F.per = P.ktiles;
+        F.streamk = true;
+    } else if (!force_split && fixup_on && np == 1 && streamk_on) {
         // Stream-K: the flattened (tile, k-step) space cut into equal ranges, one
         // per persistent CTA, so every SM gets the same work (uniform k-chunks
         // quantise to whole waves: 2048^3 has 256 tiles on 148 SMs).  Pieces of a

@@ -137,3 +137,28 @@ def test_cooperative_fixup_bitwise_equal_to_single_owner(cuda):
         sums[name] = [ln for ln in out.stdout.splitlines() if ln.startswith("sum ")]
         assert len(sums[name]) == 10
     assert sums["off"] == sums["on"] == sums["on+sk"]
+
+
+@pytest.mark.parametrize("shape", [(2304, 2304, 2304), (2816, 2432, 700), (2301, 2417, 777),
+                                   (3000, 3000, 520)])
+def test_classical_stream_k_between_two_and_four_waves(cuda, shape):
+    """Classical launches of two to four waves of 128 x 128 tiles run stream-K over all
+    the tiles instead of whole waves of tile owners (engine.cpp plan_fused): within the
+    BASELINE bound of cuBLAS, repeatable, and the host-pointer call (never windowed under
+    four waves) bitwise equal to the device call."""
+    import numpy as np
+    import torch
+    m, n, k = shape
+    ctx = S.Ctx()
+    first = _check(ctx, "dgemm", 0, m, n, k, 0, -0.5, seed=m + n + k)
+    second = _check(ctx, "dgemm", 0, m, n, k, 0, -0.5, seed=m + n + k)
+    assert torch.equal(first, second)
+    g = torch.Generator(device="cuda").manual_seed(m + n + k)
+    A = (torch.rand(k, m, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    B = (torch.rand(n, k, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    C0 = (torch.rand(n, m, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    a, b = np.asfortranarray(A.cpu().numpy()), np.asfortranarray(B.cpu().numpy())
+    c = np.asfortranarray(C0.cpu().numpy())
+    ctx.gemm("dgemm", 0, -0.5, a, b, c)              # host pointers through strassen_gemm
+    assert np.array_equal(c, first.cpu().numpy())
+    ctx.close()
