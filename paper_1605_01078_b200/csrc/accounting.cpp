@@ -319,9 +319,25 @@ static double predict_core(strassen_variant v, int L, long m, long n, long k, in
         ks = ks_fit;
         ctas *= ks;
     }
+    // executed flops: whole 128 x 128 x 16 tile steps -- partial tiles at the quadrant
+    // edges run padded (2304^3 at level 2: quadrants of 576 = 4.5 tiles, 23% more work;
+    // profiles/r02_mid_scan_variants.log)
+    const double flops_q = tiles * 128.0 * 128.0 * std::ceil(qk / 16.0) * 16.0;
     // per-CTA fixed cost (barrier init, pipeline fill, epilogue): ~4 us per wave
-    double t = mul * 2.0 * qm * qn * qk / (P * e_mm * waves_eff(ctas, sms)) +
+    double t = mul * 2.0 * flops_q / (P * e_mm * waves_eff(ctas, sms)) +
                4e-6 * std::ceil(ctas / sms);
+    if (mul == 1 && fused && tiles < 4.0 * sms) {
+        // classical launches of two to four waves of tiles: stream-K over all the tiles
+        // where engine.cpp plan_fused's comparison says so; 2.22 us per k-step and the
+        // pieces' fixup fitted to profiles/r02_streamk_wide_ab.log (2304^3 734 us,
+        // 2816^3 1303 us back to back)
+        const double kt = std::ceil(qk / 16.0), total = tiles * kt;
+        const double len = std::ceil(total / std::max(1.0, std::min<double>(sms, std::floor(total / 8))));
+        const double t_k = 2.1e-6, t_cta = 3e-6;
+        const double t_uni = std::ceil(tiles / sms) * (kt * t_k + t_cta);
+        const double t_sk = len * t_k + std::ceil(len / kt + 1.0) * t_cta + 15e-6;
+        if (t_sk < 0.97 * t_uni) t = len * 2.22e-6 + 14e-6;
+    }
     if (mul > 1 && split && tiles * mul < 4.0 * sms) {
         // stream-K pieces of the (product, tile, k-step) space, as engine.cpp plan_fused
         // decides them; the pieces run at ~0.8 of the mainloop rate at these sizes
@@ -333,7 +349,7 @@ static double predict_core(strassen_variant v, int L, long m, long n, long k, in
         const double t_uni = std::ceil(tiles * mul * ks / sms) * (per * t_k + t_cta);
         const double t_sk = len * t_k + std::ceil(len / kt + 1.0) * t_cta + 6e-6;
         if (t_sk < 0.97 * t_uni)
-            t = mul * 2.0 * qm * qn * qk / (P * e_mm * 0.8 * waves_eff(std::ceil(total / len), sms)) +
+            t = mul * 2.0 * flops_q / (P * e_mm * 0.8 * waves_eff(std::ceil(total / len), sms)) +
                 std::ceil(len / kt + 1.0) * 4e-6;
     }
     if (mul == 1 && split) {  // stream-K pieces when they beat the k-chunk waves (engine.cpp)
