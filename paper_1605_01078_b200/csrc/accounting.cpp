@@ -338,6 +338,15 @@ static double predict_core(strassen_variant v, int L, long m, long n, long k, in
         const double t_sk = len * t_k + std::ceil(len / kt + 1.0) * t_cta + 15e-6;
         if (t_sk < 0.97 * t_uni) t = len * 2.22e-6 + 14e-6;
     }
+    if (mul == 1 && fused && tiles >= 4.0 * sms) {
+        // four waves and more: whole waves of tile owners plus a stream-K tail where
+        // plan.hpp choose_tail finds one (engine.cpp plan_fused), scaled from its estimate
+        const long tm = static_cast<long>(std::ceil(qm / 128.0)), tn = static_cast<long>(std::ceil(qn / 128.0));
+        const long kt = static_cast<long>(std::ceil(qk / 16.0));
+        const TailPlan T = choose_tail(tm, tn, kt, sms);
+        if (T.cols > 0)
+            t *= T.t / (std::ceil(tiles / sms) * (static_cast<double>(kt) * 2.1e-6 + 3e-6));
+    }
     if (mul > 1 && split && tiles * mul < 4.0 * sms) {
         // stream-K pieces of the (product, tile, k-step) space, as engine.cpp plan_fused
         // decides them; the pieces run at ~0.8 of the mainloop rate at these sizes

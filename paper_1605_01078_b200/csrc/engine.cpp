@@ -351,6 +351,10 @@ struct FusedPlan {
     int ksplit = 1, per = 0;
     long long ldm = 0, mstride = 0;
     double* M = nullptr;
+    // classical hybrid (plan.hpp choose_tail): the fused tile-owner grid on the tile
+    // columns before tail_tn0, stream-K pieces (sk_*, ksplit, M, arrive above) on the rest
+    bool tail = false;
+    int tail_tn0 = 0;
 };
 
 // nprod_plan / terms_plan: plan as for this many products with this mean term
@@ -409,6 +413,37 @@ FusedPlan plan_fused(Engine& e, cudaStream_t s, const MMParams& P, bool force_sp
             fused = false;
             sk_wide = true;
         }
+    }
+    if (fused && !force_split && np == 1 && P.nprod == 1 && fixup_on && streamk_on && sk_wide_on &&
+        !windowed && !P.narrow && ntiles >= 4 * sms) {
+        // Four waves of tiles and more: whole waves of tile owners, then the last tile
+        // columns as stream-K pieces (plan.hpp choose_tail; 3840^3: 7 waves of owners ->
+        // 6 waves + a balanced tail).  Not for windowed host calls, whose windows cannot
+        // run a whole call's pieces: those keep the plain grid, so at these shapes a
+        // pipelined host call and the device call round differently (both within bounds).
+        const TailPlan T = choose_tail(P.tiles_m, P.tiles_n, P.ktiles, sms);
+        if (T.cols > 0) {
+            F.tail = true;
+            F.tail_tn0 = P.tiles_n - static_cast<int>(T.cols);
+            const long tail_tiles = static_cast<long>(P.tiles_m) * T.cols;
+            const long total = tail_tiles * P.ktiles;
+            const long len = ceil_div(total, std::max(1L, std::min<long>(sms, total / 8)));
+            F.sk_len = static_cast<int>(len);
+            F.sk_grid = static_cast<int>(ceil_div(total, len));
+            F.sk_maxp = static_cast<int>(ceil_div(len, P.ktiles) + 1);
+            F.ksplit = static_cast<int>(ceil_div(P.ktiles, len) + 1);  // partial slots per tile
+            F.per = P.ktiles;
+            F.ldm = (P.qm + 1) / 2 * 2;
+            // partial slots span the tail's columns only (the kernel indexes by the
+            // quadrant column: run_fused_window shifts the base)
+            F.mstride = F.ldm * static_cast<long long>(T.cols) * kBN;
+            F.M = e.ensure(e.mbuf, static_cast<size_t>(F.mstride) * F.ksplit * 8);
+            const size_t nt = static_cast<size_t>(P.tiles_m) * P.tiles_n;
+            F.arrive = reinterpret_cast<int*>(e.ensure(e.ticket_buf, nt * sizeof(int)));
+            ck(cudaMemsetAsync(F.arrive, 0, nt * sizeof(int), s), "arrive reset");
+            F.ticket_ld = P.tiles_n;
+        }
+        return F;
     }
     if (fused && !force_split) {
         // Fused epilogue.  Tile ownership (one CTA walks every product of its
@@ -583,6 +618,35 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
     P.tiles_m = static_cast<int>(ceil_div(r1 - r0, kBM));
     P.tn0 = static_cast<int>(c0 / bn);
     P.tiles_n = static_cast<int>(ceil_div(c1 - c0, bn));
+    if (F.tail) {
+        // classical hybrid: tile owners on the first tile columns, stream-K pieces on the
+        // rest (never windowed: the range is the whole output)
+        FusedPlan body;  // (the plain fused plan: no tickets for a single product)
+        const long split_c = static_cast<long>(F.tail_tn0) * kBN;
+        long launches = run_fused_window(e, s, P, body, dests, cq, C, alpha, r0, r1, c0,
+                                         std::min(c1, split_c), wait_c);
+        MMParams T = P;
+        T.tn0 = F.tail_tn0;
+        T.tiles_n = static_cast<int>(ceil_div(c1 - split_c, kBN));
+        T.mode = kEpiRMW;
+        T.split = 1;
+        T.ksplit = F.ksplit;
+        T.kt_per_split = F.per;
+        T.ldm = F.ldm;
+        T.mstride = F.mstride;
+        T.mbase = F.M - static_cast<long long>(split_c) * F.ldm;  // slots start at column split_c
+        T.arrive = F.arrive;
+        T.ticket_ld = F.ticket_ld;
+        T.streamk = 1;
+        T.sk_len = F.sk_len;
+        T.sk_maxp = F.sk_maxp;
+        T.grid_cap = F.sk_grid;  // the decode assumes exactly this many CTAs
+        T.trace = trace_buffer();
+        e.prof_begin("mm_kernel", s);
+        ck(launch_mm(T, s), "mm_kernel (stream-K tail)");
+        e.prof_end(s);
+        return launches + 1;
+    }
     if (!F.split) {
         wait_c();  // fused epilogue reads C
         P.mode = kEpiRMW;

@@ -40,4 +40,40 @@ inline int choose_ksplit(long ntiles, long nprod, long ktiles, long sms, double 
     return best_ks;
 }
 
+// Classical launches of four or more waves of tile owners: the last, partial wave
+// leaves SMs idle (3840^3: 900 tiles on 148 SMs run as 7 waves for 6.08 waves of work).
+// Hybrid: the first tile columns as whole waves of tile owners, the last `cols` tile
+// columns (the "tail") as stream-K pieces balanced over every SM.  Returns the tail's
+// tile columns (0 = none: the plain tile-owner grid is within 3% of it) and the
+// predicted time of the choice.
+struct TailPlan {
+    long cols = 0;
+    double t = 0.0;
+};
+inline TailPlan choose_tail(long tiles_m, long tiles_n, long ktiles, long sms) {
+    const double t_k = 2.1e-6, t_cta = 3e-6;
+    const double t_tile = static_cast<double>(ktiles) * t_k + t_cta;
+    TailPlan best;
+    best.t = std::ceil(static_cast<double>(tiles_m) * tiles_n / sms) * t_tile;
+    const double t_plain = best.t;
+    for (long ct = 1; ct < tiles_n; ++ct) {
+        const double body = static_cast<double>(tiles_m) * (tiles_n - ct);
+        const double tail = static_cast<double>(tiles_m) * ct;
+        if (tail > 2.0 * sms) break;  // (a tail of up to two waves of tiles)
+        const double len = std::ceil(tail * ktiles / sms);
+        // stream-K pieces: 2.22 us per k-step and ~30 us of fixup and launch
+        // (profiles/r02_streamk_wide_ab.log)
+        const double t = std::ceil(body / sms) * t_tile + len * 2.22e-6 + 30e-6;
+        if (t < best.t) {
+            best.t = t;
+            best.cols = ct;
+        }
+    }
+    if (best.t > 0.97 * t_plain) {
+        best.cols = 0;
+        best.t = t_plain;
+    }
+    return best;
+}
+
 }  // namespace sb200

@@ -162,3 +162,38 @@ def test_classical_stream_k_between_two_and_four_waves(cuda, shape):
     ctx.gemm("dgemm", 0, -0.5, a, b, c)              # host pointers through strassen_gemm
     assert np.array_equal(c, first.cpu().numpy())
     ctx.close()
+
+
+@pytest.mark.parametrize("shape", [(3328, 3328, 2048), (3840, 3840, 1030), (3333, 3841, 1100),
+                                   (5632, 5632, 1024)])
+def test_classical_tile_owner_waves_plus_stream_k_tail(cuda, shape):
+    """Classical launches from four waves of tiles up: whole waves of tile owners on the
+    first tile columns, stream-K pieces on the last ones (plan.hpp choose_tail) -- two
+    launches; within the BASELINE bound of cuBLAS, repeatable, and the unpipelined
+    host-pointer call bitwise equal to the device call."""
+    import numpy as np
+    import torch
+    m, n, k = shape
+    ctx = S.Ctx()
+    first = _check(ctx, "dgemm", 0, m, n, k, 0, -0.5, seed=m + n + k)
+    assert ctx.last_launches() >= 2
+    second = _check(ctx, "dgemm", 0, m, n, k, 0, -0.5, seed=m + n + k)
+    assert torch.equal(first, second)
+    g = torch.Generator(device="cuda").manual_seed(m + n + k)
+    A = (torch.rand(k, m, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    B = (torch.rand(n, k, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    C0 = (torch.rand(n, m, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
+    a, b = np.asfortranarray(A.cpu().numpy()), np.asfortranarray(B.cpu().numpy())
+    c = np.asfortranarray(C0.cpu().numpy())
+    ctx.set_pipelining(False)
+    ctx.gemm("dgemm", 0, -0.5, a, b, c)              # host pointers, one window
+    assert np.array_equal(c, first.cpu().numpy())
+    # the pipelined host call keeps the plain tile-owner grid (its windows cannot run a
+    # whole call's pieces): same bound
+    ctx.set_pipelining(True)
+    c2 = np.asfortranarray(C0.cpu().numpy())
+    ctx.gemm("dgemm", 0, -0.5, a, b, c2)
+    ref = (C0 - 0.5 * (A @ B)).cpu().numpy()
+    nw = np.linalg.norm(c2 - ref) / (np.linalg.norm(a) * np.linalg.norm(b))
+    assert nw <= 1e-12
+    ctx.close()
