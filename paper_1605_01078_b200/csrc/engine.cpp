@@ -739,7 +739,7 @@ long run_fused_window(Engine& e, cudaStream_t s, MMParams P, const FusedPlan& F,
     }();
     // Stream-K launches keep the single-owner fixup: sharing it measured no gain (1024^3
     // DGEMM 88.6 -> 86.7 us) or a loss (1024^3 ABC L1 90.8 -> 93.6, 1280^3 DGEMM 147.6 ->
-    // 150.6: profiles/r02_coop_ab.log) -- every participant then also writes its own
+    // 150.6: profiles/r02_cta_trace_coop_sk.log) -- every participant then also writes its own
     // partial, which the owner keeps in registers.
     static const bool coop_sk = [] {
         const char* v = std::getenv("STRASSEN_B200_COOP_SK");  // 0 / 1 (experiments)
