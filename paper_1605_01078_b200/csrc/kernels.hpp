@@ -154,15 +154,17 @@ struct alignas(64) MMParams {
     // fixup keeps its partials at mbase).
     int sk_store;
     long long part_off;
-    // Cooperative fixup (stream-K; k-chunk grids whose CTAs are all resident with one
-    // unit each): the pieces of a (tile, product) that are their CTA's last unit
-    // ("participants") share the fixup instead of one owner doing all of it -- each
-    // owns the 64 x 8 fragment blocks b = 4 warp + nf with b % participants == its index,
-    // writes only the blocks it does not own, waits until every piece has arrived, adds
-    // the other pieces' values of its blocks (ascending piece order) and applies the
-    // epilogue to them.  A piece with units after it (the tail piece at the start of a
-    // stream-K range) only writes its partial and arrives.  Deterministic: ownership and
-    // order are functions of the plan.
+    // Cooperative fixup (k-chunk grids whose CTAs are all resident with one unit each;
+    // stream-K launches too under STRASSEN_B200_COOP_SK, off by default: no gain
+    // measured): the pieces of a (tile, product) that are their CTA's last unit
+    // ("participants") share the fixup instead of one owner doing all of it.  Every piece
+    // stores its partial and arrives; after its unit loop -- where the accumulators and
+    // the ring state are dead, so the code costs the k-loops no registers -- a participant
+    // waits until every piece has arrived, sums the partials of the 64 x 8 fragment blocks
+    // b = 4 warp + nf with b % participants == its index (ascending piece order, the
+    // single-owner fixup's arithmetic, bit for bit) and applies the epilogue to them.  A
+    // piece with units after it (the tail piece at the start of a stream-K range) only
+    // stores its partial and arrives.
     int coop_fixup;
     // A-heavy products (more A than B terms) in one-CTA-per-unit launches run the
     // 4 x 2 warp layout (kernels.cu product_kloop1)
