@@ -450,9 +450,12 @@ double b200_predict_seconds(strassen_variant v, int level, long m, long n, long 
     if (L > 0 && (me != m || ne != n || ke != k) && me >= S * 128 && ne >= S * 128 &&
         ke >= S * 16 && work(me, ne, ke) < work(m, n, k)) {
         double t = predict_core(v, L, me, ne, ke, sms, vec(me));
-        if (ke < k) t += predict_core(STRASSEN_DGEMM, 0, me, ne, k - ke, sms, m % 2 == 0);
-        if (me < m) t += predict_core(STRASSEN_DGEMM, 0, m - me, n, k, sms, false);
-        if (ne < n) t += predict_core(STRASSEN_DGEMM, 0, me, n - ne, k, sms, m % 2 == 0);
+        // the fringe updates are streaming kernels (fringe.cu): the long operand or C
+        // once through HBM (4.5 TB/s measured at 4097^3 / 8193^3) plus their launches
+        const double BWF = 4.5e12, launch = 12e-6;
+        if (ke < k) t += 16.0 * me * ne / BWF + launch;
+        if (me < m) t += 8.0 * static_cast<double>(k) * n / BWF + 2 * launch;
+        if (ne < n) t += 8.0 * static_cast<double>(me) * k / BWF + 2 * launch;
         return t;
     }
     return predict_core(v, L, m, n, k, sms, vec(m));

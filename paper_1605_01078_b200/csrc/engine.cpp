@@ -198,7 +198,7 @@ Engine::~Engine() {
         if (ev) cudaEventDestroy(ev);
     if (ev_last) cudaEventDestroy(ev_last);
     for (DeviceBuffer* b : {&stage_a, &stage_b, &stage_c, &pack_a, &pack_b, &mbuf, &tabuf, &tbbuf, &ticket_buf,
-                               &pack_a3, &pack_b3, &l3_a, &l3_b, &l3_m, &unit_ctr_buf})
+                               &pack_a3, &pack_b3, &l3_a, &l3_b, &l3_m, &unit_ctr_buf, &fringe_buf})
         if (b->ptr) cudaFree(b->ptr);
 }
 
@@ -291,7 +291,7 @@ double* Engine::ensure(DeviceBuffer& b, size_t bytes) {
 size_t Engine::workspace_bytes() const {
     size_t t = 0;
     for (const DeviceBuffer* b : {&stage_a, &stage_b, &stage_c, &pack_a, &pack_b, &mbuf, &tabuf, &tbbuf, &ticket_buf,
-                               &pack_a3, &pack_b3, &l3_a, &l3_b, &l3_m, &unit_ctr_buf})
+                               &pack_a3, &pack_b3, &l3_a, &l3_b, &l3_m, &unit_ctr_buf, &fringe_buf})
         t += b->bytes;
     return t;
 }
@@ -1081,15 +1081,75 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
     if (!peel) return run_level(e, s, variant, level, alpha, A, B, C, win);
     long launches = run_level(e, s, variant, level, alpha, sub(A, 0, 0, me, ke),
                               sub(B, 0, 0, ke, ne), sub(C, 0, 0, me, ne), nullptr);
-    if (ke < k)
-        launches += run_strassen(e, s, STRASSEN_DGEMM, 0, alpha, sub(A, 0, ke, me, k - ke),
-                                 sub(B, ke, 0, k - ke, ne), sub(C, 0, 0, me, ne), nullptr);
-    if (me < m)
-        launches += run_strassen(e, s, STRASSEN_DGEMM, 0, alpha, sub(A, me, 0, m - me, k), B,
-                                 sub(C, me, 0, m - me, n), nullptr);
-    if (ne < n)
-        launches += run_strassen(e, s, STRASSEN_DGEMM, 0, alpha, sub(A, 0, 0, me, k),
-                                 sub(B, 0, ne, k, n - ne), sub(C, 0, ne, me, n - ne), nullptr);
+    // The three fringe updates (at most 2^L - 1 wide): streaming kernels (fringe.cu) --
+    // through the tile kernel a 1 x 4097 x 4097 update ran 33 CTAs over the whole k
+    // loop, 0.5 ms of the 4.3 ms call.  STRASSEN_B200_FRINGE=0: the tile kernel.
+    static const bool fringe_on = [] {
+        const char* v = std::getenv("STRASSEN_B200_FRINGE");  // 0 / 1 (experiments)
+        return v ? std::atoi(v) != 0 : true;
+    }();
+    const bool thin = fringe_on && S - 1 <= fringe_max_width();
+    if (thin) {  // (operands still being copied in: the core has waited on s already)
+        wait_ready(s, A);
+        wait_ready(s, B);
+        wait_ready(s, C);
+    }
+    auto part = [&](long long_len, long thin_w, long kk) {
+        return e.ensure(e.fringe_buf, fringe_partial_bytes(long_len, static_cast<int>(thin_w), kk));
+    };
+    if (ke < k) {
+        const DView a = sub(A, 0, ke, me, k - ke), b = sub(B, ke, 0, k - ke, ne);
+        const DView c = sub(C, 0, 0, me, ne);
+        if (thin) {
+            e.prof_begin("fringe_k_kernel", s);
+            ck(launch_fringe_k(a.p, a.rs, a.cs, b.p, b.rs, b.cs, c.p, c.rs, c.cs, me, ne,
+                               static_cast<int>(k - ke), alpha, s),
+               "fringe (k)");
+            e.prof_end(s);
+            ++launches;
+        } else {
+            launches += run_strassen(e, s, STRASSEN_DGEMM, 0, alpha, a, b, c, nullptr);
+        }
+    }
+    if (me < m) {
+        const DView a = sub(A, me, 0, m - me, k), c = sub(C, me, 0, m - me, n);
+        if (thin) {
+            double* w = part(n, m - me, k);
+            int nkc = 0;
+            e.prof_begin("fringe_m_kernel", s);
+            ck(launch_fringe_m(a.p, a.rs, a.cs, B.p, B.rs, B.cs, static_cast<int>(m - me), n, k,
+                               w, &nkc, s),
+               "fringe (m)");
+            e.prof_end(s);
+            e.prof_begin("fringe_reduce_kernel", s);
+            ck(launch_fringe_reduce(w, nkc, static_cast<int>(m - me), n, alpha, c.p, c.cs, c.rs, s),
+               "fringe (m) reduce");
+            e.prof_end(s);
+            launches += 2;
+        } else {
+            launches += run_strassen(e, s, STRASSEN_DGEMM, 0, alpha, a, B, c, nullptr);
+        }
+    }
+    if (ne < n) {
+        const DView a = sub(A, 0, 0, me, k), b = sub(B, 0, ne, k, n - ne);
+        const DView c = sub(C, 0, ne, me, n - ne);
+        if (thin) {
+            double* w = part(me, n - ne, k);
+            int nkc = 0;
+            e.prof_begin("fringe_n_kernel", s);
+            ck(launch_fringe_n(a.p, a.rs, a.cs, b.p, b.rs, b.cs, me, static_cast<int>(n - ne), k,
+                               w, &nkc, s),
+               "fringe (n)");
+            e.prof_end(s);
+            e.prof_begin("fringe_reduce_kernel", s);
+            ck(launch_fringe_reduce(w, nkc, static_cast<int>(n - ne), me, alpha, c.p, c.rs, c.cs, s),
+               "fringe (n) reduce");
+            e.prof_end(s);
+            launches += 2;
+        } else {
+            launches += run_strassen(e, s, STRASSEN_DGEMM, 0, alpha, a, b, c, nullptr);
+        }
+    }
     return launches;
 }
 

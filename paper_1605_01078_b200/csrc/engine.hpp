@@ -42,6 +42,7 @@ struct Engine {
     DeviceBuffer mbuf, tabuf, tbbuf;          // AB / Naive temporaries
     DeviceBuffer ticket_buf;                  // ordered fused-epilogue tickets
     DeviceBuffer unit_ctr_buf;                // persistent launches' unit counters
+    DeviceBuffer fringe_buf;                  // k-chunk partials of the peeled fringe updates
     int unit_ctr_next = 0;                    // next counter (reset per call)
     // recorded on the call stream at the end of every call; the next call's stream
     // waits on it first, so a call on another stream cannot overwrite workspace

@@ -242,6 +242,26 @@ struct StreamParams {
 };
 cudaError_t launch_stream_update(const StreamParams& p, cudaStream_t s);
 
+// ---- fringe updates of dynamic peeling (fringe.cu) ---------------------------
+// one dimension of at most fringe_max_width(): streaming kernels, the long operand read
+// once; k-chunk partials in `part` (fringe_partial_bytes) added in ascending order
+int fringe_max_width();
+size_t fringe_partial_bytes(long long_len, int thin, long K);
+// k-chunk partials of A (M x K) B (K x nf) / of A (mf x K) B (K x N), then
+// C += alpha * (their sum in ascending chunk order)
+cudaError_t launch_fringe_n(const double* A, long long rs_a, long long cs_a, const double* B,
+                            long long rs_b, long long cs_b, long M, int nf, long K, double* part,
+                            int* nkc_out, cudaStream_t s);
+cudaError_t launch_fringe_m(const double* A, long long rs_a, long long cs_a, const double* B,
+                            long long rs_b, long long cs_b, int mf, long N, long K, double* part,
+                            int* nkc_out, cudaStream_t s);
+cudaError_t launch_fringe_reduce(const double* part, int nkc, int thin, long len, double alpha,
+                                 double* C, long long sl, long long st, cudaStream_t s);
+// C (M x N) += alpha A (M x kf) B (kf x N)
+cudaError_t launch_fringe_k(const double* A, long long rs_a, long long cs_a, const double* B,
+                            long long rs_b, long long cs_b, double* C, long long rs_c,
+                            long long cs_c, long M, long N, int kf, double alpha, cudaStream_t s);
+
 // ---- beta pre-scale for the dgemm shim -------------------------------------
 cudaError_t launch_scale(double* c, long rows, long cols, long long rs, long long cs, double beta,
                          cudaStream_t s);

@@ -554,3 +554,43 @@ def test_operand_events_order_late_c(v, L):
     nw = (torch.linalg.norm(C - ref) / (torch.linalg.norm(A) * torch.linalg.norm(B))).item()
     assert nw <= 5e-12, (v, L, nw)
     ctx.close()
+
+
+@pytest.mark.parametrize("v,L,shape", [
+    ("abc", 1, (1025, 1027, 1029)),      # fringes of 1 at level 1
+    ("c", 2, (2051, 2050, 2049)),        # 3 / 2 / 1 at level 2
+    ("naive", 2, (1539, 2049, 1026)),    # 3 / 1 / 2
+    ("naive", 3, (2055, 2049, 2052)),    # 7 / 1 / 4 at level 3
+    ("c", 3, (2050, 2054, 2051)),        # 2 / 6 / 3
+])
+def test_peeled_fringe_kernels(cuda, v, L, shape):
+    """The fringe updates of dynamic peeling run as streaming kernels (csrc/fringe.cu):
+    every fringe width the levels produce, column- and row-major C, alpha != 1 -- against
+    the oracle's blocked DGEMM within the BASELINE bound, bitwise repeatable, the launch
+    count equal to the profile's, and equal within the bound to the reference's padded
+    path (peeling off)."""
+    m, n, k = shape
+    a, b, c0 = inputs(m, n, k, (81, 82, 83))
+    ref = oracle_result("dgemm", 0, -0.75, a, b, c0, use_reference_gemm=False)
+    c = S.Ctx()
+    c.set_max_level(3)
+    c.enable_profiling(True)
+    tol = {1: 1e-12, 2: 5e-12, 3: 2e-11}[L]
+    scale = np.linalg.norm(a) * np.linalg.norm(b)
+    outs = []
+    for order in ("F", "C", "F"):
+        out = np.array(c0, order=order)
+        c.gemm(v, L, -0.75, a, b, out)
+        names = [p["kernel"] for p in c.last_profile()]
+        assert c.last_launches() == len(names)
+        assert {"fringe_k_kernel", "fringe_m_kernel", "fringe_n_kernel",
+                "fringe_reduce_kernel"} <= set(names), names
+        assert np.linalg.norm(out - ref) / scale <= tol, (v, L, order)
+        outs.append(out)
+    assert np.array_equal(outs[0], outs[2])          # repeatable
+    c.set_peeling(False)                              # the reference's zero padding
+    pad = np.array(c0, order="F")
+    c.gemm(v, L, -0.75, a, b, pad)
+    assert not any(p["kernel"].startswith("fringe") for p in c.last_profile())
+    assert np.linalg.norm(pad - ref) / scale <= tol
+    c.close()
