@@ -1051,15 +1051,29 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
     const int L = (variant == STRASSEN_DGEMM) ? 0 : level;
     const long S = 1L << L;
     const long m = A.rows, k = A.cols, n = B.cols;
-    const long me = m & ~(S - 1), ne = n & ~(S - 1), ke = k & ~(S - 1);
+    // Dynamic peeling: the core is the largest problem with dimensions that are multiples
+    // of 2^L -- or, where a dimension exceeds a whole number of quadrant tiles by at most
+    // the fringe kernels' width (4100 at level 2: quadrants of 1025 = 8 tiles + 1 row,
+    // which would run a ninth, padded tile row), the multiple of 2^L x 128 below it.
+    auto core = [&](long d, long tile) { return peel_core(d, S, tile, fringe_max_width()); };
+    static const bool tile_peel = [] {
+        const char* v = std::getenv("STRASSEN_B200_TILE_PEEL");  // 0 / 1 (experiments)
+        return v ? std::atoi(v) != 0 : true;
+    }();
+    const long me = tile_peel ? core(m, kBM) : m & ~(S - 1);
+    const long ne = tile_peel ? core(n, kBN) : n & ~(S - 1);
+    const long ke = k & ~(S - 1);
     const bool ragged = me != m || ne != n || ke != k;
     // peel only when it removes padded work: compare output-tile x k-step counts
     auto work = [&](long mm, long nn, long kk) {
         return ceil_div(ceil_div(mm, S), kBM) * ceil_div(ceil_div(nn, S), kBN) *
                ceil_div(ceil_div(kk, S), kBK);
     };
-    const bool peel = L > 0 && ragged && e.peeling && me >= S * kBM && ne >= S * kBN &&
-                      ke >= S * kBK && work(me, ne, ke) < work(m, n, k);
+    const bool peel = ragged && e.peeling && me >= S * kBM && ne >= S * kBN && ke >= S * kBK &&
+                      m - me <= fringe_max_width() && n - ne <= fringe_max_width() &&
+                      (L > 0 || tile_peel) &&
+                      peel_pays(work(m, n, k), work(me, ne, ke), L == 0 ? 1 : L == 1 ? 7 : L == 2 ? 49 : 343,
+                                e.num_sms > 0 ? e.num_sms : 148, fringe_bytes(m, n, k, me, ne, ke));
     if (win && win->count() > 0 &&
         (peel || !tma_ready(A, ceil_div(m, S), static_cast<int>(S)) ||
          !tma_ready(B, ceil_div(k, S), static_cast<int>(S)))) {

@@ -32,12 +32,14 @@ __global__ void __launch_bounds__(kRowThreads)
     thin_n_kernel(const double* __restrict__ A, long long rs_a, long long cs_a,
                   const double* __restrict__ B, long long rs_b, long long cs_b, long M, long K,
                   double* __restrict__ part) {
-    __shared__ double Bs[kChunkN][NF];
+    // rows padded to an even count: one 16-byte shared load per pair of columns
+    constexpr int NP = (NF + 1) & ~1;
+    __shared__ __align__(16) double Bs[kChunkN][NP];
     const long k0 = static_cast<long>(blockIdx.y) * kChunkN;
     const int kn = static_cast<int>(min(static_cast<long>(kChunkN), K - k0));
-    for (int t = threadIdx.x; t < kn * NF; t += kRowThreads) {
-        const int kk = t / NF, j = t % NF;
-        Bs[kk][j] = B[(k0 + kk) * rs_b + j * cs_b];
+    for (int t = threadIdx.x; t < kn * NP; t += kRowThreads) {
+        const int kk = t / NP, j = t % NP;
+        Bs[kk][j] = j < NF ? B[(k0 + kk) * rs_b + j * cs_b] : 0.0;
     }
     __syncthreads();
     const long i = static_cast<long>(blockIdx.x) * kRowThreads + threadIdx.x;
@@ -50,7 +52,11 @@ __global__ void __launch_bounds__(kRowThreads)
     for (int kk = 0; kk < kn; ++kk) {
         const double x = __ldg(a + kk * cs_a);
 #pragma unroll
-        for (int j = 0; j < NF; ++j) acc[j] = fma(x, Bs[kk][j], acc[j]);
+        for (int j2 = 0; j2 < NP / 2; ++j2) {
+            const double2 bv = *reinterpret_cast<const double2*>(&Bs[kk][2 * j2]);
+            acc[2 * j2] = fma(x, bv.x, acc[2 * j2]);
+            if (2 * j2 + 1 < NF) acc[2 * j2 + 1] = fma(x, bv.y, acc[2 * j2 + 1]);
+        }
     }
 #pragma unroll
     for (int j = 0; j < NF; ++j)

@@ -40,6 +40,32 @@ inline int choose_ksplit(long ntiles, long nprod, long ktiles, long sms, double 
     return best_ks;
 }
 
+// Dynamic peeling (engine.cpp run_device): the core extent of a dimension d at level L
+// (S = 2^L) -- the multiple of S below d, or, where d exceeds a whole number of quadrant
+// tiles by at most the fringe kernels' width w, the multiple of S x tile below it.
+inline long peel_core(long d, long S, long tile, long w) {
+    const long rem = d % (S * tile);
+    if (rem > 0 && rem <= w && d > rem) return d - rem;
+    return d & ~(S - 1);
+}
+
+// Peeling pays when the padded tile steps it removes (work counts 128 x 128 x 16 steps of
+// one product; nprod = 7^L products; 2.1 us per step on one of `sms` SMs) outweigh the
+// fringe updates: their launches (~40 us) and their HBM passes (measured 2-5 TB/s;
+// profiles/r02_tile_peel_ab.log: 2052^3 classical loses, 4100^3 gains).
+inline bool peel_pays(long work_full, long work_core, long nprod, long sms, double fringe_bytes) {
+    return static_cast<double>(work_full - work_core) * nprod * 2.1e-6 / sms >
+           40e-6 + fringe_bytes / 2.0e12;
+}
+// HBM bytes of the three fringe updates of an m x n x k problem peeled to me x ne x ke
+inline double fringe_bytes(long m, long n, long k, long me, long ne, long ke) {
+    double b = 0.0;
+    if (ke < k) b += 16.0 * static_cast<double>(me) * ne;
+    if (me < m) b += 8.0 * static_cast<double>(k) * n;
+    if (ne < n) b += 8.0 * static_cast<double>(me) * k;
+    return b;
+}
+
 // Classical launches of four or more waves of tile owners: the last, partial wave
 // leaves SMs idle (3840^3: 900 tiles on 148 SMs run as 7 waves for 6.08 waves of work).
 // Hybrid: the first tile columns as whole waves of tile owners, the last `cols` tile

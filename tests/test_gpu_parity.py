@@ -557,7 +557,7 @@ def test_operand_events_order_late_c(v, L):
 
 
 @pytest.mark.parametrize("v,L,shape", [
-    ("abc", 1, (1025, 1027, 1029)),      # fringes of 1 at level 1
+    ("abc", 1, (3073, 3075, 3077)),      # fringes of 1 at level 1
     ("c", 2, (2051, 2050, 2049)),        # 3 / 2 / 1 at level 2
     ("naive", 2, (1539, 2049, 1026)),    # 3 / 1 / 2
     ("naive", 3, (2055, 2049, 2052)),    # 7 / 1 / 4 at level 3
