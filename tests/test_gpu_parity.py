@@ -588,6 +588,11 @@ def test_peeled_fringe_kernels(cuda, v, L, shape):
         assert np.linalg.norm(out - ref) / scale <= tol, (v, L, order)
         outs.append(out)
     assert np.array_equal(outs[0], outs[2])          # repeatable
+    # row-major A and B (swapped strides): the fringe kernels index the caller's views
+    out = np.array(c0, order="F")
+    c.gemm(v, L, -0.75, np.ascontiguousarray(a), np.ascontiguousarray(b), out)
+    assert any(p["kernel"].startswith("fringe") for p in c.last_profile())
+    assert np.linalg.norm(out - ref) / scale <= tol, (v, L, "row-major operands")
     c.set_peeling(False)                              # the reference's zero padding
     pad = np.array(c0, order="F")
     c.gemm(v, L, -0.75, a, b, pad)
