@@ -21,7 +21,7 @@ namespace {
 
 constexpr int kThinMax = 8;      // fringe width limit (2^L - 1 <= 7 at L <= 3)
 constexpr int kChunkK = 512;     // k per partial chunk (m fringe)
-constexpr int kChunkN = 128;     // k per partial chunk (n fringe: one thread per row of A, so
+constexpr int kChunkN = 64;      // k per partial chunk (n fringe: one thread per row of A, so
                                  // short chunks supply the CTAs that keep HBM busy)
 constexpr int kRowThreads = 128;
 
@@ -48,16 +48,25 @@ __global__ void __launch_bounds__(kRowThreads)
 #pragma unroll
     for (int j = 0; j < NF; ++j) acc[j] = 0.0;
     const double* a = A + i * rs_a + k0 * cs_a;
-#pragma unroll 8
-    for (int kk = 0; kk < kn; ++kk) {
-        const double x = __ldg(a + kk * cs_a);
+    // eight loads of A in flight per thread (the kernel is bound by their latency:
+    // ncu showed 0.14 eligible warps per scheduler with one load at a time)
+    auto step = [&](int kk, double x) {
 #pragma unroll
         for (int j2 = 0; j2 < NP / 2; ++j2) {
             const double2 bv = *reinterpret_cast<const double2*>(&Bs[kk][2 * j2]);
             acc[2 * j2] = fma(x, bv.x, acc[2 * j2]);
             if (2 * j2 + 1 < NF) acc[2 * j2 + 1] = fma(x, bv.y, acc[2 * j2 + 1]);
         }
+    };
+    int kk = 0;
+    for (; kk + 8 <= kn; kk += 8) {
+        double x[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) x[u] = __ldg(a + (kk + u) * cs_a);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) step(kk + u, x[u]);
     }
+    for (; kk < kn; ++kk) step(kk, __ldg(a + kk * cs_a));
 #pragma unroll
     for (int j = 0; j < NF; ++j)
         part[(static_cast<long long>(blockIdx.y) * NF + j) * M + i] = acc[j];
@@ -86,7 +95,18 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
         for (int i = 0; i < MF; ++i) acc[i] = 0.0;
         const double* b = B + k0 * rs_b + j * cs_b;
-        for (int kk = lane; kk < kn; kk += 32) {
+        // four loads of B in flight per lane (latency-bound otherwise, as thin_n_kernel)
+        int kk = lane;
+        for (; kk + 96 < kn; kk += 128) {
+            double x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) x[u] = __ldg(b + (kk + 32 * u) * rs_b);
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int i = 0; i < MF; ++i) acc[i] = fma(As[i][kk + 32 * u], x[u], acc[i]);
+        }
+        for (; kk < kn; kk += 32) {
             const double x = __ldg(b + kk * rs_b);
 #pragma unroll
             for (int i = 0; i < MF; ++i) acc[i] = fma(As[i][kk], x, acc[i]);
