@@ -425,13 +425,13 @@ static double predict_level3(strassen_variant v, long m, long n, long k, int sms
 double b200_predict_seconds(strassen_variant v, int level, long m, long n, long k, int sms) {
     if (level == 3 && (v == STRASSEN_NAIVE || v == STRASSEN_C)) {
         // peeling as run_device does at level 3 (fringe kernels for the three updates)
-        const long me = peel_core(m, 8, 128, 8), ne = peel_core(n, 8, 128, 8), ke = k & ~7L;
+        const long me = peel_core(m, 8, 128, 16), ne = peel_core(n, 8, 128, 16), ke = k & ~7L;
         auto work3 = [&](long mm, long nn, long kk) {
             return ceil_div(ceil_div(mm, 8), 128) * ceil_div(ceil_div(nn, 8), 128) *
                    ceil_div(ceil_div(kk, 8), 16);
         };
         if ((me != m || ne != n || ke != k) && me >= 8 * 128 && ne >= 8 * 128 && ke >= 8 * 16 &&
-            m - me <= 8 && n - ne <= 8 &&
+            m - me <= 16 && n - ne <= 16 &&
             peel_pays(work3(m, n, k), work3(me, ne, ke), 343, sms, fringe_bytes(m, n, k, me, ne, ke))) {
             const double BWF = 4.5e12, launch = 12e-6;
             double t = predict_level3(v, me, ne, ke, sms);
@@ -445,7 +445,7 @@ double b200_predict_seconds(strassen_variant v, int level, long m, long n, long 
     const int L = (v == STRASSEN_DGEMM) ? 0 : level;
     const long S = 1L << L;
     // (the fringe kernels' width, fringe.cu kThinMax)
-    const long me = peel_core(m, S, 128, 8), ne = peel_core(n, S, 128, 8), ke = k & ~(S - 1);
+    const long me = peel_core(m, S, 128, 16), ne = peel_core(n, S, 128, 16), ke = k & ~(S - 1);
     // dynamic peeling as engine.cpp run_device applies it: the even core, then
     // three classical fringe updates
     auto work = [&](long mm, long nn, long kk) {
@@ -456,7 +456,7 @@ double b200_predict_seconds(strassen_variant v, int level, long m, long n, long 
     // 16-byte epilogue
     auto vec = [&](long rows) { return m % 2 == 0 && (L == 0 || ceil_div(rows, S) % 2 == 0); };
     if ((me != m || ne != n || ke != k) && me >= S * 128 && ne >= S * 128 && ke >= S * 16 &&
-        m - me <= 8 && n - ne <= 8 &&
+        m - me <= 16 && n - ne <= 16 &&
         peel_pays(work(m, n, k), work(me, ne, ke), L == 0 ? 1 : L == 1 ? 7 : 49, sms,
                   fringe_bytes(m, n, k, me, ne, ke))) {
         double t = predict_core(v, L, me, ne, ke, sms, vec(me));

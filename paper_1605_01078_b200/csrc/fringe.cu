@@ -1,6 +1,7 @@
 // Fringe updates of dynamic peeling (engine.cpp run_device): after the even core
 // m_e x n_e x k_e has gone through Strassen, the three classical updates that finish
-// C := alpha A B + C have one dimension of at most 2^L - 1 <= 7:
+// C := alpha A B + C have one dimension of at most 16 (2^L - 1 <= 7 for odd sizes; up to
+// 16 where the core is cut back to a whole number of quadrant tiles):
 //   k fringe:  C[0:me, 0:ne] += alpha A[0:me, ke:k] B[ke:k, 0:ne]      (rank-kf update)
 //   m fringe:  C[me:m, 0:n]  += alpha A[me:m, 0:k]  B[0:k, 0:n]        (mf rows of C)
 //   n fringe:  C[0:me, ne:n] += alpha A[0:me, 0:k]  B[0:k, ne:n]       (nf columns of C)
@@ -19,8 +20,9 @@
 namespace sb200 {
 namespace {
 
-constexpr int kThinMax = 8;      // fringe width limit (2^L - 1 <= 7 at L <= 3)
-constexpr int kChunkK = 512;     // k per partial chunk (m fringe)
+constexpr int kThinMax = 16;     // fringe width limit (2^L - 1 <= 7 at L <= 3; up to 16 rows or
+                                 // columns above a whole number of tiles, engine.cpp run_device)
+constexpr int kChunkK = 256;     // k per partial chunk (m fringe: 16 x 256 doubles of shared memory)
 constexpr int kChunkN = 64;      // k per partial chunk (n fringe: one thread per row of A, so
                                  // short chunks supply the CTAs that keep HBM busy)
 constexpr int kRowThreads = 128;
@@ -204,6 +206,14 @@ cudaError_t rank_w(const double* A, long long rs_a, long long cs_a, const double
         case 6: return CALL(6);                                                         \
         case 7: return CALL(7);                                                         \
         case 8: return CALL(8);                                                         \
+        case 9: return CALL(9);                                                         \
+        case 10: return CALL(10);                                                       \
+        case 11: return CALL(11);                                                       \
+        case 12: return CALL(12);                                                       \
+        case 13: return CALL(13);                                                       \
+        case 14: return CALL(14);                                                       \
+        case 15: return CALL(15);                                                       \
+        case 16: return CALL(16);                                                       \
         default: return cudaErrorInvalidValue;                                          \
     }
 
