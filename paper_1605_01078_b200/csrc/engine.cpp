@@ -1060,8 +1060,12 @@ long run_device(Engine& e, cudaStream_t s, strassen_variant variant, int level, 
         const char* v = std::getenv("STRASSEN_B200_TILE_PEEL");  // 0 / 1 (experiments)
         return v ? std::atoi(v) != 0 : true;
     }();
-    const long me = tile_peel ? core(m, kBM) : m & ~(S - 1);
-    const long ne = tile_peel ? core(n, kBN) : n & ~(S - 1);
+    // (not for a pipelined host call: a peeled call cannot run in windows, and losing the
+    // transfer overlap costs more than the padded tiles -- it keeps the multiple-of-2^L
+    // rule, so at these shapes it rounds differently from the device call)
+    const bool windowed = win && win->count() > 0;
+    const long me = tile_peel && !windowed ? core(m, kBM) : m & ~(S - 1);
+    const long ne = tile_peel && !windowed ? core(n, kBN) : n & ~(S - 1);
     const long ke = k & ~(S - 1);
     const bool ragged = me != m || ne != n || ke != k;
     // peel only when it removes padded work: compare output-tile x k-step counts
