@@ -205,6 +205,9 @@ def test_product_groups_in_tensor_memory(cuda, variant, level, shape):
     ("dgemm", 0, (512, 512, 512)), ("dgemm", 0, (1024, 1024, 1024)), ("abc", 1, (1024, 1024, 1024)),
     ("c", 1, (1000, 900, 1100)), ("abc", 2, (2048, 2048, 2048)), ("naive", 2, (2048, 1536, 1024)),
     ("ab", 2, (1536, 1536, 1536)), ("c", 2, (4096, 4096, 512)),
+    ("dgemm", 0, (3840, 3840, 1030)),   # tile-owner waves + stream-K tail (two launches)
+    ("c", 2, (4100, 4100, 520)),        # peeled to whole tiles: fringe kernels
+    ("dgemm", 0, (768, 768, 768)),      # k-chunk grid, cooperative fixup
 ])
 def test_device_entry_under_cuda_graph_capture(cuda, variant, level, shape):
     """strassen_gemm_device issued on a capturing stream (include/strassen.h): the call's
