@@ -295,7 +295,13 @@ static double predict_core(strassen_variant v, int L, long m, long n, long k, in
     static const double tc[3][4] = {{1, 0, 0, 1}, {7, 5, 5, 12}, {49, 95, 95, 144}};
     static const double n_sums[3] = {0, 5, 45};  // multi-term operand sums per side
     const double mul = tc[L][0], cu = tc[L][3];
-    const double tiles = std::ceil(qm / 128.0) * std::ceil(qn / 128.0);
+    // (C and Naive run 64-wide tiles where the last 128-wide tile column would be at most
+    // half used, engine.cpp run_strassen: count the columns in halves there)
+    const double rem_n = std::fmod(qn, 128.0);
+    const bool half_edge = (v == STRASSEN_C || v == STRASSEN_NAIVE) && rem_n > 0 && rem_n <= 64 &&
+                           std::ceil(qn / 128.0) <= 15 && std::ceil(qk / 16.0) <= 128;
+    const double tiles = std::ceil(qm / 128.0) *
+                         (half_edge ? std::ceil(qn / 64.0) / 2.0 : std::ceil(qn / 128.0));
     // mm_kernel efficiency (executed flops / DMMA peak), fitted to the sweeps
     // (tools/model_fit.py, profiles/r02_sweep_*.csv): single-term 0.976; fused operand
     // sums 0.91 at level 1; at level 2 the 4-term sides are materialised (the default

@@ -1215,11 +1215,19 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
         const long units = tiles * (L == 0 ? 1 : L == 1 ? 7 : 49);
         const long ktiles = ceil_div(qk, kBK);
         const bool one_window = !win || win->rows * win->cols <= 1;
+        // A quadrant whose last 128-wide tile column is at most half used (2816^3 at
+        // level 2: quadrants of 704 = 5.5 tiles) wastes less on 64-wide tiles: C / Naive
+        // L2 2816^3 32.6 -> 35.0 TF/s, 3840^3 35.3 -> 38.1, 4864^3 37.8 -> 40.1, 6400^3
+        // 40.0 -> 40.5 (profiles/r02_narrow_half_edge.log).  At these sizes the programs
+        // split nothing in k, so narrow and wide tiles give bitwise the same result
+        // (tools/narrow_check.py) and windowed host calls may keep the wide tiles.
+        const long rem_n = qn % kBN;
+        const bool half_edge = rem_n > 0 && rem_n <= kNarrowBN && ceil_div(qn, kBN) <= 15;
         bool pick = false;
         if (ktiles <= 128) {
             if (variant == STRASSEN_DGEMM) pick = 3 * tiles < 2 * sms;
-            else if (variant == STRASSEN_C) pick = units < 10 * sms;
-            else if (variant == STRASSEN_NAIVE) pick = units < 4 * sms;
+            else if (variant == STRASSEN_C) pick = units < 10 * sms || half_edge;
+            else if (variant == STRASSEN_NAIVE) pick = units < 4 * sms || half_edge;
         }
         P.narrow = one_window && (narrow_env > 0 || (narrow_env < 0 && pick)) ? 1 : 0;
     }
