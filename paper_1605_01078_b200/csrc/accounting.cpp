@@ -298,7 +298,8 @@ static double predict_core(strassen_variant v, int L, long m, long n, long k, in
     // (C and Naive run 64-wide tiles where the last 128-wide tile column would be at most
     // half used, engine.cpp run_strassen: count the columns in halves there)
     const double rem_n = std::fmod(qn, 128.0);
-    const bool half_edge = (v == STRASSEN_C || v == STRASSEN_NAIVE) && rem_n > 0 && rem_n <= 64 &&
+    const bool half_edge = (v == STRASSEN_C || v == STRASSEN_NAIVE || (v == STRASSEN_AB && L == 2)) &&
+                           rem_n > 0 && rem_n <= 64 &&
                            std::ceil(qn / 128.0) <= 15 && std::ceil(qk / 16.0) <= 128;
     const double tiles = std::ceil(qm / 128.0) *
                          (half_edge ? std::ceil(qn / 64.0) / 2.0 : std::ceil(qn / 128.0));

@@ -1228,6 +1228,11 @@ long run_strassen(Engine& e, cudaStream_t s, strassen_variant variant, int level
             if (variant == STRASSEN_DGEMM) pick = 3 * tiles < 2 * sms;
             else if (variant == STRASSEN_C) pick = units < 10 * sms || half_edge;
             else if (variant == STRASSEN_NAIVE) pick = units < 4 * sms || half_edge;
+            // AB at level 2 (its 4-term sides are materialised, the rest are 2-term sums:
+            // the narrow kernel's limit) gains there too -- 3840^3 34.4 -> 36.5 TF/s, 4864^3
+            // 36.8 -> 38.2 -- and stores products like Naive, so the result is bitwise the
+            // wide one; at level 1 the gain is ~2% and ABC keeps its grouped epilogue
+            else if (variant == STRASSEN_AB && L == 2 && e.fuse_max_terms <= 2) pick = half_edge;
         }
         P.narrow = one_window && (narrow_env > 0 || (narrow_env < 0 && pick)) ? 1 : 0;
     }

@@ -16,7 +16,8 @@ for d in (2816, 3840, 4864, 6400):
     A = (torch.rand(d, d, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
     B = (torch.rand(d, d, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
     C0 = (torch.rand(d, d, dtype=torch.float64, device="cuda", generator=g) * 2 - 1).t()
-    for v, L in (("c", 2), ("naive", 2), ("c", 1), ("naive", 1), ("dgemm", 0)):
+    for v, L in (("c", 2), ("naive", 2), ("c", 1), ("naive", 1), ("ab", 2), ("ab", 1), ("abc", 2),
+                 ("dgemm", 0)):
         C = C0.t().clone().t()
         ctx.gemm_device(v, L, 1.0, A, B, C)
         torch.cuda.synchronize()
